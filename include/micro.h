@@ -1,0 +1,220 @@
+/*
+ * micro.h — C ABI of the B200-native MiCRO sparsify + aggregate path.
+ *
+ * Drop-in boundary for the reference's hot path (sparsim, /root/reference/proj):
+ * every entry point below names the reference interface it replaces
+ * (paths relative to /root/reference/proj).  Plain pointers and sizes only; no
+ * torch or C++ types.  Device pointers are CUDA global-memory addresses on the
+ * context's device; streams are cudaStream_t passed as void*.
+ *
+ * Status codes map 1:1 onto the reference's exception types:
+ *   MICRO_EINVAL     <-> std::invalid_argument
+ *   MICRO_ELOGIC     <-> std::logic_error
+ *   MICRO_ENONFINITE <-> std::runtime_error ("non-finite gradient", harness.cpp:128-130)
+ * The message of the last failing call on the calling thread is returned by
+ * micro_last_error(); it carries the reference's message text where one exists.
+ *
+ * Element types: MICRO_F32 is the north-star contract (fp32 gradients,
+ * fp32 residuals, fp64 thresholds); MICRO_F64 runs the identical kernels in the
+ * reference's own precision and is bit-exact against its compiled code.
+ */
+#ifndef MICRO_H
+#define MICRO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MICRO_ABI_VERSION 1
+#define MICRO_MAX_WORKERS 64
+
+typedef enum micro_status {
+  MICRO_OK = 0,
+  MICRO_EINVAL = 1,
+  MICRO_ELOGIC = 2,
+  MICRO_ENONFINITE = 3,
+  MICRO_ECUDA = 4,
+  MICRO_ENCCL = 5,
+  MICRO_ECAPACITY = 6,
+  MICRO_ENOMEM = 7
+} micro_status;
+
+typedef enum micro_dtype { MICRO_F32 = 0, MICRO_F64 = 1 } micro_dtype;
+
+/* sparsifier.hpp:26 PerWorkerTarget */
+typedef enum micro_target { MICRO_TARGET_SPLIT = 0, MICRO_TARGET_FULL = 1 } micro_target;
+
+int micro_abi_version(void);
+const char* micro_status_string(int status);
+/* Message of the last non-OK return on this thread ("" if none). */
+const char* micro_last_error(void);
+
+/* ---- pure host functions (no device work) ------------------------------- */
+
+/* tensor.hpp:48-63 partition(n_g, n, t, worker) -> [start, end) */
+int micro_partition(int64_t n_g, int n, int64_t t, int worker, int64_t* start, int64_t* end);
+/* sparsifier.cpp:110-116 global_target_count */
+int micro_global_target_count(double density, int64_t n_g, uint64_t* k);
+/* sparsifier.cpp:118-125 per_worker_target_count */
+int micro_per_worker_target_count(double density, int64_t n_g, int n, int target, uint64_t* k);
+/* sparsifier.cpp:69-83 micro_update_threshold (in/out *delta) */
+int micro_update_threshold(double* delta, uint64_t k_target, uint64_t k_selected, double alpha,
+                           double min_threshold);
+
+/* ---- stateless device operations (value-level API) ---------------------- *
+ * All pointers are device pointers; work is enqueued on `stream`; counts that
+ * the host needs are returned through device memory (d_count) so nothing
+ * synchronises unless stated.                                               */
+
+/* error_feedback.hpp:17-23 accumulate: acc = e + eta*g (two roundings). */
+int micro_accumulate(int dtype, const void* d_e, double eta, const void* d_g, void* d_acc,
+                     int64_t n, void* stream);
+/* sparsifier.cpp:22-37 select_by_threshold: ascending (idx, acc[idx]) with
+ * |acc| > delta inside [start, end).  Writes at most `cap` pairs; *d_count
+ * (device int64) receives the full count (> cap => MICRO_ECAPACITY at the next
+ * synchronising call of this thread, see micro_sync). */
+int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start,
+                              int64_t end, double delta, int32_t* d_idx, void* d_val,
+                              int64_t cap, int64_t* d_count, void* stream);
+/* error_feedback.hpp:27-39 compensate (in place): acc[idx[k]] = 0. */
+int micro_compensate(int dtype, void* d_acc, int64_t n_g, const int32_t* d_idx, int64_t k,
+                     void* stream);
+/* collectives.cpp:30-49 all_reduce_sparse_values: sums[k] = sum over workers
+ * in order of accs[i][union[k]], starting from +0.  h_accs: host array of n
+ * device pointers. */
+int micro_all_reduce_sparse_values(int dtype, const void* const* h_accs, int n, int64_t n_g,
+                                   const int32_t* d_union, int64_t K, void* d_sums, void* stream);
+/* collectives.cpp:51-57 all_reduce_sparse: dense n_g result, sums at the union. */
+int micro_all_reduce_sparse(int dtype, const void* const* h_accs, int n, int64_t n_g,
+                            const int32_t* d_union, int64_t K, void* d_dense, void* stream);
+/* collectives.cpp:14-28 all_gather_indices: sorted unique union of n sorted
+ * index lists (device, concatenated in worker order, h_counts on host).
+ * Synchronises; *K returns the union size. */
+int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_concat,
+                             int32_t* d_union, int64_t* K, void* stream);
+
+/* Synthetic N(0,1) gradients of include/micro_synth.h (bench/test inputs). */
+int micro_synth_gaussian(int dtype, uint64_t seed, uint32_t worker, uint64_t t, int64_t n,
+                         void* d_out, void* stream);
+
+/* ---- the MiCRO engine (run_iteration's MiCRO branch, harness.cpp:121-224) -- *
+ * A context holds `n_local` workers of an n-worker cluster on one device: the
+ * residuals e_i (harness.hpp:51), thresholds delta_i (:52), selection and
+ * union buffers, the dense averaged gradient and the look-back workspace.
+ *   n_local == n_workers : the whole cluster lives on this device (the
+ *                          reference's in-process ClusterState); micro_step
+ *                          runs the complete iteration.
+ *   n_local == 1 < n     : one rank of a multi-GPU job (one process per GPU);
+ *                          micro_compress runs K1, the host moves counts,
+ *                          indices and values between ranks (NCCL), and the
+ *                          micro_dist_* calls run the device halves.        */
+
+typedef struct micro_ctx micro_ctx;
+
+typedef struct micro_config {
+  int64_t n_g;              /* gradient length */
+  int32_t n_workers;        /* n */
+  int32_t n_local;          /* n (single-device cluster) or 1 (one rank) */
+  int32_t rank;             /* worker id of the (first) local worker */
+  int32_t dtype;            /* micro_dtype */
+  double density;           /* d in (0,1]            sparsifier.hpp:41 */
+  double initial_threshold; /* delta_0 >= 0          sparsifier.hpp:42 */
+  double scaling_factor;    /* alpha in (0,1)        sparsifier.hpp:43 */
+  double min_threshold;     /* eps_delta > 0         sparsifier.hpp:44 */
+  int32_t target;           /* micro_target          sparsifier.hpp:45 */
+  int32_t error_feedback;   /* RunConfig::error_feedback, harness.hpp:46 */
+  int32_t dense_output;     /* keep the dense averaged gradient g/n on device */
+  int32_t device;           /* CUDA device ordinal */
+  int64_t selection_capacity; /* pairs per worker; 0 = partition size (never overflows) */
+} micro_config;
+
+void micro_config_default(micro_config* cfg);
+
+int micro_ctx_create(micro_ctx** ctx, const micro_config* cfg, void* stream);
+int micro_ctx_destroy(micro_ctx* ctx);
+/* Back to t = 0 state: residuals 0, thresholds delta_0, errors cleared. */
+int micro_ctx_reset(micro_ctx* ctx);
+void* micro_ctx_stream(micro_ctx* ctx);
+
+/* Optional model x (device, n_g elements of dtype): every aggregation applies
+ * x[j] -= sum_j / n at the union (harness.cpp:210-215).  NULL disables. */
+int micro_set_model(micro_ctx* ctx, void* d_x);
+
+/* K1 for each local worker: acc_i = e_i + eta*G_i over all n_g, select
+ * |acc_i| > delta_i in partition(n_g, n, t, i), ordered compaction into
+ * (index, value) pairs, own selections zeroed in the residual.  d_grads: host
+ * array of n_local device pointers.  Asynchronous. */
+int micro_compress(micro_ctx* ctx, const void* const* d_grads, double eta, int64_t t);
+/* Single-device cluster: union + ordered all-worker reduce + foreign zeroing
+ * + threshold update + dense g/n (+ model).  Asynchronous. */
+int micro_aggregate(micro_ctx* ctx);
+/* micro_compress + micro_aggregate. */
+int micro_step(micro_ctx* ctx, const void* const* d_grads, double eta, int64_t t);
+/* End to end with host buffers: pinned host gradients (n_local * n_g) are
+ * copied in, the step runs, and the union (indices + sums, at most cap) is
+ * copied out.  Synchronises; returns MICRO_ENONFINITE / MICRO_ECAPACITY. */
+int micro_step_host(micro_ctx* ctx, const void* h_grads, double eta, int64_t t,
+                    int32_t* h_union_idx, void* h_union_sum, int64_t cap, int64_t* K);
+
+/* Synchronise the context's stream and report deferred device errors
+ * (non-finite gradient, capacity overflow).  After MICRO_ENONFINITE the
+ * context is poisoned until micro_ctx_reset (residuals hold NaN/Inf). */
+int micro_sync(micro_ctx* ctx);
+
+typedef struct micro_stats {
+  int64_t t;               /* iteration of the last step */
+  int64_t steps;           /* completed steps since create/reset */
+  int64_t K;               /* |union| of the last step */
+  int64_t total_selected;  /* sum_i k_i of the last step (== K for MiCRO) */
+  int32_t nonfinite;
+  int32_t overflow;
+} micro_stats;
+
+/* Synchronises.  counts/deltas: n_local entries each (may be NULL):
+ * k_i of the last step and delta_i for the NEXT step. */
+int micro_query(micro_ctx* ctx, micro_stats* st, int64_t* counts, double* deltas);
+/* Per-step history ring (last min(max, steps, 4096) steps), synchronises.
+ * K[s], counts[s*n_local+i], delta_used[s*n_local+i]. Returns the number of
+ * steps written in *written. */
+int micro_history(micro_ctx* ctx, int64_t max, int64_t* t, int64_t* K, int64_t* counts,
+                  double* delta_used, int64_t* written);
+
+/* Device views, valid until the next step on this context. */
+int micro_union_device(micro_ctx* ctx, const int32_t** d_idx, const void** d_sums,
+                       const int64_t** d_K);
+int micro_dense_device(micro_ctx* ctx, const void** d_dense);
+int micro_residual_device(micro_ctx* ctx, int local_worker, void** d_resid);
+int micro_selection_device(micro_ctx* ctx, int local_worker, const int32_t** d_idx,
+                           const void** d_val, const int64_t** d_count);
+int micro_threshold_device(micro_ctx* ctx, double** d_delta);
+/* Host copies (synchronise). */
+int micro_copy_union(micro_ctx* ctx, int32_t* h_idx, void* h_sums, int64_t cap, int64_t* K);
+int micro_copy_residual(micro_ctx* ctx, int local_worker, void* h_out);
+int micro_copy_dense(micro_ctx* ctx, void* h_out);
+
+/* ---- one rank of a multi-GPU job (n_local == 1 < n_workers) -------------- *
+ * Host protocol per iteration (paper_2310_00967_b200/dist.py drives it over
+ * torch.distributed / NCCL):
+ *   micro_compress                      -> own k_i and pairs on device
+ *   all-gather k (n counts)             -> h_counts on host
+ *   all-gather own indices, padded to kmax = max k -> d_all_idx[n][kmax]
+ *   micro_dist_gather_foreign           -> d_send (acc at other owners' indices,
+ *                                          rank order, segment o has k_o values)
+ *   all-to-all-v  send -> owners        -> d_recv (segment r has k_own values)
+ *   micro_dist_owner_reduce             -> d_own_sums[k_own] (rank-ordered sum)
+ *   all-gather own sums, padded to kmax -> d_all_sums[n][kmax]
+ *   micro_dist_finalize                 -> union, dense g/n, model, delta, stats */
+int micro_dist_gather_foreign(micro_ctx* ctx, const int32_t* d_all_idx, const int64_t* h_counts,
+                              int64_t kmax, void* d_send);
+int micro_dist_owner_reduce(micro_ctx* ctx, const void* d_recv, const int64_t* h_counts,
+                            void* d_own_sums);
+int micro_dist_finalize(micro_ctx* ctx, const int32_t* d_all_idx, const void* d_all_sums,
+                        const int64_t* h_counts, int64_t kmax);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MICRO_H */

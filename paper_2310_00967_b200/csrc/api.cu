@@ -1,0 +1,1051 @@
+// api.cu — the C ABI (include/micro.h): host-side engine around the sm_100a
+// kernels of select.cuh / exchange.cuh.  No CPU compute path exists: every
+// array operation below is a device kernel; the host only validates, sizes
+// launches and moves small scalars.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/micro.h"
+#include "../../include/micro_synth.h"
+#include "exchange.cuh"
+#include "select.cuh"
+
+using namespace micro;
+
+// ---------------------------------------------------------------- errors --
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t _e = (call);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(MICRO_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                               \
+  } while (0)
+
+#define TRY(call)                  \
+  do {                             \
+    int _rc = (call);              \
+    if (_rc != MICRO_OK) return _rc; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+size_t dtype_size(int dtype) { return dtype == MICRO_F64 ? 8 : 4; }
+
+int check_dtype(int dtype) {
+  if (dtype != MICRO_F32 && dtype != MICRO_F64) return fail(MICRO_EINVAL, "unknown dtype %d", dtype);
+  return MICRO_OK;
+}
+
+int num_sms(int dev) {
+  static int cache[64] = {0};
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cache[dev] = v;
+  return v;
+}
+
+// ---- pure host restatements (shared by the C ABI and the engine) ----
+
+int h_partition(int64_t n_g, int n, int64_t t, int worker, int64_t* start, int64_t* end) {
+  if (n < 1) return fail(MICRO_EINVAL, "partition: need at least one worker");
+  if (n_g < n)
+    return fail(MICRO_EINVAL, "partition: vector length %lld smaller than worker count %d",
+                (long long)n_g, n);
+  if (worker < 0 || worker >= n)
+    return fail(MICRO_EINVAL, "partition: worker id %d out of range", worker);
+  if (t < 0) return fail(MICRO_EINVAL, "partition: negative iteration");
+  partition_range(n_g, n, t, worker, start, end);
+  return MICRO_OK;
+}
+
+int h_global_target(double d, int64_t n_g, uint64_t* k) {
+  if (!(d > 0.0 && d <= 1.0)) return fail(MICRO_EINVAL, "density must lie in (0, 1]");
+  if (n_g < 1) return fail(MICRO_EINVAL, "global_target_count: empty gradient vector");
+  const long long r = std::llround(d * static_cast<double>(n_g));
+  *k = static_cast<uint64_t>(std::max(1LL, r));
+  return MICRO_OK;
+}
+
+int h_worker_target(double d, int64_t n_g, int n, int target, uint64_t* k) {
+  if (n < 1) return fail(MICRO_EINVAL, "per_worker_target_count: need at least one worker");
+  if (target == MICRO_TARGET_FULL) return h_global_target(d, n_g, k);
+  if (target != MICRO_TARGET_SPLIT) return fail(MICRO_EINVAL, "unknown per-worker target %d", target);
+  if (!(d > 0.0 && d <= 1.0)) return fail(MICRO_EINVAL, "density must lie in (0, 1]");
+  const long long r = std::llround(d * static_cast<double>(n_g) / n);
+  *k = static_cast<uint64_t>(std::max(1LL, r));
+  return MICRO_OK;
+}
+
+int h_update_threshold(double* delta, uint64_t k_target, uint64_t k_sel, double alpha, double eps) {
+  if (!(alpha > 0.0 && alpha < 1.0))
+    return fail(MICRO_EINVAL, "micro_update_threshold: alpha must lie in (0, 1)");
+  if (!(*delta >= 0.0)) return fail(MICRO_EINVAL, "micro_update_threshold: negative threshold");
+  if (k_sel > k_target)
+    *delta = *delta == 0.0 ? eps : *delta * (1.0 + alpha);
+  else if (k_sel < k_target)
+    *delta *= 1.0 - alpha;
+  return MICRO_OK;
+}
+
+constexpr int64_t kHistCap = 4096;
+
+template <typename T>
+int64_t p_max_for(int64_t range) {
+  return (range + tile_elems<T>() - 1) / tile_elems<T>() + 2;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ the context --
+
+struct micro_ctx {
+  micro_config cfg{};
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int n = 1, n_local = 1;
+  int64_t n_g = 0;
+  size_t esz = 4;
+  uint64_t k_worker = 0;
+  int64_t sel_cap = 0, uni_cap = 0;
+  bool cluster = true;  // n_local == n
+  // per local worker
+  std::vector<void*> resid;
+  std::vector<int32_t*> sel_idx[2];
+  std::vector<void*> sel_val[2];
+  long long* counts = nullptr;    // n_local
+  double* delta = nullptr;        // n_local
+  // union (n > 1), double-buffered for the dense sparse-clear
+  int32_t* uni_idx[2] = {nullptr, nullptr};
+  void* uni_sum[2] = {nullptr, nullptr};
+  long long* Kbuf = nullptr;      // [2]
+  void* dense = nullptr;
+  void* model = nullptr;
+  // K1 workspace
+  unsigned long long* status = nullptr;
+  int64_t p_max = 0;
+  unsigned int* ticket = nullptr;
+  unsigned int epoch = 0;
+  int* flags = nullptr;
+  // history
+  long long *hist_t = nullptr, *hist_K = nullptr, *hist_counts = nullptr;
+  double* hist_delta = nullptr;
+  // host-side step state
+  int64_t steps = 0;      // completed aggregations
+  int64_t t_cur = -1;     // iteration of the pending/last compress
+  int buf = 0;            // buffer parity of the pending/last step
+  bool compressed = false;
+  bool poisoned = false;
+  bool ever_stepped = false;
+  void* staging = nullptr;  // micro_step_host gradient staging (lazy)
+  std::vector<void*> allocs;
+
+  int alloc(void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess)
+      return fail(MICRO_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    allocs.push_back(*p);
+    return MICRO_OK;
+  }
+};
+
+namespace {
+
+int check_ctx(micro_ctx* c) {
+  if (!c) return fail(MICRO_EINVAL, "null context");
+  return MICRO_OK;
+}
+
+int check_poison(micro_ctx* c) {
+  if (c->poisoned)
+    return fail(MICRO_ENONFINITE,
+                "context poisoned by a non-finite gradient at iteration %lld; call micro_ctx_reset",
+                (long long)c->t_cur);
+  return MICRO_OK;
+}
+
+template <typename T>
+int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
+  int64_t ps, pe;
+  partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
+  SelectArgs a{};
+  a.grad = grad;
+  a.resid = c->resid[i];
+  a.n_g = c->n_g;
+  a.p_start = ps;
+  a.p_end = pe;
+  a.eta = eta;
+  a.delta = c->delta + i;
+  a.sel_idx = c->sel_idx[c->buf][i];
+  a.sel_val = c->sel_val[c->buf][i];
+  a.cap = c->sel_cap;
+  a.count = c->counts + i;
+  a.status = c->status;
+  a.p_max = c->p_max;
+  a.ticket = c->ticket;
+  a.epoch = ++c->epoch;
+  a.tile_lo = 0;
+  a.num_tiles = (c->n_g + tile_elems<T>() - 1) / tile_elems<T>();
+  a.flags = c->flags;
+  const dim3 grid((unsigned)a.num_tiles);
+  const bool ef = c->cfg.error_feedback != 0;
+  if (ef)
+    k1_fused_select<T, true, kWriteZeroSel><<<grid, kThreads, 0, c->stream>>>(a);
+  else if (c->n > 1)
+    k1_fused_select<T, true, kWriteAcc><<<grid, kThreads, 0, c->stream>>>(a);
+  else
+    k1_fused_select<T, true, kWriteNone><<<grid, kThreads, 0, c->stream>>>(a);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+template <typename T>
+int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_from_counts) {
+  FinalizeArgs f{};
+  f.n = c->n;
+  f.n_local = c->n_local;
+  f.n_g = c->n_g;
+  f.t = c->t_cur;
+  f.counts = c->counts;
+  f.delta = c->delta;
+  f.k_target = c->k_worker;
+  f.alpha = c->cfg.scaling_factor;
+  f.min_threshold = c->cfg.min_threshold;
+  f.k_from_counts = k_from_counts;
+  f.K = c->Kbuf + c->buf;
+  f.union_idx = uidx;
+  f.union_sum = usum;
+  const int pb = c->buf ^ 1;
+  if (c->ever_stepped && c->dense) {
+    f.prev_idx = c->n == 1 ? c->sel_idx[pb][0] : c->uni_idx[pb];
+    f.prev_K = c->Kbuf + pb;
+  }
+  f.dense = c->dense;
+  f.model = c->model;
+  f.slot = c->steps % kHistCap;
+  f.hist_t = c->hist_t;
+  f.hist_K = c->hist_K;
+  f.hist_counts = c->hist_counts;
+  f.hist_delta = c->hist_delta;
+  int blocks = 1;
+  if (c->dense || c->model) {
+    const int64_t want = (c->n_g + 65535) / 65536;
+    blocks = (int)std::min<int64_t>(std::max<int64_t>(want, 1), 4 * num_sms(c->dev));
+  }
+  k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
+  CU(cudaGetLastError());
+  if (!c->cfg.error_feedback && c->n > 1)
+    for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
+  c->steps++;
+  c->ever_stepped = true;
+  c->compressed = false;
+  return MICRO_OK;
+}
+
+template <typename T>
+int aggregate_cluster(micro_ctx* c) {
+  if (c->n == 1) return launch_finalize<T>(c, c->sel_idx[c->buf][0], c->sel_val[c->buf][0], 1);
+  WorkerPtrs w{};
+  for (int i = 0; i < c->n; ++i) {
+    w.sel_idx[i] = c->sel_idx[c->buf][i];
+    w.sel_val[i] = c->sel_val[c->buf][i];
+    w.resid[i] = c->resid[i];
+  }
+  const int64_t expect = std::max<int64_t>((int64_t)c->k_worker * 3 / 2, 256);
+  const unsigned gx = (unsigned)std::min<int64_t>((expect + 255) / 256, 2048);
+  const dim3 grid(gx, (unsigned)c->n);
+  if (c->cfg.error_feedback)
+    k_cluster_reduce<T, true><<<grid, 256, 0, c->stream>>>(w, c->counts, c->n, c->t_cur,
+                                                            c->uni_idx[c->buf], (T*)c->uni_sum[c->buf]);
+  else
+    k_cluster_reduce<T, false><<<grid, 256, 0, c->stream>>>(w, c->counts, c->n, c->t_cur,
+                                                             c->uni_idx[c->buf], (T*)c->uni_sum[c->buf]);
+  CU(cudaGetLastError());
+  return launch_finalize<T>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 1);
+}
+
+int validate_config(const micro_config* g) {
+  if (!g) return fail(MICRO_EINVAL, "null config");
+  TRY(check_dtype(g->dtype));
+  if (g->n_workers < 1) return fail(MICRO_EINVAL, "run config: workers must be >= 1");
+  if (g->n_workers > MICRO_MAX_WORKERS)
+    return fail(MICRO_EINVAL, "run config: at most %d workers supported", MICRO_MAX_WORKERS);
+  if (g->n_g < g->n_workers)
+    return fail(MICRO_EINVAL, "run config: gradient length %lld smaller than worker count %d",
+                (long long)g->n_g, g->n_workers);
+  if (g->n_g >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "n_g must be < 2^31 (int32 indices)");
+  if (!(g->n_local == g->n_workers || (g->n_local == 1 && g->n_workers > 1)))
+    return fail(MICRO_EINVAL, "n_local must equal n_workers or be 1");
+  if (g->rank < 0 || g->rank + g->n_local > g->n_workers)
+    return fail(MICRO_EINVAL, "rank %d out of range", g->rank);
+  if (!(g->density > 0.0 && g->density <= 1.0)) return fail(MICRO_EINVAL, "run config: density must lie in (0, 1]");
+  if (!(g->initial_threshold >= 0.0) || !std::isfinite(g->initial_threshold))
+    return fail(MICRO_EINVAL, "run config: delta0 must be finite and nonnegative");
+  if (!(g->scaling_factor > 0.0 && g->scaling_factor < 1.0))
+    return fail(MICRO_EINVAL, "run config: alpha must lie in (0, 1)");
+  if (!(g->min_threshold > 0.0)) return fail(MICRO_EINVAL, "run config: eps-delta must be positive");
+  if (g->target != MICRO_TARGET_SPLIT && g->target != MICRO_TARGET_FULL)
+    return fail(MICRO_EINVAL, "unknown per-worker target %d", g->target);
+  if (g->selection_capacity < 0) return fail(MICRO_EINVAL, "negative selection capacity");
+  return MICRO_OK;
+}
+
+int reset_state(micro_ctx* c) {
+  DeviceGuard dg(c->dev);
+  for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
+  std::vector<double> d0(c->n_local, c->cfg.initial_threshold);
+  CU(cudaMemcpyAsync(c->delta, d0.data(), sizeof(double) * c->n_local, cudaMemcpyHostToDevice, c->stream));
+  CU(cudaMemsetAsync(c->counts, 0, sizeof(long long) * c->n_local, c->stream));
+  CU(cudaMemsetAsync(c->Kbuf, 0, sizeof(long long) * 2, c->stream));
+  CU(cudaMemsetAsync(c->flags, 0, sizeof(int), c->stream));
+  if (c->dense) CU(cudaMemsetAsync(c->dense, 0, c->n_g * c->esz, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  c->steps = 0;
+  c->t_cur = -1;
+  c->buf = 0;
+  c->compressed = false;
+  c->poisoned = false;
+  c->ever_stepped = false;
+  return MICRO_OK;
+}
+
+int read_flags(micro_ctx* c, int* flags) {
+  CU(cudaMemcpyAsync(flags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (*flags & 1) c->poisoned = true;
+  return MICRO_OK;
+}
+
+template <typename T>
+__global__ void k_synth(uint64_t seed, uint32_t worker, uint64_t t, int64_t n, T* out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q * 4 >= n) return;
+  float z[4];
+  ms_gaussian4(seed, worker, t, (uint64_t)q, z);
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (q * 4 + c < n) out[q * 4 + c] = (T)z[c];
+}
+
+template <typename T>
+__global__ void k_accumulate(const T* e, T eta, const T* g, T* acc, int64_t n) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    acc[j] = add_rn(e[j], mul_rn(eta, g[j]));
+}
+
+template <typename T>
+__global__ void k_compensate(T* acc, int64_t n_g, const int32_t* idx, int64_t k, int* bad) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < k;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = idx[m];
+    if (j < 0 || j >= n_g) atomicOr(bad, 1);
+    else acc[j] = (T)0;
+  }
+}
+
+template <typename T>
+__global__ void k_reduce_values(WorkerPtrs w, int n, int64_t n_g, const int32_t* uidx, int64_t K,
+                                T* sums, T* dense, int* bad) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < K;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = uidx[m];
+    if (j < 0 || j >= n_g) { atomicOr(bad, 1); continue; }
+    T s = (T)0;
+    for (int r = 0; r < n; ++r) s = add_rn(s, ((const T*)w.sel_val[r])[j]);
+    if (sums) sums[m] = s;
+    if (dense) dense[j] = s;
+  }
+}
+
+unsigned grid_for(int64_t work, int dev) {
+  const int64_t b = (work + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 8 * num_sms(dev)));
+}
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+}  // namespace
+
+// ============================================================== C ABI ====
+
+extern "C" {
+
+int micro_abi_version(void) { return MICRO_ABI_VERSION; }
+
+const char* micro_status_string(int s) {
+  switch (s) {
+    case MICRO_OK: return "MICRO_OK";
+    case MICRO_EINVAL: return "MICRO_EINVAL (invalid_argument)";
+    case MICRO_ELOGIC: return "MICRO_ELOGIC (logic_error)";
+    case MICRO_ENONFINITE: return "MICRO_ENONFINITE (runtime_error: non-finite gradient)";
+    case MICRO_ECUDA: return "MICRO_ECUDA";
+    case MICRO_ENCCL: return "MICRO_ENCCL";
+    case MICRO_ECAPACITY: return "MICRO_ECAPACITY";
+    case MICRO_ENOMEM: return "MICRO_ENOMEM";
+  }
+  return "unknown status";
+}
+
+const char* micro_last_error(void) { return g_err.c_str(); }
+
+int micro_partition(int64_t n_g, int n, int64_t t, int worker, int64_t* start, int64_t* end) {
+  return h_partition(n_g, n, t, worker, start, end);
+}
+
+int micro_global_target_count(double density, int64_t n_g, uint64_t* k) {
+  return h_global_target(density, n_g, k);
+}
+
+int micro_per_worker_target_count(double density, int64_t n_g, int n, int target, uint64_t* k) {
+  return h_worker_target(density, n_g, n, target, k);
+}
+
+int micro_update_threshold(double* delta, uint64_t k_target, uint64_t k_selected, double alpha,
+                           double min_threshold) {
+  return h_update_threshold(delta, k_target, k_selected, alpha, min_threshold);
+}
+
+void micro_config_default(micro_config* g) {
+  std::memset(g, 0, sizeof *g);
+  g->n_workers = 1;
+  g->n_local = 1;
+  g->dtype = MICRO_F32;
+  g->density = 0.01;
+  g->initial_threshold = 0.01;
+  g->scaling_factor = 0.01;
+  g->min_threshold = 1e-12;
+  g->target = MICRO_TARGET_SPLIT;
+  g->error_feedback = 1;
+  g->dense_output = 1;
+}
+
+int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
+  if (!out) return fail(MICRO_EINVAL, "null output pointer");
+  *out = nullptr;
+  TRY(validate_config(cfg));
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (cfg->device < 0 || cfg->device >= ndev)
+    return fail(MICRO_EINVAL, "device %d out of range (%d devices)", cfg->device, ndev);
+  auto* c = new micro_ctx;
+  c->cfg = *cfg;
+  c->dev = cfg->device;
+  c->n = cfg->n_workers;
+  c->n_local = cfg->n_local;
+  c->n_g = cfg->n_g;
+  c->esz = dtype_size(cfg->dtype);
+  c->cluster = c->n_local == c->n;
+  int rc = h_worker_target(cfg->density, cfg->n_g, cfg->n_workers, cfg->target, &c->k_worker);
+  if (rc) { delete c; return rc; }
+  DeviceGuard dg(c->dev);
+  auto cleanup = [&](int code) {
+    micro_ctx_destroy(c);
+    return code;
+  };
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return fail(MICRO_ECUDA, "stream: %s", cudaGetErrorString(e)); }
+    c->own_stream = true;
+  }
+  const int64_t max_range = (c->n_g + c->n - 1) / c->n;
+  c->sel_cap = cfg->selection_capacity ? std::min<int64_t>(cfg->selection_capacity, max_range) : max_range;
+  c->uni_cap = std::min<int64_t>(c->n_g, (int64_t)c->n * c->sel_cap);
+  c->p_max = c->esz == 4 ? p_max_for<float>(max_range) : p_max_for<double>(max_range);
+  const int nbuf = c->n == 1 ? 2 : 1;
+  c->resid.assign(c->n_local, nullptr);
+  for (int b = 0; b < 2; ++b) {
+    c->sel_idx[b].assign(c->n_local, nullptr);
+    c->sel_val[b].assign(c->n_local, nullptr);
+  }
+  for (int i = 0; i < c->n_local; ++i) {
+    if ((rc = c->alloc(&c->resid[i], c->n_g * c->esz))) return cleanup(rc);
+    for (int b = 0; b < nbuf; ++b) {
+      if ((rc = c->alloc((void**)&c->sel_idx[b][i], c->sel_cap * 4))) return cleanup(rc);
+      if ((rc = c->alloc(&c->sel_val[b][i], c->sel_cap * c->esz))) return cleanup(rc);
+    }
+    if (nbuf == 1) {
+      c->sel_idx[1][i] = c->sel_idx[0][i];
+      c->sel_val[1][i] = c->sel_val[0][i];
+    }
+  }
+  if (c->n > 1)
+    for (int b = 0; b < 2; ++b) {
+      if ((rc = c->alloc((void**)&c->uni_idx[b], c->uni_cap * 4))) return cleanup(rc);
+      if ((rc = c->alloc(&c->uni_sum[b], c->uni_cap * c->esz))) return cleanup(rc);
+    }
+  if ((rc = c->alloc((void**)&c->counts, sizeof(long long) * c->n_local))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->delta, sizeof(double) * c->n_local))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->Kbuf, sizeof(long long) * 2))) return cleanup(rc);
+  if (cfg->dense_output && (rc = c->alloc(&c->dense, c->n_g * c->esz))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->status, sizeof(unsigned long long) * c->p_max))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->flags, sizeof(int)))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->hist_t, sizeof(long long) * kHistCap))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->hist_K, sizeof(long long) * kHistCap))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->hist_counts, sizeof(long long) * kHistCap * c->n_local))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->hist_delta, sizeof(double) * kHistCap * c->n_local))) return cleanup(rc);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->p_max, c->stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
+    return cleanup(fail(MICRO_ECUDA, "memset: %s", cudaGetErrorString(e)));
+  if ((rc = reset_state(c))) return cleanup(rc);
+  *out = c;
+  return MICRO_OK;
+}
+
+int micro_ctx_destroy(micro_ctx* c) {
+  if (!c) return MICRO_OK;
+  DeviceGuard dg(c->dev);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->staging) cudaFree(c->staging);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return MICRO_OK;
+}
+
+int micro_ctx_reset(micro_ctx* c) {
+  TRY(check_ctx(c));
+  return reset_state(c);
+}
+
+void* micro_ctx_stream(micro_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int micro_set_model(micro_ctx* c, void* d_x) {
+  TRY(check_ctx(c));
+  if (d_x && ((uintptr_t)d_x % c->esz)) return fail(MICRO_EINVAL, "model pointer misaligned");
+  c->model = d_x;
+  return MICRO_OK;
+}
+
+int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t t) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (!d_grads) return fail(MICRO_EINVAL, "null gradient array");
+  if (!(eta > 0.0)) return fail(MICRO_EINVAL, "accumulate: eta must be positive");
+  if (t < 0) return fail(MICRO_EINVAL, "partition: negative iteration");
+  if (c->compressed) return fail(MICRO_ELOGIC, "micro_compress called twice without aggregation");
+  for (int i = 0; i < c->n_local; ++i) {
+    if (!d_grads[i]) return fail(MICRO_EINVAL, "null gradient for local worker %d", i);
+    if ((uintptr_t)d_grads[i] % 16) return fail(MICRO_EINVAL, "gradient %d not 16-byte aligned", i);
+  }
+  DeviceGuard dg(c->dev);
+  c->t_cur = t;
+  c->buf = (int)(c->steps & 1);
+  for (int i = 0; i < c->n_local; ++i) {
+    if (c->esz == 4) TRY(launch_k1<float>(c, i, d_grads[i], eta, t));
+    else TRY(launch_k1<double>(c, i, d_grads[i], eta, t));
+  }
+  c->compressed = true;
+  return MICRO_OK;
+}
+
+int micro_aggregate(micro_ctx* c) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (!c->cluster)
+    return fail(MICRO_ELOGIC, "micro_aggregate: multi-rank context; use the micro_dist_* protocol");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_aggregate without a preceding micro_compress");
+  DeviceGuard dg(c->dev);
+  return c->esz == 4 ? aggregate_cluster<float>(c) : aggregate_cluster<double>(c);
+}
+
+int micro_step(micro_ctx* c, const void* const* d_grads, double eta, int64_t t) {
+  TRY(micro_compress(c, d_grads, eta, t));
+  return micro_aggregate(c);
+}
+
+int micro_sync(micro_ctx* c) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->dev);
+  int flags = 0;
+  TRY(read_flags(c, &flags));
+  if (flags & 1) return check_poison(c);
+  if (flags & 2) return fail(MICRO_ECAPACITY, "selection exceeded capacity %lld", (long long)c->sel_cap);
+  return MICRO_OK;
+}
+
+int micro_step_host(micro_ctx* c, const void* h_grads, double eta, int64_t t, int32_t* h_idx,
+                    void* h_sums, int64_t cap, int64_t* K) {
+  TRY(check_ctx(c));
+  if (!c->cluster) return fail(MICRO_ELOGIC, "micro_step_host: single-device clusters only");
+  DeviceGuard dg(c->dev);
+  const size_t bytes = (size_t)c->n_local * c->n_g * c->esz;
+  if (!c->staging) {
+    cudaError_t e = cudaMalloc(&c->staging, bytes);
+    if (e != cudaSuccess) return fail(MICRO_ENOMEM, "staging: %s", cudaGetErrorString(e));
+  }
+  CU(cudaMemcpyAsync(c->staging, h_grads, bytes, cudaMemcpyHostToDevice, c->stream));
+  std::vector<const void*> g(c->n_local);
+  for (int i = 0; i < c->n_local; ++i) g[i] = (const char*)c->staging + (size_t)i * c->n_g * c->esz;
+  TRY(micro_step(c, g.data(), eta, t));
+  return micro_copy_union(c, h_idx, h_sums, cap, K);
+}
+
+int micro_query(micro_ctx* c, micro_stats* st, int64_t* counts, double* deltas) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->dev);
+  int flags = 0;
+  TRY(read_flags(c, &flags));
+  long long K = 0;
+  std::vector<long long> k(c->n_local);
+  if (c->ever_stepped) {
+    const int b = (int)((c->steps - 1) & 1);
+    CU(cudaMemcpy(&K, c->Kbuf + b, sizeof K, cudaMemcpyDeviceToHost));
+  }
+  CU(cudaMemcpy(k.data(), c->counts, sizeof(long long) * c->n_local, cudaMemcpyDeviceToHost));
+  if (counts)
+    for (int i = 0; i < c->n_local; ++i) counts[i] = k[i];
+  if (deltas) CU(cudaMemcpy(deltas, c->delta, sizeof(double) * c->n_local, cudaMemcpyDeviceToHost));
+  if (st) {
+    st->t = c->t_cur;
+    st->steps = c->steps;
+    st->K = K;
+    long long tot = 0;
+    for (long long v : k) tot += v;
+    st->total_selected = c->cluster ? tot : K;
+    st->nonfinite = flags & 1;
+    st->overflow = (flags >> 1) & 1;
+  }
+  return MICRO_OK;
+}
+
+int micro_history(micro_ctx* c, int64_t max, int64_t* t, int64_t* K, int64_t* counts,
+                  double* delta_used, int64_t* written) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->dev);
+  CU(cudaStreamSynchronize(c->stream));
+  const int64_t n = std::min<int64_t>(std::min<int64_t>(max, c->steps), kHistCap);
+  std::vector<long long> ht(kHistCap), hk(kHistCap), hc(kHistCap * c->n_local);
+  std::vector<double> hd(kHistCap * c->n_local);
+  CU(cudaMemcpy(ht.data(), c->hist_t, sizeof(long long) * kHistCap, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hk.data(), c->hist_K, sizeof(long long) * kHistCap, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hc.data(), c->hist_counts, sizeof(long long) * hc.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hd.data(), c->hist_delta, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost));
+  for (int64_t s = 0; s < n; ++s) {
+    const int64_t step = c->steps - n + s;
+    const int64_t slot = step % kHistCap;
+    if (t) t[s] = ht[slot];
+    if (K) K[s] = hk[slot];
+    for (int i = 0; i < c->n_local; ++i) {
+      if (counts) counts[s * c->n_local + i] = hc[slot * c->n_local + i];
+      if (delta_used) delta_used[s * c->n_local + i] = hd[slot * c->n_local + i];
+    }
+  }
+  if (written) *written = n;
+  return MICRO_OK;
+}
+
+int micro_union_device(micro_ctx* c, const int32_t** d_idx, const void** d_sums, const int64_t** d_K) {
+  TRY(check_ctx(c));
+  const int b = c->ever_stepped ? (int)((c->steps - 1) & 1) : 0;
+  if (d_idx) *d_idx = c->n == 1 ? c->sel_idx[b][0] : c->uni_idx[b];
+  if (d_sums) *d_sums = c->n == 1 ? c->sel_val[b][0] : c->uni_sum[b];
+  if (d_K) *d_K = (const int64_t*)(c->Kbuf + b);
+  return MICRO_OK;
+}
+
+int micro_dense_device(micro_ctx* c, const void** d_dense) {
+  TRY(check_ctx(c));
+  if (!c->dense) return fail(MICRO_ELOGIC, "dense output disabled (micro_config.dense_output = 0)");
+  *d_dense = c->dense;
+  return MICRO_OK;
+}
+
+int micro_residual_device(micro_ctx* c, int i, void** d) {
+  TRY(check_ctx(c));
+  if (i < 0 || i >= c->n_local) return fail(MICRO_EINVAL, "local worker %d out of range", i);
+  *d = c->resid[i];
+  return MICRO_OK;
+}
+
+int micro_selection_device(micro_ctx* c, int i, const int32_t** d_idx, const void** d_val,
+                           const int64_t** d_count) {
+  TRY(check_ctx(c));
+  if (i < 0 || i >= c->n_local) return fail(MICRO_EINVAL, "local worker %d out of range", i);
+  if (d_idx) *d_idx = c->sel_idx[c->buf][i];
+  if (d_val) *d_val = c->sel_val[c->buf][i];
+  if (d_count) *d_count = (const int64_t*)(c->counts + i);
+  return MICRO_OK;
+}
+
+int micro_threshold_device(micro_ctx* c, double** d) {
+  TRY(check_ctx(c));
+  *d = c->delta;
+  return MICRO_OK;
+}
+
+int micro_copy_union(micro_ctx* c, int32_t* h_idx, void* h_sums, int64_t cap, int64_t* K) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->dev);
+  int flags = 0;
+  TRY(read_flags(c, &flags));
+  if (flags & 1) return check_poison(c);
+  if (flags & 2) return fail(MICRO_ECAPACITY, "selection exceeded capacity %lld", (long long)c->sel_cap);
+  if (!c->ever_stepped) {
+    if (K) *K = 0;
+    return MICRO_OK;
+  }
+  const int32_t* di;
+  const void* ds;
+  const int64_t* dK;
+  TRY(micro_union_device(c, &di, &ds, &dK));
+  long long k = 0;
+  CU(cudaMemcpy(&k, dK, sizeof k, cudaMemcpyDeviceToHost));
+  if (K) *K = k;
+  if (k > cap) return fail(MICRO_ECAPACITY, "union of %lld exceeds host capacity %lld", k, (long long)cap);
+  if (k) {
+    if (h_idx) CU(cudaMemcpyAsync(h_idx, di, (size_t)k * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (h_sums) CU(cudaMemcpyAsync(h_sums, ds, (size_t)k * c->esz, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+  }
+  return MICRO_OK;
+}
+
+int micro_copy_residual(micro_ctx* c, int i, void* h) {
+  TRY(check_ctx(c));
+  if (i < 0 || i >= c->n_local) return fail(MICRO_EINVAL, "local worker %d out of range", i);
+  DeviceGuard dg(c->dev);
+  CU(cudaMemcpyAsync(h, c->resid[i], c->n_g * c->esz, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MICRO_OK;
+}
+
+int micro_copy_dense(micro_ctx* c, void* h) {
+  TRY(check_ctx(c));
+  if (!c->dense) return fail(MICRO_ELOGIC, "dense output disabled (micro_config.dense_output = 0)");
+  DeviceGuard dg(c->dev);
+  CU(cudaMemcpyAsync(h, c->dense, c->n_g * c->esz, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  return MICRO_OK;
+}
+
+// ---- one rank of a multi-GPU job ----
+
+static int dist_counts(micro_ctx* c, const int64_t* h_counts, Counts* out, bool own_segments) {
+  if (!h_counts) return fail(MICRO_EINVAL, "null counts");
+  long long off = 0;
+  const int me = c->cfg.rank;
+  for (int r = 0; r < c->n; ++r) {
+    if (h_counts[r] < 0) return fail(MICRO_EINVAL, "negative count");
+    out->k[r] = h_counts[r];
+    out->off[r] = off;
+    // send layout: segment o has k_o values (o != me); recv layout: segment r has k_me values
+    if (r != me) off += own_segments ? h_counts[me] : h_counts[r];
+  }
+  return MICRO_OK;
+}
+
+int micro_dist_gather_foreign(micro_ctx* c, const int32_t* d_all_idx, const int64_t* h_counts,
+                              int64_t kmax, void* d_send) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_gather_foreign before micro_compress");
+  Counts cs{};
+  TRY(dist_counts(c, h_counts, &cs, false));
+  DeviceGuard dg(c->dev);
+  long long mx = 0;
+  for (int r = 0; r < c->n; ++r) mx = std::max<long long>(mx, cs.k[r]);
+  if (mx > kmax) return fail(MICRO_EINVAL, "kmax %lld smaller than a count %lld", (long long)kmax, mx);
+  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
+  if (c->esz == 4) {
+    if (c->cfg.error_feedback)
+      k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                      (float*)c->resid[0], (float*)d_send);
+    else
+      k_dist_gather_foreign<float, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                       (float*)c->resid[0], (float*)d_send);
+  } else {
+    if (c->cfg.error_feedback)
+      k_dist_gather_foreign<double, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                       (double*)c->resid[0], (double*)d_send);
+    else
+      k_dist_gather_foreign<double, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                        (double*)c->resid[0], (double*)d_send);
+  }
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+int micro_dist_owner_reduce(micro_ctx* c, const void* d_recv, const int64_t* h_counts, void* d_own_sums) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
+  Counts cs{};
+  TRY(dist_counts(c, h_counts, &cs, true));
+  DeviceGuard dg(c->dev);
+  const int me = c->cfg.rank;
+  const long long k = cs.k[me];
+  const unsigned grid = grid_for(k, c->dev);
+  if (c->esz == 4)
+    k_dist_owner_reduce<float><<<grid, 256, 0, c->stream>>>((const float*)c->sel_val[c->buf][0], k,
+                                                            (const float*)d_recv, cs, c->n, me, (float*)d_own_sums);
+  else
+    k_dist_owner_reduce<double><<<grid, 256, 0, c->stream>>>((const double*)c->sel_val[c->buf][0], k,
+                                                             (const double*)d_recv, cs, c->n, me,
+                                                             (double*)d_own_sums);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_all_sums,
+                        const int64_t* h_counts, int64_t kmax) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_finalize before micro_compress");
+  Counts cs{};
+  TRY(dist_counts(c, h_counts, &cs, false));
+  long long K = 0, mx = 0;
+  for (int r = 0; r < c->n; ++r) {
+    K += cs.k[r];
+    mx = std::max<long long>(mx, cs.k[r]);
+  }
+  if (K > c->uni_cap) return fail(MICRO_ECAPACITY, "union %lld exceeds capacity %lld", K, (long long)c->uni_cap);
+  DeviceGuard dg(c->dev);
+  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
+  if (c->esz == 4) {
+    k_dist_build_union<float><<<grid, 256, 0, c->stream>>>(d_all_idx, (const float*)d_all_sums, kmax, cs, c->n,
+                                                           c->t_cur, c->uni_idx[c->buf],
+                                                           (float*)c->uni_sum[c->buf], c->Kbuf + c->buf);
+    CU(cudaGetLastError());
+    return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+  }
+  k_dist_build_union<double><<<grid, 256, 0, c->stream>>>(d_all_idx, (const double*)d_all_sums, kmax, cs, c->n,
+                                                          c->t_cur, c->uni_idx[c->buf],
+                                                          (double*)c->uni_sum[c->buf], c->Kbuf + c->buf);
+  CU(cudaGetLastError());
+  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+}
+
+// ---- stateless value-level operations ----
+
+int micro_synth_gaussian(int dtype, uint64_t seed, uint32_t worker, uint64_t t, int64_t n, void* d_out,
+                         void* stream) {
+  TRY(check_dtype(dtype));
+  if (n < 0 || (n && !d_out)) return fail(MICRO_EINVAL, "bad output");
+  if (!n) return MICRO_OK;
+  const int64_t q = (n + 3) / 4;
+  const unsigned grid = (unsigned)((q + 255) / 256);
+  if (dtype == MICRO_F32) k_synth<float><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, worker, t, n, (float*)d_out);
+  else k_synth<double><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, worker, t, n, (double*)d_out);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+int micro_accumulate(int dtype, const void* d_e, double eta, const void* d_g, void* d_acc, int64_t n,
+                     void* stream) {
+  TRY(check_dtype(dtype));
+  if (!(eta > 0.0)) return fail(MICRO_EINVAL, "accumulate: eta must be positive");
+  if (n < 0) return fail(MICRO_EINVAL, "accumulate: negative length");
+  if (!n) return MICRO_OK;
+  const unsigned grid = grid_for(n, current_device());
+  if (dtype == MICRO_F32)
+    k_accumulate<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)d_e, (float)eta, (const float*)d_g,
+                                                                (float*)d_acc, n);
+  else
+    k_accumulate<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)d_e, eta, (const double*)d_g,
+                                                                 (double*)d_acc, n);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end,
+                              double delta, int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count,
+                              void* stream) {
+  TRY(check_dtype(dtype));
+  if (start < 0 || end < start || end > n_g)
+    return fail(MICRO_EINVAL, "selection: range [%lld, %lld) invalid for vector of length %lld",
+                (long long)start, (long long)end, (long long)n_g);
+  if (!(delta >= 0.0) || !std::isfinite(delta))
+    return fail(MICRO_EINVAL, "selection: threshold must be finite and nonnegative");
+  if (n_g >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "n_g must be < 2^31 (int32 indices)");
+  if (!d_count) return fail(MICRO_EINVAL, "null count pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (end == start) {
+    CU(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+    return MICRO_OK;
+  }
+  if ((uintptr_t)d_acc % 16) return fail(MICRO_EINVAL, "acc not 16-byte aligned");
+  const int TILE = dtype == MICRO_F32 ? tile_elems<float>() : tile_elems<double>();
+  const int64_t tlo = start / TILE, thi = (end - 1) / TILE;
+  const int64_t ntiles = thi - tlo + 1;
+  const int64_t pmax = ntiles + 2;
+  // scratch: status words, ticket, flags (stream-ordered allocator)
+  char* ws = nullptr;
+  const size_t wbytes = sizeof(unsigned long long) * pmax + 16;
+  CU(cudaMallocAsync((void**)&ws, wbytes, s));
+  CU(cudaMemsetAsync(ws, 0, wbytes, s));
+  SelectArgs a{};
+  a.grad = nullptr;
+  a.resid = const_cast<void*>(d_acc);
+  a.n_g = n_g;
+  a.p_start = start;
+  a.p_end = end;
+  a.eta = 1.0;
+  a.delta = nullptr;
+  a.delta_value = delta;
+  a.sel_idx = d_idx;
+  a.sel_val = d_val;
+  a.cap = cap;
+  a.count = (long long*)d_count;
+  a.status = (unsigned long long*)ws;
+  a.p_max = pmax;
+  a.ticket = (unsigned int*)(ws + sizeof(unsigned long long) * pmax);
+  a.flags = (int*)(ws + sizeof(unsigned long long) * pmax + 8);
+  a.epoch = 1;
+  a.tile_lo = tlo;
+  a.num_tiles = ntiles;
+  if (dtype == MICRO_F32)
+    k1_fused_select<float, false, kWriteNone><<<(unsigned)ntiles, kThreads, 0, s>>>(a);
+  else
+    k1_fused_select<double, false, kWriteNone><<<(unsigned)ntiles, kThreads, 0, s>>>(a);
+  CU(cudaGetLastError());
+  CU(cudaFreeAsync(ws, s));
+  return MICRO_OK;
+}
+
+int micro_compensate(int dtype, void* d_acc, int64_t n_g, const int32_t* d_idx, int64_t k, void* stream) {
+  TRY(check_dtype(dtype));
+  if (k < 0) return fail(MICRO_EINVAL, "compensate: negative count");
+  if (!k) return MICRO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int* bad = nullptr;
+  CU(cudaMallocAsync((void**)&bad, sizeof(int), s));
+  CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  const unsigned grid = grid_for(k, current_device());
+  if (dtype == MICRO_F32) k_compensate<float><<<grid, 256, 0, s>>>((float*)d_acc, n_g, d_idx, k, bad);
+  else k_compensate<double><<<grid, 256, 0, s>>>((double*)d_acc, n_g, d_idx, k, bad);
+  CU(cudaGetLastError());
+  int hbad = 0;
+  CU(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(bad, s));
+  CU(cudaStreamSynchronize(s));
+  if (hbad) return fail(MICRO_EINVAL, "compensate: index out of range");
+  return MICRO_OK;
+}
+
+static int reduce_values(int dtype, const void* const* h_accs, int n, int64_t n_g, const int32_t* d_union,
+                         int64_t K, void* d_sums, void* d_dense, void* stream) {
+  TRY(check_dtype(dtype));
+  if (n < 1 || !h_accs) return fail(MICRO_EINVAL, "all_reduce_sparse: no workers");
+  if (n > kMaxWorkers) return fail(MICRO_EINVAL, "all_reduce_sparse: at most %d workers", kMaxWorkers);
+  if (K < 0) return fail(MICRO_EINVAL, "all_reduce_sparse: negative union size");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t esz = dtype_size(dtype);
+  if (d_dense) CU(cudaMemsetAsync(d_dense, 0, n_g * esz, s));
+  if (!K) return MICRO_OK;
+  WorkerPtrs w{};
+  for (int r = 0; r < n; ++r) w.sel_val[r] = h_accs[r];
+  int* bad = nullptr;
+  CU(cudaMallocAsync((void**)&bad, sizeof(int), s));
+  CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  const unsigned grid = grid_for(K, current_device());
+  if (dtype == MICRO_F32)
+    k_reduce_values<float><<<grid, 256, 0, s>>>(w, n, n_g, d_union, K, (float*)d_sums, (float*)d_dense, bad);
+  else
+    k_reduce_values<double><<<grid, 256, 0, s>>>(w, n, n_g, d_union, K, (double*)d_sums, (double*)d_dense, bad);
+  CU(cudaGetLastError());
+  int hbad = 0;
+  CU(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(bad, s));
+  CU(cudaStreamSynchronize(s));
+  if (hbad) return fail(MICRO_EINVAL, "all_reduce_sparse: index out of range");
+  return MICRO_OK;
+}
+
+int micro_all_reduce_sparse_values(int dtype, const void* const* h_accs, int n, int64_t n_g,
+                                   const int32_t* d_union, int64_t K, void* d_sums, void* stream) {
+  return reduce_values(dtype, h_accs, n, n_g, d_union, K, d_sums, nullptr, stream);
+}
+
+int micro_all_reduce_sparse(int dtype, const void* const* h_accs, int n, int64_t n_g,
+                            const int32_t* d_union, int64_t K, void* d_dense, void* stream) {
+  if (!d_dense) return fail(MICRO_EINVAL, "null dense output");
+  return reduce_values(dtype, h_accs, n, n_g, d_union, K, nullptr, d_dense, stream);
+}
+
+int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_concat, int32_t* d_union,
+                             int64_t* K, void* stream) {
+  if (n < 0 || (n && !h_counts)) return fail(MICRO_EINVAL, "bad selection list");
+  if (!K) return fail(MICRO_EINVAL, "null K");
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    if (h_counts[i] < 0) return fail(MICRO_EINVAL, "negative count");
+    total += h_counts[i];
+  }
+  *K = 0;
+  if (!total) return MICRO_OK;
+  if (total >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "too many indices");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int items = (int)total;
+  int32_t* sorted = nullptr;
+  int* d_num = nullptr;
+  void* tmp = nullptr;
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b1, d_concat, (int32_t*)nullptr, items, 0, 32, s);
+  cub::DeviceSelect::Unique(nullptr, b2, (const int32_t*)nullptr, (int32_t*)nullptr, (int*)nullptr, items, s);
+  const size_t tb = std::max(b1, b2);
+  CU(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * items, s));
+  CU(cudaMallocAsync((void**)&d_num, sizeof(int), s));
+  CU(cudaMallocAsync(&tmp, tb, s));
+  size_t tb1 = tb, tb2 = tb;
+  CU(cub::DeviceRadixSort::SortKeys(tmp, tb1, d_concat, sorted, items, 0, 32, s));
+  CU(cub::DeviceSelect::Unique(tmp, tb2, (const int32_t*)sorted, d_union, d_num, items, s));
+  int hn = 0;
+  CU(cudaMemcpyAsync(&hn, d_num, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(sorted, s));
+  CU(cudaFreeAsync(d_num, s));
+  CU(cudaFreeAsync(tmp, s));
+  CU(cudaStreamSynchronize(s));
+  *K = hn;
+  return MICRO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// common.cuh — shared device helpers for the MiCRO sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace micro {
+
+constexpr int kMaxWorkers = 64;  // MICRO_MAX_WORKERS
+
+// 16-byte vector of T: 4 floats or 2 doubles per load/store.
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using V = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct Vec<double> {
+  using V = double2;
+  static constexpr int N = 2;
+};
+
+__device__ __forceinline__ float comp(const float4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ double comp(const double2& v, int c) { return c == 0 ? v.x : v.y; }
+__device__ __forceinline__ void set_comp(float4& v, int c, float x) {
+  if (c == 0) v.x = x; else if (c == 1) v.y = x; else if (c == 2) v.z = x; else v.w = x;
+}
+__device__ __forceinline__ void set_comp(double2& v, int c, double x) {
+  if (c == 0) v.x = x; else v.y = x;
+}
+
+// Explicitly rounded arithmetic: never contracted into FMA.
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// The selection threshold in T such that |x| > thr  <=>  (double)|x| > delta
+// for every x of type T (SURVEY.md §8c fp32 contract): round delta down.
+__device__ __forceinline__ float threshold_as(double delta, float*) { return __double2float_rd(delta); }
+__device__ __forceinline__ double threshold_as(double delta, double*) { return delta; }
+
+__device__ __forceinline__ float absx(float x) { return fabsf(x); }
+__device__ __forceinline__ double absx(double x) { return fabs(x); }
+
+__device__ __forceinline__ bool finite(float x) { return isfinite(x); }
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+// Streaming loads/stores (data touched once per pass).
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4* p, const float4& v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2* p, const double2& v) { __stcs(p, v); }
+
+// gpu-scope relaxed 64-bit status words (look-back).
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// cycle = (t % n + worker) % n; balanced contiguous ranges, remainder first
+// (tensor.hpp:48-63).  Device copy of the host function.
+__host__ __device__ __forceinline__ void partition_range(int64_t n_g, int n, int64_t t, int worker,
+                                                         int64_t* start, int64_t* end) {
+  const int64_t cycle = (t % n + worker) % n;
+  const int64_t base = n_g / n, rem = n_g % n;
+  const int64_t s = cycle * base + (cycle < rem ? cycle : rem);
+  *start = s;
+  *end = s + base + (cycle < rem ? 1 : 0);
+}
+
+// Owner (worker id) of partition p at iteration t: (t % n + i) % n == p.
+__host__ __device__ __forceinline__ int partition_owner(int p, int n, int64_t t) {
+  return (int)(((int64_t)p - t % n + n) % n);
+}
+
+}  // namespace micro

@@ -1,0 +1,217 @@
+// exchange.cuh — the aggregation half of the MiCRO step (K4..K9).
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   union U = sorted unique of all S_i          collectives.cpp:14-28
+//     (MiCRO partitions are disjoint, so U is the concatenation of the S_i
+//      in PARTITION order — no sort; acceptance.cpp:93-118)
+//   s_j = 0; for i = 0..n-1: s_j += acc_i[j]    collectives.cpp:39-47 (P1, P2)
+//   delta_i <- update(delta_i, k_w, k_i)        harness.cpp:201-208
+//   x[j] -= s_j / n                             harness.cpp:212-215
+//   acc_i[j] = 0 for j in U, every worker       harness.cpp:219-221 (P3)
+#pragma once
+
+#include "common.cuh"
+
+namespace micro {
+
+struct WorkerPtrs {
+  const int32_t* sel_idx[kMaxWorkers];
+  const void* sel_val[kMaxWorkers];
+  void* resid[kMaxWorkers];
+};
+
+struct Counts {
+  long long k[kMaxWorkers];    // per worker (rank order)
+  long long off[kMaxWorkers];  // per worker: segment offset in a packed buffer
+};
+
+// Single-device cluster, n > 1: one block row per partition p; the owner's
+// own value comes from its K1 pairs (its residual entry is already zeroed),
+// every other worker's from its accumulator, summed in worker order.
+template <typename T, bool kZero>
+__global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long long* counts,
+                                                        int n, int64_t t, int32_t* union_idx,
+                                                        T* union_sum) {
+  const int p = blockIdx.y;
+  const int owner = partition_owner(p, n, t);
+  long long off = 0;
+  for (int q = 0; q < p; ++q) off += counts[partition_owner(q, n, t)];
+  const long long k = counts[owner];
+  const int32_t* __restrict__ idx = w.sel_idx[owner];
+  const T* __restrict__ val = (const T*)w.sel_val[owner];
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
+       m += (long long)gridDim.x * blockDim.x) {
+    const int32_t j = idx[m];
+    T s = (T)0;
+    for (int r = 0; r < n; ++r) {
+      T v;
+      if (r == owner) {
+        v = val[m];
+      } else {
+        T* e = (T*)w.resid[r];
+        v = e[j];
+        if (kZero) e[j] = (T)0;
+      }
+      s = add_rn(s, v);
+    }
+    union_idx[off + m] = j;
+    union_sum[off + m] = s;
+  }
+}
+
+// One rank: gather own accumulator at every OTHER owner's indices into the
+// send buffer (segment per destination, rank order) and zero them.
+template <typename T, bool kZero>
+__global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_idx, int64_t kmax,
+                                                             Counts c, int me, T* resid, T* send) {
+  const int o = blockIdx.y;
+  if (o == me) return;
+  const long long k = c.k[o];
+  const int32_t* __restrict__ idx = all_idx + (int64_t)o * kmax;
+  T* __restrict__ out = send + c.off[o];
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
+       m += (long long)gridDim.x * blockDim.x) {
+    const int32_t j = idx[m];
+    out[m] = resid[j];
+    if (kZero) resid[j] = (T)0;
+  }
+}
+
+// One rank, as owner: s = 0; for r in rank order: s += contribution_r.
+template <typename T>
+__global__ void __launch_bounds__(256) k_dist_owner_reduce(const T* own_val, long long k_own,
+                                                           const T* recv, Counts c, int n, int me,
+                                                           T* sums) {
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k_own;
+       m += (long long)gridDim.x * blockDim.x) {
+    T s = (T)0;
+    for (int r = 0; r < n; ++r) s = add_rn(s, r == me ? own_val[m] : recv[c.off[r] + m]);
+    sums[m] = s;
+  }
+}
+
+// One rank: lay the gathered (index, sum) lists out as the union in
+// partition order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_dist_build_union(const int32_t* all_idx, const T* all_sums,
+                                                          int64_t kmax, Counts c, int n, int64_t t,
+                                                          int32_t* union_idx, T* union_sum,
+                                                          long long* K_out) {
+  const int p = blockIdx.y;
+  const int owner = partition_owner(p, n, t);
+  long long off = 0, K = 0;
+  for (int q = 0; q < n; ++q) {
+    const long long kq = c.k[partition_owner(q, n, t)];
+    if (q < p) off += kq;
+    K += kq;
+  }
+  if (p == 0 && blockIdx.x == 0 && threadIdx.x == 0) *K_out = K;
+  const long long k = c.k[owner];
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
+       m += (long long)gridDim.x * blockDim.x) {
+    union_idx[off + m] = all_idx[(int64_t)owner * kmax + m];
+    union_sum[off + m] = all_sums[(int64_t)owner * kmax + m];
+  }
+}
+
+struct FinalizeArgs {
+  int n;                      // cluster size (divisor of the average)
+  int n_local;
+  int64_t n_g;
+  int64_t t;
+  const long long* counts;    // n_local, this step's k_i
+  double* delta;              // n_local, updated in place
+  unsigned long long k_target;
+  double alpha, min_threshold;
+  int k_from_counts;          // 1: K = sum counts (single-device cluster)
+  long long* K;               // in (k_from_counts == 0) / out
+  const int32_t* union_idx;
+  const void* union_sum;
+  const int32_t* prev_idx;    // previous union (dense sparse-clear), may be NULL
+  const long long* prev_K;
+  void* dense;                // n_g or NULL
+  void* model;                // n_g or NULL
+  // history ring
+  int64_t slot;
+  long long* hist_t;
+  long long* hist_K;
+  long long* hist_counts;
+  double* hist_delta;
+};
+
+__device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long n, int64_t key) {
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Threshold update + history (block 0) and the dense g/n maintenance: the
+// index space is cut into gridDim.x segments; each block first clears the
+// previous union inside its segment, then scatters the new one, so every
+// dense[j] is written by exactly one block in a fixed order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
+  __shared__ long long s_rng[4];
+  __shared__ long long s_K;
+  if (threadIdx.x == 0) {
+    long long K;
+    if (a.k_from_counts) {
+      K = 0;
+      for (int i = 0; i < a.n_local; ++i) K += a.counts[i];
+    } else {
+      K = *a.K;
+    }
+    s_K = K;
+  }
+  __syncthreads();
+  const long long K = s_K;
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      if (a.k_from_counts) *a.K = K;
+      a.hist_t[a.slot] = a.t;
+      a.hist_K[a.slot] = K;
+    }
+    if (threadIdx.x < a.n_local) {
+      const int i = threadIdx.x;
+      const unsigned long long k = (unsigned long long)a.counts[i];
+      double d = a.delta[i];
+      a.hist_counts[a.slot * a.n_local + i] = (long long)k;
+      a.hist_delta[a.slot * a.n_local + i] = d;
+      // sparsifier.cpp:77-81
+      if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
+      else if (k < a.k_target) d *= 1.0 - a.alpha;
+      a.delta[i] = d;
+    }
+  }
+  if (!a.dense && !a.model) return;
+  const int64_t seg = (a.n_g + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * seg;
+  const int64_t hi = lo + seg < a.n_g ? lo + seg : a.n_g;
+  if (threadIdx.x == 0) {
+    const long long pK = a.prev_idx ? *a.prev_K : 0;
+    s_rng[0] = a.prev_idx ? lower_bound_i32(a.prev_idx, pK, lo) : 0;
+    s_rng[1] = a.prev_idx ? lower_bound_i32(a.prev_idx, pK, hi) : 0;
+    s_rng[2] = lower_bound_i32(a.union_idx, K, lo);
+    s_rng[3] = lower_bound_i32(a.union_idx, K, hi);
+  }
+  __syncthreads();
+  T* dense = (T*)a.dense;
+  T* x = (T*)a.model;
+  const T* sums = (const T*)a.union_sum;
+  const T nf = (T)a.n;
+  if (dense) {
+    for (long long m = s_rng[0] + threadIdx.x; m < s_rng[1]; m += blockDim.x) dense[a.prev_idx[m]] = (T)0;
+    __syncthreads();
+  }
+  for (long long m = s_rng[2] + threadIdx.x; m < s_rng[3]; m += blockDim.x) {
+    const int32_t j = a.union_idx[m];
+    const T avg = div_rn(sums[m], nf);
+    if (dense) dense[j] = avg;
+    if (x) x[j] = x[j] - avg;  // harness.cpp:214, one rounding after the division
+  }
+}
+
+}  // namespace micro

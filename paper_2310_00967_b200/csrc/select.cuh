@@ -1,0 +1,274 @@
+// select.cuh — K1: the fused accumulate + threshold select + ordered
+// compaction + own-residual-zero pass (one HBM sweep).
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   acc_i = e_i + eta * G_i over ALL n_g            harness.cpp:131 (P4)
+//   non-finite G  -> runtime_error                  harness.cpp:128-130
+//   S_i = { j in partition : |acc_i[j]| > delta_i } sparsifier.cpp:22-37,
+//         ascending, strict, (index, acc value)     tensor.hpp:48-63
+//   e_{i,t+1}[j] = 0 for j in S_i (own part of the union zeroing)
+//                                                   harness.cpp:219-221
+//
+// Layout: one tile = kThreads x kChunks 16-byte vectors per operand
+// (4096 fp32 / 2048 fp64 elements).  Thread t of a tile handles vectors
+// v = i*kThreads + t (i < kChunks), so every load/store instruction of a warp
+// is one fully coalesced 512-byte segment.  Index order inside a tile is
+// (chunk i, thread t, component c); the per-thread selection counts of the
+// four chunks are packed into one 64-bit word (16 bits each, max 1024) and
+// scanned once across the block, giving the ordered rank of every selected
+// element without sorting.  Tiles are ordered across the grid by a ticket
+// counter and chained by decoupled look-back over 64-bit status words
+// (epoch:24 | flag:2 | count:38), so the pass is single-read and the output
+// is globally index-sorted.
+#pragma once
+
+#include "common.cuh"
+
+namespace micro {
+
+constexpr int kThreads = 256;
+constexpr int kChunks = 4;
+constexpr int kWarps = kThreads / 32;
+
+template <typename T>
+__host__ __device__ constexpr int tile_elems() {
+  return kThreads * kChunks * Vec<T>::N;
+}
+
+constexpr unsigned long long kFlagAgg = 1ull << 38;
+constexpr unsigned long long kFlagInc = 2ull << 38;
+constexpr unsigned long long kCountMask = (1ull << 38) - 1;
+
+enum WriteMode : int {
+  kWriteZeroSel = 0,  // e <- acc with own selections zeroed (error feedback on)
+  kWriteAcc = 1,      // e <- acc (error feedback off, n > 1: peers still read acc)
+  kWriteNone = 2,     // no residual write (EF off at n = 1, or select-only)
+};
+
+struct SelectArgs {
+  const void* grad;           // G (T*), unused when !kAccum
+  void* resid;                // e (T*): in e_t (or acc when !kAccum), out per WriteMode
+  int64_t n_g;
+  int64_t p_start, p_end;     // selection range
+  double eta;
+  const double* delta;        // device pointer to delta_i (NULL -> delta_value)
+  double delta_value;
+  int32_t* sel_idx;
+  void* sel_val;              // T*
+  int64_t cap;
+  long long* count;           // device: k_i
+  unsigned long long* status; // look-back words, >= p_max entries
+  int64_t p_max;
+  unsigned int* ticket;       // tile ticket counter (self-resetting)
+  unsigned int epoch;         // launch epoch (24 bits used)
+  int64_t tile_lo;            // first tile of the grid
+  int64_t num_tiles;          // tiles in the grid
+  int* flags;                 // bit0 non-finite, bit1 capacity overflow
+};
+
+// Warp 0 only.  Publishes this tile's aggregate, walks back over the
+// predecessors' status words and returns the exclusive prefix.
+__device__ __forceinline__ long long lookback(unsigned long long* st, int64_t pt,
+                                              unsigned long long agg, unsigned int epoch, int lane) {
+  const unsigned long long ep = (unsigned long long)(epoch & 0xFFFFFFu) << 40;
+  if (pt == 0) {
+    if (lane == 0) st_relaxed_u64(&st[0], ep | kFlagInc | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed_u64(&st[pt], ep | kFlagAgg | agg);
+  unsigned long long excl = 0;
+  int64_t top = pt - 1;
+  while (true) {
+    const int64_t idx = top - lane;
+    unsigned long long v = ep | kFlagInc;  // beyond tile 0: neutral
+    if (idx >= 0) {
+      int spins = 0;
+      while (true) {
+        v = ld_relaxed_u64(&st[idx]);
+        if ((v >> 40) == (epoch & 0xFFFFFFu) && (v & (3ull << 38)) != 0) break;
+        if (++spins > 8) __nanosleep(32);
+      }
+    }
+    const unsigned inc_mask = __ballot_sync(0xffffffffu, (v & (3ull << 38)) == kFlagInc);
+    unsigned long long c = v & kCountMask;
+    if (inc_mask) {
+      const int first = __ffs(inc_mask) - 1;  // nearest inclusive predecessor
+      if (lane > first) c = 0;
+      excl += warp_sum_u64(c);
+      break;
+    }
+    excl += warp_sum_u64(c);
+    top -= 32;
+  }
+  if (lane == 0) st_relaxed_u64(&st[pt], ep | kFlagInc | (excl + agg));
+  return (long long)excl;
+}
+
+template <typename T, bool kAccum, int kMode>
+__global__ void __launch_bounds__(kThreads, 4) k1_fused_select(SelectArgs a) {
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
+  constexpr int TILE = tile_elems<T>();
+
+  __shared__ unsigned int s_ticket;
+  __shared__ unsigned long long s_warp[kWarps];
+  __shared__ long long s_excl;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    const unsigned int tk = atomicAdd(a.ticket, 1u);
+    if (tk == (unsigned int)(a.num_tiles - 1)) atomicExch(a.ticket, 0u);  // last ticket: reset
+    s_ticket = tk;
+  }
+  __syncthreads();
+  const int64_t tile = a.tile_lo + (int64_t)s_ticket;
+  const int64_t base = tile * TILE;
+  const int64_t n_g = a.n_g;
+
+  const double delta = a.delta ? *a.delta : a.delta_value;
+  const T thr = threshold_as(delta, (T*)nullptr);
+  const T eta = (T)a.eta;
+  const T* __restrict__ G = (const T*)a.grad;
+  T* __restrict__ E = (T*)a.resid;
+
+  // ---- load ------------------------------------------------------------
+  V g[kChunks], e[kChunks];
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    const int64_t j0 = base + (int64_t)(i * kThreads + tid) * VN;
+    if (j0 + VN <= n_g) {
+      if (kAccum) g[i] = ld_stream(reinterpret_cast<const V*>(G + j0));
+      e[i] = ld_stream(reinterpret_cast<const V*>(E + j0));
+    } else {
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        const bool in = j0 + c < n_g;
+        if (kAccum) set_comp(g[i], c, in ? G[j0 + c] : (T)0);
+        set_comp(e[i], c, in ? E[j0 + c] : (T)0);
+      }
+    }
+  }
+
+  // ---- accumulate, compare ----------------------------------------------
+  const int64_t p_start = a.p_start, p_end = a.p_end;
+  unsigned int mask[kChunks];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    const int64_t j0 = base + (int64_t)(i * kThreads + tid) * VN;
+    mask[i] = 0;
+#pragma unroll
+    for (int c = 0; c < VN; ++c) {
+      const int64_t j = j0 + c;
+      T acc = comp(e[i], c);
+      if (kAccum) {
+        const T gv = comp(g[i], c);
+        bad |= (j < n_g) && !finite(gv);
+        acc = add_rn(acc, mul_rn(eta, gv));  // e + (eta*G): two roundings, no FMA
+        set_comp(e[i], c, acc);
+      }
+      const bool sel = (j >= p_start) && (j < p_end) && (absx(acc) > thr);
+      mask[i] |= (unsigned)sel << c;
+    }
+  }
+
+  // ---- residual write (independent of the look-back) ---------------------
+  if (kMode != kWriteNone) {
+#pragma unroll
+    for (int i = 0; i < kChunks; ++i) {
+      const int64_t j0 = base + (int64_t)(i * kThreads + tid) * VN;
+      V out = e[i];
+      if (kMode == kWriteZeroSel) {
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+          if (mask[i] & (1u << c)) set_comp(out, c, (T)0);
+      }
+      if (j0 + VN <= n_g) {
+        st_stream(reinterpret_cast<V*>(E + j0), out);
+      } else {
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+          if (j0 + c < n_g) E[j0 + c] = comp(out, c);
+      }
+    }
+  }
+
+  if (kAccum) {
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(a.flags, 1);
+  }
+
+  // ---- ordered compaction (tiles that intersect the selection range) -----
+  const bool in_range = base < p_end && base + TILE > p_start;
+  if (!in_range) return;  // block-uniform
+
+  unsigned long long packed = 0;
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) packed |= (unsigned long long)__popc(mask[i]) << (16 * i);
+  unsigned long long incl = packed;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  unsigned long long warp_prefix = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const unsigned long long s = s_warp[w];
+    warp_prefix += (w < warp) ? s : 0ull;
+    total += s;
+  }
+  const unsigned long long excl_thread = warp_prefix + incl - packed;
+  int chunk_base[kChunks];
+  int tile_count = 0;
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    chunk_base[i] = tile_count;
+    tile_count += (int)((total >> (16 * i)) & 0xFFFFu);
+  }
+
+  const int64_t first_tile = p_start / TILE;
+  const int64_t pt = tile - first_tile;
+  const int64_t last_pt = (p_end - 1) / TILE - first_tile;
+  if (warp == 0) {
+    const long long ex = lookback(a.status, pt, (unsigned long long)tile_count, a.epoch, lane);
+    if (lane == 0) {
+      s_excl = ex;
+      if (pt == last_pt) {
+        const long long k = ex + tile_count;
+        *a.count = k;
+        if (k > a.cap) atomicOr(a.flags, 2);
+        // epoch hygiene: every status word [0, p_max) carries this launch's
+        // epoch once the launch ends, so stale words can never alias.
+        const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
+        for (int64_t q = last_pt + 1; q < a.p_max; ++q) st_relaxed_u64(&a.status[q], ep);
+      }
+    }
+  }
+  __syncthreads();
+  const long long tile_off = s_excl;
+  if (tile_count == 0) return;
+
+  int32_t* __restrict__ out_idx = a.sel_idx;
+  T* __restrict__ out_val = (T*)a.sel_val;
+  const long long cap = a.cap;
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
+    if (!mask[i]) continue;
+    long long pos = tile_off + chunk_base[i] + (long long)((excl_thread >> (16 * i)) & 0xFFFFu);
+    const int64_t j0 = base + (int64_t)(i * kThreads + tid) * VN;
+#pragma unroll
+    for (int c = 0; c < VN; ++c) {
+      if (mask[i] & (1u << c)) {
+        if (pos < cap) {
+          out_idx[pos] = (int32_t)(j0 + c);
+          out_val[pos] = comp(e[i], c);
+        }
+        ++pos;
+      }
+    }
+  }
+}
+
+}  // namespace micro

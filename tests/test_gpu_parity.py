@@ -1,0 +1,231 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle — GPU only.
+
+Chain of trust, link 2: GPU fp32 == C restatement fp32, and GPU fp64 == the
+reference's own compiled code (oracle/_ref) and its golden runs, BIT FOR BIT:
+per-worker counts, union indices, reduced sums, thresholds, residuals, the
+dense averaged gradient and the model.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import Oracle, OracleCluster, RefCluster
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2310_00967_b200 import engine
+    from paper_2310_00967_b200._lib import (CapacityError, InvalidArgument, LogicError,
+                                            NonFiniteGradient)
+
+SEED, ETA = 7, 0.01
+
+
+def gen(o, n, n_g, t, dtype):
+    return np.stack([o.gaussian(SEED, i, t, n_g) for i in range(n)]).astype(dtype)
+
+
+def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, oracle="restatement",
+             check_every=1):
+    o = Oracle()
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, target="full" if full else "split",
+                     error_feedback=ef)
+    x = torch.zeros(n_g, dtype=tdt, device="cuda")
+    m.set_model(x)
+    if oracle == "reference":
+        ref = RefCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, model=True)
+    else:
+        ref = OracleCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, dtype=dtype, model=True)
+    for t in range(iters):
+        G = gen(o, n, n_g, t, dtype)
+        Gd = torch.from_numpy(G).cuda()
+        m.step(list(Gd), ETA, t)
+        r = ref.step(G, ETA, t)
+        if t % check_every and t != iters - 1:
+            continue
+        st = m.query()
+        idx, sums = m.union()
+        assert np.array_equal(st.counts, r["counts"]), t
+        assert st.K == r["union_idx"].size, t
+        assert np.array_equal(idx.astype(np.int64), r["union_idx"]), t
+        assert np.array_equal(sums, r["union_sum"].astype(sums.dtype)), t
+        assert np.array_equal(st.deltas, r["delta_next"]), t
+        res = np.stack([m.residual(i) for i in range(n)])
+        want = ref.residuals() if oracle == "reference" else ref.e
+        assert np.array_equal(res, want.astype(res.dtype)), t
+        dense = m.dense()
+        dw = np.zeros(n_g, dense.dtype)
+        dw[r["union_idx"]] = (r["union_sum"] / n).astype(dense.dtype) if dtype == np.float64 else \
+            (r["union_sum"].astype(np.float32) / np.float32(n))
+        assert np.array_equal(dense, dw), t
+        assert np.array_equal(x.cpu().numpy(), ref.x.astype(dense.dtype)), t
+    h = m.history(iters)
+    assert h["t"].tolist() == list(range(iters))
+    m.close()
+
+
+@pytest.mark.parametrize("n_g,n,d,delta0", [
+    (10_000, 1, 0.01, 0.01),
+    (10_007, 2, 0.01, 0.02),
+    (9_999, 3, 0.05, 0.01),
+    (65_537, 4, 0.01, 0.025),
+    (100_003, 8, 0.02, 0.01),
+    (4_096, 16, 0.01, 0.01),
+    (5, 5, 0.5, 0.0),          # n_g == n: one element per partition
+    (4_095, 1, 0.3, 0.5),      # one partial tile
+    (123_457, 7, 0.001, 0.03),
+])
+def test_gpu_f32_matches_restatement(n_g, n, d, delta0):
+    run_pair(n_g, n, d, delta0, iters=25)
+
+
+@pytest.mark.parametrize("full,ef", [(True, True), (False, False), (True, False)])
+def test_gpu_f32_modes(full, ef):
+    run_pair(20_000, 4, 0.01, 0.01, iters=15, full=full, ef=ef)
+    run_pair(20_000, 1, 0.01, 0.01, iters=15, full=full, ef=ef)
+
+
+def test_gpu_density_one_threshold_zero():
+    """test_harness.cpp:60-76: d = 1, delta0 = 0 -> everything nonzero is sent."""
+    run_pair(8_192, 4, 1.0, 0.0, iters=8)
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("n_g,n,d,delta0", [(10_000, 1, 0.01, 0.01), (10_007, 2, 0.01, 0.02),
+                                             (12_345, 8, 0.02, 0.01), (3_001, 3, 0.1, 0.05)])
+def test_gpu_f64_matches_reference_code(n_g, n, d, delta0):
+    run_pair(n_g, n, d, delta0, iters=20, dtype=np.float64, oracle="reference")
+
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "micro_ref64_*.npz")))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[12:-4] for p in GOLDEN])
+def test_gpu_f64_reproduces_golden(path):
+    z = np.load(path)
+    n_g, n, d, delta0, full, ef, iters, seed, eta = z["config"].tolist()
+    n_g, n, iters, seed = int(n_g), int(n), int(iters), int(seed)
+    o = Oracle()
+    m = engine.Micro(n_g, n, dtype=torch.float64, density=d, initial_threshold=delta0,
+                     target="full" if full else "split", error_feedback=bool(ef))
+    x = torch.zeros(n_g, dtype=torch.float64, device="cuda")
+    m.set_model(x)
+    off = 0
+    for t in range(iters):
+        G = torch.from_numpy(np.stack([o.gaussian(seed, i, t, n_g) for i in range(n)]).astype(np.float64)).cuda()
+        m.step(list(G), eta, t)
+        K = int(z["K"][t])
+        st = m.query()
+        idx, sums = m.union()
+        assert np.array_equal(st.counts, z["counts"][t])
+        assert np.array_equal(idx, z["union_idx"][off:off + K])
+        assert np.array_equal(sums, z["union_sum"][off:off + K])
+        assert np.array_equal(st.deltas, z["delta_next"][t])
+        off += K
+    assert np.array_equal(np.stack([m.residual(i) for i in range(n)]), z["residuals"])
+    assert np.array_equal(x.cpu().numpy(), z["model"])
+
+
+def test_synthetic_gradients_bit_identical_host_device():
+    o = Oracle()
+    for n, w, t in [(1_000_003, 0, 0), (4097, 3, 11), (7, 1, 2**33)]:
+        g = torch.empty(n, device="cuda")
+        engine.synth_gaussian(g, SEED, w, t)
+        assert np.array_equal(g.cpu().numpy().view(np.uint32), o.gaussian(SEED, w, t, n).view(np.uint32))
+
+
+def test_nonfinite_gradient_poisons_until_reset():
+    m = engine.Micro(10_000, 2)
+    G = torch.randn(2, 10_000, device="cuda")
+    G[1, 1234] = float("nan")
+    m.step(list(G), ETA, 0)
+    with pytest.raises(NonFiniteGradient, match="non-finite gradient"):
+        m.sync()
+    with pytest.raises(NonFiniteGradient):
+        m.step(list(torch.randn(2, 10_000, device="cuda")), ETA, 1)
+    m.reset()
+    m.step(list(torch.randn(2, 10_000, device="cuda")), ETA, 0)
+    m.sync()
+    G = torch.randn(1, 10_000, device="cuda")
+    G[0, 5] = float("inf")
+    m1 = engine.Micro(10_000, 1)
+    m1.step(list(G), ETA, 0)
+    with pytest.raises(NonFiniteGradient):
+        m1.sync()
+
+
+def test_capacity_overflow_reported():
+    m = engine.Micro(50_000, 1, selection_capacity=100, initial_threshold=0.0)
+    m.step([torch.randn(50_000, device="cuda")], ETA, 0)
+    with pytest.raises(CapacityError):
+        m.sync()
+
+
+def test_config_rejections():
+    with pytest.raises(InvalidArgument):
+        engine.Micro(3, 4)
+    with pytest.raises(InvalidArgument):
+        engine.Micro(100, 2, density=0.0)
+    with pytest.raises(InvalidArgument):
+        engine.Micro(100, 2, scaling_factor=1.0)
+    with pytest.raises(InvalidArgument):
+        engine.Micro(100, 2, initial_threshold=-1.0)
+    with pytest.raises(InvalidArgument):
+        engine.Micro(100, 2, min_threshold=0.0)
+    m = engine.Micro(100, 1)
+    with pytest.raises(InvalidArgument):
+        m.step([torch.randn(100, device="cuda")], 0.0, 0)   # eta must be positive
+    with pytest.raises(InvalidArgument):
+        m.step([torch.randn(100, device="cuda")], ETA, -1)  # negative iteration
+    with pytest.raises(LogicError):
+        m.aggregate()                                       # without compress
+
+
+def test_step_host_end_to_end():
+    o = Oracle()
+    n_g = 50_001
+    m = engine.Micro(n_g, 2)
+    ref = OracleCluster(n_g, 2)
+    for t in range(5):
+        G = gen(o, 2, n_g, t, np.float32)
+        h = torch.from_numpy(G).pin_memory()
+        idx, sums = m.step_host(h, ETA, t)
+        r = ref.step(G, ETA, t)
+        assert np.array_equal(idx, r["union_idx"]) and np.array_equal(sums, r["union_sum"])
+
+
+def test_full_size_properties_138M():
+    """BASELINE C3 size at n = 1 (and one n = 8 step): size-independent
+    properties — ordered unique indices inside the partition, |acc| > delta,
+    conservation e_{t+1} + sent == e_t + eta*G elementwise, count == the
+    torch-computed count, dense == sums at the union."""
+    n_g = 138_000_000
+    torch.cuda.empty_cache()
+    m = engine.Micro(n_g, 1, initial_threshold=2.576 * ETA)
+    G = torch.empty(n_g, device="cuda")
+    for t in range(3):
+        engine.synth_gaussian(G, SEED, 0, t)
+        e0 = m.residual_device(0).clone()
+        m.step([G], ETA, t)
+        st = m.query()
+        delta = m.history(1)["delta_used"][0, 0]
+        acc = e0 + torch.tensor(ETA, dtype=torch.float32) * G
+        sel = acc.abs().double() > delta
+        assert int(sel.sum()) == st.K
+        idx, sums = m.union()
+        it = torch.from_numpy(idx.astype(np.int64)).cuda()
+        assert torch.equal(it, torch.nonzero(sel).flatten())
+        assert torch.equal(torch.from_numpy(sums).cuda(), acc[it])
+        e1 = m.residual_device(0)
+        sent = torch.zeros_like(acc)
+        sent[it] = acc[it]
+        assert torch.equal(e1 + sent, acc)
+        dense = m.dense_device()
+        assert torch.equal(dense[it], acc[it]) and int((dense != 0).sum()) == st.K
+        del e0, acc, sel, sent
+    m.close()
+    torch.cuda.empty_cache()
