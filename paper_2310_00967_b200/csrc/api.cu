@@ -227,12 +227,19 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   a.flags = c->flags;
   const dim3 grid((unsigned)a.num_tiles);
   const bool ef = c->cfg.error_feedback != 0;
-  if (ef)
-    k1_fused_select<T, true, kWriteZeroSel><<<grid, kThreads, 0, c->stream>>>(a);
+  const bool al = ((uintptr_t)grad % 16) == 0;
+  if (ef && al)
+    k1_fused_select<T, true, kWriteZeroSel, true><<<grid, kThreads, 0, c->stream>>>(a);
+  else if (ef)
+    k1_fused_select<T, true, kWriteZeroSel, false><<<grid, kThreads, 0, c->stream>>>(a);
+  else if (c->n > 1 && al)
+    k1_fused_select<T, true, kWriteAcc, true><<<grid, kThreads, 0, c->stream>>>(a);
   else if (c->n > 1)
-    k1_fused_select<T, true, kWriteAcc><<<grid, kThreads, 0, c->stream>>>(a);
+    k1_fused_select<T, true, kWriteAcc, false><<<grid, kThreads, 0, c->stream>>>(a);
+  else if (al)
+    k1_fused_select<T, true, kWriteNone, true><<<grid, kThreads, 0, c->stream>>>(a);
   else
-    k1_fused_select<T, true, kWriteNone><<<grid, kThreads, 0, c->stream>>>(a);
+    k1_fused_select<T, true, kWriteNone, false><<<grid, kThreads, 0, c->stream>>>(a);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
@@ -485,13 +492,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     micro_ctx_destroy(c);
     return code;
   };
-  if (stream) {
-    c->stream = (cudaStream_t)stream;
-  } else {
-    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
-    if (e != cudaSuccess) { delete c; return fail(MICRO_ECUDA, "stream: %s", cudaGetErrorString(e)); }
-    c->own_stream = true;
-  }
+  c->stream = (cudaStream_t)stream;  // NULL = the legacy default stream, like every CUDA API
   const int64_t max_range = (c->n_g + c->n - 1) / c->n;
   c->sel_cap = cfg->selection_capacity ? std::min<int64_t>(cfg->selection_capacity, max_range) : max_range;
   c->uni_cap = std::min<int64_t>(c->n_g, (int64_t)c->n * c->sel_cap);
@@ -541,7 +542,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
 int micro_ctx_destroy(micro_ctx* c) {
   if (!c) return MICRO_OK;
   DeviceGuard dg(c->dev);
-  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->staging) cudaFree(c->staging);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -572,7 +573,7 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
   if (c->compressed) return fail(MICRO_ELOGIC, "micro_compress called twice without aggregation");
   for (int i = 0; i < c->n_local; ++i) {
     if (!d_grads[i]) return fail(MICRO_EINVAL, "null gradient for local worker %d", i);
-    if ((uintptr_t)d_grads[i] % 16) return fail(MICRO_EINVAL, "gradient %d not 16-byte aligned", i);
+    if ((uintptr_t)d_grads[i] % c->esz) return fail(MICRO_EINVAL, "gradient %d misaligned for its dtype", i);
   }
   DeviceGuard dg(c->dev);
   c->t_cur = t;

@@ -104,7 +104,7 @@ __device__ __forceinline__ long long lookback(unsigned long long* st, int64_t pt
   return (long long)excl;
 }
 
-template <typename T, bool kAccum, int kMode>
+template <typename T, bool kAccum, int kMode, bool kGAligned = true>
 __global__ void __launch_bounds__(kThreads, 4) k1_fused_select(SelectArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -137,7 +137,14 @@ __global__ void __launch_bounds__(kThreads, 4) k1_fused_select(SelectArgs a) {
   for (int i = 0; i < kChunks; ++i) {
     const int64_t j0 = base + (int64_t)(i * kThreads + tid) * VN;
     if (j0 + VN <= n_g) {
-      if (kAccum) g[i] = ld_stream(reinterpret_cast<const V*>(G + j0));
+      if (kAccum) {
+        if (kGAligned) {
+          g[i] = ld_stream(reinterpret_cast<const V*>(G + j0));
+        } else {  // caller's gradient not 16-byte aligned: same coalescing, scalar loads
+#pragma unroll
+          for (int c = 0; c < VN; ++c) set_comp(g[i], c, __ldcs(G + j0 + c));
+        }
+      }
       e[i] = ld_stream(reinterpret_cast<const V*>(E + j0));
     } else {
 #pragma unroll

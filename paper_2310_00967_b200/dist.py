@@ -1,0 +1,124 @@
+"""One process per GPU: the MiCRO exchange over torch.distributed (NCCL).
+
+Each rank is one worker i of the n-worker cluster.  Per iteration
+(reference semantics collectives.cpp:14-57, harness.cpp:185-224):
+
+  K1   micro_compress: acc_i = e_i + eta*G_i, own selection S_i (partition
+       (t % n + i) % n), own residual entries zeroed          [device]
+  K2   all-gather k_i                                          [NCCL]
+  K3   all-gather S_i indices, padded to kmax = max_i k_i      [NCCL]
+  K4   gather acc_i at every other owner's indices, zero them  [device]
+  K5   all-to-all-v: contributions -> their owners             [NCCL]
+  K6   owner: s = 0; s += contribution_r for r = 0..n-1        [device]
+  K7   all-gather the owners' sums, padded to kmax             [NCCL]
+  K8   union in partition order, dense g/n, model, delta_i     [device]
+
+The partitions are exclusive, so the union restricted to partition p is the
+selection of p's owner: no sort, no build-up, and every sum is formed in
+worker order from +0 exactly like all_reduce_sparse_values.  `ncclAllReduce`
+is never used: its reduction order is not the reference's.
+
+The protocol is written once against an ``ops`` object; :class:`DeviceOps`
+binds it to the CUDA engine.  The CPU tests bind it to the oracle and run it
+over gloo (tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import check, lib
+from .engine import Micro, device_view
+
+
+def exchange(ops, group=None) -> int:
+    """Run K2..K8 for one rank after ops' compress.  Returns |union|."""
+    n = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = ops.device
+    cnt = torch.empty(n, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(cnt, ops.own_count(), group=group)            # K2
+    counts = [int(v) for v in cnt.cpu().tolist()]
+    kmax = max(counts)
+    if kmax == 0:
+        ops.finalize(None, None, counts, 0)
+        return 0
+    all_idx = torch.empty(n * kmax, dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(all_idx, ops.own_indices(kmax), group=group)  # K3
+    send = ops.gather_foreign(all_idx, counts, kmax)                           # K4
+    recv = torch.empty((n - 1) * counts[me], dtype=ops.dtype, device=dev)
+    dist.all_to_all_single(recv, send,                                          # K5
+                           output_split_sizes=[0 if r == me else counts[me] for r in range(n)],
+                           input_split_sizes=[0 if o == me else counts[o] for o in range(n)],
+                           group=group)
+    own_sums = ops.owner_reduce(recv, counts, kmax)                            # K6
+    all_sums = torch.empty(n * kmax, dtype=ops.dtype, device=dev)
+    dist.all_gather_into_tensor(all_sums, own_sums, group=group)               # K7
+    ops.finalize(all_idx, all_sums, counts, kmax)                               # K8
+    return sum(counts)
+
+
+class DeviceOps:
+    """Binds :func:`exchange` to one rank's `micro_ctx` (n_local == 1)."""
+
+    def __init__(self, m: Micro):
+        self.m = m
+        self.device, self.dtype = m.device, m.dtype
+
+    def own_count(self) -> torch.Tensor:
+        _, _, cnt = self.m.selection_device(0)
+        return cnt
+
+    def own_indices(self, kmax: int) -> torch.Tensor:
+        pi, _, _ = self.m.selection_device(0)
+        return device_view(pi, kmax, torch.int32, self.device)  # kmax <= selection capacity
+
+    def gather_foreign(self, all_idx, counts, kmax):
+        me = self.m.rank
+        send = torch.empty(max(sum(counts) - counts[me], 1), dtype=self.dtype, device=self.device)
+        hc = (C.c_int64 * len(counts))(*counts)
+        check(lib().micro_dist_gather_foreign(self.m.handle, C.c_void_p(all_idx.data_ptr()), hc, kmax,
+                                              C.c_void_p(send.data_ptr())))
+        return send[: sum(counts) - counts[me]]
+
+    def owner_reduce(self, recv, counts, kmax):
+        out = torch.zeros(kmax, dtype=self.dtype, device=self.device)
+        hc = (C.c_int64 * len(counts))(*counts)
+        check(lib().micro_dist_owner_reduce(self.m.handle, C.c_void_p(recv.data_ptr() if recv.numel() else 0), hc,
+                                            C.c_void_p(out.data_ptr())))
+        return out
+
+    def finalize(self, all_idx, all_sums, counts, kmax):
+        hc = (C.c_int64 * len(counts))(*counts)
+        check(lib().micro_dist_finalize(self.m.handle, C.c_void_p(all_idx.data_ptr() if all_idx is not None else 0),
+                                        C.c_void_p(all_sums.data_ptr() if all_sums is not None else 0), hc, kmax))
+
+
+class DistMicro:
+    """One rank's MiCRO engine; same calls as :class:`engine.Micro`."""
+
+    def __init__(self, n_g: int, group=None, **kw):
+        if not dist.is_initialized():
+            raise _lib.LogicError(_lib.MICRO_ELOGIC, "torch.distributed is not initialized")
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.m = Micro(n_g, self.world, n_local=1, rank=self.rank, **kw)
+        self.ops = DeviceOps(self.m)
+        self.n_g = n_g
+
+    def compress(self, grads, eta: float, t: int):
+        self.m.compress(grads, eta, t)
+
+    def aggregate(self) -> int:
+        return exchange(self.ops, self.group)
+
+    def step(self, grads, eta: float, t: int) -> int:
+        self.compress(grads, eta, t)
+        return self.aggregate()
+
+    def __getattr__(self, name):  # query, history, union, residual, dense, set_model, sync ...
+        return getattr(self.m, name)
