@@ -257,6 +257,7 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.alpha = c->cfg.scaling_factor;
   f.min_threshold = c->cfg.min_threshold;
   f.k_from_counts = k_from_counts;
+  f.cap = c->sel_cap;
   f.K = c->Kbuf + c->buf;
   f.union_idx = uidx;
   f.union_sum = usum;
@@ -300,10 +301,10 @@ int aggregate_cluster(micro_ctx* c) {
   const unsigned gx = (unsigned)std::min<int64_t>((expect + 255) / 256, 2048);
   const dim3 grid(gx, (unsigned)c->n);
   if (c->cfg.error_feedback)
-    k_cluster_reduce<T, true><<<grid, 256, 0, c->stream>>>(w, c->counts, c->n, c->t_cur,
+    k_cluster_reduce<T, true><<<grid, 256, 0, c->stream>>>(w, c->counts, c->sel_cap, c->n, c->t_cur,
                                                             c->uni_idx[c->buf], (T*)c->uni_sum[c->buf]);
   else
-    k_cluster_reduce<T, false><<<grid, 256, 0, c->stream>>>(w, c->counts, c->n, c->t_cur,
+    k_cluster_reduce<T, false><<<grid, 256, 0, c->stream>>>(w, c->counts, c->sel_cap, c->n, c->t_cur,
                                                              c->uni_idx[c->buf], (T*)c->uni_sum[c->buf]);
   CU(cudaGetLastError());
   return launch_finalize<T>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 1);

@@ -28,15 +28,19 @@ struct Counts {
 // Single-device cluster, n > 1: one block row per partition p; the owner's
 // own value comes from its K1 pairs (its residual entry is already zeroed),
 // every other worker's from its accumulator, summed in worker order.
+// Counts beyond the selection capacity were not stored (K1 raised the
+// overflow flag, reported at the next sync); consumers read at most `cap`.
+__device__ __forceinline__ long long clamp_count(long long k, long long cap) { return k < cap ? k : cap; }
+
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long long* counts,
-                                                        int n, int64_t t, int32_t* union_idx,
-                                                        T* union_sum) {
+                                                        long long cap, int n, int64_t t,
+                                                        int32_t* union_idx, T* union_sum) {
   const int p = blockIdx.y;
   const int owner = partition_owner(p, n, t);
   long long off = 0;
-  for (int q = 0; q < p; ++q) off += counts[partition_owner(q, n, t)];
-  const long long k = counts[owner];
+  for (int q = 0; q < p; ++q) off += clamp_count(counts[partition_owner(q, n, t)], cap);
+  const long long k = clamp_count(counts[owner], cap);
   const int32_t* __restrict__ idx = w.sel_idx[owner];
   const T* __restrict__ val = (const T*)w.sel_val[owner];
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
@@ -124,6 +128,7 @@ struct FinalizeArgs {
   unsigned long long k_target;
   double alpha, min_threshold;
   int k_from_counts;          // 1: K = sum counts (single-device cluster)
+  long long cap;              // selection capacity per worker
   long long* K;               // in (k_from_counts == 0) / out
   const int32_t* union_idx;
   const void* union_sum;
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
     long long K;
     if (a.k_from_counts) {
       K = 0;
-      for (int i = 0; i < a.n_local; ++i) K += a.counts[i];
+      for (int i = 0; i < a.n_local; ++i) K += clamp_count(a.counts[i], a.cap);
     } else {
       K = *a.K;
     }

@@ -43,6 +43,9 @@ def exchange(ops, group=None) -> int:
     dist.all_gather_into_tensor(cnt, ops.own_count(), group=group)            # K2
     counts = [int(v) for v in cnt.cpu().tolist()]
     kmax = max(counts)
+    if kmax > ops.capacity:  # every rank sees the same counts, so every rank raises
+        raise _lib.CapacityError(_lib.MICRO_ECAPACITY,
+                                 f"selection of {kmax} exceeds capacity {ops.capacity} on some rank")
     if kmax == 0:
         ops.finalize(None, None, counts, 0)
         return 0
@@ -67,6 +70,7 @@ class DeviceOps:
     def __init__(self, m: Micro):
         self.m = m
         self.device, self.dtype = m.device, m.dtype
+        self.capacity = m.selection_capacity
 
     def own_count(self) -> torch.Tensor:
         _, _, cnt = self.m.selection_device(0)

@@ -89,6 +89,8 @@ class Micro:
         self.cfg = cfg
         self.device, self.dtype = dev, dtype
         self.n_g, self.n, self.n_local, self.rank = n_g, n_workers, cfg.n_local, rank
+        max_range = -(-n_g // max(n_workers, 1))
+        self.selection_capacity = min(selection_capacity, max_range) if selection_capacity else max_range
         with torch.cuda.device(dev):
             self.stream = stream or torch.cuda.current_stream(dev)
         h = C.c_void_p()

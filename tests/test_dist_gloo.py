@@ -19,6 +19,7 @@ class OracleOps:
 
     device = torch.device("cpu")
     dtype = torch.float32
+    capacity = 1 << 40
 
     def __init__(self, o, n_g, n, rank, d, delta0, alpha=0.01, eps=1e-12, ef=True):
         self.o, self.n_g, self.n, self.rank = o, n_g, n, rank
@@ -32,7 +33,7 @@ class OracleOps:
         self.idx, self.val = self.o.select(acc, s, e, self.delta)
         if self.ef:
             acc[self.idx] = 0
-        self.e, self.t, self.acc_full = acc, t, None
+        self.e, self.t = acc, t
 
     def own_count(self):
         return torch.tensor([self.idx.size], dtype=torch.int64)
