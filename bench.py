@@ -189,19 +189,28 @@ def our_arm(args, wl):
         m = engine.Micro(n_g, 1, density=d, initial_threshold=delta0, scaling_factor=ALPHA)
     stream = torch.cuda.current_stream(dev)
 
-    # R resident gradients, rotated.  The threshold adapts over the SAME
-    # rotation for `prime` untimed iterations so the timed window is in the
-    # stationary regime the density target refers to.
-    R = max(2, min(args.buffers, int(0.5 * torch.cuda.mem_get_info(dev)[0] // (4 * n_g))))
+    # The threshold adapts for `prime` untimed iterations on fresh N(0,1)
+    # gradients (generated between steps), reaching the stationary regime the
+    # density target refers to.  The warm-up and timed steps
+    # then read gradients that are already resident in HBM: one fresh buffer
+    # per step when memory allows (same statistics as the prime phase),
+    # otherwise R buffers rotated.
+    t = 0
+    gen = torch.empty(n_g, device=dev)
+    for _ in range(args.prime):
+        engine.synth_gaussian(gen, SEED, rank, t)
+        m.step([gen], ETA, t)
+        t += 1
+    del gen
+    torch.cuda.synchronize()
+    need = args.warmup + args.steps
+    R = max(2, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (4 * n_g))))
     G = [torch.empty(n_g, device=dev) for _ in range(R)]
     for r in range(R):
-        engine.synth_gaussian(G[r], SEED, rank, r)
-    t = 0
-    for _ in range(args.prime):
-        m.step([G[t % R]], ETA, t)
-        t += 1
+        engine.synth_gaussian(G[r], SEED, rank, t + r)
+    t0_bufs = t
     for s in range(args.warmup):
-        m.step([G[t % R]], ETA, t)
+        m.step([G[(t - t0_bufs) % R]], ETA, t)
         t += 1
     torch.cuda.synchronize()
 
@@ -216,7 +225,7 @@ def our_arm(args, wl):
         start.record(stream)
         for s in range(args.steps):
             evs[s][0].record(stream)
-            m.compress([G[t % R]], ETA, t)
+            m.compress([G[(t - t0_bufs) % R]], ETA, t)
             evs[s][1].record(stream)
             m.aggregate()
             t += 1
@@ -281,7 +290,7 @@ def our_arm(args, wl):
             "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world,
                        "one_worker_per_gpu": True, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
-                       "inputs": f"{R} resident N(0,1) gradients rotated; each 4*n_g bytes > L2 (no flush needed)"
+                       "inputs": (f"{R} resident N(0,1) gradients ({\"one fresh per step\" if R >= args.warmup + args.steps else \"rotated\"}); each 4*n_g bytes > L2 (no flush needed)")
                        if 4 * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
                        "parallelism": f"dp{world} (exclusive cyclic partitions)"},
             "density": density, "density_rel_err": density / d - 1.0,
@@ -309,7 +318,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
     ap.add_argument("--prime", type=int, default=1000, help="untimed threshold-adaptation iterations")
-    ap.add_argument("--buffers", type=int, default=8, help="resident gradient buffers (rotated)")
+    ap.add_argument("--buffers", type=int, default=256, help="max resident gradient buffers")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -95,6 +95,14 @@ int micro_all_reduce_sparse(int dtype, const void* const* h_accs, int n, int64_t
 int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_concat,
                              int32_t* d_union, int64_t* K, void* stream);
 
+/* Device memory plumbing for hosts without the CUDA runtime (the C++
+ * drop-in, sparsim_b200.hpp).  kind: 0 host->device, 1 device->host,
+ * 2 device->device.  micro_memcpy synchronises `stream`. */
+int micro_device_malloc(void** d_ptr, int64_t bytes, int device);
+int micro_device_free(void* d_ptr);
+int micro_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream);
+int micro_device_count(int* count);
+
 /* Synthetic N(0,1) gradients of include/micro_synth.h (bench/test inputs). */
 int micro_synth_gaussian(int dtype, uint64_t seed, uint32_t worker, uint64_t t, int64_t n,
                          void* d_out, void* stream);

@@ -85,6 +85,10 @@ _SIGS = {
     "micro_all_reduce_sparse": ([I32, C.POINTER(VP), I32, I64, VP, I64, VP, VP], I32),
     "micro_all_gather_indices": ([I32, PI64, VP, VP, PI64, VP], I32),
     "micro_synth_gaussian": ([I32, U64, U32, U64, I64, VP, VP], I32),
+    "micro_device_malloc": ([C.POINTER(VP), I64, I32], I32),
+    "micro_device_free": ([VP], I32),
+    "micro_memcpy": ([VP, VP, I64, I32, VP], I32),
+    "micro_device_count": ([C.POINTER(I32)], I32),
     "micro_config_default": ([C.POINTER(micro_config)], None),
     "micro_ctx_create": ([C.POINTER(VP), C.POINTER(micro_config), VP], I32),
     "micro_ctx_destroy": ([VP], I32),

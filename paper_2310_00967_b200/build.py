@@ -46,3 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force=True, verbose="-v" in sys.argv))
+
+
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
+
+
+def build_cpp_tests() -> str:
+    """The reference's hot-path unit tests restated against the C++ drop-in
+    header (include/sparsim_b200.hpp), linked against the in-tree library."""
+    build()
+    os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), CPP_TEST_SRC,
+                    "-L", LIBDIR, "-lmicro_b200", "-Wl,-rpath,$ORIGIN/../../../paper_2310_00967_b200/lib", "-o", CPP_TEST_BIN], check=True)
+    return CPP_TEST_BIN

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -18,6 +19,7 @@
 #include "../../include/micro_synth.h"
 #include "exchange.cuh"
 #include "select.cuh"
+#include "select_tma.cuh"
 
 using namespace micro;
 
@@ -139,7 +141,6 @@ struct micro_ctx {
   micro_config cfg{};
   int dev = 0;
   cudaStream_t stream = nullptr;
-  bool own_stream = false;
   int n = 1, n_local = 1;
   int64_t n_g = 0;
   size_t esz = 4;
@@ -161,6 +162,10 @@ struct micro_ctx {
   // K1 workspace
   unsigned long long* status = nullptr;
   int64_t p_max = 0;
+  int64_t status_len = 0;
+  bool use_tma = true;          // K1 = k1_tma_select (MICRO_K1_KERNEL=tile: k1_fused_select)
+  int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
+  void* stage_val = nullptr;
   unsigned int* ticket = nullptr;
   unsigned int epoch = 0;
   int* flags = nullptr;
@@ -202,10 +207,52 @@ int check_poison(micro_ctx* c) {
   return MICRO_OK;
 }
 
+template <typename T, int kMode>
+int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
+  static bool attr_set[64] = {false};  // per instantiation and device
+  if (c->dev >= 64 || !attr_set[c->dev]) {
+    CU(cudaFuncSetAttribute(k1_tma_select<T, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes));
+    if (c->dev < 64) attr_set[c->dev] = true;
+  }
+  k1_tma_select<T, kMode><<<num_sms(c->dev), kTmaThreads, kTmaSmemBytes, c->stream>>>(a);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+template <typename T>
+int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe) {
+  constexpr int TILE = tma_tile_elems<T>();
+  TmaSelectArgs a{};
+  a.grad = grad;
+  a.resid = c->resid[i];
+  a.n_g = c->n_g;
+  a.p_start = ps;
+  a.p_end = pe;
+  a.eta = eta;
+  a.delta = c->delta + i;
+  a.sel_idx = c->sel_idx[c->buf][i];
+  a.sel_val = c->sel_val[c->buf][i];
+  a.cap = c->sel_cap;
+  a.count = c->counts + i;
+  a.stage_idx = c->stage_idx;
+  a.stage_val = c->stage_val;
+  a.status = c->status;
+  a.status_len = c->status_len;
+  a.epoch = ++c->epoch;
+  a.flags = c->flags;
+  a.num_tiles = (c->n_g + TILE - 1) / TILE;
+  a.ptile_lo = ps / TILE;
+  a.ptile_hi = (pe - 1) / TILE;
+  if (c->cfg.error_feedback) return launch_k1_tma_mode<T, kWriteZeroSel>(c, a);
+  if (c->n > 1) return launch_k1_tma_mode<T, kWriteAcc>(c, a);
+  return launch_k1_tma_mode<T, kWriteNone>(c, a);
+}
+
 template <typename T>
 int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   int64_t ps, pe;
   partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
+  if (c->use_tma && ((uintptr_t)grad % 16) == 0) return launch_k1_tma<T>(c, i, grad, eta, ps, pe);
   SelectArgs a{};
   a.grad = grad;
   a.resid = c->resid[i];
@@ -274,8 +321,8 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_counts = c->hist_counts;
   f.hist_delta = c->hist_delta;
   int blocks = 1;
-  if (c->dense || c->model) {
-    const int64_t want = (c->n_g + 65535) / 65536;
+  if (c->dense || c->model) {  // grid-stride over the union entries
+    const int64_t want = ((int64_t)c->k_worker * c->n * 3 / 2 + 255) / 256;
     blocks = (int)std::min<int64_t>(std::max<int64_t>(want, 1), 4 * num_sms(c->dev));
   }
   k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
@@ -498,6 +545,11 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->sel_cap = cfg->selection_capacity ? std::min<int64_t>(cfg->selection_capacity, max_range) : max_range;
   c->uni_cap = std::min<int64_t>(c->n_g, (int64_t)c->n * c->sel_cap);
   c->p_max = c->esz == 4 ? p_max_for<float>(max_range) : p_max_for<double>(max_range);
+  c->status_len = std::max<int64_t>(c->p_max, 4 * num_sms(c->dev));
+  {
+    const char* k = std::getenv("MICRO_K1_KERNEL");
+    c->use_tma = !(k && std::strcmp(k, "tile") == 0);
+  }
   const int nbuf = c->n == 1 ? 2 : 1;
   c->resid.assign(c->n_local, nullptr);
   for (int b = 0; b < 2; ++b) {
@@ -524,7 +576,12 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((rc = c->alloc((void**)&c->delta, sizeof(double) * c->n_local))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->Kbuf, sizeof(long long) * 2))) return cleanup(rc);
   if (cfg->dense_output && (rc = c->alloc(&c->dense, c->n_g * c->esz))) return cleanup(rc);
-  if ((rc = c->alloc((void**)&c->status, sizeof(unsigned long long) * c->p_max))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->status, sizeof(unsigned long long) * c->status_len))) return cleanup(rc);
+  if (c->use_tma) {
+    const int64_t stage = c->p_max * (int64_t)tma_tile_elems<float>() * 4 / (int64_t)c->esz;
+    if ((rc = c->alloc((void**)&c->stage_idx, stage * 4))) return cleanup(rc);
+    if ((rc = c->alloc(&c->stage_val, stage * c->esz))) return cleanup(rc);
+  }
   if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->flags, sizeof(int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_t, sizeof(long long) * kHistCap))) return cleanup(rc);
@@ -532,7 +589,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((rc = c->alloc((void**)&c->hist_counts, sizeof(long long) * kHistCap * c->n_local))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_delta, sizeof(double) * kHistCap * c->n_local))) return cleanup(rc);
   cudaError_t e;
-  if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->p_max, c->stream)) != cudaSuccess ||
+  if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
     return cleanup(fail(MICRO_ECUDA, "memset: %s", cudaGetErrorString(e)));
   if ((rc = reset_state(c))) return cleanup(rc);
@@ -546,7 +603,6 @@ int micro_ctx_destroy(micro_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->staging) cudaFree(c->staging);
-  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return MICRO_OK;
 }
@@ -864,6 +920,38 @@ int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_al
                                                           (double*)c->uni_sum[c->buf], c->Kbuf + c->buf);
   CU(cudaGetLastError());
   return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+}
+
+// ---- device memory plumbing ----
+
+int micro_device_count(int* count) {
+  if (!count) return fail(MICRO_EINVAL, "null count");
+  CU(cudaGetDeviceCount(count));
+  return MICRO_OK;
+}
+
+int micro_device_malloc(void** d, int64_t bytes, int device) {
+  if (!d || bytes < 0) return fail(MICRO_EINVAL, "bad allocation request");
+  *d = nullptr;
+  DeviceGuard dg(device);
+  cudaError_t e = cudaMalloc(d, bytes ? (size_t)bytes : 16);
+  if (e != cudaSuccess) return fail(MICRO_ENOMEM, "cudaMalloc(%lld): %s", (long long)bytes, cudaGetErrorString(e));
+  return MICRO_OK;
+}
+
+int micro_device_free(void* d) {
+  if (d) CU(cudaFree(d));
+  return MICRO_OK;
+}
+
+int micro_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
+  if (bytes < 0 || kind < 0 || kind > 2) return fail(MICRO_EINVAL, "bad copy request");
+  if (!bytes) return MICRO_OK;
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost
+                                                                          : cudaMemcpyDeviceToDevice;
+  CU(cudaMemcpyAsync(dst, src, (size_t)bytes, k, (cudaStream_t)stream));
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  return MICRO_OK;
 }
 
 // ---- stateless value-level operations ----

@@ -153,13 +153,18 @@ __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long
   return lo;
 }
 
-// Threshold update + history (block 0) and the dense g/n maintenance: the
-// index space is cut into gridDim.x segments; each block first clears the
-// previous union inside its segment, then scatters the new one, so every
-// dense[j] is written by exactly one block in a fixed order.
+// Threshold update + history (block 0), then the dense g/n maintenance with
+// whole 32-byte sectors: the dense vector is zero outside the union, so the
+// full content of every sector that the previous or the current union
+// touches is known — avg at current-union slots, 0 elsewhere.  Each touched
+// sector is written exactly once, in full, by one owner thread (the first
+// current-union entry in it, else the first previous-union entry), so there
+// is no partial-sector read-modify-write in HBM and no ordering between the
+// clear and the scatter.  The optional model update x -= avg
+// (harness.cpp:212-215) is done by the same owner for its sector's entries.
 template <typename T>
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
-  __shared__ long long s_rng[4];
+  constexpr int SEC = 32 / (int)sizeof(T);  // elements per 32-byte sector
   __shared__ long long s_K;
   if (threadIdx.x == 0) {
     long long K;
@@ -192,30 +197,61 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
     }
   }
   if (!a.dense && !a.model) return;
-  const int64_t seg = (a.n_g + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = (int64_t)blockIdx.x * seg;
-  const int64_t hi = lo + seg < a.n_g ? lo + seg : a.n_g;
-  if (threadIdx.x == 0) {
-    const long long pK = a.prev_idx ? *a.prev_K : 0;
-    s_rng[0] = a.prev_idx ? lower_bound_i32(a.prev_idx, pK, lo) : 0;
-    s_rng[1] = a.prev_idx ? lower_bound_i32(a.prev_idx, pK, hi) : 0;
-    s_rng[2] = lower_bound_i32(a.union_idx, K, lo);
-    s_rng[3] = lower_bound_i32(a.union_idx, K, hi);
-  }
-  __syncthreads();
   T* dense = (T*)a.dense;
   T* x = (T*)a.model;
   const T* sums = (const T*)a.union_sum;
+  const int32_t* cur = a.union_idx;
   const T nf = (T)a.n;
-  if (dense) {
-    for (long long m = s_rng[0] + threadIdx.x; m < s_rng[1]; m += blockDim.x) dense[a.prev_idx[m]] = (T)0;
-    __syncthreads();
+  const long long pK = a.prev_idx ? *a.prev_K : 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < K; m += stride) {
+    const int64_t s = cur[m] / SEC;
+    if (m > 0 && cur[m - 1] / SEC == s) continue;  // not the sector's owner
+    T v[SEC];
+#pragma unroll
+    for (int c = 0; c < SEC; ++c) v[c] = (T)0;
+    for (long long q = m; q < K && cur[q] / SEC == s; ++q) {
+      const int32_t j = cur[q];
+      const T avg = div_rn(sums[q], nf);
+      v[j % SEC] = avg;
+      if (x) x[j] = x[j] - avg;  // one rounding after the division
+    }
+    if (dense) {
+      T* p = dense + s * SEC;
+      if ((s + 1) * SEC <= a.n_g) {
+        using V = typename Vec<T>::V;
+        constexpr int VN = Vec<T>::N;
+#pragma unroll
+        for (int h = 0; h < SEC / VN; ++h) {
+          V w;
+#pragma unroll
+          for (int c = 0; c < VN; ++c) set_comp(w, c, v[h * VN + c]);
+          reinterpret_cast<V*>(p)[h] = w;
+        }
+      } else {
+        for (int c = 0; c < SEC && s * SEC + c < a.n_g; ++c) p[c] = v[c];
+      }
+    }
   }
-  for (long long m = s_rng[2] + threadIdx.x; m < s_rng[3]; m += blockDim.x) {
-    const int32_t j = a.union_idx[m];
-    const T avg = div_rn(sums[m], nf);
-    if (dense) dense[j] = avg;
-    if (x) x[j] = x[j] - avg;  // harness.cpp:214, one rounding after the division
+  if (!dense || !a.prev_idx) return;
+  const int32_t* prev = a.prev_idx;
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < pK; m += stride) {
+    const int64_t s = prev[m] / SEC;
+    if (m > 0 && prev[m - 1] / SEC == s) continue;
+    const long long r = lower_bound_i32(cur, K, s * SEC);
+    if (r < K && cur[r] < (s + 1) * SEC) continue;  // the current union owns this sector
+    T* p = dense + s * SEC;
+    if ((s + 1) * SEC <= a.n_g) {
+      using V = typename Vec<T>::V;
+      constexpr int VN = Vec<T>::N;
+      V z;
+#pragma unroll
+      for (int c = 0; c < VN; ++c) set_comp(z, c, (T)0);
+#pragma unroll
+      for (int h = 0; h < SEC / VN; ++h) reinterpret_cast<V*>(p)[h] = z;
+    } else {
+      for (int c = 0; c < SEC && s * SEC + c < a.n_g; ++c) p[c] = (T)0;
+    }
   }
 }
 

@@ -68,6 +68,14 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     m.close()
 
 
+@pytest.fixture(params=["tma", "tile"])
+def k1_kernel(request, monkeypatch):
+    """K1 implementation: the TMA-staged persistent kernel (default) or the
+    per-tile look-back kernel (fallback for unaligned gradients)."""
+    monkeypatch.setenv("MICRO_K1_KERNEL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("n_g,n,d,delta0", [
     (10_000, 1, 0.01, 0.01),
     (10_007, 2, 0.01, 0.02),
@@ -79,12 +87,12 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     (4_095, 1, 0.3, 0.5),      # one partial tile
     (123_457, 7, 0.001, 0.03),
 ])
-def test_gpu_f32_matches_restatement(n_g, n, d, delta0):
+def test_gpu_f32_matches_restatement(n_g, n, d, delta0, k1_kernel):
     run_pair(n_g, n, d, delta0, iters=25)
 
 
 @pytest.mark.parametrize("full,ef", [(True, True), (False, False), (True, False)])
-def test_gpu_f32_modes(full, ef):
+def test_gpu_f32_modes(full, ef, k1_kernel):
     run_pair(20_000, 4, 0.01, 0.01, iters=15, full=full, ef=ef)
     run_pair(20_000, 1, 0.01, 0.01, iters=15, full=full, ef=ef)
 
@@ -97,7 +105,7 @@ def test_gpu_density_one_threshold_zero():
 @pytest.mark.ref
 @pytest.mark.parametrize("n_g,n,d,delta0", [(10_000, 1, 0.01, 0.01), (10_007, 2, 0.01, 0.02),
                                              (12_345, 8, 0.02, 0.01), (3_001, 3, 0.1, 0.05)])
-def test_gpu_f64_matches_reference_code(n_g, n, d, delta0):
+def test_gpu_f64_matches_reference_code(n_g, n, d, delta0, k1_kernel):
     run_pair(n_g, n, d, delta0, iters=20, dtype=np.float64, oracle="reference")
 
 
