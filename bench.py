@@ -290,7 +290,9 @@ def our_arm(args, wl):
             "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world,
                        "one_worker_per_gpu": True, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
-                       "inputs": (f"{R} resident N(0,1) gradients ({\"one fresh per step\" if R >= args.warmup + args.steps else \"rotated\"}); each 4*n_g bytes > L2 (no flush needed)")
+                       "inputs": (f"{R} resident N(0,1) gradients ("
+                                  + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
+                                  + "); each 4*n_g bytes > L2 (no flush needed)")
                        if 4 * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
                        "parallelism": f"dp{world} (exclusive cyclic partitions)"},
             "density": density, "density_rel_err": density / d - 1.0,
