@@ -325,6 +325,10 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
     const int64_t want = ((int64_t)c->k_worker * c->n * 3 / 2 + 255) / 256;
     blocks = (int)std::min<int64_t>(std::max<int64_t>(want, 1), 4 * num_sms(c->dev));
   }
+  if (f.prev_idx) {
+    k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
+    CU(cudaGetLastError());
+  }
   k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
   CU(cudaGetLastError());
   if (!c->cfg.error_feedback && c->n > 1)

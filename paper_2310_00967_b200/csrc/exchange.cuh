@@ -154,14 +154,12 @@ __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long
 }
 
 // Threshold update + history (block 0), then the dense g/n maintenance with
-// whole 32-byte sectors: the dense vector is zero outside the union, so the
-// full content of every sector that the previous or the current union
-// touches is known — avg at current-union slots, 0 elsewhere.  Each touched
-// sector is written exactly once, in full, by one owner thread (the first
-// current-union entry in it, else the first previous-union entry), so there
-// is no partial-sector read-modify-write in HBM and no ordering between the
-// clear and the scatter.  The optional model update x -= avg
-// (harness.cpp:212-215) is done by the same owner for its sector's entries.
+// whole 32-byte sectors: after k_dense_clear the dense vector is zero outside
+// the current union, so the full content of every sector the union touches
+// is known — avg at union slots, 0 elsewhere.  Each such sector is written
+// once, in full, by its owner thread (its first union entry): no
+// partial-sector read-modify-write in HBM.  The optional model update
+// x -= avg (harness.cpp:212-215) is done by the same owner.
 template <typename T>
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   constexpr int SEC = 32 / (int)sizeof(T);  // elements per 32-byte sector
@@ -202,7 +200,6 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   const T* sums = (const T*)a.union_sum;
   const int32_t* cur = a.union_idx;
   const T nf = (T)a.n;
-  const long long pK = a.prev_idx ? *a.prev_K : 0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < K; m += stride) {
     const int64_t s = cur[m] / SEC;
@@ -233,24 +230,31 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
       }
     }
   }
-  if (!dense || !a.prev_idx) return;
-  const int32_t* prev = a.prev_idx;
+}
+
+// Clear the previous union's sectors of the dense g/n (whole 32-byte sectors,
+// one owner per sector).  Launched before k_finalize, which then rewrites the
+// sectors of the current union in full, so no membership test is needed.
+template <typename T>
+__global__ void __launch_bounds__(256) k_dense_clear(const int32_t* prev, const long long* prev_K,
+                                                     T* dense, int64_t n_g) {
+  constexpr int SEC = 32 / (int)sizeof(T);
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
+  const long long pK = *prev_K;
+  const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < pK; m += stride) {
     const int64_t s = prev[m] / SEC;
     if (m > 0 && prev[m - 1] / SEC == s) continue;
-    const long long r = lower_bound_i32(cur, K, s * SEC);
-    if (r < K && cur[r] < (s + 1) * SEC) continue;  // the current union owns this sector
     T* p = dense + s * SEC;
-    if ((s + 1) * SEC <= a.n_g) {
-      using V = typename Vec<T>::V;
-      constexpr int VN = Vec<T>::N;
+    if ((s + 1) * SEC <= n_g) {
       V z;
 #pragma unroll
       for (int c = 0; c < VN; ++c) set_comp(z, c, (T)0);
 #pragma unroll
       for (int h = 0; h < SEC / VN; ++h) reinterpret_cast<V*>(p)[h] = z;
     } else {
-      for (int c = 0; c < SEC && s * SEC + c < a.n_g; ++c) p[c] = (T)0;
+      for (int c = 0; c < SEC && s * SEC + c < n_g; ++c) p[c] = (T)0;
     }
   }
 }
