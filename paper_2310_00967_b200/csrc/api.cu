@@ -211,17 +211,17 @@ template <typename T, int kMode>
 int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
   static bool attr_set[64] = {false};  // per instantiation and device
   if (c->dev >= 64 || !attr_set[c->dev]) {
-    CU(cudaFuncSetAttribute(k1_tma_select<T, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes));
+    CU(cudaFuncSetAttribute(k1_tma_select<T, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmemBytes));
     if (c->dev < 64) attr_set[c->dev] = true;
   }
-  k1_tma_select<T, kMode><<<num_sms(c->dev), kTmaThreads, kTmaSmemBytes, c->stream>>>(a);
+  k1_tma_select<T, kMode><<<num_sms(c->dev), kWsThreads, kWsSmemBytes, c->stream>>>(a);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
 
 template <typename T>
 int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe) {
-  constexpr int TILE = tma_tile_elems<T>();
+  constexpr int UNIT = ws_unit_elems<T>();
   TmaSelectArgs a{};
   a.grad = grad;
   a.resid = c->resid[i];
@@ -240,9 +240,9 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
   a.status_len = c->status_len;
   a.epoch = ++c->epoch;
   a.flags = c->flags;
-  a.num_tiles = (c->n_g + TILE - 1) / TILE;
-  a.ptile_lo = ps / TILE;
-  a.ptile_hi = (pe - 1) / TILE;
+  a.num_units = (c->n_g + UNIT - 1) / UNIT;
+  a.unit_lo = ps / UNIT;
+  a.unit_hi = (pe - 1) / UNIT;
   if (c->cfg.error_feedback) return launch_k1_tma_mode<T, kWriteZeroSel>(c, a);
   if (c->n > 1) return launch_k1_tma_mode<T, kWriteAcc>(c, a);
   return launch_k1_tma_mode<T, kWriteNone>(c, a);
@@ -582,7 +582,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if (cfg->dense_output && (rc = c->alloc(&c->dense, c->n_g * c->esz))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->status, sizeof(unsigned long long) * c->status_len))) return cleanup(rc);
   if (c->use_tma) {
-    const int64_t stage = c->p_max * (int64_t)tma_tile_elems<float>() * 4 / (int64_t)c->esz;
+    const int64_t stage = c->p_max * (int64_t)tile_elems<float>() * 4 / (int64_t)c->esz;  // >= units(partition) * unit
     if ((rc = c->alloc((void**)&c->stage_idx, stage * 4))) return cleanup(rc);
     if ((rc = c->alloc(&c->stage_val, stage * c->esz))) return cleanup(rc);
   }

@@ -1,26 +1,33 @@
-// select_tma.cuh — K1, persistent TMA-staged variant (the production path).
+// select_tma.cuh — K1, persistent warp-streaming variant (the production path).
 //
 // Same semantics as k1_fused_select (select.cuh; reference harness.cpp:131,
 // sparsifier.cpp:22-37, harness.cpp:219-221), different schedule:
 //
-//  * one CTA per SM (grid = #SMs), persistent; 16 consumer warps + 1
-//    producer warp;
-//  * the producer streams e_t and G tiles (16 KB per operand) into a 4-stage
-//    shared-memory ring with cp.async.bulk (the TMA bulk-copy engine),
-//    completion tracked by mbarrier transaction counts, so 128 KB per SM are
-//    always in flight independent of what the consumers are doing;
-//  * consumers compute acc = e + eta*G, write e_{t+1} straight back to HBM
-//    (coalesced 16-byte streaming stores), compact the selected (index,
-//    value) pairs tile by tile into a per-CTA staging run (block scan, no
-//    cross-CTA dependency inside the streaming loop);
-//  * each CTA owns a contiguous, balanced slice of the partition's tiles (so
-//    its staged run is globally ordered) plus a slice of the other tiles;
-//    after its partition slice it publishes its count, resolves its global
-//    offset with ONE decoupled look-back over the #SMs CTAs, and copies its
-//    run into place while the producer keeps prefetching.
+//  * one CTA per SM (grid = #SMs), 8 warps, every warp an independent
+//    streaming engine over its own contiguous range of the vector;
+//  * each warp runs its own 4-stage shared-memory ring: its lane 0 streams
+//    2 KB units of e_t and G with cp.async.bulk (the TMA bulk-copy engine),
+//    completion tracked by per-warp mbarrier transaction counts, and refills
+//    a stage as soon as the warp has read it — 16 KB per warp, 128 KB per SM
+//    in flight, with no cross-warp synchronisation in the streaming loop;
+//  * the warp computes acc = e + eta*G with explicitly rounded arithmetic,
+//    writes e_{t+1} straight back with coalesced 16-byte streaming stores,
+//    and compacts selected (index, value) pairs with one packed warp scan
+//    per unit into its own staged run (ordered: warps own contiguous,
+//    balanced slices of the partition, in (CTA, warp) order);
+//  * after the partition slices every CTA sums its warps' runs, resolves its
+//    global offset with ONE decoupled look-back over the #SMs CTAs, and each
+//    warp copies its run into place; then the warps stream the units outside
+//    the partition (accumulate only).
 //
-// Cost per worker: 12*n_g bytes (read e, G; write e) + 8 bytes per selected
-// pair + 16 bytes per pair of staging round trip (0.16 B/elem at d = 1%).
+// ncu on the first TMA version (one CTA-wide ring, 16 consumer warps, a
+// block scan + barrier per 16 KB tile) showed 56 instructions per element
+// and an ALU pipe at 68 %: the consumers, not HBM, were the limit.  Here the
+// inner loop is ~8 instructions per element and warps never wait on each
+// other while streaming.
+//
+// Bytes per worker: 12*n_g (read e, G; write e) + 8 per selected pair
+// + 16 per pair for the staging round trip (0.16 B/elem at d = 1%).
 #pragma once
 
 #include "common.cuh"
@@ -28,16 +35,15 @@
 
 namespace micro {
 
-constexpr int kTmaConsumerWarps = 16;
-constexpr int kTmaConsumers = kTmaConsumerWarps * 32;       // 512
-constexpr int kTmaThreads = kTmaConsumers + 32;             // + producer warp
-constexpr int kTmaStages = 4;
-constexpr int kTmaTileBytes = 16384;                        // per operand per stage
-constexpr int kTmaSmemBytes = kTmaStages * 2 * kTmaTileBytes + 1024;
+constexpr int kWsWarps = 8;
+constexpr int kWsThreads = kWsWarps * 32;
+constexpr int kWsStages = 4;
+constexpr int kWsUnitBytes = 2048;  // per operand per stage per warp
+constexpr int kWsSmemBytes = kWsWarps * kWsStages * 2 * kWsUnitBytes + kWsWarps * kWsStages * 8 + 128;
 
 template <typename T>
-__host__ __device__ constexpr int tma_tile_elems() {
-  return kTmaTileBytes / (int)sizeof(T);  // 4096 fp32 / 2048 fp64
+__host__ __device__ constexpr int ws_unit_elems() {
+  return kWsUnitBytes / (int)sizeof(T);  // 512 fp32 / 256 fp64
 }
 
 struct TmaSelectArgs {
@@ -51,14 +57,14 @@ struct TmaSelectArgs {
   void* sel_val;
   int64_t cap;
   long long* count;
-  int32_t* stage_idx;          // staging runs, (ptile_hi - ptile_lo + 1) * TILE pairs
+  int32_t* stage_idx;          // staging runs, (unit_hi - unit_lo + 1) * UNIT pairs
   void* stage_val;
   unsigned long long* status;  // >= status_len words
   int64_t status_len;
   unsigned int epoch;
   int* flags;
-  int64_t num_tiles;
-  int64_t ptile_lo, ptile_hi;  // tiles intersecting [p_start, p_end)
+  int64_t num_units;
+  int64_t unit_lo, unit_hi;    // units intersecting [p_start, p_end)
 };
 
 // ---- mbarrier / bulk-copy primitives (inline PTX, sm_90+) ----
@@ -71,9 +77,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -91,151 +94,153 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void consumer_sync() {  // named barrier over the 512 consumer threads
-  asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Tile sequence of CTA b: its slice of the partition tiles, then its slice of
-// the remaining tiles.
-struct TilePlan {
-  int64_t p_lo, p_n;  // partition tiles [p_lo, p_lo + p_n)
-  int64_t o_lo, o_n;  // index range in the outside-tile list
+__device__ __forceinline__ float nan_probe(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
+__device__ __forceinline__ double nan_probe(double g, double acc) { return __fma_rn(g, 0.0, acc); }
+
+// The units of warp gw (of GW): its slice of the partition units, then its
+// slice of the remaining units.
+struct WarpPlan {
+  int64_t p_first, p_n;  // partition units [p_first, p_first + p_n)
+  int64_t o_first, o_n;  // index range in the outside-unit list
   int64_t gap_lo, gap_n;
   __device__ __forceinline__ int64_t count() const { return p_n + o_n; }
-  __device__ __forceinline__ int64_t tile(int64_t k) const {
-    if (k < p_n) return p_lo + k;
-    const int64_t q = o_lo + (k - p_n);
-    return q < gap_lo ? q : q + gap_n;  // skip over the partition tiles
+  __device__ __forceinline__ int64_t unit(int64_t k) const {
+    if (k < p_n) return p_first + k;
+    const int64_t q = o_first + (k - p_n);
+    return q < gap_lo ? q : q + gap_n;
   }
 };
 
-__device__ __forceinline__ TilePlan make_plan(const TmaSelectArgs& a, int b, int G) {
-  TilePlan pl;
-  const int64_t P = a.ptile_hi - a.ptile_lo + 1;
-  const int64_t O = a.num_tiles - P;
-  const int64_t p0 = P * b / G, p1 = P * (b + 1) / G;
-  const int64_t o0 = O * b / G, o1 = O * (b + 1) / G;
-  pl.p_lo = a.ptile_lo + p0;
-  pl.p_n = p1 - p0;
-  pl.o_lo = o0;
-  pl.o_n = o1 - o0;
-  pl.gap_lo = a.ptile_lo;
-  pl.gap_n = P;
-  return pl;
-}
-
 template <typename T, int kMode>
-__global__ void __launch_bounds__(kTmaThreads, 1) k1_tma_select(TmaSelectArgs a) {
+__global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
-  constexpr int TILE = tma_tile_elems<T>();
-  constexpr int VPT = TILE / VN / kTmaConsumers;  // vectors per consumer thread per operand (2)
-  static_assert(VPT * VN * kTmaConsumers == TILE, "tile/threads mismatch");
+  constexpr int UE = ws_unit_elems<T>();
+  constexpr int VPL = UE / VN / 32;  // vectors per lane per operand per unit (4)
+  static_assert(VPL * VN * 32 == UE, "unit/lanes mismatch");
+  static_assert(VPL <= 4, "packed 8-bit counts hold 4 vectors");
 
   extern __shared__ __align__(1024) unsigned char smem[];
-  T* s_e = reinterpret_cast<T*>(smem);                                  // [stages][TILE]
-  T* s_g = reinterpret_cast<T*>(smem + kTmaStages * kTmaTileBytes);     // [stages][TILE]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kTmaStages * kTmaTileBytes);
-  uint64_t* empty = full + kTmaStages;
-  __shared__ unsigned int s_warp[2][kTmaConsumerWarps];
+  __shared__ long long s_run[kWsWarps];
   __shared__ long long s_excl;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
-  const TilePlan pl = make_plan(a, b, G);
-  const int64_t ntiles = pl.count();
-  const int64_t n_g = a.n_g;
+  const int64_t gw = (int64_t)b * kWsWarps + w, GW = (int64_t)G * kWsWarps;
 
-  if (tid == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kTmaConsumerWarps);
-    }
+  // per-warp ring: [stage][e | g][UE]
+  T* ring = reinterpret_cast<T*>(smem + (size_t)w * kWsStages * 2 * kWsUnitBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kWsWarps * kWsStages * 2 * kWsUnitBytes) +
+                   w * kWsStages;
+
+  WarpPlan pl;
+  {
+    const int64_t P = a.unit_hi - a.unit_lo + 1, O = a.num_units - P;
+    const int64_t p0 = P * gw / GW, p1 = P * (gw + 1) / GW;
+    const int64_t o0 = O * gw / GW, o1 = O * (gw + 1) / GW;
+    pl.p_first = a.unit_lo + p0;
+    pl.p_n = p1 - p0;
+    pl.o_first = o0;
+    pl.o_n = o1 - o0;
+    pl.gap_lo = a.unit_lo;
+    pl.gap_n = P;
+  }
+  const int64_t nk = pl.count();
+  const int64_t n_g = a.n_g;
+  const T* __restrict__ Gp = (const T*)a.grad;
+  T* __restrict__ E = (T*)a.resid;
+
+  if (lane == 0) {
+    for (int s = 0; s < kWsStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  __syncwarp();
 
-  if (warp == kTmaConsumerWarps) {
-    // ================= producer warp: one elected lane streams tiles =========
-    if (lane == 0) {
-      const T* E = (const T*)a.resid;
-      const T* Gp = (const T*)a.grad;
-      for (int64_t k = 0; k < ntiles; ++k) {
-        const int s = (int)(k % kTmaStages);
-        const uint32_t round = (uint32_t)(k / kTmaStages);
-        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int64_t tile = pl.tile(k);
-        const int64_t base = tile * TILE;
-        int64_t elems = n_g - base < TILE ? n_g - base : TILE;
-        const uint32_t bytes = (uint32_t)((elems * (int64_t)sizeof(T)) & ~(int64_t)15);
-        mbar_arrive_expect_tx(&full[s], 2 * bytes);
-        if (bytes) {
-          bulk_g2s(s_e + (size_t)s * TILE, E + base, bytes, &full[s]);
-          bulk_g2s(s_g + (size_t)s * TILE, Gp + base, bytes, &full[s]);
-        }
-      }
+  auto issue = [&](int64_t k) {  // lane 0 only
+    const int s = (int)(k % kWsStages);
+    const int64_t base = pl.unit(k) * UE;
+    const int64_t elems = n_g - base < UE ? n_g - base : UE;
+    const uint32_t bytes = (uint32_t)((elems * (int64_t)sizeof(T)) & ~(int64_t)15);
+    mbar_arrive_expect_tx(&full[s], 2 * bytes);
+    if (bytes) {
+      bulk_g2s(ring + (size_t)(2 * s) * UE, E + base, bytes, &full[s]);
+      bulk_g2s(ring + (size_t)(2 * s + 1) * UE, Gp + base, bytes, &full[s]);
     }
-    return;
-  }
+  };
+  if (lane == 0)
+    for (int64_t k = 0; k < nk && k < kWsStages; ++k) issue(k);
 
-  // ================= consumers ===============================================
   const double delta = *a.delta;
   const T thr = threshold_as(delta, (T*)nullptr);
   const T eta = (T)a.eta;
-  T* __restrict__ E = (T*)a.resid;
-  const T* __restrict__ Gp = (const T*)a.grad;
   int32_t* __restrict__ st_idx = a.stage_idx;
   T* __restrict__ st_val = (T*)a.stage_val;
-  const int64_t run_base = (pl.p_lo - a.ptile_lo) * TILE;  // this CTA's staging run
-  long long run = 0;                                       // pairs staged so far
-  bool bad = false;
+  const int64_t run_base = (pl.p_first - a.unit_lo) * UE;  // this warp's staging run
+  long long run = 0;
+  T probe = (T)0;  // becomes NaN iff some G is Inf/NaN
 
-  for (int64_t k = 0; k < ntiles; ++k) {
-    const int s = (int)(k % kTmaStages);
-    const uint32_t round = (uint32_t)(k / kTmaStages);
-    const int64_t tile = pl.tile(k);
-    const int64_t base = tile * TILE;
-    const int64_t elems = n_g - base < TILE ? n_g - base : TILE;
-    const int64_t vec_elems = ((elems * (int64_t)sizeof(T)) & ~(int64_t)15) / (int64_t)sizeof(T);
-    mbar_wait(&full[s], round & 1);
-
-    V e[VPT];
-    unsigned mask[VPT];
+  // One unit: wait, read the stage, refill it, accumulate, store e_{t+1},
+  // and (partition units) compact the selections into the warp's run.
+  auto process = [&](int64_t k, bool in_partition) {
+    const int s = (int)(k % kWsStages);
+    const int64_t base = pl.unit(k) * UE;
+    const int64_t elems = n_g - base < UE ? n_g - base : UE;
+    const int vec_elems = (int)(((elems * (int64_t)sizeof(T)) & ~(int64_t)15) / (int64_t)sizeof(T));
+    mbar_wait(&full[s], (uint32_t)(k / kWsStages) & 1u);
+    const V* se = reinterpret_cast<const V*>(ring + (size_t)(2 * s) * UE);
+    const V* sg = reinterpret_cast<const V*>(ring + (size_t)(2 * s + 1) * UE);
+    V e[VPL], g[VPL];
 #pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const int v = i * kTmaConsumers + tid;
-      const int64_t off = (int64_t)v * VN;
-      V g;
+    for (int i = 0; i < VPL; ++i) {
+      const int off = (i * 32 + lane) * VN;
       if (off + VN <= vec_elems) {
-        e[i] = reinterpret_cast<const V*>(s_e + (size_t)s * TILE)[v];
-        g = reinterpret_cast<const V*>(s_g + (size_t)s * TILE)[v];
-      } else {  // the vector's tail (last tile only): straight from global
+        e[i] = se[i * 32 + lane];
+        g[i] = sg[i * 32 + lane];
+      } else {  // the last unit's tail: straight from global
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
           const bool in = off + c < elems;
           set_comp(e[i], c, in ? E[base + off + c] : (T)0);
-          set_comp(g, c, in ? Gp[base + off + c] : (T)0);
+          set_comp(g[i], c, in ? Gp[base + off + c] : (T)0);
         }
-      }
-      mask[i] = 0;
-#pragma unroll
-      for (int c = 0; c < VN; ++c) {
-        const int64_t j = base + off + c;
-        const T gv = comp(g, c);
-        bad |= (off + c < elems) && !finite(gv);
-        const T acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
-        set_comp(e[i], c, acc);
-        mask[i] |= (unsigned)((j >= a.p_start) && (j < a.p_end) && (absx(acc) > thr)) << c;
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
-
+    if (lane == 0 && k + kWsStages < nk) {
+      fence_proxy_async_smem();  // our generic reads of stage s precede the async refill
+      issue(k + kWsStages);
+    }
+    // warp-uniform classification of the unit against the partition
+    const bool all_in = in_partition && base >= a.p_start && base + elems <= a.p_end;
+    unsigned mask[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      mask[i] = 0;
+      const int off = (i * 32 + lane) * VN;
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        const T gv = comp(g[i], c);
+        probe = nan_probe(gv, probe);
+        const T acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
+        set_comp(e[i], c, acc);
+        if (in_partition) {
+          bool sel = absx(acc) > thr;
+          if (!all_in) {
+            const int64_t j = base + off + c;
+            sel = sel && j >= a.p_start && j < a.p_end;
+          }
+          mask[i] |= (unsigned)sel << c;
+        }
+      }
+    }
     if (kMode != kWriteNone) {
 #pragma unroll
-      for (int i = 0; i < VPT; ++i) {
-        const int v = i * kTmaConsumers + tid;
-        const int64_t off = (int64_t)v * VN;
+      for (int i = 0; i < VPL; ++i) {
+        const int off = (i * 32 + lane) * VN;
         V out = e[i];
         if (kMode == kWriteZeroSel) {
 #pragma unroll
@@ -251,91 +256,80 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k1_tma_select(TmaSelectArgs a)
         }
       }
     }
-
-    if (k < pl.p_n) {
-      // ---- ordered compaction of this partition tile into the CTA's run ----
+    if (in_partition) {
+      // order inside a unit: (vector i, lane, component c); per-lane counts of
+      // the VPL vectors packed as 8-bit fields (warp totals <= 128)
       unsigned packed = 0;
 #pragma unroll
-      for (int i = 0; i < VPT; ++i) packed |= (unsigned)__popc(mask[i]) << (16 * i);
+      for (int i = 0; i < VPL; ++i) packed |= (unsigned)__popc(mask[i]) << (8 * i);
       unsigned incl = packed;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      const int par = (int)(k & 1);
-      if (lane == 31) s_warp[par][warp] = incl;
-      consumer_sync();
-      unsigned wpre = 0, tot = 0;
+      const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+      const unsigned excl = incl - packed;
+      unsigned cb = 0;
 #pragma unroll
-      for (int w = 0; w < kTmaConsumerWarps; ++w) {
-        const unsigned x = s_warp[par][w];
-        wpre += w < warp ? x : 0u;
-        tot += x;
+      for (int i = 0; i < VPL; ++i) {
+        if (mask[i]) {
+          long long pos = run_base + run + cb + ((excl >> (8 * i)) & 0xFFu);
+          const int64_t j0 = base + (i * 32 + lane) * VN;
+#pragma unroll
+          for (int c = 0; c < VN; ++c)
+            if (mask[i] & (1u << c)) {
+              st_idx[pos] = (int32_t)(j0 + c);
+              st_val[pos] = comp(e[i], c);
+              ++pos;
+            }
+        }
+        cb += (tot >> (8 * i)) & 0xFFu;
       }
-      const unsigned excl = wpre + incl - packed;
-      int cbase[VPT];
-      int tcount = 0;
-#pragma unroll
-      for (int i = 0; i < VPT; ++i) {
-        cbase[i] = tcount;
-        tcount += (int)((tot >> (16 * i)) & 0xFFFFu);
-      }
-#pragma unroll
-      for (int i = 0; i < VPT; ++i) {
-        if (!mask[i]) continue;
-        long long pos = run_base + run + cbase[i] + (long long)((excl >> (16 * i)) & 0xFFFFu);
-        const int64_t j0 = base + (int64_t)(i * kTmaConsumers + tid) * VN;
-#pragma unroll
-        for (int c = 0; c < VN; ++c)
-          if (mask[i] & (1u << c)) {
-            st_idx[pos] = (int32_t)(j0 + c);
-            st_val[pos] = comp(e[i], c);
-            ++pos;
-          }
-      }
-      run += tcount;
+      run += cb;
     }
+  };
 
-    if (k + 1 == pl.p_n || (pl.p_n == 0 && k == 0)) {
-      // ---- partition slice done: global offset by one look-back, copy run ----
-      consumer_sync();  // staged pairs of all warps written
-      if (warp == 0) {
-        const long long ex = lookback(a.status, b, (unsigned long long)run, a.epoch, lane);
-        if (lane == 0) {
-          s_excl = ex;
-          if (b == G - 1) {
-            const long long total = ex + run;
-            *a.count = total;
-            if (total > a.cap) atomicOr(a.flags, 2);
-            const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
-            for (int64_t q = G; q < a.status_len; ++q) st_relaxed_u64(&a.status[q], ep);
-          }
-        }
-      }
-      consumer_sync();
-      const long long dst0 = s_excl;
-      int32_t* __restrict__ out_idx = a.sel_idx;
-      T* __restrict__ out_val = (T*)a.sel_val;
-      for (long long m = tid; m < run; m += kTmaConsumers) {
-        const long long d = dst0 + m;
-        if (d < a.cap) {
-          out_idx[d] = st_idx[run_base + m];
-          out_val[d] = st_val[run_base + m];
-        }
+  int64_t k = 0;
+  for (; k < pl.p_n; ++k) process(k, true);
+
+  // ---- partition slices done: CTA offset by one look-back, runs into place ----
+  if (lane == 0) s_run[w] = run;
+  __syncthreads();
+  if (w == 0) {
+    long long cta = 0;
+#pragma unroll
+    for (int q = 0; q < kWsWarps; ++q) cta += s_run[q];
+    const long long ex = lookback(a.status, b, (unsigned long long)cta, a.epoch, lane);
+    if (lane == 0) {
+      s_excl = ex;
+      if (b == G - 1) {
+        const long long total = ex + cta;
+        *a.count = total;
+        if (total > a.cap) atomicOr(a.flags, 2);
+        const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
+        for (int64_t q = G; q < a.status_len; ++q) st_relaxed_u64(&a.status[q], ep);
       }
     }
   }
-  if (ntiles == 0 && warp == 0) {  // CTA without tiles still closes its link of the chain
-    const long long ex = lookback(a.status, b, 0ull, a.epoch, lane);
-    if (lane == 0 && b == G - 1) {
-      *a.count = ex;
-      if (ex > a.cap) atomicOr(a.flags, 2);
-      const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
-      for (int64_t q = G; q < a.status_len; ++q) st_relaxed_u64(&a.status[q], ep);
+  __syncthreads();
+  {
+    long long dst0 = s_excl;
+    for (int q = 0; q < w; ++q) dst0 += s_run[q];
+    int32_t* __restrict__ out_idx = a.sel_idx;
+    T* __restrict__ out_val = (T*)a.sel_val;
+    for (long long m = lane; m < run; m += 32) {
+      const long long d = dst0 + m;
+      if (d < a.cap) {
+        out_idx[d] = st_idx[run_base + m];
+        out_val[d] = st_val[run_base + m];
+      }
     }
   }
-  if (bad) atomicOr(a.flags, 1);
+
+  for (; k < nk; ++k) process(k, false);
+
+  if (probe != probe) atomicOr(a.flags, 1);
 }
 
 }  // namespace micro
