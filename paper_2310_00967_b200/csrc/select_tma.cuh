@@ -30,6 +30,8 @@
 // + 16 per pair for the staging round trip (0.16 B/elem at d = 1%).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "select.cuh"
 
@@ -185,11 +187,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
 
   // One unit: wait, read the stage, refill it, accumulate, store e_{t+1},
   // and (partition units) compact the selections into the warp's run.
-  auto process = [&](int64_t k, bool in_partition) {
+  // FULL: a whole unit (every unit but the vector's last) — no bounds tests;
+  // SEL: a partition unit; CHECK: per-element partition-range test (the two
+  // boundary units of the partition only).
+  auto body = [&](int64_t k, int64_t base, int elems, auto kFull, auto kSel, auto kCheck) {
+    constexpr bool FULL = decltype(kFull)::value;
+    constexpr bool SEL = decltype(kSel)::value;
+    constexpr bool CHECK = decltype(kCheck)::value;
     const int s = (int)(k % kWsStages);
-    const int64_t base = pl.unit(k) * UE;
-    const int64_t elems = n_g - base < UE ? n_g - base : UE;
-    const int vec_elems = (int)(((elems * (int64_t)sizeof(T)) & ~(int64_t)15) / (int64_t)sizeof(T));
+    const int vec_elems = FULL ? UE : (int)((elems * (int)sizeof(T)) & ~15) / (int)sizeof(T);
     mbar_wait(&full[s], (uint32_t)(k / kWsStages) & 1u);
     const V* se = reinterpret_cast<const V*>(ring + (size_t)(2 * s) * UE);
     const V* sg = reinterpret_cast<const V*>(ring + (size_t)(2 * s + 1) * UE);
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int off = (i * 32 + lane) * VN;
-      if (off + VN <= vec_elems) {
+      if (FULL || off + VN <= vec_elems) {
         e[i] = se[i * 32 + lane];
         g[i] = sg[i * 32 + lane];
       } else {  // the last unit's tail: straight from global
@@ -214,8 +220,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
       fence_proxy_async_smem();  // our generic reads of stage s precede the async refill
       issue(k + kWsStages);
     }
-    // warp-uniform classification of the unit against the partition
-    const bool all_in = in_partition && base >= a.p_start && base + elems <= a.p_end;
     unsigned mask[VPL];
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
@@ -227,9 +231,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
         probe = nan_probe(gv, probe);
         const T acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
         set_comp(e[i], c, acc);
-        if (in_partition) {
+        if (SEL) {
           bool sel = absx(acc) > thr;
-          if (!all_in) {
+          if (CHECK) {
             const int64_t j = base + off + c;
             sel = sel && j >= a.p_start && j < a.p_end;
           }
@@ -242,12 +246,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
       for (int i = 0; i < VPL; ++i) {
         const int off = (i * 32 + lane) * VN;
         V out = e[i];
-        if (kMode == kWriteZeroSel) {
+        if (kMode == kWriteZeroSel && SEL) {
 #pragma unroll
           for (int c = 0; c < VN; ++c)
             if (mask[i] & (1u << c)) set_comp(out, c, (T)0);
         }
-        if (off + VN <= elems) {
+        if (FULL || off + VN <= elems) {
           st_stream(reinterpret_cast<V*>(E + base + off), out);
         } else {
 #pragma unroll
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
         }
       }
     }
-    if (in_partition) {
+    if (SEL) {
       // order inside a unit: (vector i, lane, component c); per-lane counts of
       // the VPL vectors packed as 8-bit fields (warp totals <= 128)
       unsigned packed = 0;
@@ -269,24 +273,41 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
         if (lane >= o) incl += y;
       }
       const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
-      const unsigned excl = incl - packed;
-      unsigned cb = 0;
+      if (tot) {
+        const unsigned excl = incl - packed;
+        unsigned cb = 0;
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        if (mask[i]) {
-          long long pos = run_base + run + cb + ((excl >> (8 * i)) & 0xFFu);
-          const int64_t j0 = base + (i * 32 + lane) * VN;
+        for (int i = 0; i < VPL; ++i) {
+          if (mask[i]) {
+            long long pos = run_base + run + cb + ((excl >> (8 * i)) & 0xFFu);
+            const int64_t j0 = base + (i * 32 + lane) * VN;
 #pragma unroll
-          for (int c = 0; c < VN; ++c)
-            if (mask[i] & (1u << c)) {
-              st_idx[pos] = (int32_t)(j0 + c);
-              st_val[pos] = comp(e[i], c);
-              ++pos;
-            }
+            for (int c = 0; c < VN; ++c)
+              if (mask[i] & (1u << c)) {
+                st_idx[pos] = (int32_t)(j0 + c);
+                st_val[pos] = comp(e[i], c);
+                ++pos;
+              }
+          }
+          cb += (tot >> (8 * i)) & 0xFFu;
         }
-        cb += (tot >> (8 * i)) & 0xFFu;
+        run += cb;
       }
-      run += cb;
+    }
+  };
+  using TT = std::true_type;
+  using FF = std::false_type;
+  auto process = [&](int64_t k, bool in_partition) {
+    const int64_t base = pl.unit(k) * UE;
+    const int elems = n_g - base < UE ? (int)(n_g - base) : UE;
+    const bool full_unit = elems == UE;
+    if (in_partition) {
+      const bool all_in = base >= a.p_start && base + elems <= a.p_end;
+      if (full_unit && all_in) body(k, base, elems, TT{}, TT{}, FF{});
+      else body(k, base, elems, FF{}, TT{}, TT{});
+    } else {
+      if (full_unit) body(k, base, elems, TT{}, FF{}, FF{});
+      else body(k, base, elems, FF{}, FF{}, FF{});
     }
   };
 
