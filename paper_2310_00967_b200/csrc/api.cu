@@ -164,6 +164,7 @@ struct micro_ctx {
   int64_t p_max = 0;
   int64_t status_len = 0;
   bool use_tma = true;          // K1 = k1_tma_select (MICRO_K1_KERNEL=tile: k1_fused_select)
+  int k1_cfg = 0;               // streaming configuration (MICRO_K1_CFG)
   int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
   void* stage_val = nullptr;
   unsigned int* ticket = nullptr;
@@ -207,21 +208,43 @@ int check_poison(micro_ctx* c) {
   return MICRO_OK;
 }
 
-template <typename T, int kMode>
-int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
+// K1 streaming configurations (warps, stages, unit bytes); MICRO_K1_CFG picks one.
+using K1Cfg0 = WsCfg<8, 4, 2048>;
+using K1Cfg1 = WsCfg<16, 4, 1024>;
+using K1Cfg2 = WsCfg<16, 2, 2048>;
+using K1Cfg3 = WsCfg<12, 3, 2048>;
+using K1Cfg4 = WsCfg<32, 2, 1024>;
+constexpr int kNumK1Cfg = 5;
+
+template <typename T, int kMode, class Cfg>
+int launch_k1_tma_cfg(micro_ctx* c, TmaSelectArgs a) {
   static bool attr_set[64] = {false};  // per instantiation and device
   if (c->dev >= 64 || !attr_set[c->dev]) {
-    CU(cudaFuncSetAttribute(k1_tma_select<T, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWsSmemBytes));
+    CU(cudaFuncSetAttribute(k1_tma_select<T, kMode, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     if (c->dev < 64) attr_set[c->dev] = true;
   }
-  k1_tma_select<T, kMode><<<num_sms(c->dev), kWsThreads, kWsSmemBytes, c->stream>>>(a);
+  constexpr int UNIT = Cfg::UNIT_BYTES / (int)sizeof(T);
+  a.num_units = (c->n_g + UNIT - 1) / UNIT;
+  a.unit_lo = a.p_start / UNIT;
+  a.unit_hi = (a.p_end - 1) / UNIT;
+  k1_tma_select<T, kMode, Cfg><<<num_sms(c->dev), Cfg::THREADS, Cfg::SMEM, c->stream>>>(a);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
 
+template <typename T, int kMode>
+int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
+  switch (c->k1_cfg) {
+    case 1: return launch_k1_tma_cfg<T, kMode, K1Cfg1>(c, a);
+    case 2: return launch_k1_tma_cfg<T, kMode, K1Cfg2>(c, a);
+    case 3: return launch_k1_tma_cfg<T, kMode, K1Cfg3>(c, a);
+    case 4: return launch_k1_tma_cfg<T, kMode, K1Cfg4>(c, a);
+    default: return launch_k1_tma_cfg<T, kMode, K1Cfg0>(c, a);
+  }
+}
+
 template <typename T>
 int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe) {
-  constexpr int UNIT = ws_unit_elems<T>();
   TmaSelectArgs a{};
   a.grad = grad;
   a.resid = c->resid[i];
@@ -240,9 +263,6 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
   a.status_len = c->status_len;
   a.epoch = ++c->epoch;
   a.flags = c->flags;
-  a.num_units = (c->n_g + UNIT - 1) / UNIT;
-  a.unit_lo = ps / UNIT;
-  a.unit_hi = (pe - 1) / UNIT;
   if (c->cfg.error_feedback) return launch_k1_tma_mode<T, kWriteZeroSel>(c, a);
   if (c->n > 1) return launch_k1_tma_mode<T, kWriteAcc>(c, a);
   return launch_k1_tma_mode<T, kWriteNone>(c, a);
@@ -553,6 +573,9 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   {
     const char* k = std::getenv("MICRO_K1_KERNEL");
     c->use_tma = !(k && std::strcmp(k, "tile") == 0);
+    const char* cf = std::getenv("MICRO_K1_CFG");
+    c->k1_cfg = cf ? std::atoi(cf) : 0;
+    if (c->k1_cfg < 0 || c->k1_cfg >= kNumK1Cfg) c->k1_cfg = 0;
   }
   const int nbuf = c->n == 1 ? 2 : 1;
   c->resid.assign(c->n_local, nullptr);

@@ -37,16 +37,16 @@
 
 namespace micro {
 
-constexpr int kWsWarps = 8;
-constexpr int kWsThreads = kWsWarps * 32;
-constexpr int kWsStages = 4;
-constexpr int kWsUnitBytes = 2048;  // per operand per stage per warp
-constexpr int kWsSmemBytes = kWsWarps * kWsStages * 2 * kWsUnitBytes + kWsWarps * kWsStages * 8 + 128;
-
-template <typename T>
-__host__ __device__ constexpr int ws_unit_elems() {
-  return kWsUnitBytes / (int)sizeof(T);  // 512 fp32 / 256 fp64
-}
+// Streaming configuration: warps per CTA, ring stages per warp, bytes per
+// unit (per operand).  Shared memory = WARPS * STAGES * 2 * UNIT_BYTES.
+template <int WARPS_, int STAGES_, int UNIT_BYTES_>
+struct WsCfg {
+  static constexpr int WARPS = WARPS_;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int UNIT_BYTES = UNIT_BYTES_;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int SMEM = WARPS * STAGES * 2 * UNIT_BYTES + WARPS * STAGES * 8 + 128;
+};
 
 struct TmaSelectArgs {
   const void* grad;
@@ -105,23 +105,24 @@ __device__ __forceinline__ double nan_probe(double g, double acc) { return __fma
 
 // The units of warp gw (of GW): its slice of the partition units, then its
 // slice of the remaining units.
-struct WarpPlan {
-  int64_t p_first, p_n;  // partition units [p_first, p_first + p_n)
-  int64_t o_first, o_n;  // index range in the outside-unit list
-  int64_t gap_lo, gap_n;
-  __device__ __forceinline__ int64_t count() const { return p_n + o_n; }
-  __device__ __forceinline__ int64_t unit(int64_t k) const {
+struct WarpPlan {  // unit indices fit int32: n_g < 2^31 (checked on the host)
+  int p_first, p_n;  // partition units [p_first, p_first + p_n)
+  int o_first, o_n;  // index range in the outside-unit list
+  int gap_lo, gap_n;
+  __device__ __forceinline__ int count() const { return p_n + o_n; }
+  __device__ __forceinline__ int unit(int k) const {
     if (k < p_n) return p_first + k;
-    const int64_t q = o_first + (k - p_n);
+    const int q = o_first + (k - p_n);
     return q < gap_lo ? q : q + gap_n;
   }
 };
 
-template <typename T, int kMode>
-__global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) {
+template <typename T, int kMode, class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
-  constexpr int UE = ws_unit_elems<T>();
+  constexpr int kWsWarps = Cfg::WARPS, kWsStages = Cfg::STAGES, kWsUnitBytes = Cfg::UNIT_BYTES;
+  constexpr int UE = kWsUnitBytes / (int)sizeof(T);
   constexpr int VPL = UE / VN / 32;  // vectors per lane per operand per unit (4)
   static_assert(VPL * VN * 32 == UE, "unit/lanes mismatch");
   static_assert(VPL <= 4, "packed 8-bit counts hold 4 vectors");
@@ -144,15 +145,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
     const int64_t P = a.unit_hi - a.unit_lo + 1, O = a.num_units - P;
     const int64_t p0 = P * gw / GW, p1 = P * (gw + 1) / GW;
     const int64_t o0 = O * gw / GW, o1 = O * (gw + 1) / GW;
-    pl.p_first = a.unit_lo + p0;
-    pl.p_n = p1 - p0;
-    pl.o_first = o0;
-    pl.o_n = o1 - o0;
-    pl.gap_lo = a.unit_lo;
-    pl.gap_n = P;
+    pl.p_first = (int)(a.unit_lo + p0);
+    pl.p_n = (int)(p1 - p0);
+    pl.o_first = (int)o0;
+    pl.o_n = (int)(o1 - o0);
+    pl.gap_lo = (int)a.unit_lo;
+    pl.gap_n = (int)P;
   }
-  const int64_t nk = pl.count();
-  const int64_t n_g = a.n_g;
+  const int nk = pl.count();
+  const int n_g = (int)a.n_g;
+  const int p_start = (int)a.p_start, p_end = (int)a.p_end;
   const T* __restrict__ Gp = (const T*)a.grad;
   T* __restrict__ E = (T*)a.resid;
 
@@ -162,11 +164,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
   }
   __syncwarp();
 
-  auto issue = [&](int64_t k) {  // lane 0 only
-    const int s = (int)(k % kWsStages);
-    const int64_t base = pl.unit(k) * UE;
-    const int64_t elems = n_g - base < UE ? n_g - base : UE;
-    const uint32_t bytes = (uint32_t)((elems * (int64_t)sizeof(T)) & ~(int64_t)15);
+  auto issue = [&](int k) {  // lane 0 only
+    const int s = k % kWsStages;
+    const int base = pl.unit(k) * UE;
+    const int elems = n_g - base < UE ? n_g - base : UE;
+    const uint32_t bytes = (uint32_t)(elems * (int)sizeof(T)) & ~15u;
     mbar_arrive_expect_tx(&full[s], 2 * bytes);
     if (bytes) {
       bulk_g2s(ring + (size_t)(2 * s) * UE, E + base, bytes, &full[s]);
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
     }
   };
   if (lane == 0)
-    for (int64_t k = 0; k < nk && k < kWsStages; ++k) issue(k);
+    for (int k = 0; k < nk && k < kWsStages; ++k) issue(k);
 
   const double delta = *a.delta;
   const T thr = threshold_as(delta, (T*)nullptr);
@@ -190,11 +192,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
   // FULL: a whole unit (every unit but the vector's last) — no bounds tests;
   // SEL: a partition unit; CHECK: per-element partition-range test (the two
   // boundary units of the partition only).
-  auto body = [&](int64_t k, int64_t base, int elems, auto kFull, auto kSel, auto kCheck) {
+  auto body = [&](int k, int base, int elems, auto kFull, auto kSel, auto kCheck) {
     constexpr bool FULL = decltype(kFull)::value;
     constexpr bool SEL = decltype(kSel)::value;
     constexpr bool CHECK = decltype(kCheck)::value;
-    const int s = (int)(k % kWsStages);
+    const int s = k % kWsStages;
     const int vec_elems = FULL ? UE : (int)((elems * (int)sizeof(T)) & ~15) / (int)sizeof(T);
     mbar_wait(&full[s], (uint32_t)(k / kWsStages) & 1u);
     const V* se = reinterpret_cast<const V*>(ring + (size_t)(2 * s) * UE);
@@ -234,8 +236,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
         if (SEL) {
           bool sel = absx(acc) > thr;
           if (CHECK) {
-            const int64_t j = base + off + c;
-            sel = sel && j >= a.p_start && j < a.p_end;
+            const int j = base + off + c;
+            sel = sel && j >= p_start && j < p_end;
           }
           mask[i] |= (unsigned)sel << c;
         }
@@ -275,34 +277,42 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
       const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
       if (tot) {
         const unsigned excl = incl - packed;
+        unsigned any = 0;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) any |= mask[i];
+        if (any) {
         unsigned cb = 0;
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
           if (mask[i]) {
             long long pos = run_base + run + cb + ((excl >> (8 * i)) & 0xFFu);
-            const int64_t j0 = base + (i * 32 + lane) * VN;
+            const int j0 = base + (i * 32 + lane) * VN;
 #pragma unroll
             for (int c = 0; c < VN; ++c)
               if (mask[i] & (1u << c)) {
-                st_idx[pos] = (int32_t)(j0 + c);
+                st_idx[pos] = j0 + c;
                 st_val[pos] = comp(e[i], c);
                 ++pos;
               }
           }
           cb += (tot >> (8 * i)) & 0xFFu;
         }
-        run += cb;
+        }
+        unsigned sum = 0;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) sum += (tot >> (8 * i)) & 0xFFu;
+        run += sum;
       }
     }
   };
   using TT = std::true_type;
   using FF = std::false_type;
-  auto process = [&](int64_t k, bool in_partition) {
-    const int64_t base = pl.unit(k) * UE;
-    const int elems = n_g - base < UE ? (int)(n_g - base) : UE;
+  auto process = [&](int k, bool in_partition) {
+    const int base = pl.unit(k) * UE;
+    const int elems = n_g - base < UE ? n_g - base : UE;
     const bool full_unit = elems == UE;
     if (in_partition) {
-      const bool all_in = base >= a.p_start && base + elems <= a.p_end;
+      const bool all_in = base >= p_start && base + elems <= p_end;
       if (full_unit && all_in) body(k, base, elems, TT{}, TT{}, FF{});
       else body(k, base, elems, FF{}, TT{}, TT{});
     } else {
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k1_tma_select(TmaSelectArgs a) 
     }
   };
 
-  int64_t k = 0;
+  int k = 0;
   for (; k < pl.p_n; ++k) process(k, true);
 
   // ---- partition slices done: CTA offset by one look-back, runs into place ----
