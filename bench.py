@@ -248,7 +248,9 @@ def our_arm(args, wl):
     k1_bytes = 12.0 * n_g + 8.0 * float(k_own.mean())
     achieved = k1_bytes / (k1_avg_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
-    launches_per_step = 2 if world == 1 else 5
+    # our kernels per step: K1 + dense clear + finalize (n = 1);
+    # + gather_foreign, owner_reduce, build_union at n > 1 (NCCL kernels not counted)
+    launches_per_step = 3 if world == 1 else 6
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (N = 1) ----
@@ -296,6 +298,9 @@ def our_arm(args, wl):
                        if 4 * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
                        "parallelism": f"dp{world} (exclusive cyclic partitions)"},
             "density": density, "density_rel_err": density / d - 1.0,
+            "density_window": {"first_quarter": float(K[: max(1, len(K) // 4)].mean() / n_g),
+                               "last_quarter": float(K[-max(1, len(K) // 4):].mean() / n_g),
+                               "median": float(np.median(K) / n_g)},
             "select_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),

@@ -214,7 +214,9 @@ using K1Cfg1 = WsCfg<16, 4, 1024>;
 using K1Cfg2 = WsCfg<16, 2, 2048>;
 using K1Cfg3 = WsCfg<12, 3, 2048>;
 using K1Cfg4 = WsCfg<32, 2, 1024>;
-constexpr int kNumK1Cfg = 5;
+using K1Cfg5 = WsCfg<8, 6, 2048>;
+using K1Cfg6 = WsCfg<16, 3, 2048>;
+constexpr int kNumK1Cfg = 7;
 
 template <typename T, int kMode, class Cfg>
 int launch_k1_tma_cfg(micro_ctx* c, TmaSelectArgs a) {
@@ -239,6 +241,8 @@ int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
     case 2: return launch_k1_tma_cfg<T, kMode, K1Cfg2>(c, a);
     case 3: return launch_k1_tma_cfg<T, kMode, K1Cfg3>(c, a);
     case 4: return launch_k1_tma_cfg<T, kMode, K1Cfg4>(c, a);
+    case 5: return launch_k1_tma_cfg<T, kMode, K1Cfg5>(c, a);
+    case 6: return launch_k1_tma_cfg<T, kMode, K1Cfg6>(c, a);
     default: return launch_k1_tma_cfg<T, kMode, K1Cfg0>(c, a);
   }
 }
