@@ -181,6 +181,11 @@ struct micro_ctx {
   bool poisoned = false;
   bool ever_stepped = false;
   void* staging = nullptr;  // micro_step_host gradient staging (lazy)
+  // the previous union's dense clear runs on `aux`, overlapping K1 (fork at
+  // compress, join before finalize)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool clear_pending = false;
   std::vector<void*> allocs;
 
   int alloc(void** p, size_t bytes) {
@@ -315,6 +320,8 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   return MICRO_OK;
 }
 
+int finalize_blocks(micro_ctx* c);
+
 template <typename T>
 int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_from_counts) {
   FinalizeArgs f{};
@@ -344,12 +351,11 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_K = c->hist_K;
   f.hist_counts = c->hist_counts;
   f.hist_delta = c->hist_delta;
-  int blocks = 1;
-  if (c->dense || c->model) {  // grid-stride over the union entries
-    const int64_t want = ((int64_t)c->k_worker * c->n * 3 / 2 + 255) / 256;
-    blocks = (int)std::min<int64_t>(std::max<int64_t>(want, 1), 4 * num_sms(c->dev));
-  }
-  if (f.prev_idx) {
+  const int blocks = (c->dense || c->model) ? finalize_blocks(c) : 1;  // grid-stride over the union
+  if (c->clear_pending) {
+    CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    c->clear_pending = false;
+  } else if (f.prev_idx) {
     k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
     CU(cudaGetLastError());
   }
@@ -360,6 +366,27 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   c->steps++;
   c->ever_stepped = true;
   c->compressed = false;
+  return MICRO_OK;
+}
+
+int finalize_blocks(micro_ctx* c) {
+  const int64_t want = ((int64_t)c->k_worker * c->n * 3 / 2 + 255) / 256;
+  return (int)std::min<int64_t>(std::max<int64_t>(want, 1), 64 * num_sms(c->dev));
+}
+
+// Clear the previous union's sectors of the dense g/n on the aux stream, so
+// the (small, latency-bound) clear overlaps the HBM-bound K1.
+template <typename T>
+int fork_dense_clear(micro_ctx* c) {
+  if (!c->dense || !c->ever_stepped || !c->aux) return MICRO_OK;
+  const int pb = c->buf ^ 1;
+  const int32_t* prev = c->n == 1 ? c->sel_idx[pb][0] : c->uni_idx[pb];
+  CU(cudaEventRecord(c->ev_fork, c->stream));
+  CU(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
+  k_dense_clear<T><<<finalize_blocks(c), 256, 0, c->aux>>>(prev, c->Kbuf + pb, (T*)c->dense, c->n_g);
+  CU(cudaGetLastError());
+  CU(cudaEventRecord(c->ev_join, c->aux));
+  c->clear_pending = true;
   return MICRO_OK;
 }
 
@@ -413,6 +440,8 @@ int validate_config(const micro_config* g) {
 
 int reset_state(micro_ctx* c) {
   DeviceGuard dg(c->dev);
+  if (c->aux) CU(cudaStreamSynchronize(c->aux));
+  c->clear_pending = false;
   for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
   std::vector<double> d0(c->n_local, c->cfg.initial_threshold);
   CU(cudaMemcpyAsync(c->delta, d0.data(), sizeof(double) * c->n_local, cudaMemcpyHostToDevice, c->stream));
@@ -623,6 +652,12 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
     return cleanup(fail(MICRO_ECUDA, "memset: %s", cudaGetErrorString(e)));
+  if (c->dense) {
+    if ((e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+      return cleanup(fail(MICRO_ECUDA, "aux stream: %s", cudaGetErrorString(e)));
+  }
   if ((rc = reset_state(c))) return cleanup(rc);
   *out = c;
   return MICRO_OK;
@@ -632,8 +667,12 @@ int micro_ctx_destroy(micro_ctx* c) {
   if (!c) return MICRO_OK;
   DeviceGuard dg(c->dev);
   cudaStreamSynchronize(c->stream);
+  if (c->aux) cudaStreamSynchronize(c->aux);
   for (void* p : c->allocs) cudaFree(p);
   if (c->staging) cudaFree(c->staging);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->aux) cudaStreamDestroy(c->aux);
   delete c;
   return MICRO_OK;
 }
@@ -666,6 +705,7 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
   DeviceGuard dg(c->dev);
   c->t_cur = t;
   c->buf = (int)(c->steps & 1);
+  TRY(c->esz == 4 ? fork_dense_clear<float>(c) : fork_dense_clear<double>(c));
   for (int i = 0; i < c->n_local; ++i) {
     if (c->esz == 4) TRY(launch_k1<float>(c, i, d_grads[i], eta, t));
     else TRY(launch_k1<double>(c, i, d_grads[i], eta, t));
