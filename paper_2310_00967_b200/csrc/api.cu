@@ -221,20 +221,30 @@ using K1Cfg3 = WsCfg<12, 3, 2048>;
 using K1Cfg4 = WsCfg<32, 2, 1024>;
 using K1Cfg5 = WsCfg<8, 6, 2048>;
 using K1Cfg6 = WsCfg<16, 3, 2048>;
-constexpr int kNumK1Cfg = 7;
+using K1Cfg7 = WsCfg<8, 1, 1024, false, 6>;   // LDG streaming, 48 warps/SM
+using K1Cfg8 = WsCfg<8, 1, 2048, false, 4>;   // LDG streaming, 32 warps/SM, 4 vectors/lane
+using K1Cfg9 = WsCfg<8, 1, 1024, false, 8>;   // LDG streaming, 64 warps/SM
+constexpr int kNumK1Cfg = 10;
 
 template <typename T, int kMode, class Cfg>
 int launch_k1_tma_cfg(micro_ctx* c, TmaSelectArgs a) {
-  static bool attr_set[64] = {false};  // per instantiation and device
-  if (c->dev >= 64 || !attr_set[c->dev]) {
-    CU(cudaFuncSetAttribute(k1_tma_select<T, kMode, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    if (c->dev < 64) attr_set[c->dev] = true;
+  static int resident[64] = {0};  // CTAs per SM, per instantiation and device
+  if (c->dev >= 64 || !resident[c->dev]) {
+    if (Cfg::SMEM)
+      CU(cudaFuncSetAttribute(k1_tma_select<T, kMode, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg::SMEM));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_tma_select<T, kMode, Cfg>, Cfg::THREADS, Cfg::SMEM));
+    if (occ < 1) return fail(MICRO_ECUDA, "K1 configuration does not fit on an SM");
+    if (c->dev < 64) resident[c->dev] = std::min(occ, Cfg::MINB);
   }
+  const int per_sm = c->dev < 64 ? resident[c->dev] : 1;
   constexpr int UNIT = Cfg::UNIT_BYTES / (int)sizeof(T);
   a.num_units = (c->n_g + UNIT - 1) / UNIT;
   a.unit_lo = a.p_start / UNIT;
   a.unit_hi = (a.p_end - 1) / UNIT;
-  k1_tma_select<T, kMode, Cfg><<<num_sms(c->dev), Cfg::THREADS, Cfg::SMEM, c->stream>>>(a);
+  // persistent: every CTA resident (the look-back waits only on earlier CTAs)
+  k1_tma_select<T, kMode, Cfg><<<num_sms(c->dev) * per_sm, Cfg::THREADS, Cfg::SMEM, c->stream>>>(a);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
@@ -248,6 +258,9 @@ int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
     case 4: return launch_k1_tma_cfg<T, kMode, K1Cfg4>(c, a);
     case 5: return launch_k1_tma_cfg<T, kMode, K1Cfg5>(c, a);
     case 6: return launch_k1_tma_cfg<T, kMode, K1Cfg6>(c, a);
+    case 7: return launch_k1_tma_cfg<T, kMode, K1Cfg7>(c, a);
+    case 8: return launch_k1_tma_cfg<T, kMode, K1Cfg8>(c, a);
+    case 9: return launch_k1_tma_cfg<T, kMode, K1Cfg9>(c, a);
     default: return launch_k1_tma_cfg<T, kMode, K1Cfg0>(c, a);
   }
 }

@@ -55,6 +55,19 @@ __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 // Streaming loads/stores (data touched once per pass).
 __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+// read-only, no L1 allocation (the gradient: read once per pass)
+__device__ __forceinline__ float4 ld_nc_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_nc_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+               : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void st_stream(float4* p, const float4& v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, const double2& v) { __stcs(p, v); }
 

@@ -39,13 +39,17 @@ namespace micro {
 
 // Streaming configuration: warps per CTA, ring stages per warp, bytes per
 // unit (per operand).  Shared memory = WARPS * STAGES * 2 * UNIT_BYTES.
-template <int WARPS_, int STAGES_, int UNIT_BYTES_>
+// TMA = false: the warps load straight from HBM with 16-byte LDGs instead of
+// bulk copies (no ring); MINB CTAs per SM are then resident.
+template <int WARPS_, int STAGES_, int UNIT_BYTES_, bool TMA_ = true, int MINB_ = 1>
 struct WsCfg {
   static constexpr int WARPS = WARPS_;
   static constexpr int STAGES = STAGES_;
   static constexpr int UNIT_BYTES = UNIT_BYTES_;
+  static constexpr bool TMA = TMA_;
+  static constexpr int MINB = MINB_;
   static constexpr int THREADS = WARPS * 32;
-  static constexpr int SMEM = WARPS * STAGES * 2 * UNIT_BYTES + WARPS * STAGES * 8 + 128;
+  static constexpr int SMEM = TMA ? WARPS * STAGES * 2 * UNIT_BYTES + WARPS * STAGES * 8 + 128 : 0;
 };
 
 struct TmaSelectArgs {
@@ -118,7 +122,7 @@ struct WarpPlan {  // unit indices fit int32: n_g < 2^31 (checked on the host)
 };
 
 template <typename T, int kMode, class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a) {
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSelectArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
   constexpr int kWsWarps = Cfg::WARPS, kWsStages = Cfg::STAGES, kWsUnitBytes = Cfg::UNIT_BYTES;
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a
   const T* __restrict__ Gp = (const T*)a.grad;
   T* __restrict__ E = (T*)a.resid;
 
-  if (lane == 0) {
+  if (Cfg::TMA && lane == 0) {
     for (int s = 0; s < kWsStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a
       bulk_g2s(ring + (size_t)(2 * s + 1) * UE, Gp + base, bytes, &full[s]);
     }
   };
-  if (lane == 0)
+  if (Cfg::TMA && lane == 0)
     for (int k = 0; k < nk && k < kWsStages; ++k) issue(k);
 
   const double delta = *a.delta;
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a
     constexpr bool CHECK = decltype(kCheck)::value;
     const int s = k % kWsStages;
     const int vec_elems = FULL ? UE : (int)((elems * (int)sizeof(T)) & ~15) / (int)sizeof(T);
-    mbar_wait(&full[s], (uint32_t)(k / kWsStages) & 1u);
+    if constexpr (Cfg::TMA) mbar_wait(&full[s], (uint32_t)(k / kWsStages) & 1u);
     const V* se = reinterpret_cast<const V*>(ring + (size_t)(2 * s) * UE);
     const V* sg = reinterpret_cast<const V*>(ring + (size_t)(2 * s + 1) * UE);
     V e[VPL], g[VPL];
@@ -206,8 +210,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a
     for (int i = 0; i < VPL; ++i) {
       const int off = (i * 32 + lane) * VN;
       if (FULL || off + VN <= vec_elems) {
-        e[i] = se[i * 32 + lane];
-        g[i] = sg[i * 32 + lane];
+        if constexpr (Cfg::TMA) {
+          e[i] = se[i * 32 + lane];
+          g[i] = sg[i * 32 + lane];
+        } else {
+          e[i] = ld_stream(reinterpret_cast<const V*>(E + base + off));
+          g[i] = ld_nc_stream(reinterpret_cast<const V*>(Gp + base + off));
+        }
       } else {  // the last unit's tail: straight from global
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
@@ -217,10 +226,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) k1_tma_select(TmaSelectArgs a
         }
       }
     }
-    __syncwarp();
-    if (lane == 0 && k + kWsStages < nk) {
-      fence_proxy_async_smem();  // our generic reads of stage s precede the async refill
-      issue(k + kWsStages);
+    if constexpr (Cfg::TMA) {
+      __syncwarp();
+      if (lane == 0 && k + kWsStages < nk) {
+        fence_proxy_async_smem();  // our generic reads of stage s precede the async refill
+        issue(k + kWsStages);
+      }
     }
     unsigned mask[VPL];
 #pragma unroll
