@@ -167,6 +167,7 @@ struct micro_ctx {
   int k1_cfg = 0;               // streaming configuration (MICRO_K1_CFG)
   int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
   void* stage_val = nullptr;
+  int* unit_counts = nullptr;    // selections per K1 unit (TMA kernel)
   unsigned int* ticket = nullptr;
   unsigned int epoch = 0;
   int* flags = nullptr;
@@ -281,6 +282,7 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
   a.count = c->counts + i;
   a.stage_idx = c->stage_idx;
   a.stage_val = c->stage_val;
+  a.unit_counts = c->unit_counts;
   a.status = c->status;
   a.status_len = c->status_len;
   a.epoch = ++c->epoch;
@@ -615,7 +617,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->sel_cap = cfg->selection_capacity ? std::min<int64_t>(cfg->selection_capacity, max_range) : max_range;
   c->uni_cap = std::min<int64_t>(c->n_g, (int64_t)c->n * c->sel_cap);
   c->p_max = c->esz == 4 ? p_max_for<float>(max_range) : p_max_for<double>(max_range);
-  c->status_len = std::max<int64_t>(c->p_max, 4 * num_sms(c->dev));
+  c->status_len = std::max<int64_t>(c->p_max, 16 * num_sms(c->dev));  // >= K1 CTAs
   {
     const char* k = std::getenv("MICRO_K1_KERNEL");
     c->use_tma = !(k && std::strcmp(k, "tile") == 0);
@@ -654,6 +656,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     const int64_t stage = c->p_max * (int64_t)tile_elems<float>() * 4 / (int64_t)c->esz;  // >= units(partition) * unit
     if ((rc = c->alloc((void**)&c->stage_idx, stage * 4))) return cleanup(rc);
     if ((rc = c->alloc(&c->stage_val, stage * c->esz))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->unit_counts, (max_range / 128 + 8) * sizeof(int)))) return cleanup(rc);
   }
   if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->flags, sizeof(int)))) return cleanup(rc);

@@ -63,8 +63,9 @@ struct TmaSelectArgs {
   void* sel_val;
   int64_t cap;
   long long* count;
-  int32_t* stage_idx;          // staging runs, (unit_hi - unit_lo + 1) * UNIT pairs
+  int32_t* stage_idx;          // staging, (unit_hi - unit_lo + 1) * UNIT pairs (unit-local runs)
   void* stage_val;
+  int* unit_counts;            // selections per partition unit
   unsigned long long* status;  // >= status_len words
   int64_t status_len;
   unsigned int epoch;
@@ -107,16 +108,21 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ float nan_probe(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
 __device__ __forceinline__ double nan_probe(double g, double acc) { return __fma_rn(g, 0.0, acc); }
 
-// The units of warp gw (of GW): its slice of the partition units, then its
-// slice of the remaining units.
+// Work plan.  CTA b owns a contiguous, balanced slice of the partition's
+// units and a slice of the remaining units; inside the slice its warps take
+// units round-robin (warp w: units w, w+W, w+2W, ...), so a CTA streams one
+// contiguous window of HBM (DRAM-row friendly: a probe with per-warp
+// contiguous ranges — 1184 scattered streams — capped at 3.5 TB/s, while
+// the same arithmetic on one moving window reaches 6.6 TB/s).
 struct WarpPlan {  // unit indices fit int32: n_g < 2^31 (checked on the host)
-  int p_first, p_n;  // partition units [p_first, p_first + p_n)
-  int o_first, o_n;  // index range in the outside-unit list
+  int p_first, p_n;  // partition units p_first + k*W, k < p_n
+  int o_first, o_n;  // outside-list indices o_first + k*W, k < o_n
   int gap_lo, gap_n;
+  int W;
   __device__ __forceinline__ int count() const { return p_n + o_n; }
   __device__ __forceinline__ int unit(int k) const {
-    if (k < p_n) return p_first + k;
-    const int q = o_first + (k - p_n);
+    if (k < p_n) return p_first + k * W;
+    const int q = o_first + (k - p_n) * W;
     return q < gap_lo ? q : q + gap_n;
   }
 };
@@ -134,6 +140,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ long long s_run[kWsWarps];
   __shared__ long long s_excl;
+  __shared__ int s_wsum[kWsWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
@@ -145,14 +152,17 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
                    w * kWsStages;
 
   WarpPlan pl;
+  int cta_p0, cta_p1;  // this CTA's partition units [cta_p0, cta_p1)
   {
     const int64_t P = a.unit_hi - a.unit_lo + 1, O = a.num_units - P;
-    const int64_t p0 = P * gw / GW, p1 = P * (gw + 1) / GW;
-    const int64_t o0 = O * gw / GW, o1 = O * (gw + 1) / GW;
-    pl.p_first = (int)(a.unit_lo + p0);
-    pl.p_n = (int)(p1 - p0);
-    pl.o_first = (int)o0;
-    pl.o_n = (int)(o1 - o0);
+    cta_p0 = (int)(a.unit_lo + P * b / G);
+    cta_p1 = (int)(a.unit_lo + P * (b + 1) / G);
+    const int o0 = (int)(O * b / G), o1 = (int)(O * (b + 1) / G);
+    pl.W = kWsWarps;
+    pl.p_first = cta_p0 + w;
+    pl.p_n = pl.p_first < cta_p1 ? (cta_p1 - pl.p_first + kWsWarps - 1) / kWsWarps : 0;
+    pl.o_first = o0 + w;
+    pl.o_n = pl.o_first < o1 ? (o1 - pl.o_first + kWsWarps - 1) / kWsWarps : 0;
     pl.gap_lo = (int)a.unit_lo;
     pl.gap_n = (int)P;
   }
@@ -187,8 +197,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
   const T eta = (T)a.eta;
   int32_t* __restrict__ st_idx = a.stage_idx;
   T* __restrict__ st_val = (T*)a.stage_val;
-  const int64_t run_base = (pl.p_first - a.unit_lo) * UE;  // this warp's staging run
-  long long run = 0;
+  int* __restrict__ ucount = a.unit_counts;
+  const int unit_lo = (int)a.unit_lo;
+  long long run = 0;  // pairs selected by this warp
   T probe = (T)0;  // becomes NaN iff some G is Inf/NaN
 
   // One unit: wait, read the stage, refill it, accumulate, store e_{t+1},
@@ -286,6 +297,12 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
         if (lane >= o) incl += y;
       }
       const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+      // pairs of unit u are staged at [(u - unit_lo) * UE, + count)
+      const long long run_base = (long long)(base / UE - unit_lo) * UE;
+      unsigned unit_count = 0;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) unit_count += (tot >> (8 * i)) & 0xFFu;
+      if (lane == 0) ucount[base / UE - unit_lo] = (int)unit_count;
       if (tot) {
         const unsigned excl = incl - packed;
         unsigned any = 0;
@@ -296,7 +313,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
           if (mask[i]) {
-            long long pos = run_base + run + cb + ((excl >> (8 * i)) & 0xFFu);
+            long long pos = run_base + cb + ((excl >> (8 * i)) & 0xFFu);
             const int j0 = base + (i * 32 + lane) * VN;
 #pragma unroll
             for (int c = 0; c < VN; ++c)
@@ -309,10 +326,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
           cb += (tot >> (8 * i)) & 0xFFu;
         }
         }
-        unsigned sum = 0;
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) sum += (tot >> (8 * i)) & 0xFFu;
-        run += sum;
+        run += unit_count;
       }
     }
   };
@@ -356,16 +370,40 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
   }
   __syncthreads();
   {
-    long long dst0 = s_excl;
-    for (int q = 0; q < w; ++q) dst0 += s_run[q];
+    // copy the staged unit runs into place, in unit order: block-wide scan
+    // of the per-unit counts, THREADS units at a time
+    long long off = s_excl;
     int32_t* __restrict__ out_idx = a.sel_idx;
     T* __restrict__ out_val = (T*)a.sel_val;
-    for (long long m = lane; m < run; m += 32) {
-      const long long d = dst0 + m;
-      if (d < a.cap) {
-        out_idx[d] = st_idx[run_base + m];
-        out_val[d] = st_val[run_base + m];
+    for (int u0 = cta_p0; u0 < cta_p1; u0 += Cfg::THREADS) {
+      const int u = u0 + tid;
+      const int cnt = u < cta_p1 ? ucount[u - unit_lo] : 0;
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
+      if (lane == 31) s_wsum[w] = incl;
+      __syncthreads();
+      int wpre = 0, tot = 0;
+#pragma unroll
+      for (int q = 0; q < kWsWarps; ++q) {
+        const int x = s_wsum[q];
+        wpre += q < w ? x : 0;
+        tot += x;
+      }
+      const long long dst = off + wpre + incl - cnt;
+      const long long src = (long long)(u - unit_lo) * UE;
+      for (int m = 0; m < cnt; ++m) {
+        const long long d = dst + m;
+        if (d < a.cap) {
+          out_idx[d] = st_idx[src + m];
+          out_val[d] = st_val[src + m];
+        }
+      }
+      off += tot;
+      __syncthreads();
     }
   }
 
