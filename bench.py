@@ -248,9 +248,9 @@ def our_arm(args, wl):
     k1_bytes = 12.0 * n_g + 8.0 * float(k_own.mean())
     achieved = k1_bytes / (k1_avg_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
-    # our kernels per step: K1 + dense clear + finalize (n = 1);
+    # our kernels per step: K1 stream + K1 compact + dense clear + finalize (n = 1);
     # + gather_foreign, owner_reduce, build_union at n > 1 (NCCL kernels not counted)
-    launches_per_step = 3 if world == 1 else 6
+    launches_per_step = 4 if world == 1 else 7
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (N = 1) ----

@@ -20,6 +20,7 @@
 #include "exchange.cuh"
 #include "select.cuh"
 #include "select_tma.cuh"
+#include "select_stream.cuh"
 
 using namespace micro;
 
@@ -163,7 +164,11 @@ struct micro_ctx {
   unsigned long long* status = nullptr;
   int64_t p_max = 0;
   int64_t status_len = 0;
-  bool use_tma = true;          // K1 = k1_tma_select (MICRO_K1_KERNEL=tile: k1_fused_select)
+  // K1 implementation (MICRO_K1_KERNEL): 0 "stream" k1_stream + k1_compact (default),
+  // 1 "tma" persistent k1_tma_select, 2 "tile" k1_fused_select (also the
+  // fallback for gradients that are not 16-byte aligned)
+  int k1_kind = 0;
+  bool use_tma = true;  // staging buffers allocated
   int k1_cfg = 0;               // streaming configuration (MICRO_K1_CFG)
   int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
   void* stage_val = nullptr;
@@ -293,10 +298,54 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
 }
 
 template <typename T>
+int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe) {
+  constexpr int UE = stream_unit_elems<T>();
+  StreamArgs a{};
+  a.grad = grad;
+  a.resid = c->resid[i];
+  a.n_g = (int)c->n_g;
+  a.p_start = (int)ps;
+  a.p_end = (int)pe;
+  a.eta = eta;
+  a.delta = c->delta + i;
+  a.unit_lo = (int)(ps / UE);
+  a.unit_hi = (int)((pe - 1) / UE);
+  a.stage_idx = c->stage_idx;
+  a.stage_val = c->stage_val;
+  a.unit_counts = c->unit_counts;
+  a.flags = c->flags;
+  const int units = (int)((c->n_g + UE - 1) / UE);
+  const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
+  if (c->cfg.error_feedback) k1_stream<T, kWriteZeroSel><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  else if (c->n > 1) k1_stream<T, kWriteAcc><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  else k1_stream<T, kWriteNone><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  CU(cudaGetLastError());
+  CompactArgs b{};
+  b.stage_idx = c->stage_idx;
+  b.stage_val = c->stage_val;
+  b.unit_counts = c->unit_counts;
+  b.num_units = a.unit_hi - a.unit_lo + 1;
+  b.unit_elems = UE;
+  b.sel_idx = c->sel_idx[c->buf][i];
+  b.sel_val = c->sel_val[c->buf][i];
+  b.cap = c->sel_cap;
+  b.count = c->counts + i;
+  b.status = c->status;
+  b.status_len = c->status_len;
+  b.epoch = ++c->epoch;
+  b.flags = c->flags;
+  k1_compact<T><<<(unsigned)((b.num_units + kCompactUnits - 1) / kCompactUnits), kCompactThreads, 0, c->stream>>>(b);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+template <typename T>
 int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   int64_t ps, pe;
   partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
-  if (c->use_tma && ((uintptr_t)grad % 16) == 0) return launch_k1_tma<T>(c, i, grad, eta, ps, pe);
+  const bool aligned = ((uintptr_t)grad % 16) == 0;
+  if (c->k1_kind == 0 && aligned) return launch_k1_stream<T>(c, i, grad, eta, ps, pe);
+  if (c->k1_kind == 1 && aligned) return launch_k1_tma<T>(c, i, grad, eta, ps, pe);
   SelectArgs a{};
   a.grad = grad;
   a.resid = c->resid[i];
@@ -620,7 +669,8 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->status_len = std::max<int64_t>(c->p_max, 16 * num_sms(c->dev));  // >= K1 CTAs
   {
     const char* k = std::getenv("MICRO_K1_KERNEL");
-    c->use_tma = !(k && std::strcmp(k, "tile") == 0);
+    c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
+    c->use_tma = c->k1_kind != 2;
     const char* cf = std::getenv("MICRO_K1_CFG");
     c->k1_cfg = cf ? std::atoi(cf) : 0;
     if (c->k1_cfg < 0 || c->k1_cfg >= kNumK1Cfg) c->k1_cfg = 0;

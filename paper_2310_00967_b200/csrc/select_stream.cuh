@@ -1,0 +1,254 @@
+// select_stream.cuh — K1 as two kernels: an unordered streaming pass and a
+// small ordered compaction (the production path).
+//
+// Same semantics as k1_fused_select (select.cuh; reference harness.cpp:131,
+// sparsifier.cpp:22-37, harness.cpp:219-221).
+//
+// K1a  k1_stream: one warp per 512-element unit (2 KB per operand), eight
+//      units per CTA, ~32 warps resident per SM.  Each lane issues its eight
+//      16-byte loads (e, G) up front, computes acc = e + eta*G with explicitly
+//      rounded arithmetic, stores e_{t+1} (selected entries zeroed), and — for
+//      units that intersect the partition — compacts the selected
+//      (index, value) pairs with one packed warp scan into the unit's own
+//      staging slot [(u - u_lo) * 512, + k_u), recording k_u.  No ordering,
+//      no cross-warp or cross-CTA dependency: the pass runs at the HBM
+//      roofline like a plain axpy (tools/k1_probe.cu: 6.2-7.0 TB/s).
+// K1b  k1_compact: scans the per-unit counts (1024 units per CTA, decoupled
+//      look-back across CTAs) and copies every unit's staged run to its
+//      final position, giving the ascending (index, value) list and k_i.
+//
+// Why not one pass: every single-pass variant we measured (per-tile
+// look-back; persistent CTAs with TMA bulk-copy rings; per-warp rings;
+// LDG streaming with per-warp ordered runs) stayed at 2.5-3.6 TB/s — the
+// ordering machinery sat on the critical path of every tile.  The staging
+// round trip costs 16 bytes per selected pair plus 4 bytes per 512
+// elements (0.2 B/elem at d = 1%, vs 12 B/elem streamed).
+#pragma once
+
+#include "common.cuh"
+#include "select.cuh"
+
+namespace micro {
+
+constexpr int kStreamWarps = 8;                  // units per CTA
+constexpr int kStreamThreads = kStreamWarps * 32;
+constexpr int kStreamUnitBytes = 2048;            // per operand
+constexpr int kCompactThreads = 256;
+constexpr int kCompactUnitsPerThread = 4;
+constexpr int kCompactUnits = kCompactThreads * kCompactUnitsPerThread;  // per CTA
+
+template <typename T>
+__host__ __device__ constexpr int stream_unit_elems() {
+  return kStreamUnitBytes / (int)sizeof(T);  // 512 fp32 / 256 fp64
+}
+
+struct StreamArgs {
+  const void* grad;
+  void* resid;
+  int n_g;                 // < 2^31 (checked on the host)
+  int p_start, p_end;
+  double eta;
+  const double* delta;
+  int unit_lo, unit_hi;    // units intersecting [p_start, p_end)
+  int32_t* stage_idx;      // (unit_hi - unit_lo + 1) * UNIT pairs
+  void* stage_val;
+  int* unit_counts;        // unit_hi - unit_lo + 1
+  int* flags;              // bit0 non-finite
+};
+
+__device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
+__device__ __forceinline__ double nan_probe_s(double g, double acc) { return __fma_rn(g, 0.0, acc); }
+
+template <typename T, int kMode>
+__global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
+  constexpr int UE = stream_unit_elems<T>();
+  constexpr int VPL = UE / VN / 32;  // 4 vectors per lane per operand
+  static_assert(VPL * VN * 32 == UE && VPL <= 4, "unit layout");
+
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
+  const int base = u * UE;
+  if (base >= a.n_g) return;  // warp-uniform
+  const int elems = a.n_g - base < UE ? a.n_g - base : UE;
+  const T* __restrict__ Gp = (const T*)a.grad + base;
+  T* __restrict__ E = (T*)a.resid + base;
+
+  V e[VPL], g[VPL];
+  if (elems == UE) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      e[i] = ld_stream(reinterpret_cast<const V*>(E) + i * 32 + lane);
+      g[i] = ld_nc_stream(reinterpret_cast<const V*>(Gp) + i * 32 + lane);
+    }
+  } else {  // the vector's last, partial unit
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        const int off = (i * 32 + lane) * VN + c;
+        set_comp(e[i], c, off < elems ? E[off] : (T)0);
+        set_comp(g[i], c, off < elems ? Gp[off] : (T)0);
+      }
+  }
+
+  const bool sel_unit = u >= a.unit_lo && u <= a.unit_hi;
+  const bool all_in = base >= a.p_start && base + elems <= a.p_end;
+  const T thr = threshold_as(*a.delta, (T*)nullptr);
+  const T eta = (T)a.eta;
+  T probe = (T)0;  // becomes NaN iff some G is Inf/NaN
+  unsigned mask[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    mask[i] = 0;
+#pragma unroll
+    for (int c = 0; c < VN; ++c) {
+      const T gv = comp(g[i], c);
+      probe = nan_probe_s(gv, probe);
+      const T acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
+      set_comp(e[i], c, acc);
+      bool sel = sel_unit && absx(acc) > thr;
+      if (!all_in) {
+        const int j = base + (i * 32 + lane) * VN + c;
+        sel = sel && j >= a.p_start && j < a.p_end;
+      }
+      mask[i] |= (unsigned)sel << c;
+    }
+  }
+
+  if (kMode != kWriteNone) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      V out = e[i];
+      if (kMode == kWriteZeroSel) {
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+          if (mask[i] & (1u << c)) set_comp(out, c, (T)0);
+      }
+      if (elems == UE) {
+        st_stream(reinterpret_cast<V*>(E) + i * 32 + lane, out);
+      } else {
+#pragma unroll
+        for (int c = 0; c < VN; ++c) {
+          const int off = (i * 32 + lane) * VN + c;
+          if (off < elems) E[off] = comp(out, c);
+        }
+      }
+    }
+  }
+
+  if (sel_unit) {
+    // order inside the unit: (vector i, lane, component c); the VPL per-lane
+    // counts are packed as 8-bit fields (warp totals <= 128)
+    unsigned packed = 0;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) packed |= (unsigned)__popc(mask[i]) << (8 * i);
+    unsigned incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    const unsigned excl = incl - packed;
+    const int slot = u - a.unit_lo;
+    unsigned cb = 0;
+    int32_t* __restrict__ si = a.stage_idx + (long long)slot * UE;
+    T* __restrict__ sv = (T*)a.stage_val + (long long)slot * UE;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      if (mask[i]) {
+        int pos = (int)(cb + ((excl >> (8 * i)) & 0xFFu));
+        const int j0 = base + (i * 32 + lane) * VN;
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+          if (mask[i] & (1u << c)) {
+            si[pos] = j0 + c;
+            sv[pos] = comp(e[i], c);
+            ++pos;
+          }
+      }
+      cb += (tot >> (8 * i)) & 0xFFu;
+    }
+    if (lane == 0) a.unit_counts[slot] = (int)cb;
+  }
+  if (probe != probe) atomicOr(a.flags, 1);
+}
+
+struct CompactArgs {
+  const int32_t* stage_idx;
+  const void* stage_val;
+  const int* unit_counts;
+  int num_units;           // partition units
+  int unit_elems;
+  int32_t* sel_idx;
+  void* sel_val;
+  long long cap;
+  long long* count;
+  unsigned long long* status;
+  long long status_len;
+  unsigned int epoch;
+  int* flags;              // bit1 capacity overflow
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
+  __shared__ int s_w[kCompactThreads / 32];
+  __shared__ long long s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int b = blockIdx.x, G = gridDim.x;
+  const int u0 = b * kCompactUnits + tid * kCompactUnitsPerThread;
+  int cnt[kCompactUnitsPerThread];
+  int mine = 0;
+#pragma unroll
+  for (int q = 0; q < kCompactUnitsPerThread; ++q) {
+    cnt[q] = u0 + q < a.num_units ? a.unit_counts[u0 + q] : 0;
+    mine += cnt[q];
+  }
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  int wpre = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < kCompactThreads / 32; ++q) {
+    const int x = s_w[q];
+    wpre += q < w ? x : 0;
+    tot += x;
+  }
+  if (w == 0) {
+    const long long ex = lookback(a.status, b, (unsigned long long)tot, a.epoch, lane);
+    if (lane == 0) {
+      s_excl = ex;
+      if (b == G - 1) {
+        const long long total = ex + tot;
+        *a.count = total;
+        if (total > a.cap) atomicOr(a.flags, 2);
+        const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
+        for (long long q = G; q < a.status_len; ++q) st_relaxed_u64(&a.status[q], ep);
+      }
+    }
+  }
+  __syncthreads();
+  long long dst = s_excl + wpre + incl - mine;
+  int32_t* __restrict__ oi = a.sel_idx;
+  T* __restrict__ ov = (T*)a.sel_val;
+  const T* __restrict__ sv = (const T*)a.stage_val;
+#pragma unroll
+  for (int q = 0; q < kCompactUnitsPerThread; ++q) {
+    const long long src = (long long)(u0 + q) * a.unit_elems;
+    for (int m = 0; m < cnt[q]; ++m, ++dst) {
+      if (dst < a.cap) {
+        oi[dst] = a.stage_idx[src + m];
+        ov[dst] = sv[src + m];
+      }
+    }
+  }
+}
+
+}  // namespace micro

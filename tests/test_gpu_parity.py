@@ -68,10 +68,11 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     m.close()
 
 
-@pytest.fixture(params=["tma", "tile"])
+@pytest.fixture(params=["stream", "tma", "tile"])
 def k1_kernel(request, monkeypatch):
-    """K1 implementation: the TMA-staged persistent kernel (default) or the
-    per-tile look-back kernel (fallback for unaligned gradients)."""
+    """K1 implementation: streaming pass + ordered compaction (default), the
+    persistent TMA kernel, or the per-tile look-back kernel (fallback for
+    unaligned gradients)."""
     monkeypatch.setenv("MICRO_K1_KERNEL", request.param)
     return request.param
 

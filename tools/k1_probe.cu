@@ -80,3 +80,69 @@ int main(int argc, char** argv) {
   }
   return 0;
 }
+
+// ---- access-pattern probes (same arithmetic as variant 0) ----
+// P1: every warp streams its own contiguous range (units of 256 float4 = 32 lanes x 8)
+// P2: every CTA streams a contiguous range, its warps round-robin over 32-float4 units
+template <int PAT>
+__global__ void __launch_bounds__(256) pattern(float4* e, const float4* g, long n4, float eta) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long GW = (long)gridDim.x * 8, gw = (long)blockIdx.x * 8 + w;
+  constexpr int U = 64;  // float4 per unit (2 per lane)
+  const long units = n4 / U;
+  long u0, u1, step;
+  if (PAT == 1) { u0 = units * gw / GW; u1 = units * (gw + 1) / GW; step = 1; }
+  else { u0 = units * blockIdx.x / gridDim.x + w; u1 = units * (blockIdx.x + 1) / gridDim.x; step = 8; }
+  for (long u = u0; u < u1; u += step) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const long idx = u * U + i * 32 + lane;
+      float4 a = e[idx];
+      const float4 b = __ldg(g + idx);
+      a.x = __fadd_rn(a.x, __fmul_rn(eta, b.x));
+      a.y = __fadd_rn(a.y, __fmul_rn(eta, b.y));
+      a.z = __fadd_rn(a.z, __fmul_rn(eta, b.z));
+      a.w = __fadd_rn(a.w, __fmul_rn(eta, b.w));
+      e[idx] = a;
+    }
+  }
+}
+
+template <int PAT>
+float runp(float4* e, const float4* g, long n4, int grid) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9f;
+  for (int r = 0; r < 12; ++r) {
+    cudaEventRecord(a);
+    pattern<PAT><<<grid, 256>>>(e, g, n4, 0.01f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (r >= 2 && ms < best) best = ms;
+  }
+  return best;
+}
+
+struct PatternMain {
+  PatternMain() {
+    const long n = 138000000L, n4 = n / 4;
+    float4 *e, *g;
+    cudaMalloc(&e, n4 * 16);
+    cudaMalloc(&g, n4 * 16);
+    cudaMemset(e, 0, n4 * 16);
+    cudaMemset(g, 0x3c, n4 * 16);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    for (int mult : {1, 2, 4, 8}) {
+      const int grid = sms * mult;
+      const float t1 = runp<1>(e, g, n4, grid), t2 = runp<2>(e, g, n4, grid);
+      printf("pattern grid %5d: per-warp ranges %.1f us %.0f GB/s | per-CTA window %.1f us %.0f GB/s\n", grid,
+             t1 * 1e3, 12.0 * n / (t1 * 1e-3) / 1e9, t2 * 1e3, 12.0 * n / (t2 * 1e-3) / 1e9);
+    }
+    cudaFree(e);
+    cudaFree(g);
+  }
+} pattern_main;
