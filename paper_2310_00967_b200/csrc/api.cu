@@ -334,7 +334,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.status_len = c->status_len;
   b.epoch = ++c->epoch;
   b.flags = c->flags;
-  k1_compact<T><<<(unsigned)((b.num_units + kCompactUnits - 1) / kCompactUnits), kCompactThreads, 0, c->stream>>>(b);
+  k1_compact<T><<<(unsigned)((b.num_units + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, c->stream>>>(b);
   CU(cudaGetLastError());
   return MICRO_OK;
 }

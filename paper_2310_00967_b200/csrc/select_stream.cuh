@@ -33,9 +33,7 @@ namespace micro {
 constexpr int kStreamWarps = 8;                  // units per CTA
 constexpr int kStreamThreads = kStreamWarps * 32;
 constexpr int kStreamUnitBytes = 2048;            // per operand
-constexpr int kCompactThreads = 256;
-constexpr int kCompactUnitsPerThread = 4;
-constexpr int kCompactUnits = kCompactThreads * kCompactUnitsPerThread;  // per CTA
+constexpr int kCompactThreads = 256;  // units per CTA of k1_compact
 
 template <typename T>
 __host__ __device__ constexpr int stream_unit_elems() {
@@ -192,26 +190,26 @@ struct CompactArgs {
   int* flags;              // bit1 capacity overflow
 };
 
+// One thread per unit count, 256 units per CTA.  Offsets: warp scan + CTA
+// scan + one decoupled look-back across CTAs.  Copy: each warp moves the
+// pairs of its 32 units as one flattened list — lane L handles pairs
+// L, L+32, ... and finds its unit by a 5-step shuffle binary search over
+// the warp's inclusive prefix — so loads and stores are coalesced.
 template <typename T>
 __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
   __shared__ int s_w[kCompactThreads / 32];
   __shared__ long long s_excl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
-  const int u0 = b * kCompactUnits + tid * kCompactUnitsPerThread;
-  int cnt[kCompactUnitsPerThread];
-  int mine = 0;
-#pragma unroll
-  for (int q = 0; q < kCompactUnitsPerThread; ++q) {
-    cnt[q] = u0 + q < a.num_units ? a.unit_counts[u0 + q] : 0;
-    mine += cnt[q];
-  }
-  int incl = mine;
+  const int u = b * kCompactThreads + tid;
+  const int cnt = u < a.num_units ? a.unit_counts[u] : 0;
+  int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
+  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
   if (lane == 31) s_w[w] = incl;
   __syncthreads();
   int wpre = 0, tot = 0;
@@ -235,18 +233,26 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
     }
   }
   __syncthreads();
-  long long dst = s_excl + wpre + incl - mine;
+  const long long dst0 = s_excl + wpre;
+  const int u_first = b * kCompactThreads + w * 32;  // the warp's first unit
   int32_t* __restrict__ oi = a.sel_idx;
   T* __restrict__ ov = (T*)a.sel_val;
+  const int32_t* __restrict__ si = a.stage_idx;
   const T* __restrict__ sv = (const T*)a.stage_val;
+  for (int p = lane; p < wtot; p += 32) {
+    // unit q of the warp holding pair p: smallest q with incl_q > p
+    int q = 0;
 #pragma unroll
-  for (int q = 0; q < kCompactUnitsPerThread; ++q) {
-    const long long src = (long long)(u0 + q) * a.unit_elems;
-    for (int m = 0; m < cnt[q]; ++m, ++dst) {
-      if (dst < a.cap) {
-        oi[dst] = a.stage_idx[src + m];
-        ov[dst] = sv[src + m];
-      }
+    for (int step = 16; step > 0; step >>= 1) {
+      const int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
+      if (v <= p) q += step;
+    }
+    const int before = __shfl_sync(0xffffffffu, incl - cnt, q);
+    const long long src = (long long)(u_first + q) * a.unit_elems + (p - before);
+    const long long d = dst0 + p;
+    if (d < a.cap) {
+      oi[d] = si[src];
+      ov[d] = sv[src];
     }
   }
 }
