@@ -163,7 +163,8 @@ struct micro_ctx {
   // K1 workspace
   unsigned long long* status = nullptr;
   int64_t p_max = 0;
-  int64_t status_len = 0;
+  int64_t status_len = 0;       // allocated look-back words
+  int64_t status_hwm = 0;       // highest look-back index any launch has used
   // K1 implementation (MICRO_K1_KERNEL): 0 "stream" k1_stream + k1_compact (default),
   // 1 "tma" persistent k1_tma_select, 2 "tile" k1_fused_select (also the
   // fallback for gradients that are not 16-byte aligned)
@@ -232,6 +233,21 @@ using K1Cfg8 = WsCfg<8, 1, 2048, false, 4>;   // LDG streaming, 32 warps/SM, 4 v
 using K1Cfg9 = WsCfg<8, 1, 1024, false, 8>;   // LDG streaming, 64 warps/SM
 constexpr int kNumK1Cfg = 10;
 
+// Look-back words are shared by every ordered launch of a context: a launch
+// with G CTAs stamps [0, G) through its chain and its last CTA stamps
+// [G, hwm) with the same epoch, so when the next launch starts every word it
+// can read carries a different epoch (epochs are 24-bit and skip 0, the
+// memset value of never-used words).
+unsigned int next_epoch(micro_ctx* c) {
+  unsigned int e = ++c->epoch;
+  if ((e & 0xFFFFFFu) == 0) e = ++c->epoch;
+  return e;
+}
+int64_t status_span(micro_ctx* c, int64_t G) {
+  c->status_hwm = std::max(c->status_hwm, G);
+  return c->status_hwm;
+}
+
 template <typename T, int kMode, class Cfg>
 int launch_k1_tma_cfg(micro_ctx* c, TmaSelectArgs a) {
   static int resident[64] = {0};  // CTAs per SM, per instantiation and device
@@ -250,7 +266,10 @@ int launch_k1_tma_cfg(micro_ctx* c, TmaSelectArgs a) {
   a.unit_lo = a.p_start / UNIT;
   a.unit_hi = (a.p_end - 1) / UNIT;
   // persistent: every CTA resident (the look-back waits only on earlier CTAs)
-  k1_tma_select<T, kMode, Cfg><<<num_sms(c->dev) * per_sm, Cfg::THREADS, Cfg::SMEM, c->stream>>>(a);
+  const int64_t grid = (int64_t)num_sms(c->dev) * per_sm;
+  if (grid > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
+  a.status_len = status_span(c, grid);
+  k1_tma_select<T, kMode, Cfg><<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, c->stream>>>(a);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
@@ -289,8 +308,7 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
   a.stage_val = c->stage_val;
   a.unit_counts = c->unit_counts;
   a.status = c->status;
-  a.status_len = c->status_len;
-  a.epoch = ++c->epoch;
+  a.epoch = next_epoch(c);
   a.flags = c->flags;
   if (c->cfg.error_feedback) return launch_k1_tma_mode<T, kWriteZeroSel>(c, a);
   if (c->n > 1) return launch_k1_tma_mode<T, kWriteAcc>(c, a);
@@ -331,10 +349,12 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.cap = c->sel_cap;
   b.count = c->counts + i;
   b.status = c->status;
-  b.status_len = c->status_len;
-  b.epoch = ++c->epoch;
+  b.epoch = next_epoch(c);
   b.flags = c->flags;
-  k1_compact<T><<<(unsigned)((b.num_units + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, c->stream>>>(b);
+  const int64_t blocks = (b.num_units + kCompactThreads - 1) / kCompactThreads;
+  if (blocks > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
+  b.status_len = status_span(c, blocks);
+  k1_compact<T><<<(unsigned)blocks, kCompactThreads, 0, c->stream>>>(b);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
@@ -359,9 +379,12 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   a.cap = c->sel_cap;
   a.count = c->counts + i;
   a.status = c->status;
-  a.p_max = c->p_max;
+  {
+    const int64_t P_cur = (pe - 1) / tile_elems<T>() - ps / tile_elems<T>() + 1;
+    a.p_max = status_span(c, P_cur);
+  }
   a.ticket = c->ticket;
-  a.epoch = ++c->epoch;
+  a.epoch = next_epoch(c);
   a.tile_lo = 0;
   a.num_tiles = (c->n_g + tile_elems<T>() - 1) / tile_elems<T>();
   a.flags = c->flags;

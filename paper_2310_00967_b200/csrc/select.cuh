@@ -246,11 +246,13 @@ __global__ void __launch_bounds__(kThreads, 4) k1_fused_select(SelectArgs a) {
         const long long k = ex + tile_count;
         *a.count = k;
         if (k > a.cap) atomicOr(a.flags, 2);
-        // epoch hygiene: every status word [0, p_max) carries this launch's
-        // epoch once the launch ends, so stale words can never alias.
-        const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
-        for (int64_t q = last_pt + 1; q < a.p_max; ++q) st_relaxed_u64(&a.status[q], ep);
       }
+    }
+    if (pt == last_pt) {
+      // epoch hygiene: every status word [0, p_max) carries this launch's
+      // epoch once the launch ends, so stale words can never alias.
+      const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
+      for (int64_t q = last_pt + 1 + lane; q < a.p_max; q += 32) st_relaxed_u64(&a.status[q], ep);
     }
   }
   __syncthreads();

@@ -227,9 +227,11 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
         const long long total = ex + tot;
         *a.count = total;
         if (total > a.cap) atomicOr(a.flags, 2);
-        const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
-        for (long long q = G; q < a.status_len; ++q) st_relaxed_u64(&a.status[q], ep);
       }
+    }
+    if (b == G - 1) {  // stamp the unused look-back words with this epoch
+      const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
+      for (long long q = G + lane; q < a.status_len; q += 32) st_relaxed_u64(&a.status[q], ep);
     }
   }
   __syncthreads();

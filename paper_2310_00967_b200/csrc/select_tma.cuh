@@ -363,9 +363,11 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
         const long long total = ex + cta;
         *a.count = total;
         if (total > a.cap) atomicOr(a.flags, 2);
-        const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
-        for (int64_t q = G; q < a.status_len; ++q) st_relaxed_u64(&a.status[q], ep);
       }
+    }
+    if (b == G - 1) {  // stamp the unused look-back words with this epoch
+      const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
+      for (int64_t q = G + lane; q < a.status_len; q += 32) st_relaxed_u64(&a.status[q], ep);
     }
   }
   __syncthreads();
