@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
   T* __restrict__ ov = (T*)a.sel_val;
   const int32_t* __restrict__ si = a.stage_idx;
   const T* __restrict__ sv = (const T*)a.stage_val;
-  for (int p = lane; p < wtot; p += 32) {
+  for (int p0 = 0; p0 < wtot; p0 += 32) {  // whole-warp iterations: the shuffles need every lane
+    const int p = p0 + lane;
     // unit q of the warp holding pair p: smallest q with incl_q > p
     int q = 0;
 #pragma unroll
@@ -249,10 +250,10 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
       const int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
       if (v <= p) q += step;
     }
-    const int before = __shfl_sync(0xffffffffu, incl - cnt, q);
+    const int before = __shfl_sync(0xffffffffu, incl - cnt, q & 31);
     const long long src = (long long)(u_first + q) * a.unit_elems + (p - before);
     const long long d = dst0 + p;
-    if (d < a.cap) {
+    if (p < wtot && d < a.cap) {
       oi[d] = si[src];
       ov[d] = sv[src];
     }
