@@ -187,12 +187,17 @@ struct micro_ctx {
   bool compressed = false;
   bool poisoned = false;
   bool ever_stepped = false;
-  void* staging = nullptr;  // micro_step_host gradient staging (lazy)
+  void* staging = nullptr;  // gradient staging (lazy): host inputs, unaligned device inputs
+  size_t staging_stride = 0;  // bytes per worker row (256-byte aligned)
   // the previous union's dense clear runs on `aux`, overlapping K1 (fork at
   // compress, join before finalize)
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool clear_pending = false;
+  // n = 1 with the streaming K1: the dense g/n is maintained inside K1
+  // (k1_stream<..., kDense>) with one dirty bit per 32-byte sector
+  bool dense_fused = false;
+  unsigned long long* dense_dirty = nullptr;
   std::vector<void*> allocs;
 
   int alloc(void** p, size_t bytes) {
@@ -209,6 +214,17 @@ namespace {
 
 int check_ctx(micro_ctx* c) {
   if (!c) return fail(MICRO_EINVAL, "null context");
+  return MICRO_OK;
+}
+
+int ensure_staging(micro_ctx* c) {
+  if (c->staging) return MICRO_OK;
+  c->staging_stride = ((size_t)c->n_g * c->esz + 255) / 256 * 256;
+  cudaError_t e = cudaMalloc(&c->staging, c->staging_stride * c->n_local);
+  if (e != cudaSuccess) {
+    c->staging = nullptr;
+    return fail(MICRO_ENOMEM, "gradient staging: %s", cudaGetErrorString(e));
+  }
   return MICRO_OK;
 }
 
@@ -332,11 +348,20 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.stage_val = c->stage_val;
   a.unit_counts = c->unit_counts;
   a.flags = c->flags;
+  a.dense = c->dense;
+  a.dirty = c->dense_dirty;
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
-  if (c->cfg.error_feedback) k1_stream<T, kWriteZeroSel><<<grid, kStreamThreads, 0, c->stream>>>(a);
-  else if (c->n > 1) k1_stream<T, kWriteAcc><<<grid, kStreamThreads, 0, c->stream>>>(a);
-  else k1_stream<T, kWriteNone><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  const bool fused = c->dense_fused;
+  if (c->cfg.error_feedback) {
+    if (fused) k1_stream<T, kWriteZeroSel, true><<<grid, kStreamThreads, 0, c->stream>>>(a);
+    else k1_stream<T, kWriteZeroSel, false><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  } else if (c->n > 1) {
+    k1_stream<T, kWriteAcc, false><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  } else {
+    if (fused) k1_stream<T, kWriteNone, true><<<grid, kStreamThreads, 0, c->stream>>>(a);
+    else k1_stream<T, kWriteNone, false><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  }
   CU(cudaGetLastError());
   CompactArgs b{};
   b.stage_idx = c->stage_idx;
@@ -427,18 +452,18 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.union_idx = uidx;
   f.union_sum = usum;
   const int pb = c->buf ^ 1;
-  if (c->ever_stepped && c->dense) {
+  if (c->ever_stepped && c->dense && !c->dense_fused) {
     f.prev_idx = c->n == 1 ? c->sel_idx[pb][0] : c->uni_idx[pb];
     f.prev_K = c->Kbuf + pb;
   }
-  f.dense = c->dense;
+  f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
   f.model = c->model;
   f.slot = c->steps % kHistCap;
   f.hist_t = c->hist_t;
   f.hist_K = c->hist_K;
   f.hist_counts = c->hist_counts;
   f.hist_delta = c->hist_delta;
-  const int blocks = (c->dense || c->model) ? finalize_blocks(c) : 1;  // grid-stride over the union
+  const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
   if (c->clear_pending) {
     CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     c->clear_pending = false;
@@ -465,7 +490,7 @@ int finalize_blocks(micro_ctx* c) {
 // the (small, latency-bound) clear overlaps the HBM-bound K1.
 template <typename T>
 int fork_dense_clear(micro_ctx* c) {
-  if (!c->dense || !c->ever_stepped || !c->aux) return MICRO_OK;
+  if (!c->dense || c->dense_fused || !c->ever_stepped || !c->aux) return MICRO_OK;
   const int pb = c->buf ^ 1;
   const int32_t* prev = c->n == 1 ? c->sel_idx[pb][0] : c->uni_idx[pb];
   CU(cudaEventRecord(c->ev_fork, c->stream));
@@ -536,6 +561,7 @@ int reset_state(micro_ctx* c) {
   CU(cudaMemsetAsync(c->Kbuf, 0, sizeof(long long) * 2, c->stream));
   CU(cudaMemsetAsync(c->flags, 0, sizeof(int), c->stream));
   if (c->dense) CU(cudaMemsetAsync(c->dense, 0, c->n_g * c->esz, c->stream));
+  if (c->dense_dirty) CU(cudaMemsetAsync(c->dense_dirty, 0, (c->n_g / 256 + 8) * 8, c->stream));
   CU(cudaStreamSynchronize(c->stream));
   c->steps = 0;
   c->t_cur = -1;
@@ -693,6 +719,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   {
     const char* k = std::getenv("MICRO_K1_KERNEL");
     c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
+    c->dense_fused = c->n == 1 && cfg->dense_output && c->k1_kind == 0;
     c->use_tma = c->k1_kind != 2;
     const char* cf = std::getenv("MICRO_K1_CFG");
     c->k1_cfg = cf ? std::atoi(cf) : 0;
@@ -724,6 +751,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((rc = c->alloc((void**)&c->delta, sizeof(double) * c->n_local))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->Kbuf, sizeof(long long) * 2))) return cleanup(rc);
   if (cfg->dense_output && (rc = c->alloc(&c->dense, c->n_g * c->esz))) return cleanup(rc);
+  if (c->dense_fused && (rc = c->alloc((void**)&c->dense_dirty, (c->n_g / 256 + 8) * 8))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->status, sizeof(unsigned long long) * c->status_len))) return cleanup(rc);
   if (c->use_tma) {
     const int64_t stage = c->p_max * (int64_t)tile_elems<float>() * 4 / (int64_t)c->esz;  // >= units(partition) * unit
@@ -796,8 +824,16 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
   c->buf = (int)(c->steps & 1);
   TRY(c->esz == 4 ? fork_dense_clear<float>(c) : fork_dense_clear<double>(c));
   for (int i = 0; i < c->n_local; ++i) {
-    if (c->esz == 4) TRY(launch_k1<float>(c, i, d_grads[i], eta, t));
-    else TRY(launch_k1<double>(c, i, d_grads[i], eta, t));
+    const void* g = d_grads[i];
+    if (c->k1_kind == 0 && (uintptr_t)g % 16) {
+      // the streaming K1 reads 16-byte vectors: realign once (8 B/elem copy)
+      TRY(ensure_staging(c));
+      void* dst = (char*)c->staging + (size_t)i * c->staging_stride;
+      if (dst != g) CU(cudaMemcpyAsync(dst, g, (size_t)c->n_g * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+      g = dst;
+    }
+    if (c->esz == 4) TRY(launch_k1<float>(c, i, g, eta, t));
+    else TRY(launch_k1<double>(c, i, g, eta, t));
   }
   c->compressed = true;
   return MICRO_OK;
@@ -833,14 +869,12 @@ int micro_step_host(micro_ctx* c, const void* h_grads, double eta, int64_t t, in
   TRY(check_ctx(c));
   if (!c->cluster) return fail(MICRO_ELOGIC, "micro_step_host: single-device clusters only");
   DeviceGuard dg(c->dev);
-  const size_t bytes = (size_t)c->n_local * c->n_g * c->esz;
-  if (!c->staging) {
-    cudaError_t e = cudaMalloc(&c->staging, bytes);
-    if (e != cudaSuccess) return fail(MICRO_ENOMEM, "staging: %s", cudaGetErrorString(e));
-  }
-  CU(cudaMemcpyAsync(c->staging, h_grads, bytes, cudaMemcpyHostToDevice, c->stream));
+  TRY(ensure_staging(c));
+  const size_t row = (size_t)c->n_g * c->esz;
+  CU(cudaMemcpy2DAsync(c->staging, c->staging_stride, h_grads, row, row, c->n_local, cudaMemcpyHostToDevice,
+                       c->stream));
   std::vector<const void*> g(c->n_local);
-  for (int i = 0; i < c->n_local; ++i) g[i] = (const char*)c->staging + (size_t)i * c->n_g * c->esz;
+  for (int i = 0; i < c->n_local; ++i) g[i] = (const char*)c->staging + (size_t)i * c->staging_stride;
   TRY(micro_step(c, g.data(), eta, t));
   return micro_copy_union(c, h_idx, h_sums, cap, K);
 }

@@ -52,12 +52,27 @@ struct StreamArgs {
   void* stage_val;
   int* unit_counts;        // unit_hi - unit_lo + 1
   int* flags;              // bit0 non-finite
+  // single-worker dense g/n, fused (kDense): whole 32-byte sectors, one
+  // "nonzero last step" bit per sector (64 per unit)
+  void* dense;
+  unsigned long long* dirty;
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
 __device__ __forceinline__ double nan_probe_s(double g, double acc) { return __fma_rn(g, 0.0, acc); }
 
-template <typename T, int kMode>
+// Compress the 32 lane bits of a sector ballot (lanes 2k, 2k+1 share
+// sector k) into 16 sector bits.
+__device__ __forceinline__ unsigned even_bits(unsigned x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  x = (x | (x >> 8)) & 0x0000FFFFu;
+  return x;
+}
+
+template <typename T, int kMode, bool kDense>
 __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -134,6 +149,39 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
         }
       }
     }
+  }
+
+  if (kDense) {
+    // n = 1: g/n = (0 + acc) / 1 = acc at the selections (never +-0: |acc| >
+    // delta >= 0), 0 elsewhere.  A 32-byte sector is written in full when it
+    // holds a selection now or held one last step; lanes 2k and 2k+1 own its
+    // two 16-byte halves (sector k + 16 i of the unit).
+    static_assert(VPL * 16 == 64, "64 sectors per unit");
+    const unsigned long long prev = a.dirty[u];
+    unsigned long long now = 0;
+    T* D = (T*)a.dense + base;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const bool half = mask[i] != 0;
+      const bool sec = half || __shfl_xor_sync(0xffffffffu, half, 1);
+      const unsigned secbits = even_bits(__ballot_sync(0xffffffffu, sec));
+      now |= (unsigned long long)secbits << (16 * i);
+      if (sec || ((prev >> (16 * i + (lane >> 1))) & 1ull)) {
+        V out;
+#pragma unroll
+        for (int c = 0; c < VN; ++c) set_comp(out, c, (mask[i] & (1u << c)) ? comp(e[i], c) : (T)0);
+        if (elems == UE) {
+          st_stream(reinterpret_cast<V*>(D) + i * 32 + lane, out);
+        } else {
+#pragma unroll
+          for (int c = 0; c < VN; ++c) {
+            const int off = (i * 32 + lane) * VN + c;
+            if (off < elems) D[off] = comp(out, c);
+          }
+        }
+      }
+    }
+    if (lane == 0 && now != prev) a.dirty[u] = now;
   }
 
   if (sel_unit) {
