@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const bool half = mask[i] != 0;
-      const bool sec = half || __shfl_xor_sync(0xffffffffu, half, 1);
+      const bool other = __shfl_xor_sync(0xffffffffu, half, 1);  // every lane: no short-circuit
+      const bool sec = half || other;
       const unsigned secbits = even_bits(__ballot_sync(0xffffffffu, sec));
       now |= (unsigned long long)secbits << (16 * i);
       if (sec || ((prev >> (16 * i + (lane >> 1))) & 1ull)) {
