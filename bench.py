@@ -184,10 +184,16 @@ def our_arm(args, wl):
         from paper_2310_00967_b200.dist import DistMicro
         tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
-        m = DistMicro(n_g, density=d, initial_threshold=delta0, scaling_factor=ALPHA)
+        m = DistMicro(n_g, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
     else:
-        m = engine.Micro(n_g, 1, density=d, initial_threshold=delta0, scaling_factor=ALPHA)
+        m = engine.Micro(n_g, 1, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
     stream = torch.cuda.current_stream(dev)
+    # the model update x -= g/n at the union is part of the reference's
+    # iteration (harness.cpp:212-215); a dense g/n is not (run_iteration uses
+    # the sparse sums), so it is materialised only with --dense
+    model = torch.zeros(n_g, device=dev)
+    if args.model:
+        m.set_model(model)
 
     # The threshold adapts for `prime` untimed iterations on fresh N(0,1)
     # gradients (generated between steps), reaching the stationary regime the
@@ -292,6 +298,7 @@ def our_arm(args, wl):
             "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world,
                        "one_worker_per_gpu": True, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
+                       "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
                        "inputs": (f"{R} resident N(0,1) gradients ("
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
                                   + "); each 4*n_g bytes > L2 (no flush needed)")
@@ -328,6 +335,8 @@ def main():
     ap.add_argument("--buffers", type=int, default=256, help="max resident gradient buffers")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dense", action="store_true", help="also maintain the dense g/n vector")
+    ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

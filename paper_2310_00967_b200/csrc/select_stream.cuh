@@ -88,12 +88,13 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   const T* __restrict__ Gp = (const T*)a.grad + base;
   T* __restrict__ E = (T*)a.resid + base;
 
+  const unsigned long long pol_stream = policy_evict_first();
   V e[VPL], g[VPL];
   if (elems == UE) {
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
-      e[i] = ld_stream(reinterpret_cast<const V*>(E) + i * 32 + lane);
-      g[i] = ld_nc_stream(reinterpret_cast<const V*>(Gp) + i * 32 + lane);
+      e[i] = ld_hint(reinterpret_cast<const V*>(E) + i * 32 + lane, pol_stream);
+      g[i] = ld_nc_hint(reinterpret_cast<const V*>(Gp) + i * 32 + lane, pol_stream);
     }
   } else {  // the vector's last, partial unit
 #pragma unroll
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
           if (mask[i] & (1u << c)) set_comp(out, c, (T)0);
       }
       if (elems == UE) {
-        st_stream(reinterpret_cast<V*>(E) + i * 32 + lane, out);
+        st_hint(reinterpret_cast<V*>(E) + i * 32 + lane, out, pol_stream);
       } else {
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
 #pragma unroll
         for (int c = 0; c < VN; ++c) set_comp(out, c, (mask[i] & (1u << c)) ? comp(e[i], c) : (T)0);
         if (elems == UE) {
-          st_stream(reinterpret_cast<V*>(D) + i * 32 + lane, out);
+          st_hint(reinterpret_cast<V*>(D) + i * 32 + lane, out, pol_stream);
         } else {
 #pragma unroll
           for (int c = 0; c < VN; ++c) {
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
     const unsigned excl = incl - packed;
     const int slot = u - a.unit_lo;
+    const unsigned long long pol_keep = policy_evict_last();  // read back by k1_compact, then discarded
     unsigned cb = 0;
     int32_t* __restrict__ si = a.stage_idx + (long long)slot * UE;
     T* __restrict__ sv = (T*)a.stage_val + (long long)slot * UE;
@@ -211,8 +213,8 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
 #pragma unroll
         for (int c = 0; c < VN; ++c)
           if (mask[i] & (1u << c)) {
-            si[pos] = j0 + c;
-            sv[pos] = comp(e[i], c);
+            st_hint(si + pos, j0 + c, pol_keep);
+            st_hint(sv + pos, comp(e[i], c), pol_keep);
             ++pos;
           }
       }
@@ -306,6 +308,14 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
       oi[d] = si[src];
       ov[d] = sv[src];
     }
+  }
+  // the staged runs are dead now: drop their L2 lines without write-back
+  if (cnt) {
+    const long long s0 = (long long)u * a.unit_elems;
+    const char* pi = reinterpret_cast<const char*>(si + s0);
+    const char* pv = reinterpret_cast<const char*>(sv + s0);
+    for (int off = 0; off < cnt * 4; off += 128) discard_l2_line(pi + off);
+    for (int off = 0; off < cnt * (int)sizeof(T); off += 128) discard_l2_line(pv + off);
   }
 }
 
