@@ -352,16 +352,25 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.dirty = c->dense_dirty;
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
-  const bool fused = c->dense_fused;
-  if (c->cfg.error_feedback) {
-    if (fused) k1_stream<T, kWriteZeroSel, true><<<grid, kStreamThreads, 0, c->stream>>>(a);
-    else k1_stream<T, kWriteZeroSel, false><<<grid, kStreamThreads, 0, c->stream>>>(a);
-  } else if (c->n > 1) {
-    k1_stream<T, kWriteAcc, false><<<grid, kStreamThreads, 0, c->stream>>>(a);
+  a.model = c->model;
+  const bool fd = c->dense_fused, fm = c->n == 1 && c->model != nullptr;
+  cudaStream_t st = c->stream;
+#define K1S(MODE, D, M) k1_stream<T, MODE, D, M><<<grid, kStreamThreads, 0, st>>>(a)
+  if (c->n > 1) {
+    if (c->cfg.error_feedback) K1S(kWriteZeroSel, false, false);
+    else K1S(kWriteAcc, false, false);
+  } else if (c->cfg.error_feedback) {
+    if (fd && fm) K1S(kWriteZeroSel, true, true);
+    else if (fd) K1S(kWriteZeroSel, true, false);
+    else if (fm) K1S(kWriteZeroSel, false, true);
+    else K1S(kWriteZeroSel, false, false);
   } else {
-    if (fused) k1_stream<T, kWriteNone, true><<<grid, kStreamThreads, 0, c->stream>>>(a);
-    else k1_stream<T, kWriteNone, false><<<grid, kStreamThreads, 0, c->stream>>>(a);
+    if (fd && fm) K1S(kWriteNone, true, true);
+    else if (fd) K1S(kWriteNone, true, false);
+    else if (fm) K1S(kWriteNone, false, true);
+    else K1S(kWriteNone, false, false);
   }
+#undef K1S
   CU(cudaGetLastError());
   CompactArgs b{};
   b.stage_idx = c->stage_idx;
@@ -376,7 +385,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.status = c->status;
   b.epoch = next_epoch(c);
   b.flags = c->flags;
-  const int64_t blocks = (b.num_units + kCompactThreads - 1) / kCompactThreads;
+  const int64_t blocks = (b.num_units + kCompactUnits - 1) / kCompactUnits;
   if (blocks > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
   b.status_len = status_span(c, blocks);
   k1_compact<T><<<(unsigned)blocks, kCompactThreads, 0, c->stream>>>(b);
@@ -457,7 +466,8 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
     f.prev_K = c->Kbuf + pb;
   }
   f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
-  f.model = c->model;
+  // n = 1 with the streaming K1: the model update happened inside K1
+  f.model = (c->n == 1 && c->k1_kind == 0) ? nullptr : c->model;
   f.slot = c->steps % kHistCap;
   f.hist_t = c->hist_t;
   f.hist_K = c->hist_K;

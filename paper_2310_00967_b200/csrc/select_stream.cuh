@@ -33,7 +33,9 @@ namespace micro {
 constexpr int kStreamWarps = 8;                  // units per CTA
 constexpr int kStreamThreads = kStreamWarps * 32;
 constexpr int kStreamUnitBytes = 2048;            // per operand
-constexpr int kCompactThreads = 256;  // units per CTA of k1_compact
+constexpr int kCompactThreads = 256;
+constexpr int kCompactPerThread = 8;
+constexpr int kCompactUnits = kCompactThreads * kCompactPerThread;  // per CTA of k1_compact
 
 template <typename T>
 __host__ __device__ constexpr int stream_unit_elems() {
@@ -56,6 +58,8 @@ struct StreamArgs {
   // "nonzero last step" bit per sector (64 per unit)
   void* dense;
   unsigned long long* dirty;
+  // single-worker model update x -= g/n at the selections, fused (kModel)
+  void* model;
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -72,7 +76,10 @@ __device__ __forceinline__ unsigned even_bits(unsigned x) {
   return x;
 }
 
-template <typename T, int kMode, bool kDense>
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T, int kMode, bool kDense, bool kModel = false>
 __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -186,6 +193,28 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     if (lane == 0 && now != prev) a.dirty[u] = now;
   }
 
+  if (kModel) {
+    // n = 1: x[j] -= g/n = (0 + acc) / 1 = acc at the selections
+    // (harness.cpp:212-215); only lanes holding a selection touch x
+    T* X = (T*)a.model + base;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      if (!mask[i]) continue;
+      const int off = (i * 32 + lane) * VN;
+      if (elems == UE) {
+        V x = reinterpret_cast<const V*>(X)[i * 32 + lane];
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+          if (mask[i] & (1u << c)) set_comp(x, c, sub_rn(comp(x, c), comp(e[i], c)));
+        reinterpret_cast<V*>(X)[i * 32 + lane] = x;
+      } else {
+#pragma unroll
+        for (int c = 0; c < VN; ++c)
+          if (mask[i] & (1u << c)) X[off + c] = sub_rn(X[off + c], comp(e[i], c));
+      }
+    }
+  }
+
   if (sel_unit) {
     // order inside the unit: (vector i, lane, component c); the VPL per-lane
     // counts are packed as 8-bit fields (warp totals <= 128)
@@ -241,20 +270,31 @@ struct CompactArgs {
   int* flags;              // bit1 capacity overflow
 };
 
-// One thread per unit count, 256 units per CTA.  Offsets: warp scan + CTA
-// scan + one decoupled look-back across CTAs.  Copy: each warp moves the
-// pairs of its 32 units as one flattened list — lane L handles pairs
-// L, L+32, ... and finds its unit by a 5-step shuffle binary search over
-// the warp's inclusive prefix — so loads and stores are coalesced.
+// kCompactPerThread consecutive unit counts per thread, 2048 units per CTA
+// (so the decoupled look-back spans ~130 CTAs at C3, not ~1000: with every
+// CTA resident at once, the look-back depth grows with the CTA count).
+// Offsets: warp scan + CTA scan + one look-back.  Copy: each warp moves the
+// pairs of its 256 units as one flattened list — lane L takes pairs L, L+32,
+// ... and finds its (lane, unit) by a shuffle binary search over the warp's
+// per-lane prefix, then a walk over that lane's kCompactPerThread counts —
+// so loads and stores are coalesced.  The staged runs are dead afterwards:
+// their L2 lines are discarded without write-back.
 template <typename T>
 __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
+  constexpr int UPT = kCompactPerThread;
   __shared__ int s_w[kCompactThreads / 32];
   __shared__ long long s_excl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
-  const int u = b * kCompactThreads + tid;
-  const int cnt = u < a.num_units ? a.unit_counts[u] : 0;
-  int incl = cnt;
+  const int u0 = (b * kCompactThreads + tid) * UPT;  // this thread's first unit
+  int cnt[UPT];
+  int mine = 0;
+#pragma unroll
+  for (int q = 0; q < UPT; ++q) {
+    cnt[q] = u0 + q < a.num_units ? a.unit_counts[u0 + q] : 0;
+    mine += cnt[q];
+  }
+  int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -287,35 +327,46 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
   }
   __syncthreads();
   const long long dst0 = s_excl + wpre;
-  const int u_first = b * kCompactThreads + w * 32;  // the warp's first unit
+  const int wu0 = (b * kCompactThreads + w * 32) * UPT;  // the warp's first unit
   int32_t* __restrict__ oi = a.sel_idx;
   T* __restrict__ ov = (T*)a.sel_val;
   const int32_t* __restrict__ si = a.stage_idx;
   const T* __restrict__ sv = (const T*)a.stage_val;
   for (int p0 = 0; p0 < wtot; p0 += 32) {  // whole-warp iterations: the shuffles need every lane
     const int p = p0 + lane;
-    // unit q of the warp holding pair p: smallest q with incl_q > p
-    int q = 0;
+    int q = 0;  // lane of the warp holding pair p: smallest q with incl_q > p
 #pragma unroll
     for (int step = 16; step > 0; step >>= 1) {
       const int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
       if (v <= p) q += step;
     }
-    const int before = __shfl_sync(0xffffffffu, incl - cnt, q & 31);
-    const long long src = (long long)(u_first + q) * a.unit_elems + (p - before);
+    q &= 31;
+    int r = p - __shfl_sync(0xffffffffu, incl - mine, q);  // rank inside lane q's units
+    int k = 0;
+#pragma unroll
+    for (int z = 0; z < UPT; ++z) {  // lane q's counts, every lane shuffles
+      const int cz = __shfl_sync(0xffffffffu, cnt[z], q);
+      if (k == z && r >= cz) {
+        r -= cz;
+        k = z + 1;
+      }
+    }
+    const long long src = (long long)(wu0 + q * UPT + k) * a.unit_elems + r;
     const long long d = dst0 + p;
     if (p < wtot && d < a.cap) {
       oi[d] = si[src];
       ov[d] = sv[src];
     }
   }
-  // the staged runs are dead now: drop their L2 lines without write-back
-  if (cnt) {
-    const long long s0 = (long long)u * a.unit_elems;
-    const char* pi = reinterpret_cast<const char*>(si + s0);
-    const char* pv = reinterpret_cast<const char*>(sv + s0);
-    for (int off = 0; off < cnt * 4; off += 128) discard_l2_line(pi + off);
-    for (int off = 0; off < cnt * (int)sizeof(T); off += 128) discard_l2_line(pv + off);
+#pragma unroll
+  for (int z = 0; z < UPT; ++z) {
+    if (cnt[z]) {
+      const long long s0 = (long long)(u0 + z) * a.unit_elems;
+      const char* pi = reinterpret_cast<const char*>(si + s0);
+      const char* pv = reinterpret_cast<const char*>(sv + s0);
+      for (int off = 0; off < cnt[z] * 4; off += 128) discard_l2_line(pi + off);
+      for (int off = 0; off < cnt[z] * (int)sizeof(T); off += 128) discard_l2_line(pv + off);
+    }
   }
 }
 
