@@ -352,23 +352,18 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.dirty = c->dense_dirty;
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
-  a.model = c->model;
-  const bool fd = c->dense_fused, fm = c->n == 1 && c->model != nullptr;
+  const bool fd = c->dense_fused;
   cudaStream_t st = c->stream;
-#define K1S(MODE, D, M) k1_stream<T, MODE, D, M><<<grid, kStreamThreads, 0, st>>>(a)
+#define K1S(MODE, D) k1_stream<T, MODE, D><<<grid, kStreamThreads, 0, st>>>(a)
   if (c->n > 1) {
-    if (c->cfg.error_feedback) K1S(kWriteZeroSel, false, false);
-    else K1S(kWriteAcc, false, false);
+    if (c->cfg.error_feedback) K1S(kWriteZeroSel, false);
+    else K1S(kWriteAcc, false);
   } else if (c->cfg.error_feedback) {
-    if (fd && fm) K1S(kWriteZeroSel, true, true);
-    else if (fd) K1S(kWriteZeroSel, true, false);
-    else if (fm) K1S(kWriteZeroSel, false, true);
-    else K1S(kWriteZeroSel, false, false);
+    if (fd) K1S(kWriteZeroSel, true);
+    else K1S(kWriteZeroSel, false);
   } else {
-    if (fd && fm) K1S(kWriteNone, true, true);
-    else if (fd) K1S(kWriteNone, true, false);
-    else if (fm) K1S(kWriteNone, false, true);
-    else K1S(kWriteNone, false, false);
+    if (fd) K1S(kWriteNone, true);
+    else K1S(kWriteNone, false);
   }
 #undef K1S
   CU(cudaGetLastError());
@@ -466,8 +461,7 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
     f.prev_K = c->Kbuf + pb;
   }
   f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
-  // n = 1 with the streaming K1: the model update happened inside K1
-  f.model = (c->n == 1 && c->k1_kind == 0) ? nullptr : c->model;
+  f.model = c->model;
   f.slot = c->steps % kHistCap;
   f.hist_t = c->hist_t;
   f.hist_K = c->hist_K;

@@ -201,33 +201,33 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   const int32_t* cur = a.union_idx;
   const T nf = (T)a.n;
   const long long stride = (long long)gridDim.x * blockDim.x;
+  if (x) {  // harness.cpp:212-215: x[j] -= s_j / n, one thread per union entry
+    for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < K; m += stride) {
+      const int32_t j = cur[m];
+      x[j] = x[j] - div_rn(sums[m], nf);  // one rounding after the division
+    }
+  }
+  if (!dense) return;
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < K; m += stride) {
     const int64_t s = cur[m] / SEC;
     if (m > 0 && cur[m - 1] / SEC == s) continue;  // not the sector's owner
     T v[SEC];
 #pragma unroll
     for (int c = 0; c < SEC; ++c) v[c] = (T)0;
-    for (long long q = m; q < K && cur[q] / SEC == s; ++q) {
-      const int32_t j = cur[q];
-      const T avg = div_rn(sums[q], nf);
-      v[j % SEC] = avg;
-      if (x) x[j] = x[j] - avg;  // one rounding after the division
-    }
-    if (dense) {
-      T* p = dense + s * SEC;
-      if ((s + 1) * SEC <= a.n_g) {
-        using V = typename Vec<T>::V;
-        constexpr int VN = Vec<T>::N;
+    for (long long q = m; q < K && cur[q] / SEC == s; ++q) v[cur[q] % SEC] = div_rn(sums[q], nf);
+    T* p = dense + s * SEC;
+    if ((s + 1) * SEC <= a.n_g) {
+      using V = typename Vec<T>::V;
+      constexpr int VN = Vec<T>::N;
 #pragma unroll
-        for (int h = 0; h < SEC / VN; ++h) {
-          V w;
+      for (int h = 0; h < SEC / VN; ++h) {
+        V w;
 #pragma unroll
-          for (int c = 0; c < VN; ++c) set_comp(w, c, v[h * VN + c]);
-          reinterpret_cast<V*>(p)[h] = w;
-        }
-      } else {
-        for (int c = 0; c < SEC && s * SEC + c < a.n_g; ++c) p[c] = v[c];
+        for (int c = 0; c < VN; ++c) set_comp(w, c, v[h * VN + c]);
+        reinterpret_cast<V*>(p)[h] = w;
       }
+    } else {
+      for (int c = 0; c < SEC && s * SEC + c < a.n_g; ++c) p[c] = v[c];
     }
   }
 }

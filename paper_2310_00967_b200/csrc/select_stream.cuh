@@ -34,7 +34,7 @@ constexpr int kStreamWarps = 8;                  // units per CTA
 constexpr int kStreamThreads = kStreamWarps * 32;
 constexpr int kStreamUnitBytes = 2048;            // per operand
 constexpr int kCompactThreads = 256;
-constexpr int kCompactPerThread = 8;
+constexpr int kCompactPerThread = 1;
 constexpr int kCompactUnits = kCompactThreads * kCompactPerThread;  // per CTA of k1_compact
 
 template <typename T>
@@ -58,8 +58,6 @@ struct StreamArgs {
   // "nonzero last step" bit per sector (64 per unit)
   void* dense;
   unsigned long long* dirty;
-  // single-worker model update x -= g/n at the selections, fused (kModel)
-  void* model;
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -79,7 +77,7 @@ __device__ __forceinline__ unsigned even_bits(unsigned x) {
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
-template <typename T, int kMode, bool kDense, bool kModel = false>
+template <typename T, int kMode, bool kDense>
 __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -193,28 +191,6 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     if (lane == 0 && now != prev) a.dirty[u] = now;
   }
 
-  if (kModel) {
-    // n = 1: x[j] -= g/n = (0 + acc) / 1 = acc at the selections
-    // (harness.cpp:212-215); only lanes holding a selection touch x
-    T* X = (T*)a.model + base;
-#pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      if (!mask[i]) continue;
-      const int off = (i * 32 + lane) * VN;
-      if (elems == UE) {
-        V x = reinterpret_cast<const V*>(X)[i * 32 + lane];
-#pragma unroll
-        for (int c = 0; c < VN; ++c)
-          if (mask[i] & (1u << c)) set_comp(x, c, sub_rn(comp(x, c), comp(e[i], c)));
-        reinterpret_cast<V*>(X)[i * 32 + lane] = x;
-      } else {
-#pragma unroll
-        for (int c = 0; c < VN; ++c)
-          if (mask[i] & (1u << c)) X[off + c] = sub_rn(X[off + c], comp(e[i], c));
-      }
-    }
-  }
-
   if (sel_unit) {
     // order inside the unit: (vector i, lane, component c); the VPL per-lane
     // counts are packed as 8-bit fields (warp totals <= 128)
@@ -270,9 +246,8 @@ struct CompactArgs {
   int* flags;              // bit1 capacity overflow
 };
 
-// kCompactPerThread consecutive unit counts per thread, 2048 units per CTA
-// (so the decoupled look-back spans ~130 CTAs at C3, not ~1000: with every
-// CTA resident at once, the look-back depth grows with the CTA count).
+// kCompactPerThread consecutive unit counts per thread (1: measured 8 was
+// slower — fewer warps, longer per-warp copy chains).
 // Offsets: warp scan + CTA scan + one look-back.  Copy: each warp moves the
 // pairs of its 256 units as one flattened list — lane L takes pairs L, L+32,
 // ... and finds its (lane, unit) by a shuffle binary search over the warp's

@@ -8,3 +8,5 @@ P="python bench.py --steps 5 --warmup 3 --prime 400 --no-cpu-baseline"
 timeout 300 $P > gpurun_out/prof_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 1610 -c 40 --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launch.log 2>&1
 echo launches rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_|k_finalize" -s 1203 -c 3 -o gpurun_out/k1_full $P > gpurun_out/ncu_full.log 2>&1
+echo full rc=$?
