@@ -173,7 +173,8 @@ struct micro_ctx {
   int k1_cfg = 0;               // streaming configuration (MICRO_K1_CFG)
   int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
   void* stage_val = nullptr;
-  int* unit_counts = nullptr;    // selections per K1 unit (TMA kernel)
+  int* unit_counts = nullptr;    // selections per K1 unit / per k1_stream CTA run
+  int* run_offsets = nullptr;    // k1_scan output
   unsigned int* ticket = nullptr;
   unsigned int epoch = 0;
   int* flags = nullptr;
@@ -370,9 +371,10 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   CompactArgs b{};
   b.stage_idx = c->stage_idx;
   b.stage_val = c->stage_val;
-  b.unit_counts = c->unit_counts;
-  b.num_units = a.unit_hi - a.unit_lo + 1;
-  b.unit_elems = UE;
+  b.run_counts = c->unit_counts;
+  b.run_offsets = c->run_offsets;
+  b.num_runs = a.unit_hi / kStreamWarps - a.unit_lo / kStreamWarps + 1;
+  b.run_stride = kStreamWarps * UE;
   b.sel_idx = c->sel_idx[c->buf][i];
   b.sel_val = c->sel_val[c->buf][i];
   b.cap = c->sel_cap;
@@ -380,10 +382,13 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.status = c->status;
   b.epoch = next_epoch(c);
   b.flags = c->flags;
-  const int64_t blocks = (b.num_units + kCompactUnits - 1) / kCompactUnits;
+  b.model = c->n == 1 ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
+  const int64_t blocks = (b.num_runs + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems);
   if (blocks > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
   b.status_len = status_span(c, blocks);
-  k1_compact<T><<<(unsigned)blocks, kCompactThreads, 0, c->stream>>>(b);
+  k1_scan<<<(unsigned)blocks, kScanThreads, 0, c->stream>>>(b);
+  CU(cudaGetLastError());
+  k1_gather<T><<<(unsigned)((b.num_runs + 7) / 8), 256, 0, c->stream>>>(b);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
@@ -461,7 +466,8 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
     f.prev_K = c->Kbuf + pb;
   }
   f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
-  f.model = c->model;
+  // n = 1 with the streaming K1: k1_gather applied the model update
+  f.model = (c->n == 1 && c->k1_kind == 0) ? nullptr : c->model;
   f.slot = c->steps % kHistCap;
   f.hist_t = c->hist_t;
   f.hist_K = c->hist_K;
@@ -762,6 +768,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     if ((rc = c->alloc((void**)&c->stage_idx, stage * 4))) return cleanup(rc);
     if ((rc = c->alloc(&c->stage_val, stage * c->esz))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->unit_counts, (max_range / 128 + 8) * sizeof(int)))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->run_offsets, (max_range / 128 + 8) * sizeof(int)))) return cleanup(rc);
   }
   if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->flags, sizeof(int)))) return cleanup(rc);
@@ -773,7 +780,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
     return cleanup(fail(MICRO_ECUDA, "memset: %s", cudaGetErrorString(e)));
-  if (c->dense) {
+  if (c->dense && !c->dense_fused) {
     if ((e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess)
@@ -793,6 +800,7 @@ int micro_ctx_destroy(micro_ctx* c) {
   if (c->staging) cudaFree(c->staging);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+
   if (c->aux) cudaStreamDestroy(c->aux);
   delete c;
   return MICRO_OK;

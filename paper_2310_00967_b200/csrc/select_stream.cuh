@@ -13,9 +13,10 @@
 //      staging slot [(u - u_lo) * 512, + k_u), recording k_u.  No ordering,
 //      no cross-warp or cross-CTA dependency: the pass runs at the HBM
 //      roofline like a plain axpy (tools/k1_probe.cu: 6.2-7.0 TB/s).
-// K1b  k1_compact: scans the per-unit counts (1024 units per CTA, decoupled
-//      look-back across CTAs) and copies every unit's staged run to its
-//      final position, giving the ascending (index, value) list and k_i.
+// K1b  k1_scan: exclusive prefix of the per-CTA run counts (8192 per CTA,
+//      one decoupled look-back over a handful of CTAs) -> k_i;
+// K1c  k1_gather: one warp per run copies it, coalesced, to its final
+//      position, giving the ascending (index, value) list.
 //
 // Why not one pass: every single-pass variant we measured (per-tile
 // look-back; persistent CTAs with TMA bulk-copy rings; per-warp rings;
@@ -33,9 +34,7 @@ namespace micro {
 constexpr int kStreamWarps = 8;                  // units per CTA
 constexpr int kStreamThreads = kStreamWarps * 32;
 constexpr int kStreamUnitBytes = 2048;            // per operand
-constexpr int kCompactThreads = 256;
-constexpr int kCompactPerThread = 1;
-constexpr int kCompactUnits = kCompactThreads * kCompactPerThread;  // per CTA of k1_compact
+
 
 template <typename T>
 __host__ __device__ constexpr int stream_unit_elems() {
@@ -85,17 +84,19 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   constexpr int VPL = UE / VN / 32;  // 4 vectors per lane per operand
   static_assert(VPL * VN * 32 == UE && VPL <= 4, "unit layout");
 
-  const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * kStreamWarps + (threadIdx.x >> 5);
+  __shared__ int s_cnt[kStreamWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int u = blockIdx.x * kStreamWarps + w;
   const int base = u * UE;
-  if (base >= a.n_g) return;  // warp-uniform
-  const int elems = a.n_g - base < UE ? a.n_g - base : UE;
+  // warps past the vector's end idle but still meet the CTA barrier below
+  const int elems = base >= a.n_g ? 0 : (a.n_g - base < UE ? a.n_g - base : UE);
+  const bool live = elems > 0;
   const T* __restrict__ Gp = (const T*)a.grad + base;
   T* __restrict__ E = (T*)a.resid + base;
 
   const unsigned long long pol_stream = policy_evict_first();
   V e[VPL], g[VPL];
-  if (elems == UE) {
+  if (elems == UE) {  // (elems == 0 for dead warps: the guarded path below loads nothing)
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       e[i] = ld_hint(reinterpret_cast<const V*>(E) + i * 32 + lane, pol_stream);
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
       }
   }
 
-  const bool sel_unit = u >= a.unit_lo && u <= a.unit_hi;
+  const bool sel_unit = live && u >= a.unit_lo && u <= a.unit_hi;
   const bool all_in = base >= a.p_start && base + elems <= a.p_end;
   const T thr = threshold_as(*a.delta, (T*)nullptr);
   const T eta = (T)a.eta;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     }
   }
 
-  if (kDense) {
+  if (kDense && live) {  // live is warp-uniform: the shuffles below see every lane
     // n = 1: g/n = (0 + acc) / 1 = acc at the selections (never +-0: |acc| >
     // delta >= 0), 0 elsewhere.  A 32-byte sector is written in full when it
     // holds a selection now or held one last step; lanes 2k and 2k+1 own its
@@ -191,12 +192,16 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     if (lane == 0 && now != prev) a.dirty[u] = now;
   }
 
-  if (sel_unit) {
-    // order inside the unit: (vector i, lane, component c); the VPL per-lane
-    // counts are packed as 8-bit fields (warp totals <= 128)
+  // ---- ordered compaction of the CTA's 8 units into one contiguous run ----
+  // order inside a unit: (vector i, lane, component c); the VPL per-lane
+  // counts are packed as 8-bit fields (warp totals <= 128); units in warp
+  // order inside the CTA.  Runs live at staging slot (CTA - cta_lo) * 8 * UE.
+  const int cta_lo = a.unit_lo / kStreamWarps, cta_hi = a.unit_hi / kStreamWarps;
+  const bool sel_cta = (int)blockIdx.x >= cta_lo && (int)blockIdx.x <= cta_hi;  // CTA-uniform
+  if (sel_cta) {
     unsigned packed = 0;
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) packed |= (unsigned)__popc(mask[i]) << (8 * i);
+    for (int i = 0; i < VPL; ++i) packed |= (unsigned)__popc(mask[i]) << (8 * i);  // mask = 0 unless sel_unit
     unsigned incl = packed;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -204,28 +209,42 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
       if (lane >= o) incl += y;
     }
     const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
-    const unsigned excl = incl - packed;
-    const int slot = u - a.unit_lo;
-    const unsigned long long pol_keep = policy_evict_last();  // read back by k1_compact, then discarded
-    unsigned cb = 0;
-    int32_t* __restrict__ si = a.stage_idx + (long long)slot * UE;
-    T* __restrict__ sv = (T*)a.stage_val + (long long)slot * UE;
+    unsigned unit_count = 0;
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      if (mask[i]) {
-        int pos = (int)(cb + ((excl >> (8 * i)) & 0xFFu));
-        const int j0 = base + (i * 32 + lane) * VN;
+    for (int i = 0; i < VPL; ++i) unit_count += (tot >> (8 * i)) & 0xFFu;
+    if (lane == 0) s_cnt[w] = (int)unit_count;
+    __syncthreads();
+    int woff = 0, cta_count = 0;
 #pragma unroll
-        for (int c = 0; c < VN; ++c)
-          if (mask[i] & (1u << c)) {
-            st_hint(si + pos, j0 + c, pol_keep);
-            st_hint(sv + pos, comp(e[i], c), pol_keep);
-            ++pos;
-          }
-      }
-      cb += (tot >> (8 * i)) & 0xFFu;
+    for (int q = 0; q < kStreamWarps; ++q) {
+      const int x = s_cnt[q];
+      woff += q < w ? x : 0;
+      cta_count += x;
     }
-    if (lane == 0) a.unit_counts[slot] = (int)cb;
+    const int slot = (int)blockIdx.x - cta_lo;
+    if (threadIdx.x == 0) a.unit_counts[slot] = cta_count;
+    if (unit_count) {
+      const unsigned excl = incl - packed;
+      const unsigned long long pol_keep = policy_evict_last();  // read back by k1_gather, then discarded
+      int32_t* __restrict__ si = a.stage_idx + (long long)slot * (kStreamWarps * UE) + woff;
+      T* __restrict__ sv = (T*)a.stage_val + (long long)slot * (kStreamWarps * UE) + woff;
+      unsigned cb = 0;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        if (mask[i]) {
+          int pos = (int)(cb + ((excl >> (8 * i)) & 0xFFu));
+          const int j0 = base + (i * 32 + lane) * VN;
+#pragma unroll
+          for (int c = 0; c < VN; ++c)
+            if (mask[i] & (1u << c)) {
+              st_hint(si + pos, j0 + c, pol_keep);
+              st_hint(sv + pos, comp(e[i], c), pol_keep);
+              ++pos;
+            }
+        }
+        cb += (tot >> (8 * i)) & 0xFFu;
+      }
+    }
   }
   if (probe != probe) atomicOr(a.flags, 1);
 }
@@ -233,9 +252,10 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
 struct CompactArgs {
   const int32_t* stage_idx;
   const void* stage_val;
-  const int* unit_counts;
-  int num_units;           // partition units
-  int unit_elems;
+  const int* run_counts;   // pairs per CTA run (k1_stream)
+  int* run_offsets;        // exclusive prefix (k1_scan -> k1_gather)
+  int num_runs;
+  int run_stride;          // staging elements per run slot
   int32_t* sel_idx;
   void* sel_val;
   long long cap;
@@ -244,30 +264,26 @@ struct CompactArgs {
   long long status_len;
   unsigned int epoch;
   int* flags;              // bit1 capacity overflow
+  void* model;             // n = 1: x -= g/n = acc at the selections (harness.cpp:212-215)
 };
 
-// kCompactPerThread consecutive unit counts per thread (1: measured 8 was
-// slower — fewer warps, longer per-warp copy chains).
-// Offsets: warp scan + CTA scan + one look-back.  Copy: each warp moves the
-// pairs of its 256 units as one flattened list — lane L takes pairs L, L+32,
-// ... and finds its (lane, unit) by a shuffle binary search over the warp's
-// per-lane prefix, then a walk over that lane's kCompactPerThread counts —
-// so loads and stores are coalesced.  The staged runs are dead afterwards:
-// their L2 lines are discarded without write-back.
-template <typename T>
-__global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
-  constexpr int UPT = kCompactPerThread;
-  __shared__ int s_w[kCompactThreads / 32];
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;  // run counts per thread: 8192 per CTA
+
+// Exclusive prefix of the run counts: 8192 runs per CTA, block scan, one
+// decoupled look-back across the (few) CTAs; the last CTA writes k_i.
+__global__ void __launch_bounds__(kScanThreads) k1_scan(CompactArgs a) {
+  __shared__ int s_w[kScanThreads / 32];
   __shared__ long long s_excl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
-  const int u0 = (b * kCompactThreads + tid) * UPT;  // this thread's first unit
-  int cnt[UPT];
+  const int r0 = (b * kScanThreads + tid) * kScanItems;
+  int v[kScanItems];
   int mine = 0;
 #pragma unroll
-  for (int q = 0; q < UPT; ++q) {
-    cnt[q] = u0 + q < a.num_units ? a.unit_counts[u0 + q] : 0;
-    mine += cnt[q];
+  for (int q = 0; q < kScanItems; ++q) {
+    v[q] = r0 + q < a.num_runs ? a.run_counts[r0 + q] : 0;
+    mine += v[q];
   }
   int incl = mine;
 #pragma unroll
@@ -275,22 +291,22 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
-  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
   if (lane == 31) s_w[w] = incl;
   __syncthreads();
-  int wpre = 0, tot = 0;
-#pragma unroll
-  for (int q = 0; q < kCompactThreads / 32; ++q) {
-    const int x = s_w[q];
-    wpre += q < w ? x : 0;
-    tot += x;
-  }
   if (w == 0) {
-    const long long ex = lookback(a.status, b, (unsigned long long)tot, a.epoch, lane);
+    int x = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_w[lane] = x;  // inclusive warp prefix
+    const unsigned long long tot = (unsigned long long)__shfl_sync(0xffffffffu, x, 31);
+    const long long ex = lookback(a.status, b, tot, a.epoch, lane);
     if (lane == 0) {
       s_excl = ex;
       if (b == G - 1) {
-        const long long total = ex + tot;
+        const long long total = ex + (long long)tot;
         *a.count = total;
         if (total > a.cap) atomicOr(a.flags, 2);
       }
@@ -301,48 +317,45 @@ __global__ void __launch_bounds__(kCompactThreads) k1_compact(CompactArgs a) {
     }
   }
   __syncthreads();
-  const long long dst0 = s_excl + wpre;
-  const int wu0 = (b * kCompactThreads + w * 32) * UPT;  // the warp's first unit
-  int32_t* __restrict__ oi = a.sel_idx;
-  T* __restrict__ ov = (T*)a.sel_val;
-  const int32_t* __restrict__ si = a.stage_idx;
-  const T* __restrict__ sv = (const T*)a.stage_val;
-  for (int p0 = 0; p0 < wtot; p0 += 32) {  // whole-warp iterations: the shuffles need every lane
-    const int p = p0 + lane;
-    int q = 0;  // lane of the warp holding pair p: smallest q with incl_q > p
+  long long off = s_excl + (w ? s_w[w - 1] : 0) + incl - mine;
 #pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int v = __shfl_sync(0xffffffffu, incl, q + step - 1);
-      if (v <= p) q += step;
-    }
-    q &= 31;
-    int r = p - __shfl_sync(0xffffffffu, incl - mine, q);  // rank inside lane q's units
-    int k = 0;
-#pragma unroll
-    for (int z = 0; z < UPT; ++z) {  // lane q's counts, every lane shuffles
-      const int cz = __shfl_sync(0xffffffffu, cnt[z], q);
-      if (k == z && r >= cz) {
-        r -= cz;
-        k = z + 1;
-      }
-    }
-    const long long src = (long long)(wu0 + q * UPT + k) * a.unit_elems + r;
-    const long long d = dst0 + p;
-    if (p < wtot && d < a.cap) {
-      oi[d] = si[src];
-      ov[d] = sv[src];
+  for (int q = 0; q < kScanItems; ++q) {
+    if (r0 + q < a.num_runs) a.run_offsets[r0 + q] = (int)(off < a.cap ? off : a.cap);
+    off += v[q];
+  }
+}
+
+// One warp per CTA run: coalesced copy into the ordered output, then the
+// run's staging lines are dropped from L2 without write-back.
+template <typename T>
+__global__ void __launch_bounds__(256) k1_gather(CompactArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= a.num_runs) return;
+  const int n = a.run_counts[r];
+  if (!n) return;
+  const long long off = a.run_offsets[r];
+  const long long src = (long long)r * a.run_stride;
+  const int32_t* __restrict__ si = a.stage_idx + src;
+  const T* __restrict__ sv = (const T*)a.stage_val + src;
+  int32_t* __restrict__ oi = a.sel_idx + off;
+  T* __restrict__ ov = (T*)a.sel_val + off;
+  const long long room = a.cap - off;
+  T* __restrict__ x = (T*)a.model;
+  for (int m = lane; m < n; m += 32) {
+    if (m < room) {
+      const int32_t j = si[m];
+      const T v = sv[m];
+      oi[m] = j;
+      ov[m] = v;
+      // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
+      if (x) x[j] = x[j] - v;
     }
   }
-#pragma unroll
-  for (int z = 0; z < UPT; ++z) {
-    if (cnt[z]) {
-      const long long s0 = (long long)(u0 + z) * a.unit_elems;
-      const char* pi = reinterpret_cast<const char*>(si + s0);
-      const char* pv = reinterpret_cast<const char*>(sv + s0);
-      for (int off = 0; off < cnt[z] * 4; off += 128) discard_l2_line(pi + off);
-      for (int off = 0; off < cnt[z] * (int)sizeof(T); off += 128) discard_l2_line(pv + off);
-    }
-  }
+  __syncwarp();
+  for (int o = lane * 128; o < n * 4; o += 32 * 128) discard_l2_line(reinterpret_cast<const char*>(si) + o);
+  for (int o = lane * 128; o < n * (int)sizeof(T); o += 32 * 128)
+    discard_l2_line(reinterpret_cast<const char*>(sv) + o);
 }
 
 }  // namespace micro

@@ -34,13 +34,25 @@ from ._lib import check, lib
 from .engine import Micro, device_view
 
 
-def exchange(ops, group=None) -> int:
-    """Run K2..K8 for one rank after ops' compress.  Returns |union|."""
+def exchange(ops, group=None, comm_device=None) -> int:
+    """Run K2..K8 for one rank after ops' compress.  Returns |union|.
+
+    Collectives run on ``ops.device`` tensors (NCCL).  ``comm_device`` (e.g.
+    ``"cpu"`` with gloo) stages them through another device instead — used to
+    run several ranks' device halves on one GPU in tests."""
     n = dist.get_world_size(group)
     me = dist.get_rank(group)
     dev = ops.device
-    cnt = torch.empty(n, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(cnt, ops.own_count(), group=group)            # K2
+    cdev = torch.device(comm_device) if comm_device is not None else dev
+
+    def to_c(t):
+        return t if t.device == cdev else t.to(cdev)
+
+    def to_d(t):
+        return t if t.device == dev else t.to(dev)
+
+    cnt = torch.empty(n, dtype=torch.int64, device=cdev)
+    dist.all_gather_into_tensor(cnt, to_c(ops.own_count()), group=group)      # K2
     counts = [int(v) for v in cnt.cpu().tolist()]
     kmax = max(counts)
     if kmax > ops.capacity:  # every rank sees the same counts, so every rank raises
@@ -49,18 +61,19 @@ def exchange(ops, group=None) -> int:
     if kmax == 0:
         ops.finalize(None, None, counts, 0)
         return 0
-    all_idx = torch.empty(n * kmax, dtype=torch.int32, device=dev)
-    dist.all_gather_into_tensor(all_idx, ops.own_indices(kmax), group=group)  # K3
-    send = ops.gather_foreign(all_idx, counts, kmax)                           # K4
-    recv = torch.empty((n - 1) * counts[me], dtype=ops.dtype, device=dev)
+    all_idx = torch.empty(n * kmax, dtype=torch.int32, device=cdev)
+    dist.all_gather_into_tensor(all_idx, to_c(ops.own_indices(kmax)), group=group)  # K3
+    all_idx = to_d(all_idx)
+    send = to_c(ops.gather_foreign(all_idx, counts, kmax))                     # K4
+    recv = torch.empty((n - 1) * counts[me], dtype=ops.dtype, device=cdev)
     dist.all_to_all_single(recv, send,                                          # K5
                            output_split_sizes=[0 if r == me else counts[me] for r in range(n)],
                            input_split_sizes=[0 if o == me else counts[o] for o in range(n)],
                            group=group)
-    own_sums = ops.owner_reduce(recv, counts, kmax)                            # K6
-    all_sums = torch.empty(n * kmax, dtype=ops.dtype, device=dev)
+    own_sums = to_c(ops.owner_reduce(to_d(recv), counts, kmax))                # K6
+    all_sums = torch.empty(n * kmax, dtype=ops.dtype, device=cdev)
     dist.all_gather_into_tensor(all_sums, own_sums, group=group)               # K7
-    ops.finalize(all_idx, all_sums, counts, kmax)                               # K8
+    ops.finalize(all_idx, to_d(all_sums), counts, kmax)                         # K8
     return sum(counts)
 
 
@@ -104,7 +117,7 @@ class DeviceOps:
 class DistMicro:
     """One rank's MiCRO engine; same calls as :class:`engine.Micro`."""
 
-    def __init__(self, n_g: int, group=None, **kw):
+    def __init__(self, n_g: int, group=None, comm_device=None, **kw):
         if not dist.is_initialized():
             raise _lib.LogicError(_lib.MICRO_ELOGIC, "torch.distributed is not initialized")
         self.group = group
@@ -113,12 +126,13 @@ class DistMicro:
         self.m = Micro(n_g, self.world, n_local=1, rank=self.rank, **kw)
         self.ops = DeviceOps(self.m)
         self.n_g = n_g
+        self.comm_device = comm_device
 
     def compress(self, grads, eta: float, t: int):
         self.m.compress(grads, eta, t)
 
     def aggregate(self) -> int:
-        return exchange(self.ops, self.group)
+        return exchange(self.ops, self.group, self.comm_device)
 
     def step(self, grads, eta: float, t: int) -> int:
         self.compress(grads, eta, t)

@@ -1,0 +1,82 @@
+"""The multi-rank path's DEVICE halves (micro_dist_gather_foreign /
+owner_reduce / finalize through DistMicro) on a real GPU: world size 2 and 3,
+every rank on cuda:0 (each rank is its own process and context; the ranks
+only meet in host-side gloo collectives, so no kernel waits on another
+rank's kernel).  Every rank's union, sums, residual, dense g/n and threshold
+must equal the in-process oracle cluster bit for bit.  GPU only."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, n_g, iters, ef, q):
+    import sys
+    sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+    from oracle import Oracle, OracleCluster
+
+    from paper_2310_00967_b200.dist import DistMicro
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    o = Oracle()
+    d, delta0, eta = 0.02, 0.015, 0.01
+    m = DistMicro(n_g, comm_device="cpu", density=d, initial_threshold=delta0, error_feedback=ef)
+    x = torch.zeros(n_g, device="cuda")
+    m.set_model(x)
+    ref = OracleCluster(n_g, world, density=d, delta0=delta0, error_feedback=ef, model=True)
+    bad = []
+    for t in range(iters):
+        G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)])
+        K = m.step([torch.from_numpy(G[rank]).cuda()], eta, t)
+        r = ref.step(G, eta, t)
+        idx, sums = m.union()
+        st = m.query()
+        if K != r["union_idx"].size or not np.array_equal(idx, r["union_idx"]):
+            bad.append((t, "union"))
+        if not np.array_equal(sums, r["union_sum"]):
+            bad.append((t, "sums"))
+        if st.counts[0] != r["counts"][rank]:
+            bad.append((t, "count"))
+        if not np.array_equal(m.residual(0), ref.e[rank]):
+            bad.append((t, "residual"))
+        if st.deltas[0] != r["delta_next"][rank]:
+            bad.append((t, "delta"))
+        dw = np.zeros(n_g, np.float32)
+        dw[r["union_idx"]] = r["union_sum"] / np.float32(world)
+        if not np.array_equal(m.dense(), dw):
+            bad.append((t, "dense"))
+        if not np.array_equal(x.cpu().numpy(), ref.x):
+            bad.append((t, "model"))
+    dist.destroy_process_group()
+    q.put((rank, bad))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,n_g,ef", [(2, 100_003, True), (3, 50_000, True), (2, 20_000, False)])
+def test_dist_device_halves_one_gpu(world, n_g, ef):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_g, 10, ef, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, bad in res:
+        assert not bad, (rank, bad[:5])
