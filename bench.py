@@ -227,6 +227,7 @@ def our_arm(args, wl):
         dist.barrier()
     torch.cuda.synchronize()
     t_first = t
+    m.kernel_timing(True)  # CUDA events around K1's streaming pass, inside the library
     with ClockSampler(local) as clk:
         start.record(stream)
         for s in range(args.steps):
@@ -240,7 +241,9 @@ def our_arm(args, wl):
     if dist:
         dist.barrier()
     total_ms = start.elapsed_time(end)
-    k1_ms = [a.elapsed_time(b) for a, b in evs]
+    k1_ms = [a.elapsed_time(b) for a, b in evs]  # whole compress: stream + scan + gather(+model)
+    k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone
+    m.kernel_timing(False)
     if dist:
         v = torch.tensor([total_ms, statistics.mean(k1_ms)], device=dev, dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
@@ -251,11 +254,17 @@ def our_arm(args, wl):
     k_own = hist["counts"][:, 0].astype(np.float64)
     density = float(K.mean() / n_g)
     k1_avg_ms = statistics.mean(k1_ms)
+    k1a_avg_ms = statistics.mean(k1a_ms) if k1a_ms else k1_avg_ms
+    # algorithmic bytes of the dominant kernel, k1_stream: read e and G, write
+    # e (all n_g) + one (int32, fp32) pair per selection
     k1_bytes = 12.0 * n_g + 8.0 * float(k_own.mean())
-    achieved = k1_bytes / (k1_avg_ms * 1e-3) / 1e9
+    achieved = k1_bytes / (k1a_avg_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
-    # our kernels per step: K1 stream + K1 compact + dense clear + finalize (n = 1);
-    # + gather_foreign, owner_reduce, build_union at n > 1 (NCCL kernels not counted)
+    # whole step vs the same roofline: K1 bytes + union (8 B) and, with the
+    # model update, x read+write (8 B) per union entry
+    step_bytes = k1_bytes + 8.0 * float(K.mean()) * (2 if args.model else 1)
+    # our kernels per step: k1_stream, k1_scan, k1_gather, k_finalize (n = 1);
+    # n > 1 adds gather_foreign, owner_reduce, build_union (NCCL kernels not counted)
     launches_per_step = 4 if world == 1 else 7
     clocks = clk.summary()
 
@@ -311,8 +320,10 @@ def our_arm(args, wl):
             "select_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),
-                         "kernel": "k1_fused_select", "algorithmic_bytes_per_launch": k1_bytes,
-                         "avg_launch_ms": k1_avg_ms, "peak_source": peak_kind},
+                         "kernel": "k1_stream", "algorithmic_bytes_per_launch": k1_bytes,
+                         "avg_launch_ms": k1a_avg_ms, "peak_source": peak_kind,
+                         "k1_total_ms": k1_avg_ms,
+                         "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,

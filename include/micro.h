@@ -189,6 +189,13 @@ int micro_query(micro_ctx* ctx, micro_stats* st, int64_t* counts, double* deltas
 int micro_history(micro_ctx* ctx, int64_t max, int64_t* t, int64_t* K, int64_t* counts,
                   double* delta_used, int64_t* written);
 
+/* Diagnostics: CUDA-event timing of K1's streaming pass (k1_stream) inside
+ * the library.  micro_kernel_timing(1) starts recording (up to 1024 launches,
+ * restarting the count); micro_kernel_times synchronises and returns the
+ * per-launch durations in ms. */
+int micro_kernel_timing(micro_ctx* ctx, int enable);
+int micro_kernel_times(micro_ctx* ctx, float* ms, int max, int* written);
+
 /* Device views, valid until the next step on this context. */
 int micro_union_device(micro_ctx* ctx, const int32_t** d_idx, const void** d_sums,
                        const int64_t** d_K);

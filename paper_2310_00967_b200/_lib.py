@@ -102,6 +102,8 @@ _SIGS = {
     "micro_sync": ([VP], I32),
     "micro_query": ([VP, C.POINTER(micro_stats), VP, VP], I32),
     "micro_history": ([VP, I64, VP, VP, VP, VP, PI64], I32),
+    "micro_kernel_timing": ([VP, I32], I32),
+    "micro_kernel_times": ([VP, VP, I32, C.POINTER(I32)], I32),
     "micro_union_device": ([VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)], I32),
     "micro_dense_device": ([VP, C.POINTER(VP)], I32),
     "micro_residual_device": ([VP, I32, C.POINTER(VP)], I32),

@@ -128,6 +128,7 @@ int h_update_threshold(double* delta, uint64_t k_target, uint64_t k_sel, double 
 }
 
 constexpr int64_t kHistCap = 4096;
+constexpr int kTimingCap = 1024;
 
 template <typename T>
 int64_t p_max_for(int64_t range) {
@@ -198,6 +199,10 @@ struct micro_ctx {
   // n = 1 with the streaming K1: the dense g/n is maintained inside K1
   // (k1_stream<..., kDense>) with one dirty bit per 32-byte sector
   bool dense_fused = false;
+  // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
+  bool timing = false;
+  int t_next = 0;
+  std::vector<cudaEvent_t> t_ev;
   unsigned long long* dense_dirty = nullptr;
   std::vector<void*> allocs;
 
@@ -355,6 +360,8 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
   cudaStream_t st = c->stream;
+  const bool timed = c->timing && c->t_next < kTimingCap;
+  if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
 #define K1S(MODE, D) k1_stream<T, MODE, D><<<grid, kStreamThreads, 0, st>>>(a)
   if (c->n > 1) {
     if (c->cfg.error_feedback) K1S(kWriteZeroSel, false);
@@ -368,6 +375,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   }
 #undef K1S
   CU(cudaGetLastError());
+  if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next++ + 1], st));
   CompactArgs b{};
   b.stage_idx = c->stage_idx;
   b.stage_val = c->stage_val;
@@ -797,6 +805,7 @@ int micro_ctx_destroy(micro_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->aux) cudaStreamSynchronize(c->aux);
   for (void* p : c->allocs) cudaFree(p);
+  for (cudaEvent_t ev : c->t_ev) cudaEventDestroy(ev);
   if (c->staging) cudaFree(c->staging);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -916,6 +925,28 @@ int micro_query(micro_ctx* c, micro_stats* st, int64_t* counts, double* deltas) 
     st->nonfinite = flags & 1;
     st->overflow = (flags >> 1) & 1;
   }
+  return MICRO_OK;
+}
+
+int micro_kernel_timing(micro_ctx* c, int enable) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->dev);
+  if (enable && c->t_ev.empty()) {
+    c->t_ev.resize(2 * kTimingCap);
+    for (auto& ev : c->t_ev) CU(cudaEventCreate(&ev));
+  }
+  c->timing = enable != 0;
+  c->t_next = 0;
+  return MICRO_OK;
+}
+
+int micro_kernel_times(micro_ctx* c, float* ms, int max, int* written) {
+  TRY(check_ctx(c));
+  DeviceGuard dg(c->dev);
+  CU(cudaStreamSynchronize(c->stream));
+  const int n = std::min(max, c->t_next);
+  for (int k = 0; k < n; ++k) CU(cudaEventElapsedTime(&ms[k], c->t_ev[2 * k], c->t_ev[2 * k + 1]));
+  if (written) *written = n;
   return MICRO_OK;
 }
 

@@ -187,6 +187,16 @@ class Micro:
         return dict(t=t[:m], K=K[:m], counts=cnt[: m * self.n_local].reshape(m, self.n_local),
                     delta_used=dl[: m * self.n_local].reshape(m, self.n_local))
 
+    def kernel_timing(self, enable: bool = True):
+        """Record CUDA-event durations of K1's streaming pass (diagnostics)."""
+        check(lib().micro_kernel_timing(self._h, int(enable)))
+
+    def kernel_times(self, max_n: int = 1024) -> np.ndarray:
+        out = np.empty(max_n, np.float32)
+        w = C.c_int32()
+        check(lib().micro_kernel_times(self._h, out.ctypes.data, max_n, C.byref(w)))
+        return out[: w.value].copy()
+
     def union(self):
         """(indices int32, sums) of the last step as host numpy arrays."""
         idx = np.empty(self.n_g, np.int32)
