@@ -128,6 +128,19 @@ __device__ __forceinline__ void st_hint(float* p, float v, unsigned long long po
 __device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
+// Scattered read-modify-write targets (the model x at the union): ask L2 to
+// fetch only the 64-byte half around the word instead of its default span.
+__device__ __forceinline__ float ld_rand(const float* p) {
+  float v;
+  asm volatile("ld.global.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_rand(const double* p) {
+  double v;
+  asm volatile("ld.global.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // Drop a 128-byte L2 line without writing it back (its content is dead).
 __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");

@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   if (x) {  // harness.cpp:212-215: x[j] -= s_j / n, one thread per union entry
     for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < K; m += stride) {
       const int32_t j = cur[m];
-      x[j] = x[j] - div_rn(sums[m], nf);  // one rounding after the division
+      x[j] = ld_rand(x + j) - div_rn(sums[m], nf);  // one rounding after the division
     }
   }
   if (!dense) return;

@@ -280,11 +280,17 @@ __global__ void __launch_bounds__(kScanThreads) k1_scan(CompactArgs a) {
   const int r0 = (b * kScanThreads + tid) * kScanItems;
   int v[kScanItems];
   int mine = 0;
+  if (r0 + kScanItems <= a.num_runs) {  // two 16-byte loads (runs buffer is 256-byte aligned)
+    const int4 lo = reinterpret_cast<const int4*>(a.run_counts + r0)[0];
+    const int4 hi = reinterpret_cast<const int4*>(a.run_counts + r0)[1];
+    v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
+    v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+  } else {
 #pragma unroll
-  for (int q = 0; q < kScanItems; ++q) {
-    v[q] = r0 + q < a.num_runs ? a.run_counts[r0 + q] : 0;
-    mine += v[q];
+    for (int q = 0; q < kScanItems; ++q) v[q] = r0 + q < a.num_runs ? a.run_counts[r0 + q] : 0;
   }
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) mine += v[q];
   int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -318,10 +324,19 @@ __global__ void __launch_bounds__(kScanThreads) k1_scan(CompactArgs a) {
   }
   __syncthreads();
   long long off = s_excl + (w ? s_w[w - 1] : 0) + incl - mine;
+  int o[kScanItems];
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q) {
-    if (r0 + q < a.num_runs) a.run_offsets[r0 + q] = (int)(off < a.cap ? off : a.cap);
+    o[q] = (int)(off < a.cap ? off : a.cap);
     off += v[q];
+  }
+  if (r0 + kScanItems <= a.num_runs) {
+    reinterpret_cast<int4*>(a.run_offsets + r0)[0] = make_int4(o[0], o[1], o[2], o[3]);
+    reinterpret_cast<int4*>(a.run_offsets + r0)[1] = make_int4(o[4], o[5], o[6], o[7]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q)
+      if (r0 + q < a.num_runs) a.run_offsets[r0 + q] = o[q];
   }
 }
 
@@ -349,7 +364,7 @@ __global__ void __launch_bounds__(256) k1_gather(CompactArgs a) {
       oi[m] = j;
       ov[m] = v;
       // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
-      if (x) x[j] = x[j] - v;
+      if (x) x[j] = ld_rand(x + j) - v;
     }
   }
   __syncwarp();

@@ -144,7 +144,6 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int b = blockIdx.x, G = gridDim.x;
-  const int64_t gw = (int64_t)b * kWsWarps + w, GW = (int64_t)G * kWsWarps;
 
   // per-warp ring: [stage][e | g][UE]
   T* ring = reinterpret_cast<T*>(smem + (size_t)w * kWsStages * 2 * kWsUnitBytes);
@@ -214,8 +213,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) k1_tma_select(TmaSele
     const int s = k % kWsStages;
     const int vec_elems = FULL ? UE : (int)((elems * (int)sizeof(T)) & ~15) / (int)sizeof(T);
     if constexpr (Cfg::TMA) mbar_wait(&full[s], (uint32_t)(k / kWsStages) & 1u);
-    const V* se = reinterpret_cast<const V*>(ring + (size_t)(2 * s) * UE);
-    const V* sg = reinterpret_cast<const V*>(ring + (size_t)(2 * s + 1) * UE);
+    [[maybe_unused]] const V* se = reinterpret_cast<const V*>(ring + (size_t)(2 * s) * UE);
+    [[maybe_unused]] const V* sg = reinterpret_cast<const V*>(ring + (size_t)(2 * s + 1) * UE);
     V e[VPL], g[VPL];
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
