@@ -177,6 +177,9 @@ def our_arm(args, wl):
     dev = torch.device("cuda", local)
     n_g, d = wl["n_g"], wl["d"]
     delta0 = warm_delta0(d)
+    # W workers per process: 1 (one per GPU), or --cluster-workers W at N = 1:
+    # the reference's own in-process cluster (harness.cpp:121-224) on one GPU
+    W = args.cluster_workers if (world == 1 and args.cluster_workers > 1) else 1
     dist = None
     if world > 1:
         import torch.distributed as tdist
@@ -186,7 +189,7 @@ def our_arm(args, wl):
         dist = tdist
         m = DistMicro(n_g, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
     else:
-        m = engine.Micro(n_g, 1, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
+        m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
     stream = torch.cuda.current_stream(dev)
     # the model update x -= g/n at the union is part of the reference's
     # iteration (harness.cpp:212-215); a dense g/n is not (run_iteration uses
@@ -202,21 +205,27 @@ def our_arm(args, wl):
     # per step when memory allows (same statistics as the prime phase),
     # otherwise R buffers rotated.
     t = 0
-    gen = torch.empty(n_g, device=dev)
+    gen = [torch.empty(n_g, device=dev) for _ in range(W)]
     for _ in range(args.prime):
-        engine.synth_gaussian(gen, SEED, rank, t)
-        m.step([gen], ETA, t)
+        for i in range(W):
+            engine.synth_gaussian(gen[i], SEED, rank + i, t)
+        m.step(gen, ETA, t)
         t += 1
     del gen
     torch.cuda.synchronize()
-    need = args.warmup + args.steps
-    R = max(2, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (4 * n_g))))
+    need = (args.warmup + args.steps) * W
+    R = max(W + 1, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (4 * n_g))))
     G = [torch.empty(n_g, device=dev) for _ in range(R)]
     for r in range(R):
-        engine.synth_gaussian(G[r], SEED, rank, t + r)
+        engine.synth_gaussian(G[r], SEED, rank + r % W, t + r)
     t0_bufs = t
+
+    def grads(t):
+        q = (t - t0_bufs) * W
+        return [G[(q + i) % R] for i in range(W)]
+
     for s in range(args.warmup):
-        m.step([G[(t - t0_bufs) % R]], ETA, t)
+        m.step(grads(t), ETA, t)
         t += 1
     torch.cuda.synchronize()
 
@@ -232,7 +241,7 @@ def our_arm(args, wl):
         start.record(stream)
         for s in range(args.steps):
             evs[s][0].record(stream)
-            m.compress([G[(t - t0_bufs) % R]], ETA, t)
+            m.compress(grads(t), ETA, t)
             evs[s][1].record(stream)
             m.aggregate()
             t += 1
@@ -262,17 +271,19 @@ def our_arm(args, wl):
     peak, peak_kind = peaks()
     # whole step vs the same roofline: K1 bytes + union (8 B) and, with the
     # model update, x read+write (8 B) per union entry
-    step_bytes = k1_bytes + 8.0 * float(K.mean()) * (2 if args.model else 1)
+    step_bytes = (W * k1_bytes + 8.0 * float(K.mean()) * (2 if args.model else 1)
+                  + (8.0 * float(K.mean()) * W if W > 1 else 0.0))  # cluster reduce: W reads + zeroing
     # our kernels per step: k1_stream, k1_scan, k1_gather, k_finalize (n = 1);
     # n > 1 adds gather_foreign, owner_reduce, build_union (NCCL kernels not counted)
-    launches_per_step = 4 if world == 1 else 7
+    launches_per_step = (3 * W + 1 + (1 if W > 1 else 0)) if world == 1 else 7
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (N = 1) ----
     e2e = None
     if world == 1:
-        hG = torch.empty(n_g, dtype=torch.float32).pin_memory()
-        hG.copy_(G[0].cpu())
+        hG = torch.empty(W * n_g, dtype=torch.float32).pin_memory()
+        for i in range(W):
+            hG[i * n_g:(i + 1) * n_g].copy_(G[i].cpu())
         idx = np.empty(n_g, np.int32)
         sums = np.empty(n_g, np.float32)
         m.step_host(hG, ETA, t, idx, sums)  # warm (staging allocation)
@@ -285,16 +296,16 @@ def our_arm(args, wl):
             kk.append(i_.size)
             t += 1
         e2e_s = (time.perf_counter() - t0) / ke
-        e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": 4 * n_g,
+        e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": 4 * n_g * W,
                "d2h_bytes_per_step": int(8 * statistics.mean(kk) + 8 + 4)}
 
     # ---- CPU baseline: the reference's own code on this host (rank 0, N = 1) ----
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            times = run_reference_cluster(n_g, 1, d, steps=args.cpu_steps, warmup=1)
+            times = run_reference_cluster(n_g, W, d, steps=args.cpu_steps, warmup=1)
             cpu = {"value": statistics.mean(times) * 1e6, "unit": "us/iter", "cores": 1, "kind": "reference",
-                   "sample": f"{args.cpu_steps} iterations (after 1 warm-up) of the full workload (n_g={n_g}, n=1) "
+                   "sample": f"{args.cpu_steps} iterations (after 1 warm-up) of the full workload (n_g={n_g}, n={W}) "
                              "through the reference's sparsifier/collectives TUs compiled verbatim (fp64, 1 thread)"}
         except Exception as ex:  # the checker is optional at run time; the GPU number stands
             cpu = {"value": None, "unit": "us/iter", "cores": 1, "kind": "reference", "sample": f"failed: {ex}"}
@@ -304,15 +315,16 @@ def our_arm(args, wl):
             "metric": METRIC, "value": ms_step * 1e3, "unit": "us/iter", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) fp32 gradients (include/micro_synth.h)",
-            "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world,
-                       "one_worker_per_gpu": True, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
+            "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world * W,
+                       "one_worker_per_gpu": W == 1, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
                        "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
                        "inputs": (f"{R} resident N(0,1) gradients ("
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
                                   + "); each 4*n_g bytes > L2 (no flush needed)")
                        if 4 * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
-                       "parallelism": f"dp{world} (exclusive cyclic partitions)"},
+                       "parallelism": (f"dp{world} (exclusive cyclic partitions)" if W == 1 else
+                                       f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
             "density": density, "density_rel_err": density / d - 1.0,
             "density_window": {"first_quarter": float(K[: max(1, len(K) // 4)].mean() / n_g),
                                "last_quarter": float(K[-max(1, len(K) // 4):].mean() / n_g),
@@ -347,6 +359,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dense", action="store_true", help="also maintain the dense g/n vector")
+    ap.add_argument("--cluster-workers", type=int, default=1,
+                    help="N = 1 only: W in-process workers on the GPU (the reference's in-process cluster)")
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
