@@ -229,8 +229,6 @@ def our_arm(args, wl):
         t += 1
     torch.cuda.synchronize()
 
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
@@ -240,30 +238,25 @@ def our_arm(args, wl):
     with ClockSampler(local) as clk:
         start.record(stream)
         for s in range(args.steps):
-            evs[s][0].record(stream)
-            m.compress(grads(t), ETA, t)
-            evs[s][1].record(stream)
-            m.aggregate()
+            m.step(grads(t), ETA, t)  # the whole iteration, one library call
             t += 1
         end.record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     total_ms = start.elapsed_time(end)
-    k1_ms = [a.elapsed_time(b) for a, b in evs]  # whole compress: stream + scan + gather(+model)
     k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone
     m.kernel_timing(False)
     if dist:
-        v = torch.tensor([total_ms, statistics.mean(k1_ms)], device=dev, dtype=torch.float64)
+        v = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        total_ms, k1_max = float(v[0]), float(v[1])
+        total_ms = float(v[0])
     ms_step = total_ms / args.steps
     hist = m.history(args.steps)
     K = hist["K"].astype(np.float64)
     k_own = hist["counts"][:, 0].astype(np.float64)
     density = float(K.mean() / n_g)
-    k1_avg_ms = statistics.mean(k1_ms)
-    k1a_avg_ms = statistics.mean(k1a_ms) if k1a_ms else k1_avg_ms
+    k1a_avg_ms = statistics.mean(k1a_ms)
     # algorithmic bytes of the dominant kernel, k1_stream: read e and G, write
     # e (all n_g) + one (int32, fp32) pair per selection
     k1_bytes = 12.0 * n_g + 8.0 * float(k_own.mean())
@@ -273,9 +266,11 @@ def our_arm(args, wl):
     # model update, x read+write (8 B) per union entry
     step_bytes = (W * k1_bytes + 8.0 * float(K.mean()) * (2 if args.model else 1)
                   + (8.0 * float(K.mean()) * W if W > 1 else 0.0))  # cluster reduce: W reads + zeroing
-    # our kernels per step: k1_stream, k1_scan, k1_gather, k_finalize (n = 1);
-    # n > 1 adds gather_foreign, owner_reduce, build_union (NCCL kernels not counted)
-    launches_per_step = (3 * W + 1 + (1 if W > 1 else 0)) if world == 1 else 7
+    # our kernels per step: k1_stream, k1_scan (+ threshold update), k1_gather
+    # (+ model update) at n = 1; a W-worker cluster adds k_cluster_reduce and
+    # k_finalize; n > 1 ranks: K1 x3, gather_foreign, owner_reduce,
+    # build_union, finalize (NCCL kernels not counted)
+    launches_per_step = (3 if W == 1 else 3 * W + 2) if world == 1 else 7
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (N = 1) ----
@@ -334,7 +329,6 @@ def our_arm(args, wl):
                          "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),
                          "kernel": "k1_stream", "algorithmic_bytes_per_launch": k1_bytes,
                          "avg_launch_ms": k1a_avg_ms, "peak_source": peak_kind,
-                         "k1_total_ms": k1_avg_ms,
                          "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,

@@ -199,6 +199,10 @@ struct micro_ctx {
   // n = 1 with the streaming K1: the dense g/n is maintained inside K1
   // (k1_stream<..., kDense>) with one dirty bit per 32-byte sector
   bool dense_fused = false;
+  // micro_step on a one-worker cluster with the streaming K1: k1_scan's last
+  // CTA does the threshold update + history (no k_finalize launch)
+  bool fuse_step = false;   // set for the duration of micro_step
+  bool fin_done = false;    // this step's finalize already ran inside k1_scan
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
   bool timing = false;
   int t_next = 0;
@@ -391,6 +395,20 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.epoch = next_epoch(c);
   b.flags = c->flags;
   b.model = c->n == 1 ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
+  if (c->fuse_step) {
+    b.fin_delta = c->delta + i;
+    b.k_target = c->k_worker;
+    b.alpha = c->cfg.scaling_factor;
+    b.min_threshold = c->cfg.min_threshold;
+    b.fin_K = c->Kbuf + c->buf;
+    b.fin_t = c->t_cur;
+    b.fin_slot = c->steps % kHistCap;
+    b.hist_t = c->hist_t;
+    b.hist_K = c->hist_K;
+    b.hist_counts = c->hist_counts;
+    b.hist_delta = c->hist_delta;
+    c->fin_done = true;
+  }
   const int64_t blocks = (b.num_runs + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems);
   if (blocks > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
   b.status_len = status_span(c, blocks);
@@ -482,15 +500,21 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_counts = c->hist_counts;
   f.hist_delta = c->hist_delta;
   const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
-  if (c->clear_pending) {
-    CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-    c->clear_pending = false;
-  } else if (f.prev_idx) {
-    k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
+  if (c->fin_done) {
+    // k1_scan already did the threshold update + history (n = 1, micro_step);
+    // dense (fused into K1) and model (k1_gather) are done too
+    c->fin_done = false;
+  } else {
+    if (c->clear_pending) {
+      CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+      c->clear_pending = false;
+    } else if (f.prev_idx) {
+      k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
+      CU(cudaGetLastError());
+    }
+    k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
     CU(cudaGetLastError());
   }
-  k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
-  CU(cudaGetLastError());
   if (!c->cfg.error_feedback && c->n > 1)
     for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
   c->steps++;
@@ -871,7 +895,15 @@ int micro_aggregate(micro_ctx* c) {
 }
 
 int micro_step(micro_ctx* c, const void* const* d_grads, double eta, int64_t t) {
-  TRY(micro_compress(c, d_grads, eta, t));
+  TRY(check_ctx(c));
+  // one-worker cluster, streaming K1: fold k_finalize into k1_scan
+  c->fuse_step = c->cluster && c->n == 1 && c->k1_kind == 0 && (!c->dense || c->dense_fused);
+  const int rc = micro_compress(c, d_grads, eta, t);
+  c->fuse_step = false;
+  if (rc != MICRO_OK) {
+    c->fin_done = false;
+    return rc;
+  }
   return micro_aggregate(c);
 }
 

@@ -265,7 +265,31 @@ struct CompactArgs {
   unsigned int epoch;
   int* flags;              // bit1 capacity overflow
   void* model;             // n = 1: x -= g/n = acc at the selections (harness.cpp:212-215)
+  // n = 1 single-call step (micro_step): the last scan CTA also does what
+  // k_finalize would — K, history, threshold update (sparsifier.cpp:77-81) —
+  // so the iteration is three launches.  fin_delta == NULL: not fused.
+  double* fin_delta;
+  unsigned long long k_target;
+  double alpha, min_threshold;
+  long long* fin_K;
+  long long fin_t, fin_slot;
+  long long *hist_t, *hist_K, *hist_counts;
+  double* hist_delta;
 };
+
+__device__ __forceinline__ void scan_finalize(const CompactArgs& a, long long total) {
+  const long long K = total < a.cap ? total : a.cap;
+  *a.fin_K = K;
+  a.hist_t[a.fin_slot] = a.fin_t;
+  a.hist_K[a.fin_slot] = K;
+  a.hist_counts[a.fin_slot] = total;
+  double d = *a.fin_delta;
+  a.hist_delta[a.fin_slot] = d;
+  const unsigned long long k = (unsigned long long)total;
+  if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
+  else if (k < a.k_target) d *= 1.0 - a.alpha;
+  *a.fin_delta = d;
+}
 
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 8;  // run counts per thread: 8192 per CTA
@@ -315,6 +339,7 @@ __global__ void __launch_bounds__(kScanThreads) k1_scan(CompactArgs a) {
         const long long total = ex + (long long)tot;
         *a.count = total;
         if (total > a.cap) atomicOr(a.flags, 2);
+        if (a.fin_delta) scan_finalize(a, total);
       }
     }
     if (b == G - 1) {  // stamp the unused look-back words with this epoch

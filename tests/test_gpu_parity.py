@@ -29,7 +29,7 @@ def gen(o, n, n_g, t, dtype):
 
 
 def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, oracle="restatement",
-             check_every=1):
+             check_every=1, split=False):
     o = Oracle()
     tdt = torch.float32 if dtype == np.float32 else torch.float64
     m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, target="full" if full else "split",
@@ -43,7 +43,11 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     for t in range(iters):
         G = gen(o, n, n_g, t, dtype)
         Gd = torch.from_numpy(G).cuda()
-        m.step(list(Gd), ETA, t)
+        if split:  # micro_compress + micro_aggregate (k_finalize launched separately)
+            m.compress(list(Gd), ETA, t)
+            m.aggregate()
+        else:      # micro_step (n = 1: threshold update folded into k1_scan)
+            m.step(list(Gd), ETA, t)
         r = ref.step(G, ETA, t)
         if t % check_every and t != iters - 1:
             continue
@@ -96,6 +100,13 @@ def test_gpu_f32_matches_restatement(n_g, n, d, delta0, k1_kernel):
 def test_gpu_f32_modes(full, ef, k1_kernel):
     run_pair(20_000, 4, 0.01, 0.01, iters=15, full=full, ef=ef)
     run_pair(20_000, 1, 0.01, 0.01, iters=15, full=full, ef=ef)
+
+
+@pytest.mark.parametrize("n_g,n", [(10_000, 1), (65_537, 1), (10_007, 2)])
+def test_gpu_split_compress_aggregate(n_g, n):
+    """The two-call API and the single micro_step give the same iteration."""
+    run_pair(n_g, n, 0.01, 0.01, iters=12, split=True)
+    run_pair(n_g, n, 0.01, 0.01, iters=12, dtype=np.float64, split=True)
 
 
 def test_gpu_density_one_threshold_zero():
