@@ -175,7 +175,11 @@ struct micro_ctx {
   int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
   void* stage_val = nullptr;
   int* unit_counts = nullptr;    // selections per K1 unit / per k1_stream CTA run
-  int* run_offsets = nullptr;    // k1_scan output
+  // k1_stream -> k1_gather: selections per super block of super_runs CTA
+  // runs, two parities (a launch zeroes the other one for the next launch)
+  int* super_counts = nullptr;
+  int super_runs = 8;
+  int super_par = 0;
   unsigned int* ticket = nullptr;
   unsigned int epoch = 0;
   int* flags = nullptr;
@@ -199,10 +203,10 @@ struct micro_ctx {
   // n = 1 with the streaming K1: the dense g/n is maintained inside K1
   // (k1_stream<..., kDense>) with one dirty bit per 32-byte sector
   bool dense_fused = false;
-  // micro_step on a one-worker cluster with the streaming K1: k1_scan's last
-  // CTA does the threshold update + history (no k_finalize launch)
+  // micro_step on a one-worker cluster with the streaming K1: k1_gather's
+  // block 0 does the threshold update + history (no k_finalize launch)
   bool fuse_step = false;   // set for the duration of micro_step
-  bool fin_done = false;    // this step's finalize already ran inside k1_scan
+  bool fin_done = false;    // this step's finalize already ran inside k1_gather
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
   bool timing = false;
   int t_next = 0;
@@ -360,6 +364,8 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.flags = c->flags;
   a.dense = c->dense;
   a.dirty = c->dense_dirty;
+  a.super_counts = c->super_counts + c->super_par * kMaxSupers;
+  a.super_runs = c->super_runs;
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
@@ -384,17 +390,21 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.stage_idx = c->stage_idx;
   b.stage_val = c->stage_val;
   b.run_counts = c->unit_counts;
-  b.run_offsets = c->run_offsets;
+  b.super_counts = a.super_counts;
+  c->super_par ^= 1;
+  b.super_clear = c->super_counts + c->super_par * kMaxSupers;
+  b.super_len = kMaxSupers;
   b.num_runs = a.unit_hi / kStreamWarps - a.unit_lo / kStreamWarps + 1;
+  b.super_runs = c->super_runs;
   b.run_stride = kStreamWarps * UE;
   b.sel_idx = c->sel_idx[c->buf][i];
   b.sel_val = c->sel_val[c->buf][i];
   b.cap = c->sel_cap;
   b.count = c->counts + i;
-  b.status = c->status;
-  b.epoch = next_epoch(c);
   b.flags = c->flags;
   b.model = c->n == 1 ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
+  if ((b.num_runs + b.super_runs - 1) / b.super_runs > kMaxSupers)
+    return fail(MICRO_ECAPACITY, "super-block workspace too small");
   if (c->fuse_step) {
     b.fin_delta = c->delta + i;
     b.k_target = c->k_worker;
@@ -409,12 +419,8 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.hist_delta = c->hist_delta;
     c->fin_done = true;
   }
-  const int64_t blocks = (b.num_runs + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems);
-  if (blocks > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
-  b.status_len = status_span(c, blocks);
-  k1_scan<<<(unsigned)blocks, kScanThreads, 0, c->stream>>>(b);
-  CU(cudaGetLastError());
-  k1_gather<T><<<(unsigned)((b.num_runs + 7) / 8), 256, 0, c->stream>>>(b);
+  k1_gather<T><<<(unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps), kGatherWarps * 32, 0,
+                  c->stream>>>(b);
   CU(cudaGetLastError());
   return MICRO_OK;
 }
@@ -501,7 +507,7 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_delta = c->hist_delta;
   const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
   if (c->fin_done) {
-    // k1_scan already did the threshold update + history (n = 1, micro_step);
+    // k1_gather already did the threshold update + history (n = 1, micro_step);
     // dense (fused into K1) and model (k1_gather) are done too
     c->fin_done = false;
   } else {
@@ -604,6 +610,7 @@ int reset_state(micro_ctx* c) {
   CU(cudaMemsetAsync(c->flags, 0, sizeof(int), c->stream));
   if (c->dense) CU(cudaMemsetAsync(c->dense, 0, c->n_g * c->esz, c->stream));
   if (c->dense_dirty) CU(cudaMemsetAsync(c->dense_dirty, 0, (c->n_g / 256 + 8) * 8, c->stream));
+  if (c->super_counts) CU(cudaMemsetAsync(c->super_counts, 0, 2 * kMaxSupers * sizeof(int), c->stream));
   CU(cudaStreamSynchronize(c->stream));
   c->steps = 0;
   c->t_cur = -1;
@@ -800,7 +807,14 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     if ((rc = c->alloc((void**)&c->stage_idx, stage * 4))) return cleanup(rc);
     if ((rc = c->alloc(&c->stage_val, stage * c->esz))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->unit_counts, (max_range / 128 + 8) * sizeof(int)))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->run_offsets, (max_range / 128 + 8) * sizeof(int)))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->super_counts, 2 * kMaxSupers * sizeof(int)))) return cleanup(rc);
+    {
+      // super blocks of S runs (S a multiple of the gather CTA's 8 runs), <= kMaxSupers of them
+      const int64_t ue = c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>();
+      const int64_t runs = max_range / (kStreamWarps * ue) + 2;
+      const int64_t S = (runs + kMaxSupers - 1) / kMaxSupers;
+      c->super_runs = (int)std::max<int64_t>(kGatherWarps, (S + kGatherWarps - 1) / kGatherWarps * kGatherWarps);
+    }
   }
   if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->flags, sizeof(int)))) return cleanup(rc);
@@ -896,7 +910,7 @@ int micro_aggregate(micro_ctx* c) {
 
 int micro_step(micro_ctx* c, const void* const* d_grads, double eta, int64_t t) {
   TRY(check_ctx(c));
-  // one-worker cluster, streaming K1: fold k_finalize into k1_scan
+  // one-worker cluster, streaming K1: fold k_finalize into k1_gather
   c->fuse_step = c->cluster && c->n == 1 && c->k1_kind == 0 && (!c->dense || c->dense_fused);
   const int rc = micro_compress(c, d_grads, eta, t);
   c->fuse_step = false;

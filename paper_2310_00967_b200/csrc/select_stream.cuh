@@ -13,10 +13,13 @@
 //      staging slot [(u - u_lo) * 512, + k_u), recording k_u.  No ordering,
 //      no cross-warp or cross-CTA dependency: the pass runs at the HBM
 //      roofline like a plain axpy (tools/k1_probe.cu: 6.2-7.0 TB/s).
-// K1b  k1_scan: exclusive prefix of the per-CTA run counts (8192 per CTA,
-//      one decoupled look-back over a handful of CTAs) -> k_i;
-// K1c  k1_gather: one warp per run copies it, coalesced, to its final
-//      position, giving the ascending (index, value) list.
+//      Each CTA's run count is also added (one atomic) into its "super
+//      block" of S consecutive runs (<= 1024 super blocks).
+// K1b  k1_gather: one warp per run copies it, coalesced, to its final
+//      position, giving the ascending (index, value) list.  A CTA's output
+//      offset is the sum of the super blocks before its own plus the runs
+//      before it inside its super block (<= 1024 + S L2 reads per CTA, no
+//      scan kernel, no look-back); block 0 also forms k_i.
 //
 // Why not one pass: every single-pass variant we measured (per-tile
 // look-back; persistent CTAs with TMA bulk-copy rings; per-warp rings;
@@ -57,6 +60,8 @@ struct StreamArgs {
   // "nonzero last step" bit per sector (64 per unit)
   void* dense;
   unsigned long long* dirty;
+  int* super_counts;       // selections per super block of `super_runs` CTA runs (zeroed)
+  int super_runs;
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -222,7 +227,10 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
       cta_count += x;
     }
     const int slot = (int)blockIdx.x - cta_lo;
-    if (threadIdx.x == 0) a.unit_counts[slot] = cta_count;
+    if (threadIdx.x == 0) {
+      a.unit_counts[slot] = cta_count;
+      if (cta_count) atomicAdd(a.super_counts + slot / a.super_runs, cta_count);
+    }
     if (unit_count) {
       const unsigned excl = incl - packed;
       const unsigned long long pol_keep = policy_evict_last();  // read back by k1_gather, then discarded
@@ -253,21 +261,21 @@ struct CompactArgs {
   const int32_t* stage_idx;
   const void* stage_val;
   const int* run_counts;   // pairs per CTA run (k1_stream)
-  int* run_offsets;        // exclusive prefix (k1_scan -> k1_gather)
+  const int* super_counts; // pairs per super block of `super_runs` runs (k1_stream)
+  int* super_clear;        // the other parity's super counts: zeroed here for the next launch
+  int super_len;           // entries of super_clear
   int num_runs;
+  int super_runs;
   int run_stride;          // staging elements per run slot
   int32_t* sel_idx;
   void* sel_val;
   long long cap;
   long long* count;
-  unsigned long long* status;
-  long long status_len;
-  unsigned int epoch;
   int* flags;              // bit1 capacity overflow
   void* model;             // n = 1: x -= g/n = acc at the selections (harness.cpp:212-215)
-  // n = 1 single-call step (micro_step): the last scan CTA also does what
-  // k_finalize would — K, history, threshold update (sparsifier.cpp:77-81) —
-  // so the iteration is three launches.  fin_delta == NULL: not fused.
+  // n = 1 single-call step (micro_step): block 0 also does what k_finalize
+  // would — K, history, threshold update (sparsifier.cpp:77-81) — so the
+  // iteration is two launches.  fin_delta == NULL: not fused.
   double* fin_delta;
   unsigned long long k_target;
   double alpha, min_threshold;
@@ -277,7 +285,7 @@ struct CompactArgs {
   double* hist_delta;
 };
 
-__device__ __forceinline__ void scan_finalize(const CompactArgs& a, long long total) {
+__device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long total) {
   const long long K = total < a.cap ? total : a.cap;
   *a.fin_K = K;
   a.hist_t[a.fin_slot] = a.fin_t;
@@ -291,90 +299,54 @@ __device__ __forceinline__ void scan_finalize(const CompactArgs& a, long long to
   *a.fin_delta = d;
 }
 
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 8;  // run counts per thread: 8192 per CTA
+constexpr int kGatherWarps = 8;   // runs per k1_gather CTA (divides super_runs)
+constexpr int kMaxSupers = 1024;  // super blocks per launch
 
-// Exclusive prefix of the run counts: 8192 runs per CTA, block scan, one
-// decoupled look-back across the (few) CTAs; the last CTA writes k_i.
-__global__ void __launch_bounds__(kScanThreads) k1_scan(CompactArgs a) {
-  __shared__ int s_w[kScanThreads / 32];
-  __shared__ long long s_excl;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int b = blockIdx.x, G = gridDim.x;
-  const int r0 = (b * kScanThreads + tid) * kScanItems;
-  int v[kScanItems];
-  int mine = 0;
-  if (r0 + kScanItems <= a.num_runs) {  // two 16-byte loads (runs buffer is 256-byte aligned)
-    const int4 lo = reinterpret_cast<const int4*>(a.run_counts + r0)[0];
-    const int4 hi = reinterpret_cast<const int4*>(a.run_counts + r0)[1];
-    v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w;
-    v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
-  } else {
-#pragma unroll
-    for (int q = 0; q < kScanItems; ++q) v[q] = r0 + q < a.num_runs ? a.run_counts[r0 + q] : 0;
-  }
-#pragma unroll
-  for (int q = 0; q < kScanItems; ++q) mine += v[q];
-  int incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_w[w] = incl;
+// CTA-wide sum of an int range [lo, hi) (256 threads).
+__device__ __forceinline__ long long block_sum_range(const int* p, int lo, int hi, long long* s_part) {
+  long long v = 0;
+  for (int q = lo + (int)threadIdx.x; q < hi; q += kGatherWarps * 32) v += p[q];
+  v = (long long)warp_sum_u64((unsigned long long)v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();  // s_part reuse
+  if (lane == 0) s_part[w] = v;
   __syncthreads();
-  if (w == 0) {
-    int x = s_w[lane];
+  long long t = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    s_w[lane] = x;  // inclusive warp prefix
-    const unsigned long long tot = (unsigned long long)__shfl_sync(0xffffffffu, x, 31);
-    const long long ex = lookback(a.status, b, tot, a.epoch, lane);
-    if (lane == 0) {
-      s_excl = ex;
-      if (b == G - 1) {
-        const long long total = ex + (long long)tot;
-        *a.count = total;
-        if (total > a.cap) atomicOr(a.flags, 2);
-        if (a.fin_delta) scan_finalize(a, total);
-      }
-    }
-    if (b == G - 1) {  // stamp the unused look-back words with this epoch
-      const unsigned long long ep = (unsigned long long)(a.epoch & 0xFFFFFFu) << 40;
-      for (long long q = G + lane; q < a.status_len; q += 32) st_relaxed_u64(&a.status[q], ep);
-    }
-  }
-  __syncthreads();
-  long long off = s_excl + (w ? s_w[w - 1] : 0) + incl - mine;
-  int o[kScanItems];
-#pragma unroll
-  for (int q = 0; q < kScanItems; ++q) {
-    o[q] = (int)(off < a.cap ? off : a.cap);
-    off += v[q];
-  }
-  if (r0 + kScanItems <= a.num_runs) {
-    reinterpret_cast<int4*>(a.run_offsets + r0)[0] = make_int4(o[0], o[1], o[2], o[3]);
-    reinterpret_cast<int4*>(a.run_offsets + r0)[1] = make_int4(o[4], o[5], o[6], o[7]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < kScanItems; ++q)
-      if (r0 + q < a.num_runs) a.run_offsets[r0 + q] = o[q];
-  }
+  for (int q = 0; q < kGatherWarps; ++q) t += s_part[q];
+  return t;
 }
 
-// One warp per CTA run: coalesced copy into the ordered output, then the
-// run's staging lines are dropped from L2 without write-back.
+// One warp per CTA run: coalesced copy into the ordered output at the run's
+// exclusive prefix, then the run's staging lines are dropped from L2 without
+// write-back.  n = 1: the model update rides along.
 template <typename T>
-__global__ void __launch_bounds__(256) k1_gather(CompactArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
+  __shared__ long long s_part[kGatherWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r0 = blockIdx.x * kGatherWarps;
+  const int sb = r0 / a.super_runs;
+  // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0)
+  long long base = block_sum_range(a.super_counts, 0, sb, s_part) +
+                   block_sum_range(a.run_counts, sb * a.super_runs, r0, s_part);
+  if (blockIdx.x == 0) {
+    const int nsup = (a.num_runs + a.super_runs - 1) / a.super_runs;
+    const long long total = block_sum_range(a.super_counts, 0, nsup, s_part);
+    if (threadIdx.x == 0) {
+      *a.count = total;
+      if (total > a.cap) atomicOr(a.flags, 2);
+      if (a.fin_delta) gather_finalize(a, total);
+    }
+    for (int q = threadIdx.x; q < a.super_len; q += kGatherWarps * 32) a.super_clear[q] = 0;
+  }
+  const int r = r0 + w;
+  // runs of this CTA before r (<= 7 L2 hits)
+  const int mine = (r0 + lane < a.num_runs && lane < w) ? a.run_counts[r0 + lane] : 0;
+  base += (long long)__reduce_add_sync(0xffffffffu, (unsigned)mine);
   if (r >= a.num_runs) return;
   const int n = a.run_counts[r];
   if (!n) return;
-  const long long off = a.run_offsets[r];
+  const long long off = base < a.cap ? base : a.cap;
   const long long src = (long long)r * a.run_stride;
   const int32_t* __restrict__ si = a.stage_idx + src;
   const T* __restrict__ sv = (const T*)a.stage_val + src;

@@ -46,7 +46,7 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         if split:  # micro_compress + micro_aggregate (k_finalize launched separately)
             m.compress(list(Gd), ETA, t)
             m.aggregate()
-        else:      # micro_step (n = 1: threshold update folded into k1_scan)
+        else:      # micro_step (n = 1: threshold update folded into k1_gather)
             m.step(list(Gd), ETA, t)
         r = ref.step(G, ETA, t)
         if t % check_every and t != iters - 1:
@@ -107,6 +107,12 @@ def test_gpu_split_compress_aggregate(n_g, n):
     """The two-call API and the single micro_step give the same iteration."""
     run_pair(n_g, n, 0.01, 0.01, iters=12, split=True)
     run_pair(n_g, n, 0.01, 0.01, iters=12, dtype=np.float64, split=True)
+
+
+@pytest.mark.parametrize("n_g,n", [(5_000_011, 1), (5_000_011, 3), (40_000_003, 1)])
+def test_gpu_many_super_blocks(n_g, n):
+    """k1_gather's offsets over many super blocks (40M: super blocks of > 8 runs)."""
+    run_pair(n_g, n, 0.01, 0.03, iters=3)
 
 
 def test_gpu_density_one_threshold_zero():

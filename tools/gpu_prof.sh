@@ -13,7 +13,7 @@ tail -1 gpurun_out/bench.log
 # profiling command: converged threshold (prime), then a few timed steps
 P="python bench.py --steps 5 --warmup 3 --prime 400 --no-cpu-baseline ${PROF_ARGS}"
 timeout 300 $P > gpurun_out/prof_plain.log 2>&1 && \
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 2010 -c 40 --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launch.log 2>&1
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 1190 -c 40 --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launch.log 2>&1
 echo launches rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_stream|k1_scan|k1_gather|k_finalize" -s 1604 -c 4 -o gpurun_out/k1_full $P > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1_stream|k1_gather|k_finalize" -s 806 -c 4 -o gpurun_out/k1_full $P > gpurun_out/ncu_full.log 2>&1
 echo full rc=$?
