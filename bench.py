@@ -187,9 +187,11 @@ def our_arm(args, wl):
         from paper_2310_00967_b200.dist import DistMicro
         tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
-        m = DistMicro(n_g, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
+        m = DistMicro(n_g, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
+                      record_error_norm=args.error_norm)
     else:
-        m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense)
+        m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
+                         record_error_norm=args.error_norm)
     stream = torch.cuda.current_stream(dev)
     # the model update x -= g/n at the union is part of the reference's
     # iteration (harness.cpp:212-215); a dense g/n is not (run_iteration uses
@@ -324,6 +326,7 @@ def our_arm(args, wl):
                        "one_worker_per_gpu": W == 1, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
                        "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
+                       "error_norm_recorded": bool(args.error_norm),
                        "inputs": (f"{R} resident N(0,1) gradients ("
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
                                   + "); each 4*n_g bytes > L2 (no flush needed)")
@@ -366,6 +369,8 @@ def main():
     ap.add_argument("--cluster-workers", type=int, default=1,
                     help="N = 1 only: W in-process workers on the GPU (the reference's in-process cluster)")
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
+    ap.add_argument("--no-error-norm", dest="error_norm", action="store_false",
+                    help="do not record the per-step error norm (fused into k1_stream)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MICRO_ABI_VERSION 1
+#define MICRO_ABI_VERSION 2
 #define MICRO_MAX_WORKERS 64
 
 typedef enum micro_status {
@@ -94,6 +94,13 @@ int micro_all_reduce_sparse(int dtype, const void* const* h_accs, int n, int64_t
  * Synchronises; *K returns the union size. */
 int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_concat,
                              int32_t* d_union, int64_t* K, void* stream);
+/* error_feedback.hpp:41-48 error_metric: (sum_i ||e_i||_2) / n over n device
+ * residuals of n_g entries (h_res: host array of device pointers), norms
+ * summed in worker order.  Each ||e_i||^2 is a deterministic fp64 tree sum
+ * (the reference's Eigen summation order is not pinned).
+ * Synchronises. */
+int micro_error_metric(int dtype, const void* const* h_res, int n, int64_t n_g, double* out,
+                       void* stream);
 
 /* Device memory plumbing for hosts without the CUDA runtime (the C++
  * drop-in, sparsim_b200.hpp).  kind: 0 host->device, 1 device->host,
@@ -136,6 +143,8 @@ typedef struct micro_config {
   int32_t dense_output;     /* keep the dense averaged gradient g/n on device */
   int32_t device;           /* CUDA device ordinal */
   int64_t selection_capacity; /* pairs per worker; 0 = partition size (never overflows) */
+  int32_t record_error_norm;  /* per-step error norm ||e_{t+1}||_2 (harness.cpp:230-235), fused
+                                 into K1; 0 = not recorded (NaN in micro_records) */
 } micro_config;
 
 void micro_config_default(micro_config* cfg);
@@ -188,6 +197,23 @@ int micro_query(micro_ctx* ctx, micro_stats* st, int64_t* counts, double* deltas
  * steps written in *written. */
 int micro_history(micro_ctx* ctx, int64_t max, int64_t* t, int64_t* K, int64_t* counts,
                   double* delta_used, int64_t* written);
+
+/* The reference's per-iteration record (IterationRecord, metrics.hpp:15-29;
+ * filled at harness.cpp:226-236) for the MiCRO path's scalars; the task
+ * loss and the modeled phase times are outside this path. */
+typedef struct micro_record {
+  int64_t t;
+  int64_t K;                        /* |union| */
+  int64_t total_selected;           /* sum_i k_i (this context's workers; K on a rank of n) */
+  double actual_density;            /* K / n_g (metrics.cpp:7-10) */
+  double buildup_factor;            /* K / k_global, 0 if nothing selected (collectives.cpp:59-63) */
+  double redundant_traffic_factor;  /* total_selected / K, 0 if nothing (collectives.cpp:65-69) */
+  double error_norm;                /* (sum_i ||e_{i,t+1}||_2) / n_local; NaN if not recorded */
+  double threshold;                 /* (sum_i delta_i used) / n_local (harness.cpp:139-149) */
+} micro_record;
+
+/* Records of the last min(max, steps, 4096) steps, oldest first; synchronises. */
+int micro_records(micro_ctx* ctx, int64_t max, micro_record* out, int64_t* written);
 
 /* Diagnostics: CUDA-event timing of K1's streaming pass (k1_stream) inside
  * the library.  micro_kernel_timing(1) starts recording (up to 1024 launches,

@@ -24,6 +24,7 @@
 // -lmicro_b200 (paper_2310_00967_b200/lib).
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <span>
@@ -312,6 +313,43 @@ inline double actual_density(const AggregatedSelection& agg, Index n_g) {
   return static_cast<double>(agg.indices.size()) / static_cast<double>(n_g);
 }
 
+// error_feedback.hpp:41-48: mean of the per-worker residual norms (each
+// ||e_i||^2 a deterministic fp64 tree sum on the device; the reference's
+// Eigen summation order is not pinned, so agreement is to ~1e-15 relative).
+template <class Vec>
+double error_metric(const std::vector<Vec>& residuals) {
+  if (residuals.empty()) throw std::invalid_argument("error_metric: no workers");
+  const Index n_g = (Index)residuals.front().size();
+  std::vector<b200::DeviceBuffer> bufs;
+  std::vector<const void*> ptrs;
+  bufs.reserve(residuals.size());
+  for (const auto& e : residuals) {
+    if ((Index)e.size() != n_g) throw std::invalid_argument("error_metric: residual length mismatch");
+    bufs.push_back(b200::upload(e));
+    ptrs.push_back(bufs.back().get());
+  }
+  double out = 0.0;
+  b200::check(micro_error_metric(MICRO_F64, ptrs.data(), (int)ptrs.size(), n_g, &out, nullptr));
+  return out;
+}
+
+// metrics.hpp:15-29.  The MiCRO path fills t, the four scalars and the
+// threshold; loss and the modeled phase times belong to the simulator's task
+// and cost model (outside this path) and stay 0.
+struct IterationRecord {
+  std::int64_t t = 0;
+  double actual_density = 0.0;
+  double buildup_factor = 0.0;
+  double redundant_traffic_factor = 0.0;
+  double error_norm = 0.0;
+  double threshold = 0.0;
+  double loss = 0.0;
+  double time_grad = 0.0;
+  double time_select = 0.0;
+  double time_comm = 0.0;
+  double time_overhead = 0.0;
+};
+
 // The per-iteration MiCRO step of run_iteration (harness.cpp:121-224) for
 // `workers` in-process workers on one device, with their residuals and
 // thresholds resident in HBM.  step() takes host gradients (workers * n_g,
@@ -376,6 +414,25 @@ class MicroEngine {
     for (Index j = 0; j < n_g_; ++j)
       out[(std::size_t)j] = esz_ == 8 ? reinterpret_cast<const double*>(raw.data())[j]
                                       : reinterpret_cast<const float*>(raw.data())[j];
+    return out;
+  }
+
+  // Records of the last min(max_steps, 4096) steps, oldest first.
+  std::vector<IterationRecord> records(std::int64_t max_steps = 4096) const {
+    std::vector<micro_record> raw((std::size_t)std::max<std::int64_t>(max_steps, 1));
+    std::int64_t w = 0;
+    b200::check(micro_records(ctx_, max_steps, raw.data(), &w));
+    std::vector<IterationRecord> out((std::size_t)w);
+    for (std::int64_t s = 0; s < w; ++s) {
+      const micro_record& r = raw[(std::size_t)s];
+      IterationRecord& o = out[(std::size_t)s];
+      o.t = r.t;
+      o.actual_density = r.actual_density;
+      o.buildup_factor = r.buildup_factor;
+      o.redundant_traffic_factor = r.redundant_traffic_factor;
+      o.error_norm = r.error_norm;
+      o.threshold = r.threshold;
+    }
     return out;
   }
 

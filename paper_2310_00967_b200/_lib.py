@@ -26,13 +26,19 @@ class micro_config(C.Structure):
         ("n_g", I64), ("n_workers", I32), ("n_local", I32), ("rank", I32), ("dtype", I32),
         ("density", DBL), ("initial_threshold", DBL), ("scaling_factor", DBL), ("min_threshold", DBL),
         ("target", I32), ("error_feedback", I32), ("dense_output", I32), ("device", I32),
-        ("selection_capacity", I64),
+        ("selection_capacity", I64), ("record_error_norm", I32),
     ]
 
 
 class micro_stats(C.Structure):
     _fields_ = [("t", I64), ("steps", I64), ("K", I64), ("total_selected", I64),
                 ("nonfinite", I32), ("overflow", I32)]
+
+
+class micro_record(C.Structure):
+    _fields_ = [("t", I64), ("K", I64), ("total_selected", I64), ("actual_density", DBL),
+                ("buildup_factor", DBL), ("redundant_traffic_factor", DBL), ("error_norm", DBL),
+                ("threshold", DBL)]
 
 
 class MicroError(RuntimeError):
@@ -84,6 +90,7 @@ _SIGS = {
     "micro_all_reduce_sparse_values": ([I32, C.POINTER(VP), I32, I64, VP, I64, VP, VP], I32),
     "micro_all_reduce_sparse": ([I32, C.POINTER(VP), I32, I64, VP, I64, VP, VP], I32),
     "micro_all_gather_indices": ([I32, PI64, VP, VP, PI64, VP], I32),
+    "micro_error_metric": ([I32, C.POINTER(VP), I32, I64, PDBL, VP], I32),
     "micro_synth_gaussian": ([I32, U64, U32, U64, I64, VP, VP], I32),
     "micro_device_malloc": ([C.POINTER(VP), I64, I32], I32),
     "micro_device_free": ([VP], I32),
@@ -102,6 +109,7 @@ _SIGS = {
     "micro_sync": ([VP], I32),
     "micro_query": ([VP, C.POINTER(micro_stats), VP, VP], I32),
     "micro_history": ([VP, I64, VP, VP, VP, VP, PI64], I32),
+    "micro_records": ([VP, I64, VP, PI64], I32),
     "micro_kernel_timing": ([VP, I32], I32),
     "micro_kernel_times": ([VP, VP, I32, C.POINTER(I32)], I32),
     "micro_union_device": ([VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP)], I32),
@@ -137,7 +145,7 @@ def lib() -> C.CDLL:
                 f = getattr(L, name)
                 f.argtypes = args
                 f.restype = res
-            if L.micro_abi_version() != 1:
+            if L.micro_abi_version() != 2:
                 raise ImportError("libmicro_b200.so ABI version mismatch")
             _lib = L
     return _lib

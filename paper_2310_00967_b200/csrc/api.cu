@@ -186,6 +186,15 @@ struct micro_ctx {
   // history
   long long *hist_t = nullptr, *hist_K = nullptr, *hist_counts = nullptr;
   double* hist_delta = nullptr;
+  double* hist_err = nullptr;
+  // error norm (record_error_norm, EF on): ||e_{t+1}||^2 per worker, fused into K1
+  bool norm = false;
+  int64_t norm_ctas = 0;               // slots for the largest producing grid
+  double* norm_part = nullptr;
+  double* norm_group = nullptr;
+  unsigned* norm_ticket = nullptr;     // norm_groups + 1
+  double* norm_sq = nullptr;           // n_local
+  double* norm_corr = nullptr;         // n_local: squares of foreign entries zeroed by the exchange
   // host-side step state
   int64_t steps = 0;      // completed aggregations
   int64_t t_cur = -1;     // iteration of the pending/last compress
@@ -273,6 +282,26 @@ unsigned int next_epoch(micro_ctx* c) {
   if ((e & 0xFFFFFFu) == 0) e = ++c->epoch;
   return e;
 }
+SumSqSlots norm_slots(micro_ctx* c, int i) {
+  SumSqSlots q{};
+  q.part = c->norm_part;
+  q.group = c->norm_group;
+  q.ticket = c->norm_ticket;
+  q.out = c->norm_sq + i;
+  return q;
+}
+
+int norm_mode(const micro_ctx* c) { return !c->cfg.error_feedback ? 2 : c->norm ? 1 : 0; }
+
+// ||resid_i||^2 by a standalone pass (K1 variants without the fused sum).
+template <typename T>
+int launch_sumsq(micro_ctx* c, int i) {
+  const int64_t grid = std::min<int64_t>(c->norm_ctas, 4 * (int64_t)num_sms(c->dev));
+  k_sumsq<T><<<(unsigned)grid, 256, 0, c->stream>>>((const T*)c->resid[i], c->n_g, norm_slots(c, i));
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
 int64_t status_span(micro_ctx* c, int64_t G) {
   c->status_hwm = std::max(c->status_hwm, G);
   return c->status_hwm;
@@ -366,24 +395,32 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.dirty = c->dense_dirty;
   a.super_counts = c->super_counts + c->super_par * kMaxSupers;
   a.super_runs = c->super_runs;
+  a.sq = norm_slots(c, i);
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
   cudaStream_t st = c->stream;
   const bool timed = c->timing && c->t_next < kTimingCap;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
-#define K1S(MODE, D) k1_stream<T, MODE, D><<<grid, kStreamThreads, 0, st>>>(a)
+#define K1S(MODE, D) k1_stream<T, MODE, D, false><<<grid, kStreamThreads, 0, st>>>(a)
+#define K1N(D)                                                                       \
+  do {                                                                               \
+    if (c->norm) k1_stream<T, kWriteZeroSel, D, true><<<grid, kStreamThreads, 0, st>>>(a); \
+    else K1S(kWriteZeroSel, D);                                                      \
+  } while (0)
+  if ((int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
   if (c->n > 1) {
-    if (c->cfg.error_feedback) K1S(kWriteZeroSel, false);
+    if (c->cfg.error_feedback) K1N(false);
     else K1S(kWriteAcc, false);
   } else if (c->cfg.error_feedback) {
-    if (fd) K1S(kWriteZeroSel, true);
-    else K1S(kWriteZeroSel, false);
+    if (fd) K1N(true);
+    else K1N(false);
   } else {
     if (fd) K1S(kWriteNone, true);
     else K1S(kWriteNone, false);
   }
 #undef K1S
+#undef K1N
   CU(cudaGetLastError());
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next++ + 1], st));
   CompactArgs b{};
@@ -417,6 +454,9 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.hist_K = c->hist_K;
     b.hist_counts = c->hist_counts;
     b.hist_delta = c->hist_delta;
+    b.hist_err = c->hist_err;
+    b.norm_mode = norm_mode(c);
+    b.sq = c->norm_sq + i;
     c->fin_done = true;
   }
   k1_gather<T><<<(unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps), kGatherWarps * 32, 0,
@@ -431,7 +471,10 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
   const bool aligned = ((uintptr_t)grad % 16) == 0;
   if (c->k1_kind == 0 && aligned) return launch_k1_stream<T>(c, i, grad, eta, ps, pe);
-  if (c->k1_kind == 1 && aligned) return launch_k1_tma<T>(c, i, grad, eta, ps, pe);
+  if (c->k1_kind == 1 && aligned) {
+    TRY(launch_k1_tma<T>(c, i, grad, eta, ps, pe));
+    return c->norm ? launch_sumsq<T>(c, i) : MICRO_OK;
+  }
   SelectArgs a{};
   a.grad = grad;
   a.resid = c->resid[i];
@@ -470,7 +513,7 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   else
     k1_fused_select<T, true, kWriteNone, false><<<grid, kThreads, 0, c->stream>>>(a);
   CU(cudaGetLastError());
-  return MICRO_OK;
+  return c->norm ? launch_sumsq<T>(c, i) : MICRO_OK;
 }
 
 int finalize_blocks(micro_ctx* c);
@@ -505,6 +548,10 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_K = c->hist_K;
   f.hist_counts = c->hist_counts;
   f.hist_delta = c->hist_delta;
+  f.hist_err = c->hist_err;
+  f.norm_mode = norm_mode(c);
+  f.sq = c->norm_sq;
+  f.sq_corr = c->n > 1 ? c->norm_corr : nullptr;
   const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
   if (c->fin_done) {
     // k1_gather already did the threshold update + history (n = 1, micro_step);
@@ -564,10 +611,12 @@ int aggregate_cluster(micro_ctx* c) {
   const dim3 grid(gx, (unsigned)c->n);
   if (c->cfg.error_feedback)
     k_cluster_reduce<T, true><<<grid, 256, 0, c->stream>>>(w, c->counts, c->sel_cap, c->n, c->t_cur,
-                                                            c->uni_idx[c->buf], (T*)c->uni_sum[c->buf]);
+                                                            c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
+                                                            c->norm ? c->norm_corr : nullptr);
   else
     k_cluster_reduce<T, false><<<grid, 256, 0, c->stream>>>(w, c->counts, c->sel_cap, c->n, c->t_cur,
-                                                             c->uni_idx[c->buf], (T*)c->uni_sum[c->buf]);
+                                                             c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
+                                                             nullptr);
   CU(cudaGetLastError());
   return launch_finalize<T>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 1);
 }
@@ -611,6 +660,11 @@ int reset_state(micro_ctx* c) {
   if (c->dense) CU(cudaMemsetAsync(c->dense, 0, c->n_g * c->esz, c->stream));
   if (c->dense_dirty) CU(cudaMemsetAsync(c->dense_dirty, 0, (c->n_g / 256 + 8) * 8, c->stream));
   if (c->super_counts) CU(cudaMemsetAsync(c->super_counts, 0, 2 * kMaxSupers * sizeof(int), c->stream));
+  if (c->norm) {
+    CU(cudaMemsetAsync(c->norm_ticket, 0, sizeof(unsigned) * (sumsq_groups(c->norm_ctas) + 1), c->stream));
+    CU(cudaMemsetAsync(c->norm_sq, 0, sizeof(double) * c->n_local, c->stream));
+    CU(cudaMemsetAsync(c->norm_corr, 0, sizeof(double) * c->n_local, c->stream));
+  }
   CU(cudaStreamSynchronize(c->stream));
   c->steps = 0;
   c->t_cur = -1;
@@ -734,6 +788,7 @@ void micro_config_default(micro_config* g) {
   g->target = MICRO_TARGET_SPLIT;
   g->error_feedback = 1;
   g->dense_output = 1;
+  g->record_error_norm = 1;
 }
 
 int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
@@ -822,6 +877,20 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((rc = c->alloc((void**)&c->hist_K, sizeof(long long) * kHistCap))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_counts, sizeof(long long) * kHistCap * c->n_local))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_delta, sizeof(double) * kHistCap * c->n_local))) return cleanup(rc);
+  if ((rc = c->alloc((void**)&c->hist_err, sizeof(double) * kHistCap * c->n_local))) return cleanup(rc);
+  c->norm = cfg->record_error_norm && cfg->error_feedback;
+  if (c->norm) {
+    // producing grids: k1_stream (one CTA per 8 units) or k_sumsq (4 per SM)
+    const int64_t ue = c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>();
+    const int64_t units = (c->n_g + ue - 1) / ue;
+    c->norm_ctas = std::max<int64_t>((units + kStreamWarps - 1) / kStreamWarps, 4 * (int64_t)num_sms(c->dev));
+    const int64_t groups = sumsq_groups(c->norm_ctas);
+    if ((rc = c->alloc((void**)&c->norm_part, sizeof(double) * c->norm_ctas))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->norm_group, sizeof(double) * groups))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->norm_ticket, sizeof(unsigned) * (groups + 1)))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->norm_sq, sizeof(double) * c->n_local))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->norm_corr, sizeof(double) * c->n_local))) return cleanup(rc);
+  }
   cudaError_t e;
   if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
@@ -1022,6 +1091,48 @@ int micro_history(micro_ctx* c, int64_t max, int64_t* t, int64_t* K, int64_t* co
   return MICRO_OK;
 }
 
+int micro_records(micro_ctx* c, int64_t max, micro_record* out, int64_t* written) {
+  TRY(check_ctx(c));
+  if (max < 0 || (max && !out)) return fail(MICRO_EINVAL, "bad record buffer");
+  DeviceGuard dg(c->dev);
+  CU(cudaStreamSynchronize(c->stream));
+  const int64_t n = std::min<int64_t>(std::min<int64_t>(max, c->steps), kHistCap);
+  const int nl = c->n_local;
+  std::vector<long long> ht(kHistCap), hk(kHistCap), hc(kHistCap * nl);
+  std::vector<double> hd(kHistCap * nl), he(kHistCap * nl);
+  CU(cudaMemcpy(ht.data(), c->hist_t, sizeof(long long) * kHistCap, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hk.data(), c->hist_K, sizeof(long long) * kHistCap, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hc.data(), c->hist_counts, sizeof(long long) * hc.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hd.data(), c->hist_delta, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(he.data(), c->hist_err, sizeof(double) * he.size(), cudaMemcpyDeviceToHost));
+  uint64_t k_global = 0;
+  TRY(h_global_target(c->cfg.density, c->n_g, &k_global));
+  for (int64_t s = 0; s < n; ++s) {
+    const int64_t slot = (c->steps - n + s) % kHistCap;
+    micro_record r{};
+    r.t = ht[slot];
+    r.K = hk[slot];
+    long long tot = 0;
+    double dsum = 0.0, esum = 0.0;
+    for (int i = 0; i < nl; ++i) {  // worker order, like the reference's loops
+      tot += hc[slot * nl + i];
+      dsum += hd[slot * nl + i];
+      esum += he[slot * nl + i];
+    }
+    // a rank of an n-GPU job sees only its own k_i; the partitions are
+    // disjoint, so sum_i k_i = |union| there
+    r.total_selected = c->cluster ? tot : r.K;
+    r.actual_density = (double)r.K / (double)c->n_g;                                   // metrics.cpp:7-10
+    r.buildup_factor = r.total_selected == 0 ? 0.0 : (double)r.K / (double)k_global;   // collectives.cpp:59-63
+    r.redundant_traffic_factor = r.total_selected == 0 ? 0.0 : (double)r.total_selected / (double)r.K;
+    r.error_norm = esum / nl;                                                          // harness.cpp:230-235
+    r.threshold = dsum / nl;                                                           // harness.cpp:149
+    out[s] = r;
+  }
+  if (written) *written = n;
+  return MICRO_OK;
+}
+
 int micro_union_device(micro_ctx* c, const int32_t** d_idx, const void** d_sums, const int64_t** d_K) {
   TRY(check_ctx(c));
   const int b = c->ever_stepped ? (int)((c->steps - 1) & 1) : 0;
@@ -1135,20 +1246,21 @@ int micro_dist_gather_foreign(micro_ctx* c, const int32_t* d_all_idx, const int6
   for (int r = 0; r < c->n; ++r) mx = std::max<long long>(mx, cs.k[r]);
   if (mx > kmax) return fail(MICRO_EINVAL, "kmax %lld smaller than a count %lld", (long long)kmax, mx);
   const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
+  double* corr = c->norm ? c->norm_corr : nullptr;
   if (c->esz == 4) {
     if (c->cfg.error_feedback)
       k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                      (float*)c->resid[0], (float*)d_send);
+                                                                      (float*)c->resid[0], (float*)d_send, corr);
     else
       k_dist_gather_foreign<float, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                       (float*)c->resid[0], (float*)d_send);
+                                                                       (float*)c->resid[0], (float*)d_send, corr);
   } else {
     if (c->cfg.error_feedback)
       k_dist_gather_foreign<double, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                       (double*)c->resid[0], (double*)d_send);
+                                                                       (double*)c->resid[0], (double*)d_send, corr);
     else
       k_dist_gather_foreign<double, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                        (double*)c->resid[0], (double*)d_send);
+                                                                        (double*)c->resid[0], (double*)d_send, corr);
   }
   CU(cudaGetLastError());
   return MICRO_OK;
@@ -1418,6 +1530,45 @@ int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_co
   CU(cudaFreeAsync(tmp, s));
   CU(cudaStreamSynchronize(s));
   *K = hn;
+  return MICRO_OK;
+}
+
+int micro_error_metric(int dtype, const void* const* h_res, int n, int64_t n_g, double* out, void* stream) {
+  TRY(check_dtype(dtype));
+  if (n < 1 || !h_res) return fail(MICRO_EINVAL, "error_metric: no workers");
+  if (n_g < 0 || !out) return fail(MICRO_EINVAL, "error_metric: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_g + 255) / 256, 4 * (int64_t)num_sms(dev)));
+  const int64_t groups = sumsq_groups(grid);
+  // one scratch block: per-worker slots (part, group, ticket) + n totals
+  const size_t bytes = sizeof(double) * (size_t)n * (grid + groups + 1) + sizeof(unsigned) * (size_t)n * (groups + 1);
+  char* scratch = nullptr;
+  CU(cudaMallocAsync((void**)&scratch, bytes, s));
+  CU(cudaMemsetAsync(scratch, 0, bytes, s));
+  double* part = (double*)scratch;
+  double* grp = part + (size_t)n * grid;
+  double* tot = grp + (size_t)n * groups;
+  unsigned* tick = (unsigned*)(tot + n);
+  for (int i = 0; i < n; ++i) {
+    if (n_g && !h_res[i]) {
+      cudaFreeAsync(scratch, s);
+      return fail(MICRO_EINVAL, "error_metric: null residual %d", i);
+    }
+    SumSqSlots q{part + (size_t)i * grid, grp + (size_t)i * groups, tick + (size_t)i * (groups + 1), tot + i};
+    if (n_g == 0) continue;
+    if (dtype == MICRO_F32) k_sumsq<float><<<(unsigned)grid, 256, 0, s>>>((const float*)h_res[i], n_g, q);
+    else k_sumsq<double><<<(unsigned)grid, 256, 0, s>>>((const double*)h_res[i], n_g, q);
+    CU(cudaGetLastError());
+  }
+  std::vector<double> h(n);
+  CU(cudaMemcpyAsync(h.data(), tot, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(scratch, s));
+  CU(cudaStreamSynchronize(s));
+  double sum = 0.0;  // error_feedback.hpp:44-47: norms summed in worker order, then / n
+  for (int i = 0; i < n; ++i) sum += std::sqrt(h[i]);
+  *out = sum / (double)n;
   return MICRO_OK;
 }
 

@@ -11,6 +11,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "norm.cuh"
 
 namespace micro {
 
@@ -35,31 +36,63 @@ __device__ __forceinline__ long long clamp_count(long long k, long long cap) { r
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long long* counts,
                                                         long long cap, int n, int64_t t,
-                                                        int32_t* union_idx, T* union_sum) {
+                                                        int32_t* union_idx, T* union_sum,
+                                                        double* sq_corr) {
+  // sq_corr (kZero, error norm on): per worker, the squares of the residual
+  // entries zeroed here (foreign union indices), subtracted from K1's
+  // ||e||^2 by k_finalize.  Lane r of each warp accumulates worker r
+  // (r + 32 in a second register); one global atomic per block and worker.
+  __shared__ double s_corr[8][kMaxWorkers];
   const int p = blockIdx.y;
   const int owner = partition_owner(p, n, t);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   long long off = 0;
   for (int q = 0; q < p; ++q) off += clamp_count(counts[partition_owner(q, n, t)], cap);
   const long long k = clamp_count(counts[owner], cap);
   const int32_t* __restrict__ idx = w.sel_idx[owner];
   const T* __restrict__ val = (const T*)w.sel_val[owner];
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
-       m += (long long)gridDim.x * blockDim.x) {
-    const int32_t j = idx[m];
+  const bool corr = kZero && sq_corr != nullptr;  // grid-uniform
+  double c_lo = 0.0, c_hi = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = (long long)blockIdx.x * blockDim.x; b < k; b += stride) {  // warp-uniform trip count
+    const long long m = b + threadIdx.x;
+    const bool act = m < k;
+    const int32_t j = act ? idx[m] : 0;
     T s = (T)0;
     for (int r = 0; r < n; ++r) {
-      T v;
-      if (r == owner) {
-        v = val[m];
-      } else {
-        T* e = (T*)w.resid[r];
-        v = e[j];
-        if (kZero) e[j] = (T)0;
+      T v = (T)0;
+      if (act) {
+        if (r == owner) {
+          v = val[m];
+        } else {
+          T* e = (T*)w.resid[r];
+          v = e[j];
+          if (kZero) e[j] = (T)0;
+        }
       }
       s = add_rn(s, v);
+      if (corr && r != owner) {
+        const double q = warp_sum_f64(act ? (double)v * (double)v : 0.0);
+        if (lane == (r & 31)) {
+          if (r < 32) c_lo += q;
+          else c_hi += q;
+        }
+      }
     }
-    union_idx[off + m] = j;
-    union_sum[off + m] = s;
+    if (act) {
+      union_idx[off + m] = j;
+      union_sum[off + m] = s;
+    }
+  }
+  if (corr) {
+    if (lane < n) s_corr[wid][lane] = c_lo;
+    if (lane + 32 < n) s_corr[wid][lane + 32] = c_hi;
+    __syncthreads();
+    if ((int)threadIdx.x < n) {
+      double tot = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += s_corr[q][threadIdx.x];
+      if (tot != 0.0) atomicAdd(sq_corr + threadIdx.x, tot);
+    }
   }
 }
 
@@ -67,17 +100,34 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
 // send buffer (segment per destination, rank order) and zero them.
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_idx, int64_t kmax,
-                                                             Counts c, int me, T* resid, T* send) {
+                                                             Counts c, int me, T* resid, T* send,
+                                                             double* sq_corr) {
+  __shared__ double s_corr[8];
   const int o = blockIdx.y;
-  if (o == me) return;
+  if (o == me) return;  // block-uniform
   const long long k = c.k[o];
   const int32_t* __restrict__ idx = all_idx + (int64_t)o * kmax;
   T* __restrict__ out = send + c.off[o];
+  double q = 0.0;
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
        m += (long long)gridDim.x * blockDim.x) {
     const int32_t j = idx[m];
-    out[m] = resid[j];
-    if (kZero) resid[j] = (T)0;
+    const T v = resid[j];
+    out[m] = v;
+    if (kZero) {
+      resid[j] = (T)0;
+      q += (double)v * (double)v;
+    }
+  }
+  if (kZero && sq_corr) {  // squares of the zeroed entries (error norm, see k_cluster_reduce)
+    q = warp_sum_f64(q);
+    if ((threadIdx.x & 31) == 0) s_corr[threadIdx.x >> 5] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_corr[w];
+      if (tot != 0.0) atomicAdd(sq_corr, tot);
+    }
   }
 }
 
@@ -142,6 +192,10 @@ struct FinalizeArgs {
   long long* hist_K;
   long long* hist_counts;
   double* hist_delta;
+  double* hist_err;           // per worker ||e_{t+1}||_2 (error_norm record)
+  int norm_mode;              // 0: not recorded (NaN), 1: sqrt(sq - sq_corr), 2: residual is zero (EF off)
+  const double* sq;           // per worker ||e||^2 after K1 (own selections zeroed)
+  double* sq_corr;            // per worker squares of the foreign entries zeroed by the exchange (reset here)
 };
 
 __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long n, int64_t key) {
@@ -188,6 +242,15 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
       double d = a.delta[i];
       a.hist_counts[a.slot * a.n_local + i] = (long long)k;
       a.hist_delta[a.slot * a.n_local + i] = d;
+      double err = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not recorded
+      if (a.norm_mode == 1) {
+        const double sq = a.sq[i] - (a.sq_corr ? a.sq_corr[i] : 0.0);
+        err = sqrt(sq > 0.0 ? sq : 0.0);
+        if (a.sq_corr) a.sq_corr[i] = 0.0;
+      } else if (a.norm_mode == 2) {
+        err = 0.0;
+      }
+      a.hist_err[a.slot * a.n_local + i] = err;
       // sparsifier.cpp:77-81
       if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
       else if (k < a.k_target) d *= 1.0 - a.alpha;

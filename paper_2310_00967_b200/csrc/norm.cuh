@@ -1,0 +1,91 @@
+// norm.cuh — deterministic fp64 sums of squares for the reference's
+// per-iteration error norm: error_norm = (sum_i ||e_{i,t+1}||_2) / n
+// (harness.cpp:230-235; error_metric, error_feedback.hpp:41-48).
+//
+// Every CTA of the producing grid reduces its threads' partial sums with a
+// fixed butterfly (bit-identical in every lane) and publishes one double;
+// the last CTA of each group of kSqGroup CTAs (atomic ticket) sums the
+// group in index order, and the last group sums the groups.  The result
+// depends only on the grid shape, never on CTA timing; tickets are reset by
+// the CTAs that consume them, so the slots are ready for the next launch.
+#pragma once
+
+#include "common.cuh"
+
+namespace micro {
+
+constexpr int kSqGroup = 64;
+
+struct SumSqSlots {
+  double* part;       // one per CTA of the producing grid
+  double* group;      // one per group of kSqGroup CTAs
+  unsigned* ticket;   // groups + 1 (the last one is the top-level ticket); zero between launches
+  double* out;        // the total
+};
+
+__host__ __device__ constexpr long long sumsq_groups(long long ctas) { return (ctas + kSqGroup - 1) / kSqGroup; }
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Called by every thread of the CTA (contains a __syncthreads) at the end of
+// the kernel: after it returns, only warp 0 of the finishing CTAs has done
+// anything further.
+__device__ __forceinline__ void cta_sumsq_publish(double v, const SumSqSlots& s) {
+  __shared__ double s_red[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  v = warp_sum_f64(v);
+  if (lane == 0) s_red[w] = v;
+  __syncthreads();
+  if (w != 0) return;
+  double t = lane < nw ? s_red[lane] : 0.0;
+  t = warp_sum_f64(t);
+  const unsigned nblk = gridDim.x, b = blockIdx.x, g = b / kSqGroup;
+  const unsigned gsize = min((unsigned)kSqGroup, nblk - g * kSqGroup);
+  const unsigned ngroups = (nblk + kSqGroup - 1) / kSqGroup;
+  unsigned prev = 0;
+  if (lane == 0) {
+    s.part[b] = t;
+    __threadfence();
+    prev = atomicAdd(s.ticket + g, 1u);
+  }
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != gsize - 1) return;
+  __threadfence();
+  double gs = 0.0;
+  for (unsigned q = lane; q < gsize; q += 32) gs += __ldcg(s.part + g * kSqGroup + q);
+  gs = warp_sum_f64(gs);
+  if (lane == 0) {
+    s.group[g] = gs;
+    s.ticket[g] = 0;
+    __threadfence();
+    prev = atomicAdd(s.ticket + ngroups, 1u);
+  }
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != ngroups - 1) return;
+  __threadfence();
+  double tot = 0.0;
+  for (unsigned q = lane; q < ngroups; q += 32) tot += __ldcg(s.group + q);
+  tot = warp_sum_f64(tot);
+  if (lane == 0) {
+    *s.out = tot;
+    s.ticket[ngroups] = 0;
+  }
+}
+
+// Standalone sum of squares of one vector (the value-level error_metric):
+// fixed grid, each thread sums its grid-stride elements in order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sumsq(const T* __restrict__ x, int64_t n, SumSqSlots s) {
+  double v = 0.0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double y = (double)x[j];
+    v += y * y;
+  }
+  cta_sumsq_publish(v, s);
+}
+
+}  // namespace micro

@@ -30,6 +30,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "norm.cuh"
 #include "select.cuh"
 
 namespace micro {
@@ -62,6 +63,7 @@ struct StreamArgs {
   unsigned long long* dirty;
   int* super_counts;       // selections per super block of `super_runs` CTA runs (zeroed)
   int super_runs;
+  SumSqSlots sq;           // kNorm: ||e_{t+1}||^2 of this worker (before union zeroing of foreign entries)
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -81,7 +83,7 @@ __device__ __forceinline__ unsigned even_bits(unsigned x) {
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
-template <typename T, int kMode, bool kDense>
+template <typename T, int kMode, bool kDense, bool kNorm>
 __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -255,6 +257,18 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     }
   }
   if (probe != probe) atomicOr(a.flags, 1);
+  if (kNorm) {  // the stored e_{t+1}: acc with the own selections zeroed (EF on)
+    double sq = 0.0;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c)
+        if (!(mask[i] & (1u << c))) {
+          const double y = (double)comp(e[i], c);
+          sq += y * y;
+        }
+    cta_sumsq_publish(sq, a.sq);
+  }
 }
 
 struct CompactArgs {
@@ -283,6 +297,9 @@ struct CompactArgs {
   long long fin_t, fin_slot;
   long long *hist_t, *hist_K, *hist_counts;
   double* hist_delta;
+  double* hist_err;
+  int norm_mode;           // as FinalizeArgs (no foreign entries at n = 1)
+  const double* sq;
 };
 
 __device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long total) {
@@ -293,6 +310,8 @@ __device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long 
   a.hist_counts[a.fin_slot] = total;
   double d = *a.fin_delta;
   a.hist_delta[a.fin_slot] = d;
+  a.hist_err[a.fin_slot] = a.norm_mode == 1 ? sqrt(*a.sq)
+                           : a.norm_mode == 2 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
   const unsigned long long k = (unsigned long long)total;
   if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
   else if (k < a.k_target) d *= 1.0 - a.alpha;

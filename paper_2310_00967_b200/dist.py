@@ -138,5 +138,25 @@ class DistMicro:
         self.compress(grads, eta, t)
         return self.aggregate()
 
+    def records(self, max_steps: int = 4096) -> list[dict]:
+        """IterationRecord scalars (metrics.hpp:15-29) of the whole job: each
+        rank holds its own ||e_r|| and delta_r, combined here in rank order
+        like the reference's worker loops (harness.cpp:149, :230-235).
+        Collective: every rank must call it."""
+        recs = self.m.records(max_steps)
+        dev = torch.device(self.comm_device) if self.comm_device else self.m.device
+        mine = torch.tensor([[r["error_norm"], r["threshold"]] for r in recs] or [[0.0, 0.0]],
+                            dtype=torch.float64, device=dev)
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(parts, mine, group=self.group)
+        cols = [p.cpu().numpy() for p in parts]
+        for s, r in enumerate(recs):
+            en = th = 0.0
+            for c in cols:  # rank order
+                en += float(c[s, 0])
+                th += float(c[s, 1])
+            r["error_norm"], r["threshold"] = en / self.world, th / self.world
+        return recs
+
     def __getattr__(self, name):  # query, history, union, residual, dense, set_model, sync ...
         return getattr(self.m, name)

@@ -67,7 +67,8 @@ class Micro:
                  initial_threshold: float = 0.01, scaling_factor: float = 0.01,
                  min_threshold: float = 1e-12, target: str = "split", error_feedback: bool = True,
                  dense_output: bool = True, device: int | torch.device | None = None,
-                 stream: torch.cuda.Stream | None = None, selection_capacity: int = 0):
+                 stream: torch.cuda.Stream | None = None, selection_capacity: int = 0,
+                 record_error_norm: bool = True):
         L = lib()
         if dtype not in _DT:
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unsupported dtype {dtype}")
@@ -86,6 +87,7 @@ class Micro:
         cfg.target = 0 if target == "split" else 1
         cfg.error_feedback, cfg.dense_output = int(error_feedback), int(dense_output)
         cfg.device, cfg.selection_capacity = dev.index, selection_capacity
+        cfg.record_error_norm = int(record_error_norm)
         self.cfg = cfg
         self.device, self.dtype = dev, dtype
         self.n_g, self.n, self.n_local, self.rank = n_g, n_workers, cfg.n_local, rank
@@ -186,6 +188,16 @@ class Micro:
         m = w.value
         return dict(t=t[:m], K=K[:m], counts=cnt[: m * self.n_local].reshape(m, self.n_local),
                     delta_used=dl[: m * self.n_local].reshape(m, self.n_local))
+
+    def records(self, max_steps: int = 4096) -> list[dict]:
+        """The reference's IterationRecord scalars (metrics.hpp:15-29) of the
+        last steps, oldest first: t, actual_density, buildup_factor,
+        redundant_traffic_factor, error_norm, threshold (+ K, total_selected)."""
+        n = min(max_steps, 4096)
+        buf = (_lib.micro_record * max(n, 1))()
+        w = C.c_int64()
+        check(lib().micro_records(self._h, n, buf, C.byref(w)))
+        return [{f: getattr(buf[i], f) for f, _ in _lib.micro_record._fields_} for i in range(w.value)]
 
     def kernel_timing(self, enable: bool = True):
         """Record CUDA-event durations of K1's streaming pass (diagnostics)."""

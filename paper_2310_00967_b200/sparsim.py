@@ -222,3 +222,18 @@ def actual_density(agg: AggregatedSelection, n_g: int) -> float:
     if n_g < 1:
         raise InvalidArgument(_lib.MICRO_EINVAL, "actual_density: n_g must be positive")
     return agg.indices.numel() / n_g
+
+
+def error_metric(residuals) -> float:
+    """error_feedback.hpp:41-48: (sum_i ||e_i||_2) / n, norms summed in worker
+    order (each ||e_i||^2 a deterministic fp64 tree sum on the device)."""
+    if len(residuals) == 0:
+        raise InvalidArgument(_lib.MICRO_EINVAL, "error_metric: no workers")
+    res = [_vec(r, "error_metric") for r in residuals]
+    if any(r.numel() != res[0].numel() or r.dtype != res[0].dtype for r in res):
+        raise InvalidArgument(_lib.MICRO_EINVAL, "error_metric: residuals must share length and dtype")
+    arr = (C.c_void_p * len(res))(*[r.data_ptr() for r in res])
+    out = C.c_double()
+    check(lib().micro_error_metric(_DT[res[0].dtype], arr, len(res), res[0].numel(), C.byref(out),
+                                   _stream(res[0].device)))
+    return out.value

@@ -150,10 +150,25 @@ int main() {
     std::mt19937_64 rng(42);
     std::normal_distribution<double> unit(0.0, 1.0);
     std::vector<double> G((std::size_t)(n * n_g));
+    std::vector<double> want_norm, want_thr, want_density;
     for (int t = 0; t < 20; ++t) {
       for (auto& v : G) v = unit(rng);
       std::vector<double> summed;
+      double thr = 0.0;
+      for (const auto& d : eng.thresholds()) thr += d.delta;
+      want_thr.push_back(thr / n);
       const auto agg = eng.step(G.data(), 0.01, t, &summed);
+      want_density.push_back(actual_density(agg, n_g));
+      std::vector<GradientVector> res;
+      for (int i = 0; i < n; ++i) res.push_back(eng.residual(i));
+      double ns = 0.0;  // error_feedback.hpp:41-48 with a sequential fp64 norm
+      for (const auto& e : res) {
+        double q = 0.0;
+        for (double v : e) q += v * v;
+        ns += std::sqrt(q);
+      }
+      want_norm.push_back(ns / n);
+      CHECK(std::fabs(error_metric(res) - ns / n) <= 1e-12 * (ns / n));
       CHECK(agg.indices.size() == agg.total_selected());  // no build-up (acceptance.cpp:93-118)
       for (std::size_t k = 1; k < agg.indices.size(); ++k) CHECK(agg.indices[k - 1] < agg.indices[k]);
       CHECK(summed.size() == agg.indices.size());
@@ -161,6 +176,16 @@ int main() {
         const auto e = eng.residual(i);
         for (Index j : agg.indices) CHECK(e[(std::size_t)j] == 0.0);
       }
+    }
+    // IterationRecord (metrics.hpp:15-29) from the device history
+    const auto recs = eng.records();
+    CHECK(recs.size() == 20);
+    for (std::size_t s = 0; s < recs.size(); ++s) {
+      CHECK(recs[s].t == (std::int64_t)s);
+      CHECK(recs[s].actual_density == want_density[s]);
+      CHECK(recs[s].redundant_traffic_factor == 1.0);
+      CHECK(recs[s].threshold == want_thr[s]);
+      CHECK(std::fabs(recs[s].error_norm - want_norm[s]) <= 1e-12 * want_norm[s]);
     }
   }
   std::printf("%s: %d failed checks\n", g_fail ? "FAIL" : "OK", g_fail);

@@ -33,7 +33,11 @@ def _worker(rank, world, port, n_g, iters, ef, q):
     m.set_model(x)
     ref = OracleCluster(n_g, world, density=d, delta0=delta0, error_feedback=ef, model=True)
     bad = []
+    want = []
     for t in range(iters):
+        thr = 0.0
+        for dl in ref.delta:
+            thr += float(dl)
         G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)])
         K = m.step([torch.from_numpy(G[rank]).cuda()], eta, t)
         r = ref.step(G, eta, t)
@@ -55,6 +59,13 @@ def _worker(rank, world, port, n_g, iters, ef, q):
             bad.append((t, "dense"))
         if not np.array_equal(x.cpu().numpy(), ref.x):
             bad.append((t, "model"))
+        en = 0.0
+        for e in ref.e:
+            en += float(np.sqrt((e.astype(np.float64) ** 2).sum()))
+        want.append((r["union_idx"].size, thr / world, en / world))
+    for t, (rec, (K, thr, en)) in enumerate(zip(m.records(iters), want)):
+        if rec["t"] != t or rec["K"] != K or rec["threshold"] != thr or abs(rec["error_norm"] - en) > 1e-12 * en:
+            bad.append((t, "record", rec, (K, thr, en)))
     dist.destroy_process_group()
     q.put((rank, bad))
 

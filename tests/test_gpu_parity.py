@@ -5,7 +5,9 @@ reference's own compiled code (oracle/_ref) and its golden runs, BIT FOR BIT:
 per-worker counts, union indices, reduced sums, thresholds, residuals, the
 dense averaged gradient and the model.
 """
+import functools
 import glob
+import operator
 import os
 
 import numpy as np
@@ -24,6 +26,11 @@ if torch.cuda.is_available():
 SEED, ETA = 7, 0.01
 
 
+def seq_sum(xs):
+    """Left-to-right fp64 sum (the reference's loops; numpy and Python's sum() are not)."""
+    return functools.reduce(operator.add, (float(x) for x in xs), 0.0)
+
+
 def gen(o, n, n_g, t, dtype):
     return np.stack([o.gaussian(SEED, i, t, n_g) for i in range(n)]).astype(dtype)
 
@@ -40,7 +47,9 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         ref = RefCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, model=True)
     else:
         ref = OracleCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, dtype=dtype, model=True)
+    want = []  # per step: (K, sum k_i, threshold used, error norm) from the checker
     for t in range(iters):
+        thr_used = seq_sum(m.query().deltas) / n
         G = gen(o, n, n_g, t, dtype)
         Gd = torch.from_numpy(G).cuda()
         if split:  # micro_compress + micro_aggregate (k_finalize launched separately)
@@ -49,6 +58,9 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         else:      # micro_step (n = 1: threshold update folded into k1_gather)
             m.step(list(Gd), ETA, t)
         r = ref.step(G, ETA, t)
+        E = ref.residuals() if oracle == "reference" else ref.e
+        norms = np.sqrt((E.astype(np.float64) ** 2).sum(axis=1))
+        want.append((r["union_idx"].size, int(np.sum(r["counts"])), thr_used, seq_sum(norms) / n))
         if t % check_every and t != iters - 1:
             continue
         st = m.query()
@@ -69,6 +81,15 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         assert np.array_equal(x.cpu().numpy(), ref.x.astype(dense.dtype)), t
     h = m.history(iters)
     assert h["t"].tolist() == list(range(iters))
+    k_glob = Oracle().global_target_count(d, n_g)
+    for t, (rec, (K, tot, thr, en)) in enumerate(zip(m.records(iters), want)):
+        # the reference's IterationRecord (harness.cpp:226-236)
+        assert rec["t"] == t and rec["K"] == K and rec["total_selected"] == tot
+        assert rec["actual_density"] == K / n_g
+        assert rec["buildup_factor"] == (K / k_glob if tot else 0.0)
+        assert rec["redundant_traffic_factor"] == (tot / K if tot else 0.0)
+        assert rec["threshold"] == thr
+        assert abs(rec["error_norm"] - en) <= 1e-12 * en + 1e-300, (t, rec["error_norm"], en)
     m.close()
 
 

@@ -140,3 +140,25 @@ def test_collectives():
         masked[agg.indices.long()] = dense[agg.indices.long()]
         assert torch.equal(S.all_reduce_sparse(accs, agg), masked)
         assert torch.equal(S.all_reduce_sparse_values(accs, agg), masked[agg.indices.long()])
+
+
+# error_feedback.hpp:41-48 error_metric (the norm's summation order is not
+# pinned by the reference: 1e-12 relative, test_tensor.cpp:57)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_error_metric(dtype):
+    ref = Reference()
+    rng = np.random.default_rng(5)
+    for n, n_g in [(1, 1), (1, 3), (2, 1000), (4, 100_003), (3, 2_000_001)]:
+        es = [rng.standard_normal(n_g) for _ in range(n)]
+        got = S.error_metric([torch.from_numpy(e).to("cuda", dtype) for e in es])
+        want = ref.error_metric([e.astype(np.float32).astype(np.float64) if dtype == torch.float32 else e
+                                 for e in es])
+        assert abs(got - want) <= 1e-12 * want, (n, n_g, got, want)
+    assert S.error_metric([torch.zeros(10, dtype=dtype, device="cuda")]) == 0.0
+    # deterministic: the same bits every call
+    e = torch.randn(3_000_017, dtype=dtype, device="cuda")
+    assert len({S.error_metric([e, e]) for _ in range(5)}) == 1
+    with pytest.raises(InvalidArgument):
+        S.error_metric([])
+    with pytest.raises(InvalidArgument):
+        S.error_metric([vec([1.0, 2.0]), vec([1.0])])
