@@ -395,7 +395,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.dirty = c->dense_dirty;
   a.super_counts = c->super_counts + c->super_par * kMaxSupers;
   a.super_runs = c->super_runs;
-  a.sq = norm_slots(c, i);
+  a.sq_part = c->norm_part;
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
@@ -408,7 +408,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     if (c->norm) k1_stream<T, kWriteZeroSel, D, true><<<grid, kStreamThreads, 0, st>>>(a); \
     else K1S(kWriteZeroSel, D);                                                      \
   } while (0)
-  if ((int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
+  if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
   if (c->n > 1) {
     if (c->cfg.error_feedback) K1N(false);
     else K1S(kWriteAcc, false);
@@ -456,11 +456,18 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.hist_delta = c->hist_delta;
     b.hist_err = c->hist_err;
     b.norm_mode = norm_mode(c);
-    b.sq = c->norm_sq + i;
     c->fin_done = true;
   }
-  k1_gather<T><<<(unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps), kGatherWarps * 32, 0,
-                  c->stream>>>(b);
+  unsigned gblocks = (unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps);
+  if (c->norm) {  // one more CTA reduces k1_stream's per-CTA partials
+    b.sq_part = c->norm_part;
+    b.sq_parts = (int)grid;
+    b.sq_out = c->norm_sq + i;
+    b.hist_err = c->hist_err;
+    b.fin_slot = c->steps % kHistCap;
+    gblocks += 1;
+  }
+  k1_gather<T><<<gblocks, kGatherWarps * 32, 0, c->stream>>>(b);
   CU(cudaGetLastError());
   return MICRO_OK;
 }

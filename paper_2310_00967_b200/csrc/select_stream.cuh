@@ -63,7 +63,7 @@ struct StreamArgs {
   unsigned long long* dirty;
   int* super_counts;       // selections per super block of `super_runs` CTA runs (zeroed)
   int super_runs;
-  SumSqSlots sq;           // kNorm: ||e_{t+1}||^2 of this worker (before union zeroing of foreign entries)
+  double* sq_part;         // kNorm: per CTA, sum of e_{t+1}^2 (own selections zeroed); reduced by k1_gather
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -267,7 +267,18 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
           const double y = (double)comp(e[i], c);
           sq += y * y;
         }
-    cta_sumsq_publish(sq, a.sq);
+    // CTA partial only: no fence, no ticket on the streaming pass (a
+    // per-CTA release costs ~20 % of K1); k1_gather's extra CTA sums them
+    __shared__ double s_sq[kStreamWarps];
+    sq = warp_sum_f64(sq);
+    if (lane == 0) s_sq[w] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kStreamWarps; ++q) t += s_sq[q];
+      a.sq_part[blockIdx.x] = t;
+    }
   }
 }
 
@@ -299,7 +310,11 @@ struct CompactArgs {
   double* hist_delta;
   double* hist_err;
   int norm_mode;           // as FinalizeArgs (no foreign entries at n = 1)
-  const double* sq;
+  // norm on: the grid's last CTA sums k1_stream's per-CTA partials in index
+  // order into *sq_out (and, fused n = 1 step, hist_err[fin_slot])
+  const double* sq_part;
+  int sq_parts;
+  double* sq_out;
 };
 
 __device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long total) {
@@ -310,8 +325,8 @@ __device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long 
   a.hist_counts[a.fin_slot] = total;
   double d = *a.fin_delta;
   a.hist_delta[a.fin_slot] = d;
-  a.hist_err[a.fin_slot] = a.norm_mode == 1 ? sqrt(*a.sq)
-                           : a.norm_mode == 2 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+  if (a.norm_mode != 1)  // mode 1: written by the reducing CTA
+    a.hist_err[a.fin_slot] = a.norm_mode == 2 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
   const unsigned long long k = (unsigned long long)total;
   if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
   else if (k < a.k_target) d *= 1.0 - a.alpha;
@@ -343,6 +358,22 @@ template <typename T>
 __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   __shared__ long long s_part[kGatherWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (a.sq_part && blockIdx.x == gridDim.x - 1) {  // the extra CTA: ||e_{t+1}||^2, fixed order
+    __shared__ double s_sq[kGatherWarps];
+    double v = 0.0;
+    for (int q = threadIdx.x; q < a.sq_parts; q += kGatherWarps * 32) v += a.sq_part[q];
+    v = warp_sum_f64(v);
+    if (lane == 0) s_sq[w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < kGatherWarps; ++q) t += s_sq[q];
+      *a.sq_out = t;
+      if (a.fin_delta) a.hist_err[a.fin_slot] = sqrt(t);
+    }
+    return;
+  }
   const int r0 = blockIdx.x * kGatherWarps;
   const int sb = r0 / a.super_runs;
   // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0)
