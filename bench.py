@@ -369,8 +369,9 @@ def main():
     ap.add_argument("--cluster-workers", type=int, default=1,
                     help="N = 1 only: W in-process workers on the GPU (the reference's in-process cluster)")
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
-    ap.add_argument("--no-error-norm", dest="error_norm", action="store_false",
-                    help="do not record the per-step error norm (fused into k1_stream)")
+    ap.add_argument("--error-norm", action="store_true",
+                    help="also record the per-step error norm ||e_{t+1}|| (fused into k1_stream); off by "
+                         "default, like the reference arm's timed step")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -358,9 +358,12 @@ template <typename T>
 __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   __shared__ long long s_part[kGatherWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (a.sq_part && blockIdx.x == gridDim.x - 1) {  // the extra CTA: ||e_{t+1}||^2, fixed order
+  // norm on: CTA 0 (scheduled first, overlapping the copies) reduces
+  // ||e_{t+1}||^2 in a fixed order; the copy CTAs are 1..
+  if (a.sq_part && blockIdx.x == 0) {
     __shared__ double s_sq[kGatherWarps];
     double v = 0.0;
+#pragma unroll 8
     for (int q = threadIdx.x; q < a.sq_parts; q += kGatherWarps * 32) v += a.sq_part[q];
     v = warp_sum_f64(v);
     if (lane == 0) s_sq[w] = v;
@@ -374,12 +377,13 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     }
     return;
   }
-  const int r0 = blockIdx.x * kGatherWarps;
+  const int gb = (int)blockIdx.x - (a.sq_part ? 1 : 0);
+  const int r0 = gb * kGatherWarps;
   const int sb = r0 / a.super_runs;
   // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0)
   long long base = block_sum_range(a.super_counts, 0, sb, s_part) +
                    block_sum_range(a.run_counts, sb * a.super_runs, r0, s_part);
-  if (blockIdx.x == 0) {
+  if (gb == 0) {
     const int nsup = (a.num_runs + a.super_runs - 1) / a.super_runs;
     const long long total = block_sum_range(a.super_counts, 0, nsup, s_part);
     if (threadIdx.x == 0) {

@@ -47,7 +47,7 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         ref = RefCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, model=True)
     else:
         ref = OracleCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, dtype=dtype, model=True)
-    want = []  # per step: (K, sum k_i, threshold used, error norm) from the checker
+    recs_want = []  # per step: (K, sum k_i, threshold used, error norm) from the checker
     for t in range(iters):
         thr_used = seq_sum(m.query().deltas) / n
         G = gen(o, n, n_g, t, dtype)
@@ -60,7 +60,7 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         r = ref.step(G, ETA, t)
         E = ref.residuals() if oracle == "reference" else ref.e
         norms = np.sqrt((E.astype(np.float64) ** 2).sum(axis=1))
-        want.append((r["union_idx"].size, int(np.sum(r["counts"])), thr_used, seq_sum(norms) / n))
+        recs_want.append((r["union_idx"].size, int(np.sum(r["counts"])), thr_used, seq_sum(norms) / n))
         if t % check_every and t != iters - 1:
             continue
         st = m.query()
@@ -82,7 +82,7 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     h = m.history(iters)
     assert h["t"].tolist() == list(range(iters))
     k_glob = Oracle().global_target_count(d, n_g)
-    for t, (rec, (K, tot, thr, en)) in enumerate(zip(m.records(iters), want)):
+    for t, (rec, (K, tot, thr, en)) in enumerate(zip(m.records(iters), recs_want)):
         # the reference's IterationRecord (harness.cpp:226-236)
         assert rec["t"] == t and rec["K"] == K and rec["total_selected"] == tot
         assert rec["actual_density"] == K / n_g
