@@ -51,6 +51,12 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     for t in range(iters):
         thr_used = seq_sum(m.query().deltas) / n
         G = gen(o, n, n_g, t, dtype)
+        # energy before the exchange zeroes foreign entries: at n > 1 the
+        # norm is ||e||^2 - (squares zeroed by the exchange), accurate to
+        # ~1e-15 of this, not of the result
+        e_now = ref.residuals() if oracle == "reference" else ref.e
+        acc = e_now.astype(dtype) + dtype(ETA) * G
+        energy = float(np.sqrt((acc.astype(np.float64) ** 2).sum(axis=1)).max())
         Gd = torch.from_numpy(G).cuda()
         if split:  # micro_compress + micro_aggregate (k_finalize launched separately)
             m.compress(list(Gd), ETA, t)
@@ -60,7 +66,7 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         r = ref.step(G, ETA, t)
         E = ref.residuals() if oracle == "reference" else ref.e
         norms = np.sqrt((E.astype(np.float64) ** 2).sum(axis=1))
-        recs_want.append((r["union_idx"].size, int(np.sum(r["counts"])), thr_used, seq_sum(norms) / n))
+        recs_want.append((r["union_idx"].size, int(np.sum(r["counts"])), thr_used, seq_sum(norms) / n, energy))
         if t % check_every and t != iters - 1:
             continue
         st = m.query()
@@ -82,14 +88,17 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     h = m.history(iters)
     assert h["t"].tolist() == list(range(iters))
     k_glob = Oracle().global_target_count(d, n_g)
-    for t, (rec, (K, tot, thr, en)) in enumerate(zip(m.records(iters), recs_want)):
+    for t, (rec, (K, tot, thr, en, energy)) in enumerate(zip(m.records(iters), recs_want)):
         # the reference's IterationRecord (harness.cpp:226-236)
         assert rec["t"] == t and rec["K"] == K and rec["total_selected"] == tot
         assert rec["actual_density"] == K / n_g
         assert rec["buildup_factor"] == (K / k_glob if tot else 0.0)
         assert rec["redundant_traffic_factor"] == (tot / K if tot else 0.0)
         assert rec["threshold"] == thr
-        assert abs(rec["error_norm"] - en) <= 1e-12 * en + 1e-300, (t, rec["error_norm"], en)
+        if n == 1 or en > 1e-6 * energy:
+            assert abs(rec["error_norm"] - en) <= 1e-12 * en + 1e-300, (t, rec["error_norm"], en)
+        else:  # (nearly) everything zeroed: the subtraction's noise floor
+            assert rec["error_norm"] <= 1e-6 * energy, (t, rec["error_norm"], en, energy)
     m.close()
 
 
