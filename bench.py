@@ -187,8 +187,8 @@ def our_arm(args, wl):
         from paper_2310_00967_b200.dist import DistMicro
         tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
-        m = DistMicro(n_g, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
-                      record_error_norm=args.error_norm)
+        m = DistMicro(n_g, transport=args.transport, density=d, initial_threshold=delta0, scaling_factor=ALPHA,
+                      dense_output=args.dense, record_error_norm=args.error_norm)
     else:
         m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
                          record_error_norm=args.error_norm)
@@ -272,7 +272,8 @@ def our_arm(args, wl):
     # update) at n = 1; a W-worker cluster: 2 per worker + k_cluster_reduce +
     # k_finalize; n > 1 ranks: K1 x2, gather_foreign, owner_reduce,
     # build_union, finalize (NCCL kernels not counted)
-    launches_per_step = (2 if W == 1 else 2 * W + 2) if world == 1 else 6
+    launches_per_step = ((2 if W == 1 else 2 * W + 2) if world == 1
+                         else (4 if args.transport == "peer" else 6))  # peer: K1 x2, exchange, finalize
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (N = 1) ----
@@ -331,7 +332,8 @@ def our_arm(args, wl):
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
                                   + "); each 4*n_g bytes > L2 (no flush needed)")
                        if 4 * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
-                       "parallelism": (f"dp{world} (exclusive cyclic partitions)" if W == 1 else
+                       "parallelism": (f"dp{world} (exclusive cyclic partitions"
+                                       + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
                                        f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
             "density": density, "density_rel_err": density / d - 1.0,
             "density_window": {"first_quarter": float(K[: max(1, len(K) // 4)].mean() / n_g),
@@ -369,6 +371,8 @@ def main():
     ap.add_argument("--cluster-workers", type=int, default=1,
                     help="N = 1 only: W in-process workers on the GPU (the reference's in-process cluster)")
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
+    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
     ap.add_argument("--error-norm", action="store_true",
                     help="also record the per-step error norm ||e_{t+1}|| (fused into k1_stream); off by "
                          "default, like the reference arm's timed step")

@@ -254,6 +254,26 @@ int micro_dist_owner_reduce(micro_ctx* ctx, const void* d_recv, const int64_t* h
 int micro_dist_finalize(micro_ctx* ctx, const int32_t* d_all_idx, const void* d_all_sums,
                         const int64_t* h_counts, int64_t kmax);
 
+/* ---- the same exchange as ONE kernel over peer memory (NVLink) ----------- *
+ * Replaces K2..K7 above (collectives.cpp:14-57 semantics, harness.cpp:185-224
+ * order) with no NCCL data movement and no host round trip:
+ *   setup:  micro_peer_export -> all-gather the handle blobs (any transport)
+ *           -> micro_peer_import(all ranks' blobs in rank order)
+ *   step:   micro_compress
+ *           barrier #1 (every rank's compress complete; e.g. a 4-byte
+ *                       ncclAllReduce on ctx's stream)
+ *           micro_peer_exchange  (owner: peer reads of acc_r[j] in rank order,
+ *                                 peer zeroing, push (j, s_j) to every rank)
+ *           barrier #2
+ *           micro_peer_finalize  (threshold, history, dense g/n, model)
+ * The handle blob holds CUDA IPC handles of this rank's residual, counts,
+ * union buffers and error-norm slot. */
+#define MICRO_PEER_HANDLE_BYTES 448
+int micro_peer_export(micro_ctx* ctx, void* out);
+int micro_peer_import(micro_ctx* ctx, const void* all_handles);
+int micro_peer_exchange(micro_ctx* ctx);
+int micro_peer_finalize(micro_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@ MICRO_OK, MICRO_EINVAL, MICRO_ELOGIC, MICRO_ENONFINITE = 0, 1, 2, 3
 MICRO_ECUDA, MICRO_ENCCL, MICRO_ECAPACITY, MICRO_ENOMEM = 4, 5, 6, 7
 MICRO_F32, MICRO_F64 = 0, 1
 MICRO_MAX_WORKERS = 64
+MICRO_PEER_HANDLE_BYTES = 448
 
 
 class micro_config(C.Structure):
@@ -123,6 +124,10 @@ _SIGS = {
     "micro_dist_gather_foreign": ([VP, VP, PI64, I64, VP], I32),
     "micro_dist_owner_reduce": ([VP, VP, PI64, VP], I32),
     "micro_dist_finalize": ([VP, VP, VP, PI64, I64], I32),
+    "micro_peer_export": ([VP, VP], I32),
+    "micro_peer_import": ([VP, VP], I32),
+    "micro_peer_exchange": ([VP], I32),
+    "micro_peer_finalize": ([VP], I32),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -18,6 +18,7 @@
 #include "../../include/micro.h"
 #include "../../include/micro_synth.h"
 #include "exchange.cuh"
+#include "peer.cuh"
 #include "select.cuh"
 #include "select_tma.cuh"
 #include "select_stream.cuh"
@@ -222,6 +223,15 @@ struct micro_ctx {
   std::vector<cudaEvent_t> t_ev;
   unsigned long long* dense_dirty = nullptr;
   std::vector<void*> allocs;
+  // peer-memory exchange (micro_peer_*): every rank's buffers mapped here
+  bool peer_ready = false;
+  bool peer_exchanged = false;
+  const long long* peer_counts[kMaxWorkers] = {};
+  void* peer_resid[kMaxWorkers] = {};
+  int32_t* peer_uidx[2][kMaxWorkers] = {};
+  void* peer_usum[2][kMaxWorkers] = {};
+  double* peer_corr[kMaxWorkers] = {};
+  std::vector<void*> peer_opened;  // cudaIpcOpenMemHandle mappings to close
 
   int alloc(void** p, size_t bytes) {
     if (bytes == 0) bytes = 16;
@@ -918,6 +928,7 @@ int micro_ctx_destroy(micro_ctx* c) {
   DeviceGuard dg(c->dev);
   cudaStreamSynchronize(c->stream);
   if (c->aux) cudaStreamSynchronize(c->aux);
+  for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocs) cudaFree(p);
   for (cudaEvent_t ev : c->t_ev) cudaEventDestroy(ev);
   if (c->staging) cudaFree(c->staging);
@@ -1292,6 +1303,125 @@ int micro_dist_owner_reduce(micro_ctx* c, const void* d_recv, const int64_t* h_c
                                                              (double*)d_own_sums);
   CU(cudaGetLastError());
   return MICRO_OK;
+}
+
+// ---- peer-memory exchange (peer.cuh) ------------------------------------
+namespace {
+constexpr int kPeerBufs = 7;  // resid, counts, uidx x2, usum x2, norm corr
+static_assert(MICRO_PEER_HANDLE_BYTES == kPeerBufs * sizeof(cudaIpcMemHandle_t), "handle layout");
+
+void* peer_buf(micro_ctx* c, int b) {
+  switch (b) {
+    case 0: return c->resid[0];
+    case 1: return c->counts;
+    case 2: return c->uni_idx[0];
+    case 3: return c->uni_idx[1];
+    case 4: return c->uni_sum[0];
+    case 5: return c->uni_sum[1];
+    default: return c->norm ? c->norm_corr : nullptr;
+  }
+}
+
+int check_peer_ctx(micro_ctx* c) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster || c->n_local != 1 || c->n < 2)
+    return fail(MICRO_ELOGIC, "micro_peer_*: needs a rank context (n_local = 1 of n > 1 workers)");
+  return MICRO_OK;
+}
+}  // namespace
+
+int micro_peer_export(micro_ctx* c, void* out) {
+  TRY(check_peer_ctx(c));
+  if (!out) return fail(MICRO_EINVAL, "null handle buffer");
+  DeviceGuard dg(c->dev);
+  auto* h = (cudaIpcMemHandle_t*)out;
+  for (int b = 0; b < kPeerBufs; ++b) {
+    std::memset(&h[b], 0, sizeof h[b]);
+    if (void* p = peer_buf(c, b)) CU(cudaIpcGetMemHandle(&h[b], p));
+  }
+  return MICRO_OK;
+}
+
+int micro_peer_import(micro_ctx* c, const void* all) {
+  TRY(check_peer_ctx(c));
+  if (!all) return fail(MICRO_EINVAL, "null handle array");
+  if (c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_import called twice");
+  DeviceGuard dg(c->dev);
+  const auto* h = (const cudaIpcMemHandle_t*)all;
+  const int me = c->cfg.rank;
+  static const cudaIpcMemHandle_t zero{};
+  for (int r = 0; r < c->n; ++r) {
+    void* p[kPeerBufs] = {};
+    for (int b = 0; b < kPeerBufs; ++b) {
+      if (r == me) {
+        p[b] = peer_buf(c, b);
+        continue;
+      }
+      const cudaIpcMemHandle_t& hb = h[(size_t)r * kPeerBufs + b];
+      if (std::memcmp(&hb, &zero, sizeof zero) == 0) continue;
+      CU(cudaIpcOpenMemHandle(&p[b], hb, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_opened.push_back(p[b]);
+    }
+    if (!p[0] || !p[1] || !p[2] || !p[3] || !p[4] || !p[5])
+      return fail(MICRO_EINVAL, "rank %d exported incomplete handles", r);
+    if (c->norm && !p[6]) return fail(MICRO_EINVAL, "rank %d does not record the error norm", r);
+    c->peer_resid[r] = p[0];
+    c->peer_counts[r] = (const long long*)p[1];
+    c->peer_uidx[0][r] = (int32_t*)p[2];
+    c->peer_uidx[1][r] = (int32_t*)p[3];
+    c->peer_usum[0][r] = p[4];
+    c->peer_usum[1][r] = p[5];
+    c->peer_corr[r] = c->norm ? (double*)p[6] : nullptr;
+  }
+  c->peer_ready = true;
+  return MICRO_OK;
+}
+
+int micro_peer_exchange(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_peer_import");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_compress");
+  if (c->peer_exchanged) return fail(MICRO_ELOGIC, "micro_peer_exchange called twice");
+  DeviceGuard dg(c->dev);
+  PeerPtrs pp{};
+  for (int r = 0; r < c->n; ++r) {
+    pp.counts[r] = c->peer_counts[r];
+    pp.resid[r] = c->peer_resid[r];
+    pp.uidx[r] = c->peer_uidx[c->buf][r];
+    pp.usum[r] = c->peer_usum[c->buf][r];
+    pp.corr[r] = c->peer_corr[r];
+  }
+  // sized for the expected selection (the kernel reads the actual count)
+  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
+  const int me = c->cfg.rank;
+  const bool ef = c->cfg.error_feedback != 0;
+  long long* Kout = c->Kbuf + c->buf;
+  if (c->esz == 4) {
+    const float* v = (const float*)c->sel_val[c->buf][0];
+    if (ef) k_peer_exchange<float, true><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                      c->sel_idx[c->buf][0], v, Kout);
+    else k_peer_exchange<float, false><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                     c->sel_idx[c->buf][0], v, Kout);
+  } else {
+    const double* v = (const double*)c->sel_val[c->buf][0];
+    if (ef) k_peer_exchange<double, true><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                       c->sel_idx[c->buf][0], v, Kout);
+    else k_peer_exchange<double, false><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                      c->sel_idx[c->buf][0], v, Kout);
+  }
+  CU(cudaGetLastError());
+  c->peer_exchanged = true;
+  return MICRO_OK;
+}
+
+int micro_peer_finalize(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (!c->peer_exchanged) return fail(MICRO_ELOGIC, "micro_peer_finalize before micro_peer_exchange");
+  DeviceGuard dg(c->dev);
+  c->peer_exchanged = false;
+  if (c->esz == 4) return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
 }
 
 int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_all_sums,

@@ -1,0 +1,110 @@
+// peer.cuh — the n-GPU exchange as ONE kernel over peer memory (NVLink /
+// NVSwitch), replacing the NCCL protocol's K2..K7 (dist.py) and its host
+// count round trip.
+//
+// Reference semantics: the union restricted to partition p is the selection
+// of p's owner (exclusive partitions, acceptance.cpp:93-118), and every sum
+// is s_j = 0; for r = 0..n-1: s_j += acc_r[j] (collectives.cpp:39-47).  So
+// each rank, as owner of its own partition, after every rank's K1 is done
+// (caller's barrier #1):
+//   * reads every rank's k_r (peer loads) -> its segment offset in partition
+//     order and K;
+//   * for each of its selected j: reads acc_r[j] from every peer's residual in
+//     rank order (its own value from the K1 pairs), sums from +0, and zeroes
+//     the peers' entries (harness.cpp:219-221 — no races: j has one owner);
+//   * pushes (j, s_j) into every rank's union buffer at its segment
+//     (peer stores).
+// After barrier #2 each rank finalizes locally (threshold, history, dense
+// g/n, model) from its own union buffer.  No kernel ever waits on another
+// rank's kernel: the two barriers are the caller's (a 4-byte NCCL
+// all-reduce on the compute stream, or a host barrier in tests).
+#pragma once
+
+#include "common.cuh"
+#include "norm.cuh"
+
+namespace micro {
+
+struct PeerPtrs {
+  const long long* counts[kMaxWorkers];  // rank r's k_r (its counts[0])
+  void* resid[kMaxWorkers];
+  int32_t* uidx[kMaxWorkers];            // union buffers of this step's parity
+  void* usum[kMaxWorkers];
+  double* corr[kMaxWorkers];             // error-norm corrections (NULL: not recorded)
+};
+
+__device__ __forceinline__ long long ld_volatile_i64(const long long* p) {
+  return *reinterpret_cast<const volatile long long*>(p);
+}
+
+template <typename T, bool kZero>
+__global__ void __launch_bounds__(256) k_peer_exchange(PeerPtrs p, int n, int me, int64_t t, long long cap,
+                                                       const int32_t* __restrict__ own_idx,
+                                                       const T* __restrict__ own_val, long long* K_out) {
+  __shared__ long long s_off, s_k;
+  __shared__ double s_corr[8][kMaxWorkers];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    const int pme = (int)((t % n + me) % n);  // my partition (tensor.hpp:57)
+    long long off = 0, K = 0;
+    for (int q = 0; q < n; ++q) {
+      const long long kq = ld_volatile_i64(p.counts[partition_owner(q, n, t)]);
+      const long long kc = kq < cap ? kq : cap;
+      if (q < pme) off += kc;
+      K += kc;
+    }
+    const long long km = ld_volatile_i64(p.counts[me]);
+    s_off = off;
+    s_k = km < cap ? km : cap;
+    if (blockIdx.x == 0) *K_out = K;
+  }
+  __syncthreads();
+  const long long off = s_off, k = s_k;
+  const bool corr = kZero && p.corr[0] != nullptr;  // grid-uniform
+  double c_lo = 0.0, c_hi = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = (long long)blockIdx.x * blockDim.x; b < k; b += stride) {  // warp-uniform trip count
+    const long long m = b + threadIdx.x;
+    const bool act = m < k;
+    const int32_t j = act ? own_idx[m] : 0;
+    T s = (T)0;
+    for (int r = 0; r < n; ++r) {
+      T v = (T)0;
+      if (act) {
+        if (r == me) {
+          v = own_val[m];
+        } else {
+          T* e = (T*)p.resid[r];
+          v = e[j];
+          if (kZero) e[j] = (T)0;
+        }
+      }
+      s = add_rn(s, v);
+      if (corr && r != me) {
+        const double q = warp_sum_f64(act ? (double)v * (double)v : 0.0);
+        if (lane == (r & 31)) {
+          if (r < 32) c_lo += q;
+          else c_hi += q;
+        }
+      }
+    }
+    if (act)
+      for (int q = 0; q < n; ++q) {
+        p.uidx[q][off + m] = j;
+        ((T*)p.usum[q])[off + m] = s;
+      }
+  }
+  if (corr) {
+    if (lane < n) s_corr[wid][lane] = c_lo;
+    if (lane + 32 < n) s_corr[wid][lane + 32] = c_hi;
+    __syncthreads();
+    if ((int)threadIdx.x < n && (int)threadIdx.x != me) {
+      double tot = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += s_corr[q][threadIdx.x];
+      if (tot != 0.0) atomicAdd(p.corr[threadIdx.x], tot);
+    }
+  }
+  __threadfence_system();  // peer stores visible before the caller's barrier
+}
+
+}  // namespace micro

@@ -115,11 +115,20 @@ class DeviceOps:
 
 
 class DistMicro:
-    """One rank's MiCRO engine; same calls as :class:`engine.Micro`."""
+    """One rank's MiCRO engine; same calls as :class:`engine.Micro`.
 
-    def __init__(self, n_g: int, group=None, comm_device=None, **kw):
+    ``transport="nccl"``: the protocol above (NCCL moves the data).
+    ``transport="peer"``: one kernel per rank over peer memory
+    (micro_peer_*, csrc/peer.cuh) between two barriers — a 4-byte NCCL
+    all-reduce on the compute stream, or, with ``comm_device="cpu"`` (tests,
+    several ranks on one GPU), a host barrier after a stream sync, so no
+    kernel ever waits on another rank's kernel."""
+
+    def __init__(self, n_g: int, group=None, comm_device=None, transport: str = "nccl", **kw):
         if not dist.is_initialized():
             raise _lib.LogicError(_lib.MICRO_ELOGIC, "torch.distributed is not initialized")
+        if transport not in ("nccl", "peer"):
+            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unknown transport {transport!r}")
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -127,14 +136,39 @@ class DistMicro:
         self.ops = DeviceOps(self.m)
         self.n_g = n_g
         self.comm_device = comm_device
+        self.transport = transport
+        if transport == "peer":
+            blob = C.create_string_buffer(_lib.MICRO_PEER_HANDLE_BYTES)
+            check(lib().micro_peer_export(self.m.handle, blob))
+            blobs = [None] * self.world
+            dist.all_gather_object(blobs, blob.raw, group=group)
+            allb = C.create_string_buffer(b"".join(blobs), _lib.MICRO_PEER_HANDLE_BYTES * self.world)
+            check(lib().micro_peer_import(self.m.handle, allb))
+            self._bar = torch.zeros(1, dtype=torch.int32, device=self.m.device)
+
+    def _barrier(self):
+        if self.comm_device is not None:  # host barrier (gloo): the stream's work is done first
+            self.m.stream.synchronize()
+            dist.barrier(group=self.group)
+        else:  # stream-ordered: NCCL's stream waits for ours, ours for NCCL's
+            with torch.cuda.stream(self.m.stream):
+                dist.all_reduce(self._bar, group=self.group)
 
     def compress(self, grads, eta: float, t: int):
         self.m.compress(grads, eta, t)
 
-    def aggregate(self) -> int:
+    def aggregate(self) -> int | None:
+        """NCCL transport: returns |union| (known on the host).  Peer
+        transport: asynchronous, returns None (``query().K`` has it)."""
+        if self.transport == "peer":
+            self._barrier()
+            check(lib().micro_peer_exchange(self.m.handle))
+            self._barrier()
+            check(lib().micro_peer_finalize(self.m.handle))
+            return None
         return exchange(self.ops, self.group, self.comm_device)
 
-    def step(self, grads, eta: float, t: int) -> int:
+    def step(self, grads, eta: float, t: int) -> int | None:
         self.compress(grads, eta, t)
         return self.aggregate()
 

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, n_g, iters, ef, q):
+def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl"):
     import sys
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Oracle, OracleCluster
@@ -28,7 +28,8 @@ def _worker(rank, world, port, n_g, iters, ef, q):
     torch.cuda.set_device(0)
     o = Oracle()
     d, delta0, eta = 0.02, 0.015, 0.01
-    m = DistMicro(n_g, comm_device="cpu", density=d, initial_threshold=delta0, error_feedback=ef)
+    m = DistMicro(n_g, comm_device="cpu", transport=transport, density=d, initial_threshold=delta0,
+                  error_feedback=ef)
     x = torch.zeros(n_g, device="cuda")
     m.set_model(x)
     ref = OracleCluster(n_g, world, density=d, delta0=delta0, error_feedback=ef, model=True)
@@ -43,6 +44,8 @@ def _worker(rank, world, port, n_g, iters, ef, q):
         r = ref.step(G, eta, t)
         idx, sums = m.union()
         st = m.query()
+        if K is None:  # peer transport: asynchronous
+            K = st.K
         if K != r["union_idx"].size or not np.array_equal(idx, r["union_idx"]):
             bad.append((t, "union"))
         if not np.array_equal(sums, r["union_sum"]):
@@ -78,12 +81,17 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("world,n_g,ef", [(2, 100_003, True), (3, 50_000, True), (2, 20_000, False)])
-def test_dist_device_halves_one_gpu(world, n_g, ef):
+def test_dist_device_halves_one_gpu(world, n_g, ef, transport):
+    """transport="nccl": the NCCL protocol's device halves (collectives staged
+    through gloo); transport="peer": the peer-memory exchange kernel, every
+    rank's buffers mapped through CUDA IPC (same device here), barriers on
+    the host so no kernel waits on another rank's."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n_g, 10, ef, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_g, 10, ef, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
