@@ -333,9 +333,12 @@ double error_metric(const std::vector<Vec>& residuals) {
   return out;
 }
 
+namespace b200 {
 // metrics.hpp:15-29.  The MiCRO path fills t, the four scalars and the
 // threshold; loss and the modeled phase times belong to the simulator's task
-// and cost model (outside this path) and stay 0.
+// and cost model (outside this path) and stay 0.  (Own type so that this
+// header can sit next to the reference's metrics.hpp: MicroEngine::records
+// fills the reference's sparsim::IterationRecord just as well.)
 struct IterationRecord {
   std::int64_t t = 0;
   double actual_density = 0.0;
@@ -349,6 +352,7 @@ struct IterationRecord {
   double time_comm = 0.0;
   double time_overhead = 0.0;
 };
+}  // namespace b200
 
 // The per-iteration MiCRO step of run_iteration (harness.cpp:121-224) for
 // `workers` in-process workers on one device, with their residuals and
@@ -417,15 +421,17 @@ class MicroEngine {
     return out;
   }
 
-  // Records of the last min(max_steps, 4096) steps, oldest first.
-  std::vector<IterationRecord> records(std::int64_t max_steps = 4096) const {
+  // Records of the last min(max_steps, 4096) steps, oldest first; Rec is any
+  // type with IterationRecord's field names (e.g. the reference's own).
+  template <class Rec = b200::IterationRecord>
+  std::vector<Rec> records(std::int64_t max_steps = 4096) const {
     std::vector<micro_record> raw((std::size_t)std::max<std::int64_t>(max_steps, 1));
     std::int64_t w = 0;
     b200::check(micro_records(ctx_, max_steps, raw.data(), &w));
-    std::vector<IterationRecord> out((std::size_t)w);
+    std::vector<Rec> out((std::size_t)w);
     for (std::int64_t s = 0; s < w; ++s) {
       const micro_record& r = raw[(std::size_t)s];
-      IterationRecord& o = out[(std::size_t)s];
+      Rec& o = out[(std::size_t)s];
       o.t = r.t;
       o.actual_density = r.actual_density;
       o.buildup_factor = r.buildup_factor;

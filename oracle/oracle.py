@@ -20,6 +20,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libmicro_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libsparsim_ref.so")
+REPORT_SO = os.path.join(HERE, "_ref", "libsparsim_report.so")
 
 i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
 f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
@@ -305,3 +306,34 @@ class RefCluster:
         out = np.empty(4, np.float64)
         self.r.lib.ref_cluster_phase_times(self.h, out)
         return out
+
+
+class ReferenceReport:
+    """The reference's own record writer (report.cpp, oracle/_ref/libsparsim_report.so)."""
+
+    TASKS = {"quadratic": 0, "logreg": 1, "mlp2": 2}
+    KINDS = {"micro": 0, "topk": 1, "cltk": 2, "hard": 3, "dense": 4}
+    FIELDS = ("actual_density", "buildup_factor", "redundant_traffic_factor", "error_norm", "threshold",
+              "loss", "time_grad", "time_select", "time_comm", "time_overhead")
+
+    def __init__(self):
+        if not os.path.exists(REPORT_SO):
+            build()
+        if not os.path.exists(REPORT_SO):
+            raise FileNotFoundError(f"{REPORT_SO} missing: build it where /root/reference exists")
+        self.lib = C.CDLL(REPORT_SO)
+        self.lib.ref_emit.argtypes = [I32, C.c_char_p, i64p, f64p, I64, i64p, f64p]
+
+    def emit(self, fmt: str, path: str, records, cfg: dict) -> None:
+        t = np.array([r["t"] for r in records] or [0], np.int64)
+        cols = np.array([[float(r.get(f, 0.0)) for f in self.FIELDS] for r in records] or [[0.0] * 10], np.float64)
+        ints = np.array([cfg["workers"], cfg["iterations"], cfg["batch_size"], cfg["seed"], self.TASKS[cfg["task"]],
+                         cfg["dimension"], cfg["samples"], 0 if cfg["per_worker_k"] == "split" else 1,
+                         cfg["decay_at"], int(cfg["error_feedback"]), self.KINDS[cfg["sparsifier"]]], np.int64)
+        dbls = np.array([cfg["density"], cfg["delta0"], cfg["alpha"], cfg["eps_delta"], cfg["lr"], cfg["decay_factor"],
+                         cfg["latency_per_collective"], cfg["bytes_per_element"], cfg["bandwidth"],
+                         cfg["compute_time_per_op"]], np.float64)
+        rc = self.lib.ref_emit(0 if fmt == "csv" else 1, path.encode(), t, np.ascontiguousarray(cols), len(records),
+                               ints, dbls)
+        if rc:
+            raise OracleError(rc, "ref_emit failed")

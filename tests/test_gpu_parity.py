@@ -285,3 +285,23 @@ def test_full_size_properties_138M():
         del e0, acc, sel, sent
     m.close()
     torch.cuda.empty_cache()
+
+
+def test_gpu_records_to_reference_format(tmp_path):
+    """§8f-2: a GPU run's records written in the reference's CSV/JSON format
+    (report.py, byte-identical to report.cpp — tests/test_report.py) and read back."""
+    from paper_2310_00967_b200 import report
+    o = Oracle()
+    m = engine.Micro(50_000, 2, density=0.01, initial_threshold=0.02)
+    for t in range(6):
+        m.step(list(torch.from_numpy(gen(o, 2, 50_000, t, np.float32)).cuda()), ETA, t)
+    recs = m.records()
+    cfg = report.config_for(m, lr=ETA, iterations=6, seed=SEED)
+    for fmt in ("csv", "json"):
+        p = tmp_path / f"run.{fmt}"
+        report.emit(cfg, recs, fmt, str(p))
+        assert p.read_text().count("\n") > 6
+    back = report.read_records_json(str(tmp_path / "run.json"))
+    assert [r["error_norm"] for r in back["records"]] == [r["error_norm"] for r in recs]
+    assert back["config"]["workers"] == 2 and back["config"]["density"] == 0.01
+    m.close()
