@@ -175,6 +175,8 @@ class Reference:
         L.ref_cluster_thresholds.argtypes = [C.c_void_p, f64p]
         L.ref_cluster_phase_times.argtypes = [C.c_void_p, f64p]
         L.ref_cluster_phase_times.restype = None
+        L.ref_cluster_step_kind.argtypes = [C.c_void_p, I32, f64p, DBL, I64, C.c_void_p, i64p, i64p, f64p,
+                                            C.POINTER(I64)]
 
     def _check(self, rc):
         if rc:
@@ -280,14 +282,20 @@ class RefCluster:
             self.r.lib.ref_cluster_destroy(h)
             self.h = None
 
-    def step(self, G, eta, t):
+    KINDS = {"micro": 0, "topk": 1, "cltk": 2, "hard": 3, "dense": 4}
+
+    def step(self, G, eta, t, kind="micro"):
         G = np.ascontiguousarray(G, np.float64).reshape(self.n, self.n_g)
         counts = np.empty(self.n, np.int64)
         uidx = np.empty(self.n_g, np.int64)
         usum = np.empty(self.n_g, np.float64)
         K = I64()
-        dused = np.empty(self.n, np.float64)
         xp = self.x.ctypes.data if self.x is not None else None
+        if kind != "micro":  # harness.cpp:152-181
+            self.r._check(self.r.lib.ref_cluster_step_kind(self.h, self.KINDS[kind], G, eta, t, xp, counts, uidx,
+                                                           usum, C.byref(K)))
+            return dict(counts=counts, union_idx=uidx[: K.value].copy(), union_sum=usum[: K.value].copy())
+        dused = np.empty(self.n, np.float64)
         self.r._check(self.r.lib.ref_cluster_step(self.h, G, eta, t, xp, counts, uidx, usum, C.byref(K), dused))
         dn = np.empty(self.n, np.float64)
         self.r.lib.ref_cluster_thresholds(self.h, dn)
@@ -337,3 +345,61 @@ class ReferenceReport:
                                ints, dbls)
         if rc:
             raise OracleError(rc, "ref_emit failed")
+
+
+class BaselineCluster:
+    """TEST INFRASTRUCTURE: numpy restatement of run_iteration's comparison
+    sparsifiers (harness.cpp:152-224) in the fp32 contract (or fp64, where it
+    is pinned bit for bit to the reference's own code by
+    tests/test_oracle_baselines.py):
+      topk   select_topk (sparsifier.cpp:39-67): k_global largest |acc| over the
+             whole vector, tie -> lower index, ascending
+      cltk   cltk_select (sparsifier.cpp:85-97): the leader t mod n only
+      hard   hard_threshold_select (sparsifier.cpp:99-101): |acc| > delta0
+      dense  select_all (sparsifier.cpp:103-108)
+    then the union (sorted unique), worker-order sums from +0, x -= s/n and
+    the union zeroed on every worker (EF off: everything)."""
+
+    def __init__(self, n_g, n, kind, density=0.01, delta0=0.01, error_feedback=True, dtype=np.float32,
+                 model=False):
+        self.n_g, self.n, self.kind = n_g, n, kind
+        self.dtype = np.dtype(dtype)
+        self.delta0 = delta0
+        self.ef = error_feedback
+        self.k = Oracle().global_target_count(density, n_g)
+        self.e = np.zeros((n, n_g), self.dtype)
+        self.x = np.zeros(n_g, self.dtype) if model else None
+
+    def _topk(self, a):
+        k = min(self.k, a.size)
+        mag = np.abs(a)
+        order = np.lexsort((np.arange(a.size), -mag))  # |acc| descending, then index ascending
+        return np.sort(order[:k])
+
+    def step(self, G, eta, t):
+        G = np.asarray(G).reshape(self.n, self.n_g).astype(self.dtype)
+        if not np.all(np.isfinite(G)):
+            raise OracleError(3, "non-finite gradient")
+        acc = self.e + self.dtype.type(eta) * G  # two roundings, like e + eta*G
+        sels = [np.empty(0, np.int64) for _ in range(self.n)]
+        if self.kind == "topk":
+            sels = [self._topk(acc[i]) for i in range(self.n)]
+        elif self.kind == "cltk":
+            sels[t % self.n] = self._topk(acc[t % self.n])
+        elif self.kind == "hard":
+            sels = [np.flatnonzero(np.abs(acc[i]).astype(np.float64) > self.delta0) for i in range(self.n)]
+        elif self.kind == "dense":
+            sels = [np.arange(self.n_g) for _ in range(self.n)]
+        else:
+            raise ValueError(self.kind)
+        union = np.unique(np.concatenate(sels)).astype(np.int64)
+        s = np.zeros(union.size, self.dtype)
+        for r in range(self.n):  # worker order from +0 (collectives.cpp:44-45)
+            s = s + acc[r][union]
+        if self.x is not None:
+            self.x[union] = self.x[union] - s / self.dtype.type(self.n)
+        acc[:, union] = 0
+        if not self.ef:
+            acc[:] = 0
+        self.e = acc
+        return dict(counts=np.array([x.size for x in sels], np.int64), union_idx=union, union_sum=s)

@@ -284,6 +284,68 @@ int ref_cluster_step(void* h, const double* G, double eta, std::int64_t t, doubl
   });
 }
 
+// The comparison sparsifiers of run_iteration (harness.cpp:152-181: top-k,
+// CLT-k, hard threshold, dense; kind = SparsifierKind 1..4), then the same
+// collectives, model update and compensate + swap as the MiCRO branch.
+int ref_cluster_step_kind(void* h, int kind, const double* G, double eta, std::int64_t t, double* x,
+                          std::int64_t* counts, std::int64_t* union_idx, double* summed, std::int64_t* K) {
+  auto& cs = *static_cast<RefCluster*>(h);
+  return guarded([&] {
+    const int n = cs.n;
+    const Index n_g = cs.n_g;
+    for (int i = 0; i < n; ++i) {
+      const double* g = G + static_cast<std::int64_t>(i) * n_g;
+      for (Index j = 0; j < n_g; ++j)
+        if (!std::isfinite(g[j]))
+          throw std::runtime_error("iteration " + std::to_string(t) +
+                                   ": non-finite gradient on worker " + std::to_string(i));
+      double* acc = cs.accumulators[static_cast<std::size_t>(i)].data();
+      const double* res = cs.residuals[static_cast<std::size_t>(i)].data();
+      for (Index j = 0; j < n_g; ++j) acc[j] = res[j] + eta * g[j];
+    }
+    std::vector<SparseSelection> selections(static_cast<std::size_t>(n));
+    const PartitionRange whole{0, n_g, 0};
+    switch (kind) {
+      case 1:
+        for (int i = 0; i < n; ++i)
+          selections[static_cast<std::size_t>(i)] =
+              select_topk(cs.accumulators[static_cast<std::size_t>(i)], whole, cs.k_global);
+        break;
+      case 2: {
+        const int leader = static_cast<int>(t % n);
+        selections[static_cast<std::size_t>(leader)] =
+            cltk_select(cs.accumulators[static_cast<std::size_t>(leader)], cs.k_global, leader, t, n);
+        break;
+      }
+      case 3:
+        for (int i = 0; i < n; ++i)
+          selections[static_cast<std::size_t>(i)] =
+              hard_threshold_select(cs.accumulators[static_cast<std::size_t>(i)], cs.sc.initial_threshold);
+        break;
+      case 4:
+        for (int i = 0; i < n; ++i)
+          selections[static_cast<std::size_t>(i)] = select_all(cs.accumulators[static_cast<std::size_t>(i)]);
+        break;
+      default:
+        throw std::invalid_argument("ref_cluster_step_kind: kind must be 1..4");
+    }
+    const AggregatedSelection agg = all_gather_indices(selections);
+    const std::vector<double> sums = all_reduce_sparse_values(cs.accumulators, agg);
+    if (x)
+      for (std::size_t k = 0; k < agg.indices.size(); ++k) x[agg.indices[k]] -= sums[k] / n;
+    for (int i = 0; i < n; ++i) {
+      auto& acc = cs.accumulators[static_cast<std::size_t>(i)];
+      for (Index j : agg.indices) acc[j] = 0.0;
+      if (!cs.error_feedback) acc.setZero();
+      std::swap(cs.residuals[static_cast<std::size_t>(i)], acc);
+    }
+    for (int i = 0; i < n; ++i) counts[i] = static_cast<std::int64_t>(agg.per_worker_counts[i]);
+    std::copy(agg.indices.begin(), agg.indices.end(), union_idx);
+    std::copy(sums.begin(), sums.end(), summed);
+    *K = static_cast<std::int64_t>(agg.indices.size());
+  });
+}
+
 int ref_cluster_residual(void* h, int i, double* out) {
   auto& cs = *static_cast<RefCluster*>(h);
   return guarded([&] {
