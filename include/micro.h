@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MICRO_ABI_VERSION 2
+#define MICRO_ABI_VERSION 3
 #define MICRO_MAX_WORKERS 64
 
 typedef enum micro_status {
@@ -145,7 +145,19 @@ typedef struct micro_config {
   int64_t selection_capacity; /* pairs per worker; 0 = partition size (never overflows) */
   int32_t record_error_norm;  /* per-step error norm ||e_{t+1}||_2 (harness.cpp:230-235), fused
                                  into K1; 0 = not recorded (NaN in micro_records) */
+  int32_t sparsifier;         /* SparsifierKind (sparsifier.hpp:21): MICRO_MICRO (default) or a
+                                 comparison sparsifier of harness.cpp:152-181 (single-device
+                                 cluster only) */
 } micro_config;
+
+/* sparsifier kinds (sparsifier.hpp:21) */
+enum {
+  MICRO_MICRO = 0,  /* threshold in the exclusive cyclic partition (the path)  */
+  MICRO_TOPK = 1,   /* select_topk over the whole vector, ties -> lower index    */
+  MICRO_CLTK = 2,   /* cltk_select: the leader t mod n's top-k only               */
+  MICRO_HARD = 3,   /* hard_threshold_select: |acc| > initial_threshold (fixed)   */
+  MICRO_DENSE = 4   /* select_all                                                 */
+};
 
 void micro_config_default(micro_config* cfg);
 

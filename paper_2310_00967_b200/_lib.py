@@ -20,6 +20,7 @@ MICRO_ECUDA, MICRO_ENCCL, MICRO_ECAPACITY, MICRO_ENOMEM = 4, 5, 6, 7
 MICRO_F32, MICRO_F64 = 0, 1
 MICRO_MAX_WORKERS = 64
 MICRO_PEER_HANDLE_BYTES = 448
+SPARSIFIERS = {"micro": 0, "topk": 1, "cltk": 2, "hard": 3, "dense": 4}  # sparsifier.hpp:21
 
 
 class micro_config(C.Structure):
@@ -27,7 +28,7 @@ class micro_config(C.Structure):
         ("n_g", I64), ("n_workers", I32), ("n_local", I32), ("rank", I32), ("dtype", I32),
         ("density", DBL), ("initial_threshold", DBL), ("scaling_factor", DBL), ("min_threshold", DBL),
         ("target", I32), ("error_feedback", I32), ("dense_output", I32), ("device", I32),
-        ("selection_capacity", I64), ("record_error_norm", I32),
+        ("selection_capacity", I64), ("record_error_norm", I32), ("sparsifier", I32),
     ]
 
 
@@ -150,7 +151,7 @@ def lib() -> C.CDLL:
                 f = getattr(L, name)
                 f.argtypes = args
                 f.restype = res
-            if L.micro_abi_version() != 2:
+            if L.micro_abi_version() != 3:
                 raise ImportError("libmicro_b200.so ABI version mismatch")
             _lib = L
     return _lib

@@ -3,6 +3,7 @@
 // array operation below is a device kernel; the host only validates, sizes
 // launches and moves small scalars.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
 
@@ -19,6 +20,7 @@
 #include "../../include/micro_synth.h"
 #include "exchange.cuh"
 #include "peer.cuh"
+#include "baselines.cuh"
 #include "select.cuh"
 #include "select_tma.cuh"
 #include "select_stream.cuh"
@@ -223,6 +225,20 @@ struct micro_ctx {
   std::vector<cudaEvent_t> t_ev;
   unsigned long long* dense_dirty = nullptr;
   std::vector<void*> allocs;
+  // comparison sparsifiers (micro_config.sparsifier, baselines.cuh)
+  int kind = 0;                 // 0 MiCRO, 1 top-k, 2 CLT-k, 3 hard threshold, 4 dense
+  bool sel_is_union = false;    // n = 1 MiCRO: the union is worker 0's selection
+  uint64_t k_global = 0;
+  TopkState* topk = nullptr;    // n_local
+  unsigned* topk_hist = nullptr;
+  unsigned* tie_counts = nullptr;
+  unsigned* bitmap = nullptr;   // union of overlapping selections
+  int* word_pc = nullptr;
+  int* word_off = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  int64_t nwords = 0;
+  double* minus_one = nullptr;  // threshold that selects everything (k >= n_g)
   // peer-memory exchange (micro_peer_*): every rank's buffers mapped here
   bool peer_ready = false;
   bool peer_exchanged = false;
@@ -385,7 +401,8 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
 }
 
 template <typename T>
-int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe) {
+int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe,
+                     const double* thr = nullptr, const long long* tie = nullptr) {
   constexpr int UE = stream_unit_elems<T>();
   StreamArgs a{};
   a.grad = grad;
@@ -394,7 +411,8 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.p_start = (int)ps;
   a.p_end = (int)pe;
   a.eta = eta;
-  a.delta = c->delta + i;
+  a.delta = thr ? thr : c->delta + i;
+  a.tie_j = tie;
   a.unit_lo = (int)(ps / UE);
   a.unit_hi = (int)((pe - 1) / UE);
   a.stage_idx = c->stage_idx;
@@ -419,7 +437,10 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     else K1S(kWriteZeroSel, D);                                                      \
   } while (0)
   if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
-  if (c->n > 1) {
+  if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
+    if (tie) k1_stream<T, kWriteAcc, false, false, true><<<grid, kStreamThreads, 0, st>>>(a);
+    else K1S(kWriteAcc, false);
+  } else if (c->n > 1) {
     if (c->cfg.error_feedback) K1N(false);
     else K1S(kWriteAcc, false);
   } else if (c->cfg.error_feedback) {
@@ -449,7 +470,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.cap = c->sel_cap;
   b.count = c->counts + i;
   b.flags = c->flags;
-  b.model = c->n == 1 ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
+  b.model = c->sel_is_union ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
   if ((b.num_runs + b.super_runs - 1) / b.super_runs > kMaxSupers)
     return fail(MICRO_ECAPACITY, "super-block workspace too small");
   if (c->fuse_step) {
@@ -469,7 +490,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     c->fin_done = true;
   }
   unsigned gblocks = (unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps);
-  if (c->norm) {  // one more CTA reduces k1_stream's per-CTA partials
+  if (c->norm && c->kind == 0) {  // one more CTA reduces k1_stream's per-CTA partials
     b.sq_part = c->norm_part;
     b.sq_parts = (int)grid;
     b.sq_out = c->norm_sq + i;
@@ -482,11 +503,59 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   return MICRO_OK;
 }
 
+unsigned grid_for(int64_t work, int dev);
+constexpr int kTieChunks = 65536;
+
+// One worker of a comparison sparsifier (harness.cpp:152-181).
+template <typename T>
+int launch_baseline(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
+  cudaStream_t st = c->stream;
+  const int kind = c->kind;
+  const int64_t n_g = c->n_g;
+  const bool selects = kind == 1 || kind == 3 || (kind == 2 && t % c->n == i);
+  const unsigned agrid = grid_for(n_g, c->dev);
+  auto accumulate_only = [&](long long count) -> int {
+    k_accumulate_probe<T><<<agrid, 256, 0, st>>>((T*)c->resid[i], (const T*)grad, eta, n_g, c->flags);
+    CU(cudaGetLastError());
+    k_fill_i64<<<1, 32, 0, st>>>(c->counts + i, 1, count);
+    CU(cudaGetLastError());
+    return MICRO_OK;
+  };
+  if (!selects) return accumulate_only(kind == 4 ? n_g : 0);
+  if (kind == 3) return launch_k1_stream<T>(c, i, grad, eta, 0, n_g);  // |acc| > delta_0 (c->delta[i])
+  // top-k (and the CLT-k leader): k_global over the whole vector
+  const long long k = (long long)c->k_global;
+  if (k == 0) return accumulate_only(0);
+  if (k >= n_g) return launch_k1_stream<T>(c, i, grad, eta, 0, n_g, c->minus_one);
+  TopkState* ts = c->topk + i;
+  k_topk_init<<<1, 1, 0, st>>>(ts, k);
+  CU(cudaGetLastError());
+  const int bits = KeyOf<T>::kBits;
+  const unsigned hgrid = (unsigned)std::min<int64_t>((n_g + 255) / 256, 4 * (int64_t)num_sms(c->dev));
+  for (int hi = bits; hi > 0; hi -= kDigitBits) {  // MSB-first digits of <= 11 bits
+    const int width = std::min(kDigitBits, hi);
+    const int shift = hi - width;
+    k_topk_hist<T><<<hgrid, 256, 0, st>>>((const T*)c->resid[i], (const T*)grad, eta, n_g, shift, width, ts,
+                                          c->topk_hist);
+    CU(cudaGetLastError());
+    k_topk_digit<T><<<1, 1024, 0, st>>>(ts, c->topk_hist, shift, width, shift == 0, n_g);
+    CU(cudaGetLastError());
+  }
+  const int64_t chunk = (n_g + kTieChunks - 1) / kTieChunks;
+  const int nch = (int)((n_g + chunk - 1) / chunk);
+  k_tie_count<T><<<nch, 256, 0, st>>>((const T*)c->resid[i], (const T*)grad, eta, n_g, chunk, ts, c->tie_counts);
+  CU(cudaGetLastError());
+  k_tie_find<T><<<1, 1024, 0, st>>>((const T*)c->resid[i], (const T*)grad, eta, n_g, chunk, nch, ts, c->tie_counts);
+  CU(cudaGetLastError());
+  return launch_k1_stream<T>(c, i, grad, eta, 0, n_g, &ts->pivot, &ts->tie_j);
+}
+
 template <typename T>
 int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   int64_t ps, pe;
   partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
   const bool aligned = ((uintptr_t)grad % 16) == 0;
+  if (c->kind) return launch_baseline<T>(c, i, grad, eta, t);  // grad realigned by micro_compress
   if (c->k1_kind == 0 && aligned) return launch_k1_stream<T>(c, i, grad, eta, ps, pe);
   if (c->k1_kind == 1 && aligned) {
     TRY(launch_k1_tma<T>(c, i, grad, eta, ps, pe));
@@ -554,12 +623,13 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.union_sum = usum;
   const int pb = c->buf ^ 1;
   if (c->ever_stepped && c->dense && !c->dense_fused) {
-    f.prev_idx = c->n == 1 ? c->sel_idx[pb][0] : c->uni_idx[pb];
+    f.prev_idx = c->sel_is_union ? c->sel_idx[pb][0] : c->uni_idx[pb];
     f.prev_K = c->Kbuf + pb;
   }
   f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
   // n = 1 with the streaming K1: k1_gather applied the model update
-  f.model = (c->n == 1 && c->k1_kind == 0) ? nullptr : c->model;
+  f.model = (c->sel_is_union && c->k1_kind == 0) ? nullptr : c->model;
+  f.update_delta = c->kind == 0;
   f.slot = c->steps % kHistCap;
   f.hist_t = c->hist_t;
   f.hist_K = c->hist_K;
@@ -568,7 +638,7 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_err = c->hist_err;
   f.norm_mode = norm_mode(c);
   f.sq = c->norm_sq;
-  f.sq_corr = c->n > 1 ? c->norm_corr : nullptr;
+  f.sq_corr = (c->n > 1 && c->kind == 0) ? c->norm_corr : nullptr;
   const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
   if (c->fin_done) {
     // k1_gather already did the threshold update + history (n = 1, micro_step);
@@ -604,7 +674,7 @@ template <typename T>
 int fork_dense_clear(micro_ctx* c) {
   if (!c->dense || c->dense_fused || !c->ever_stepped || !c->aux) return MICRO_OK;
   const int pb = c->buf ^ 1;
-  const int32_t* prev = c->n == 1 ? c->sel_idx[pb][0] : c->uni_idx[pb];
+  const int32_t* prev = c->sel_is_union ? c->sel_idx[pb][0] : c->uni_idx[pb];
   CU(cudaEventRecord(c->ev_fork, c->stream));
   CU(cudaStreamWaitEvent(c->aux, c->ev_fork, 0));
   k_dense_clear<T><<<finalize_blocks(c), 256, 0, c->aux>>>(prev, c->Kbuf + pb, (T*)c->dense, c->n_g);
@@ -614,8 +684,47 @@ int fork_dense_clear(micro_ctx* c) {
   return MICRO_OK;
 }
 
+// Union (sorted unique of overlapping selections), worker-order sums, the
+// union zeroed everywhere, then the usual finalize without a threshold update.
+template <typename T>
+int aggregate_baseline(micro_ctx* c) {
+  cudaStream_t st = c->stream;
+  int32_t* uidx = c->uni_idx[c->buf];
+  long long* K = c->Kbuf + c->buf;
+  const unsigned grid = grid_for(c->n_g, c->dev);
+  if (c->kind == 4) {
+    k_iota<<<grid, 256, 0, st>>>(uidx, c->n_g, K);
+    CU(cudaGetLastError());
+  } else {
+    for (int i = 0; i < c->n_local; ++i) {
+      k_union_mark<<<grid_for(std::min<int64_t>(c->sel_cap, 2 * (int64_t)c->k_global + 1024), c->dev), 256, 0, st>>>(
+          c->sel_idx[c->buf][i], c->counts + i, c->sel_cap, c->bitmap);
+      CU(cudaGetLastError());
+    }
+    k_word_popc<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_pc);
+    CU(cudaGetLastError());
+    size_t tb = c->cub_bytes;
+    CU(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tb, c->word_pc, c->word_off, (int)c->nwords, st));
+    k_bitmap_emit<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_off, uidx, K);
+    CU(cudaGetLastError());
+  }
+  WorkerPtrs w{};
+  for (int i = 0; i < c->n_local; ++i) w.resid[i] = c->resid[i];
+  if (c->cfg.error_feedback)
+    k_union_reduce<T, true><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf]);
+  else
+    k_union_reduce<T, false><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf]);
+  CU(cudaGetLastError());
+  if (!c->cfg.error_feedback)
+    for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, st));
+  else if (c->norm)
+    for (int i = 0; i < c->n_local; ++i) TRY(launch_sumsq<T>(c, i));
+  return launch_finalize<T>(c, uidx, c->uni_sum[c->buf], 0);
+}
+
 template <typename T>
 int aggregate_cluster(micro_ctx* c) {
+  if (c->kind) return aggregate_baseline<T>(c);
   if (c->n == 1) return launch_finalize<T>(c, c->sel_idx[c->buf][0], c->sel_val[c->buf][0], 1);
   WorkerPtrs w{};
   for (int i = 0; i < c->n; ++i) {
@@ -642,6 +751,10 @@ int validate_config(const micro_config* g) {
   if (!g) return fail(MICRO_EINVAL, "null config");
   TRY(check_dtype(g->dtype));
   if (g->n_workers < 1) return fail(MICRO_EINVAL, "run config: workers must be >= 1");
+  if (g->sparsifier < MICRO_MICRO || g->sparsifier > MICRO_DENSE)
+    return fail(MICRO_EINVAL, "unknown sparsifier kind %d", g->sparsifier);
+  if (g->sparsifier != MICRO_MICRO && g->n_local != g->n_workers)
+    return fail(MICRO_EINVAL, "the comparison sparsifiers run as a single-device cluster (n_local == n_workers)");
   if (g->n_workers > MICRO_MAX_WORKERS)
     return fail(MICRO_EINVAL, "run config: at most %d workers supported", MICRO_MAX_WORKERS);
   if (g->n_g < g->n_workers)
@@ -669,7 +782,9 @@ int reset_state(micro_ctx* c) {
   if (c->aux) CU(cudaStreamSynchronize(c->aux));
   c->clear_pending = false;
   for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
-  std::vector<double> d0(c->n_local, c->cfg.initial_threshold);
+  // MiCRO: delta_0 per worker; hard threshold: the fixed delta_0; top-k, CLT-k,
+  // dense: no threshold (the record's threshold is 0, harness.cpp:135)
+  std::vector<double> d0(c->n_local, (c->kind == 0 || c->kind == 3) ? c->cfg.initial_threshold : 0.0);
   CU(cudaMemcpyAsync(c->delta, d0.data(), sizeof(double) * c->n_local, cudaMemcpyHostToDevice, c->stream));
   CU(cudaMemsetAsync(c->counts, 0, sizeof(long long) * c->n_local, c->stream));
   CU(cudaMemsetAsync(c->Kbuf, 0, sizeof(long long) * 2, c->stream));
@@ -677,6 +792,12 @@ int reset_state(micro_ctx* c) {
   if (c->dense) CU(cudaMemsetAsync(c->dense, 0, c->n_g * c->esz, c->stream));
   if (c->dense_dirty) CU(cudaMemsetAsync(c->dense_dirty, 0, (c->n_g / 256 + 8) * 8, c->stream));
   if (c->super_counts) CU(cudaMemsetAsync(c->super_counts, 0, 2 * kMaxSupers * sizeof(int), c->stream));
+  if (c->kind) {
+    CU(cudaMemsetAsync(c->topk_hist, 0, sizeof(unsigned) * kBins, c->stream));
+    CU(cudaMemsetAsync(c->bitmap, 0, sizeof(unsigned) * c->nwords, c->stream));
+    const double m1 = -1.0;
+    CU(cudaMemcpyAsync(c->minus_one, &m1, sizeof m1, cudaMemcpyHostToDevice, c->stream));
+  }
   if (c->norm) {
     CU(cudaMemsetAsync(c->norm_ticket, 0, sizeof(unsigned) * (sumsq_groups(c->norm_ctas) + 1), c->stream));
     CU(cudaMemsetAsync(c->norm_sq, 0, sizeof(double) * c->n_local, c->stream));
@@ -824,6 +945,8 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->n_g = cfg->n_g;
   c->esz = dtype_size(cfg->dtype);
   c->cluster = c->n_local == c->n;
+  c->kind = cfg->sparsifier;
+  c->sel_is_union = c->n == 1 && c->kind == 0;
   int rc = h_worker_target(cfg->density, cfg->n_g, cfg->n_workers, cfg->target, &c->k_worker);
   if (rc) { delete c; return rc; }
   DeviceGuard dg(c->dev);
@@ -832,7 +955,8 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     return code;
   };
   c->stream = (cudaStream_t)stream;  // NULL = the legacy default stream, like every CUDA API
-  const int64_t max_range = (c->n_g + c->n - 1) / c->n;
+  // MiCRO selects inside its partition; the comparison sparsifiers over the whole vector
+  const int64_t max_range = c->kind ? c->n_g : (c->n_g + c->n - 1) / c->n;
   c->sel_cap = cfg->selection_capacity ? std::min<int64_t>(cfg->selection_capacity, max_range) : max_range;
   c->uni_cap = std::min<int64_t>(c->n_g, (int64_t)c->n * c->sel_cap);
   c->p_max = c->esz == 4 ? p_max_for<float>(max_range) : p_max_for<double>(max_range);
@@ -840,7 +964,8 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   {
     const char* k = std::getenv("MICRO_K1_KERNEL");
     c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
-    c->dense_fused = c->n == 1 && cfg->dense_output && c->k1_kind == 0;
+    if (c->kind) c->k1_kind = 0;  // the baselines compact with the streaming K1
+    c->dense_fused = c->sel_is_union && cfg->dense_output && c->k1_kind == 0;
     c->use_tma = c->k1_kind != 2;
     const char* cf = std::getenv("MICRO_K1_CFG");
     c->k1_cfg = cf ? std::atoi(cf) : 0;
@@ -863,7 +988,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
       c->sel_val[1][i] = c->sel_val[0][i];
     }
   }
-  if (c->n > 1)
+  if (!c->sel_is_union)
     for (int b = 0; b < 2; ++b) {
       if ((rc = c->alloc((void**)&c->uni_idx[b], c->uni_cap * 4))) return cleanup(rc);
       if ((rc = c->alloc(&c->uni_sum[b], c->uni_cap * c->esz))) return cleanup(rc);
@@ -896,6 +1021,21 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((rc = c->alloc((void**)&c->hist_delta, sizeof(double) * kHistCap * c->n_local))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_err, sizeof(double) * kHistCap * c->n_local))) return cleanup(rc);
   c->norm = cfg->record_error_norm && cfg->error_feedback;
+  if (c->kind) {
+    if ((rc = h_global_target(cfg->density, c->n_g, &c->k_global))) return cleanup(rc);
+    c->nwords = (c->n_g + 31) / 32;
+    if ((rc = c->alloc((void**)&c->topk, sizeof(TopkState) * c->n_local))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->topk_hist, sizeof(unsigned) * kBins))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->tie_counts, sizeof(unsigned) * kTieChunks))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->bitmap, sizeof(unsigned) * c->nwords))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->word_pc, sizeof(int) * c->nwords))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->word_off, sizeof(int) * c->nwords))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->minus_one, sizeof(double)))) return cleanup(rc);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, c->word_pc, c->word_off, (int)c->nwords, c->stream);
+    c->cub_bytes = std::max<size_t>(tb, 16);
+    if ((rc = c->alloc(&c->cub_tmp, c->cub_bytes))) return cleanup(rc);
+  }
   if (c->norm) {
     // producing grids: k1_stream (one CTA per 8 units) or k_sumsq (4 per SM)
     const int64_t ue = c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>();
@@ -998,7 +1138,7 @@ int micro_aggregate(micro_ctx* c) {
 int micro_step(micro_ctx* c, const void* const* d_grads, double eta, int64_t t) {
   TRY(check_ctx(c));
   // one-worker cluster, streaming K1: fold k_finalize into k1_gather
-  c->fuse_step = c->cluster && c->n == 1 && c->k1_kind == 0 && (!c->dense || c->dense_fused);
+  c->fuse_step = c->cluster && c->sel_is_union && c->k1_kind == 0 && (!c->dense || c->dense_fused);
   const int rc = micro_compress(c, d_grads, eta, t);
   c->fuse_step = false;
   if (rc != MICRO_OK) {
@@ -1154,8 +1294,8 @@ int micro_records(micro_ctx* c, int64_t max, micro_record* out, int64_t* written
 int micro_union_device(micro_ctx* c, const int32_t** d_idx, const void** d_sums, const int64_t** d_K) {
   TRY(check_ctx(c));
   const int b = c->ever_stepped ? (int)((c->steps - 1) & 1) : 0;
-  if (d_idx) *d_idx = c->n == 1 ? c->sel_idx[b][0] : c->uni_idx[b];
-  if (d_sums) *d_sums = c->n == 1 ? c->sel_val[b][0] : c->uni_sum[b];
+  if (d_idx) *d_idx = c->sel_is_union ? c->sel_idx[b][0] : c->uni_idx[b];
+  if (d_sums) *d_sums = c->sel_is_union ? c->sel_val[b][0] : c->uni_sum[b];
   if (d_K) *d_K = (const int64_t*)(c->Kbuf + b);
   return MICRO_OK;
 }

@@ -1,0 +1,329 @@
+// baselines.cuh — the comparison sparsifiers of run_iteration
+// (harness.cpp:152-181) on the device:
+//   top-k  select_topk (sparsifier.cpp:39-67): the k largest |acc| over the
+//          whole vector, ties to the lower index, ascending
+//   CLT-k  cltk_select (sparsifier.cpp:85-97): the leader t mod n only
+//   hard   hard_threshold_select (sparsifier.cpp:99-101): |acc| > delta_0
+//   dense  select_all (sparsifier.cpp:103-108)
+// followed by the general union (sorted unique of overlapping selections,
+// collectives.cpp:14-28) and the worker-order sums (collectives.cpp:30-49).
+//
+// Top-k is a radix select on the magnitude bits (fp32: 31 bits in 11/11/9-bit
+// digits; fp64: 63 bits in six digits), one histogram pass per digit over
+// acc = e + eta*G recomputed from (e, G) with K1's exact arithmetic, a
+// one-block digit pick after each pass (no host round trip), then — only if
+// the pivot magnitude P is shared by more elements than are still needed —
+// the index J of the last tie to keep (lowest indices first).  The selection
+// {|acc| > P} ∪ {|acc| == P, j <= J} is then exactly the reference's, and it
+// is compacted in order by K1's streaming kernel with a tie predicate.
+// The union of overlapping selections is a bitmap (atomicOr), compacted in
+// index order.
+#pragma once
+
+#include "common.cuh"
+
+namespace micro {
+
+struct TopkState {
+  unsigned long long prefix;  // key bits fixed so far
+  unsigned long long mask;    // which bits of the key are fixed
+  long long k_rem;            // elements still to take at/below the prefix
+  long long eq;               // elements in the last chosen bucket (== P after the last pass)
+  long long tie_j;            // last tie index kept (n_g: all ties)
+  double pivot;               // P as a value (threshold of the compaction)
+  int need_tie;
+};
+
+template <typename T> struct KeyOf;
+template <> struct KeyOf<float> {
+  using K = unsigned int;
+  static constexpr int kBits = 31;
+  __device__ static K key(float a) { return __float_as_uint(a) & 0x7fffffffu; }
+  __device__ static double value(unsigned long long k) { return (double)__uint_as_float((unsigned)k); }
+};
+template <> struct KeyOf<double> {
+  using K = unsigned long long;
+  static constexpr int kBits = 63;
+  __device__ static K key(double a) { return (K)__double_as_longlong(a) & 0x7fffffffffffffffull; }
+  __device__ static double value(unsigned long long k) { return __longlong_as_double((long long)k); }
+};
+
+constexpr int kDigitBits = 11;
+constexpr int kBins = 1 << kDigitBits;
+
+__global__ void k_topk_init(TopkState* st, long long k) {
+  st->prefix = 0;
+  st->mask = 0;
+  st->k_rem = k;
+  st->eq = 0;
+  st->tie_j = 0;
+  st->pivot = 0.0;
+  st->need_tie = 0;
+}
+
+// Histogram of the current digit over the elements whose higher digits match
+// the prefix.  Lanes hitting the same bin are merged with __match_any_sync
+// (the top digit holds the exponent: a handful of bins take everything).
+template <typename T>
+__global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                   int64_t n_g, int shift, int width, const TopkState* st,
+                                                   unsigned* __restrict__ hist) {
+  using KO = KeyOf<T>;
+  __shared__ unsigned s_hist[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) s_hist[b] = 0;
+  __syncthreads();
+  const unsigned long long prefix = st->prefix, mask = st->mask;
+  const unsigned dmask = (1u << width) - 1u;
+  const T eta = (T)eta_d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x;
+  for (int64_t j0 = base; j0 < n_g; j0 += stride) {  // warp-uniform trip count
+    const int64_t j = j0 + threadIdx.x;
+    int bin = -1;
+    if (j < n_g) {
+      const T acc = add_rn(e[j], mul_rn(eta, g[j]));
+      const unsigned long long key = KO::key(absx(acc));
+      if ((key & mask) == prefix) bin = (int)((key >> shift) & dmask);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[bin], __popc(peers));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
+    if (s_hist[b]) atomicAdd(&hist[b], s_hist[b]);
+}
+
+// One block of 1024: pick the bucket holding the k_rem-th largest key, fold
+// it into the prefix, clear the histogram.  last: also form the pivot and
+// whether ties must be cut.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_topk_digit(TopkState* st, unsigned* hist, int shift, int width,
+                                                     int last, int64_t n_g) {
+  __shared__ long long s_w[32];
+  __shared__ int s_bin;
+  __shared__ long long s_above;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nb = 1 << width;
+  // thread tid owns bins hi-2*tid and hi-2*tid-1 (descending order)
+  const int b0 = nb - 1 - 2 * tid, b1 = b0 - 1;
+  const long long c0 = b0 >= 0 ? hist[b0] : 0, c1 = b1 >= 0 ? hist[b1] : 0;
+  const long long mine = c0 + c1;
+  long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[w] = incl;
+  if (tid == 0) s_bin = -1;
+  __syncthreads();
+  if (w == 0) {
+    long long x = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_w[lane] = x;
+  }
+  __syncthreads();
+  const long long k = st->k_rem;
+  const long long excl = (w ? s_w[w - 1] : 0) + incl - mine;  // keys in bins above b0
+  if (b0 >= 0 && excl < k && excl + c0 >= k) {
+    s_bin = b0;
+    s_above = excl;
+  } else if (b1 >= 0 && excl + c0 < k && excl + c0 + c1 >= k) {
+    s_bin = b1;
+    s_above = excl + c0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int b = s_bin;  // always found: k_rem <= elements matching the prefix
+    st->k_rem = k - s_above;
+    st->eq = hist[b];
+    st->prefix |= (unsigned long long)b << shift;
+    st->mask |= (unsigned long long)((1u << width) - 1u) << shift;
+    if (last) {
+      st->pivot = KeyOf<T>::value(st->prefix);
+      st->need_tie = st->k_rem < st->eq;
+      st->tie_j = n_g;  // all ties (refined by k_tie_find when need_tie)
+    }
+  }
+  __syncthreads();
+  for (int b = tid; b < nb; b += blockDim.x) hist[b] = 0;
+}
+
+// Ties at the pivot per contiguous chunk (only when some must be cut).
+template <typename T>
+__global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                   int64_t n_g, int64_t chunk, const TopkState* st,
+                                                   unsigned* __restrict__ counts) {
+  if (!st->need_tie) return;
+  __shared__ unsigned s_c;
+  if (threadIdx.x == 0) s_c = 0;
+  __syncthreads();
+  const T eta = (T)eta_d;
+  const T P = (T)st->pivot;
+  const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(lo + chunk, n_g);
+  unsigned c = 0;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) c += absx(add_rn(e[j], mul_rn(eta, g[j]))) == P;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = s_c;
+}
+
+// One block of 1024: the chunk holding the k_rem-th tie, then that tie's
+// index (ties taken in index order).
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                   int64_t n_g, int64_t chunk, int nchunks, TopkState* st,
+                                                   const unsigned* __restrict__ counts) {
+  if (!st->need_tie) return;
+  __shared__ long long s_w[32];
+  __shared__ long long s_rem;
+  __shared__ int s_chunk;
+  __shared__ long long s_j;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const long long k = st->k_rem;
+  // thread tid owns chunks [tid*per, (tid+1)*per)
+  const int per = (nchunks + 1023) / 1024;
+  long long mine = 0;
+  for (int q = tid * per; q < min(nchunks, (tid + 1) * per); ++q) mine += counts[q];
+  long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    long long x = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    s_w[lane] = x;
+  }
+  __syncthreads();
+  long long run = (w ? s_w[w - 1] : 0) + incl - mine;
+  if (run < k && run + mine >= k) {
+    for (int q = tid * per; q < min(nchunks, (tid + 1) * per); ++q) {
+      if (run + counts[q] >= k) {
+        s_chunk = q;
+        s_rem = k - run;
+        break;
+      }
+      run += counts[q];
+    }
+  }
+  __syncthreads();
+  // walk the chunk in index order, 1024 elements at a time
+  const T eta = (T)eta_d;
+  const T P = (T)st->pivot;
+  const int64_t lo = (int64_t)s_chunk * chunk, hi = min(lo + chunk, n_g);
+  long long rem = s_rem;
+  if (tid == 0) s_j = -1;
+  __syncthreads();
+  for (int64_t b = lo; b < hi; b += 1024) {
+    const int64_t j = b + tid;
+    const bool tie = j < hi && absx(add_rn(e[j], mul_rn(eta, g[j]))) == P;
+    const unsigned bal = __ballot_sync(0xffffffffu, tie);
+    if (lane == 0) s_w[w] = __popc(bal);
+    __syncthreads();
+    long long before = 0, total = 0;
+    for (int q = 0; q < 32; ++q) {
+      if (q < w) before += s_w[q];
+      total += s_w[q];
+    }
+    before += __popc(bal & ((1u << lane) - 1u));
+    if (tie && before + 1 == rem) s_j = j;
+    __syncthreads();
+    if (s_j >= 0 || total >= rem) break;
+    rem -= total;
+    __syncthreads();
+  }
+  if (tid == 0) st->tie_j = s_j;
+}
+
+// acc = e + eta*G in place with the non-finite probe (workers that select
+// nothing this step: CLT-k non-leaders, dense).
+template <typename T>
+__global__ void __launch_bounds__(256) k_accumulate_probe(T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                          int64_t n_g, int* flags) {
+  const T eta = (T)eta_d;
+  T probe = (T)0;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_g; j += (int64_t)gridDim.x * blockDim.x) {
+    const T gv = g[j];
+    probe = probe + gv * (T)0;
+    e[j] = add_rn(e[j], mul_rn(eta, gv));
+  }
+  if (probe != probe) atomicOr(flags, 1);
+}
+
+// ---- union of overlapping selections: bitmap, then ordered emission ----
+__global__ void __launch_bounds__(256) k_union_mark(const int32_t* __restrict__ idx, const long long* count,
+                                                    long long cap, unsigned* __restrict__ bitmap) {
+  const long long k = min(*count, cap);
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
+    const int32_t j = idx[m];
+    atomicOr(&bitmap[j >> 5], 1u << (j & 31));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_word_popc(const unsigned* __restrict__ bitmap, int64_t nwords,
+                                                   int* __restrict__ pc) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x)
+    pc[w] = __popc(bitmap[w]);
+}
+
+// off: exclusive prefix of the popcounts.  Writes the union in index order,
+// K, and clears the bitmap for the next step.
+__global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict__ bitmap, int64_t nwords,
+                                                     const int* __restrict__ off, int32_t* __restrict__ uidx,
+                                                     long long* K) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    unsigned bits = bitmap[w];
+    int o = off[w];
+    if (w == nwords - 1) *K = (long long)o + __popc(bits);
+    if (!bits) continue;
+    bitmap[w] = 0;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      uidx[o++] = (int32_t)(w * 32 + b);
+      bits &= bits - 1;
+    }
+  }
+}
+
+__global__ void k_iota(int32_t* u, int64_t n, long long* K) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    u[j] = (int32_t)j;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *K = n;
+}
+
+__global__ void k_fill_i64(long long* p, int n, long long v) {
+  if ((int)threadIdx.x < n) p[threadIdx.x] = v;
+}
+
+// s_j = 0; for r in worker order: s_j += acc_r[j] (collectives.cpp:44-45), and
+// the union zeroed on every worker (harness.cpp:219-221).
+template <typename T, bool kZero>
+__global__ void __launch_bounds__(256) k_union_reduce(WorkerPtrs w, int n, const int32_t* __restrict__ uidx,
+                                                      const long long* K, T* __restrict__ usum) {
+  const long long k = *K;
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
+    const int32_t j = uidx[m];
+    T s = (T)0;
+    for (int r = 0; r < n; ++r) {
+      T* e = (T*)w.resid[r];
+      s = add_rn(s, e[j]);
+      if (kZero) e[j] = (T)0;
+    }
+    usum[m] = s;
+  }
+}
+
+}  // namespace micro

@@ -194,6 +194,7 @@ struct FinalizeArgs {
   double* hist_delta;
   double* hist_err;           // per worker ||e_{t+1}||_2 (error_norm record)
   int norm_mode;              // 0: not recorded (NaN), 1: sqrt(sq - sq_corr), 2: residual is zero (EF off)
+  int update_delta;           // 0: comparison sparsifiers (no threshold estimate, harness.cpp:201)
   const double* sq;           // per worker ||e||^2 after K1 (own selections zeroed)
   double* sq_corr;            // per worker squares of the foreign entries zeroed by the exchange (reset here)
 };
@@ -252,9 +253,11 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
       }
       a.hist_err[a.slot * a.n_local + i] = err;
       // sparsifier.cpp:77-81
-      if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
-      else if (k < a.k_target) d *= 1.0 - a.alpha;
-      a.delta[i] = d;
+      if (a.update_delta) {
+        if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
+        else if (k < a.k_target) d *= 1.0 - a.alpha;
+        a.delta[i] = d;
+      }
     }
   }
   if (!a.dense && !a.model) return;

@@ -64,6 +64,7 @@ struct StreamArgs {
   int* super_counts;       // selections per super block of `super_runs` CTA runs (zeroed)
   int super_runs;
   double* sq_part;         // kNorm: per CTA, sum of e_{t+1}^2 (own selections zeroed); reduced by k1_gather
+  const long long* tie_j;  // kTie (top-k baseline): also select |acc| == thr at j <= *tie_j
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -83,7 +84,7 @@ __device__ __forceinline__ unsigned even_bits(unsigned x) {
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
-template <typename T, int kMode, bool kDense, bool kNorm>
+template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false>
 __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   const bool sel_unit = live && u >= a.unit_lo && u <= a.unit_hi;
   const bool all_in = base >= a.p_start && base + elems <= a.p_end;
   const T thr = threshold_as(*a.delta, (T*)nullptr);
+  const long long tie_limit = kTie ? *a.tie_j : 0;
   const T eta = (T)a.eta;
   T probe = (T)0;  // becomes NaN iff some G is Inf/NaN
   unsigned mask[VPL];
@@ -136,6 +138,8 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
       const T acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
       set_comp(e[i], c, acc);
       bool sel = sel_unit && absx(acc) > thr;
+      if (kTie && sel_unit && absx(acc) == thr)  // top-k: ties at the pivot up to index J
+        sel = (long long)(base + (i * 32 + lane) * VN + c) <= tie_limit;
       if (!all_in) {
         const int j = base + (i * 32 + lane) * VN + c;
         sel = sel && j >= a.p_start && j < a.p_end;

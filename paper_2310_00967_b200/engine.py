@@ -68,7 +68,7 @@ class Micro:
                  min_threshold: float = 1e-12, target: str = "split", error_feedback: bool = True,
                  dense_output: bool = True, device: int | torch.device | None = None,
                  stream: torch.cuda.Stream | None = None, selection_capacity: int = 0,
-                 record_error_norm: bool = True):
+                 record_error_norm: bool = True, sparsifier: str = "micro"):
         L = lib()
         if dtype not in _DT:
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unsupported dtype {dtype}")
@@ -88,10 +88,14 @@ class Micro:
         cfg.error_feedback, cfg.dense_output = int(error_feedback), int(dense_output)
         cfg.device, cfg.selection_capacity = dev.index, selection_capacity
         cfg.record_error_norm = int(record_error_norm)
+        if sparsifier not in _lib.SPARSIFIERS:
+            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unknown sparsifier '{sparsifier}'")
+        cfg.sparsifier = _lib.SPARSIFIERS[sparsifier]
+        self.sparsifier = sparsifier
         self.cfg = cfg
         self.device, self.dtype = dev, dtype
         self.n_g, self.n, self.n_local, self.rank = n_g, n_workers, cfg.n_local, rank
-        max_range = -(-n_g // max(n_workers, 1))
+        max_range = n_g if sparsifier != "micro" else -(-n_g // max(n_workers, 1))
         self.selection_capacity = min(selection_capacity, max_range) if selection_capacity else max_range
         with torch.cuda.device(dev):
             self.stream = stream or torch.cuda.current_stream(dev)
