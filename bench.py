@@ -191,7 +191,7 @@ def our_arm(args, wl):
                       dense_output=args.dense, record_error_norm=args.error_norm)
     else:
         m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
-                         record_error_norm=args.error_norm)
+                         record_error_norm=args.error_norm, sparsifier=args.sparsifier)
     stream = torch.cuda.current_stream(dev)
     # the model update x -= g/n at the union is part of the reference's
     # iteration (harness.cpp:212-215); a dense g/n is not (run_iteration uses
@@ -274,6 +274,11 @@ def our_arm(args, wl):
     # build_union, finalize (NCCL kernels not counted)
     launches_per_step = ((2 if W == 1 else 2 * W + 2) if world == 1
                          else (4 if args.transport == "peer" else 6))  # peer: K1 x2, exchange, finalize
+    if args.sparsifier != "micro":  # baselines.cuh: per selecting worker, top-k = init + 2 per digit +
+        # tie count/find + stream + gather (fp32: 11), hard = 2, else accumulate + count = 2; then
+        # union marks (W) + popcount + scan (2) + emit + reduce + finalize (dense: iota + reduce + finalize)
+        per = {"topk": 11 * W, "cltk": 11 + 2 * (W - 1), "hard": 2 * W, "dense": 2 * W}[args.sparsifier]
+        launches_per_step = per + (3 if args.sparsifier == "dense" else W + 6)
     clocks = clk.summary()
 
     # ---- end to end through the public API with host buffers (N = 1) ----
@@ -328,6 +333,7 @@ def our_arm(args, wl):
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
                        "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
                        "error_norm_recorded": bool(args.error_norm),
+                       "sparsifier": args.sparsifier,
                        "inputs": (f"{R} resident N(0,1) gradients ("
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
                                   + "); each 4*n_g bytes > L2 (no flush needed)")
@@ -371,6 +377,8 @@ def main():
     ap.add_argument("--cluster-workers", type=int, default=1,
                     help="N = 1 only: W in-process workers on the GPU (the reference's in-process cluster)")
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
+    ap.add_argument("--sparsifier", choices=["micro", "topk", "cltk", "hard", "dense"], default="micro",
+                    help="N = 1: a comparison sparsifier of the reference's harness instead of MiCRO")
     ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
                     help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
     ap.add_argument("--error-norm", action="store_true",

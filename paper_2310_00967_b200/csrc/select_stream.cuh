@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   }
 
   const bool sel_unit = live && u >= a.unit_lo && u <= a.unit_hi;
-  const bool all_in = base >= a.p_start && base + elems <= a.p_end;
+  // (padding lanes of the last partial unit take the ranged path: a threshold < 0
+  // would otherwise select their zeros)
+  const bool all_in = base >= a.p_start && base + UE <= a.p_end;
   const T thr = threshold_as(*a.delta, (T*)nullptr);
   const long long tie_limit = kTie ? *a.tie_j : 0;
   const T eta = (T)a.eta;
