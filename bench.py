@@ -258,7 +258,8 @@ def our_arm(args, wl):
     K = hist["K"].astype(np.float64)
     k_own = hist["counts"][:, 0].astype(np.float64)
     density = float(K.mean() / n_g)
-    k1a_avg_ms = statistics.mean(k1a_ms)
+    # (dense has no selection pass: the whole step stands in for the kernel)
+    k1a_avg_ms = statistics.mean(k1a_ms) if k1a_ms else ms_step
     # algorithmic bytes of the dominant kernel, k1_stream: read e and G, write
     # e (all n_g) + one (int32, fp32) pair per selection
     k1_bytes = 12.0 * n_g + 8.0 * float(k_own.mean())

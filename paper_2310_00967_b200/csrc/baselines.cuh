@@ -65,28 +65,59 @@ __global__ void k_topk_init(TopkState* st, long long k) {
 // the prefix.  Lanes hitting the same bin are merged with __match_any_sync
 // (the top digit holds the exponent: a handful of bins take everything).
 template <typename T>
+__device__ __forceinline__ void hist_add(unsigned* s_hist, T acc, unsigned long long prefix, unsigned long long mask,
+                                         int shift, unsigned dmask, bool valid) {
+  using KO = KeyOf<T>;
+  int bin = -1;
+  if (valid) {
+    const unsigned long long key = KO::key(absx(acc));
+    if ((key & mask) == prefix) bin = (int)((key >> shift) & dmask);
+  }
+  const unsigned peers = __match_any_sync(0xffffffffu, bin);
+  if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[bin], __popc(peers));
+}
+
+// 16-byte loads of e and G (the same acc = e + eta*G as K1), every lane
+// keeping two vectors of each in flight.
+template <typename T>
 __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
                                                    int64_t n_g, int shift, int width, const TopkState* st,
                                                    unsigned* __restrict__ hist) {
-  using KO = KeyOf<T>;
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
   __shared__ unsigned s_hist[kBins];
   for (int b = threadIdx.x; b < kBins; b += blockDim.x) s_hist[b] = 0;
   __syncthreads();
   const unsigned long long prefix = st->prefix, mask = st->mask;
   const unsigned dmask = (1u << width) - 1u;
   const T eta = (T)eta_d;
+  const int64_t nv = n_g / VN;  // whole vectors (e, G are 16-byte aligned: K1 staging / caller)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t base = (int64_t)blockIdx.x * blockDim.x;
-  for (int64_t j0 = base; j0 < n_g; j0 += stride) {  // warp-uniform trip count
-    const int64_t j = j0 + threadIdx.x;
-    int bin = -1;
-    if (j < n_g) {
-      const T acc = add_rn(e[j], mul_rn(eta, g[j]));
-      const unsigned long long key = KO::key(absx(acc));
-      if ((key & mask) == prefix) bin = (int)((key >> shift) & dmask);
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * 2; v0 < nv; v0 += 2 * stride) {  // warp-uniform
+    V ev[2], gv[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t v = v0 + u * blockDim.x + threadIdx.x;
+      ok[u] = v < nv;
+      if (ok[u]) {
+        ev[u] = reinterpret_cast<const V*>(e)[v];
+        gv[u] = ld_nc_stream(reinterpret_cast<const V*>(g) + v);
+      }
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, bin);
-    if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[bin], __popc(peers));
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        const T acc = ok[u] ? add_rn(comp(ev[u], c), mul_rn(eta, comp(gv[u], c))) : (T)0;
+        hist_add<T>(s_hist, acc, prefix, mask, shift, dmask, ok[u]);
+      }
+  }
+  // the tail (n_g % VN elements)
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int64_t j = nv * VN + threadIdx.x;
+    const bool ok = j < n_g;
+    hist_add<T>(s_hist, ok ? add_rn(e[j], mul_rn(eta, g[j])) : (T)0, prefix, mask, shift, dmask, ok);
   }
   __syncthreads();
   for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
