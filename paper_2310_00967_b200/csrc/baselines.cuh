@@ -348,10 +348,16 @@ __global__ void __launch_bounds__(256) k_union_reduce(WorkerPtrs w, int n, const
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
     const int32_t j = uidx[m];
     T s = (T)0;
-    for (int r = 0; r < n; ++r) {
-      T* e = (T*)w.resid[r];
-      s = add_rn(s, e[j]);
-      if (kZero) e[j] = (T)0;
+    for (int r0 = 0; r0 < n; r0 += 8) {  // eight loads in flight, summed in worker order
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = r0 + u < n ? ld_rand((const T*)w.resid[r0 + u] + j) : (T)0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u >= n) break;
+        s = add_rn(s, v[u]);
+        if (kZero) ((T*)w.resid[r0 + u])[j] = (T)0;
+      }
     }
     usum[m] = s;
   }

@@ -68,23 +68,27 @@ __global__ void __launch_bounds__(256) k_peer_exchange(PeerPtrs p, int n, int me
     const bool act = m < k;
     const int32_t j = act ? own_idx[m] : 0;
     T s = (T)0;
-    for (int r = 0; r < n; ++r) {
-      T v = (T)0;
-      if (act) {
-        if (r == me) {
-          v = own_val[m];
-        } else {
-          T* e = (T*)p.resid[r];
-          v = e[j];
-          if (kZero) e[j] = (T)0;
-        }
+    // eight peers' entries in flight per thread, summed strictly in rank order
+    for (int r0 = 0; r0 < n; r0 += 8) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u;
+        v[u] = (T)0;
+        if (act && r < n) v[u] = r == me ? own_val[m] : ((const T*)p.resid[r])[j];
       }
-      s = add_rn(s, v);
-      if (corr && r != me) {
-        const double q = warp_sum_f64(act ? (double)v * (double)v : 0.0);
-        if (lane == (r & 31)) {
-          if (r < 32) c_lo += q;
-          else c_hi += q;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u;
+        if (r >= n) break;
+        s = add_rn(s, v[u]);
+        if (kZero && act && r != me) ((T*)p.resid[r])[j] = (T)0;
+        if (corr && r != me) {
+          const double q = warp_sum_f64(act ? (double)v[u] * (double)v[u] : 0.0);
+          if (lane == (r & 31)) {
+            if (r < 32) c_lo += q;
+            else c_hi += q;
+          }
         }
       }
     }
