@@ -78,6 +78,11 @@ int micro_accumulate(int dtype, const void* d_e, double eta, const void* d_g, vo
 int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start,
                               int64_t end, double delta, int32_t* d_idx, void* d_val,
                               int64_t cap, int64_t* d_count, void* stream);
+/* sparsifier.cpp:39-67 select_topk: the k largest |acc| in [start, end),
+ * ties to the lower index, ascending; k > end - start is MICRO_EINVAL.
+ * (cltk_select is this over the whole vector; select_all is a copy.) */
+int micro_select_topk(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end, int64_t k,
+                      int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count, void* stream);
 /* error_feedback.hpp:27-39 compensate (in place): acc[idx[k]] = 0. */
 int micro_compensate(int dtype, void* d_acc, int64_t n_g, const int32_t* d_idx, int64_t k,
                      void* stream);

@@ -5,15 +5,18 @@
 //
 //   reference header                       here
 //   tensor.hpp:25-32,48-63  PartitionRange, partition
-//   sparsifier.hpp:26-46    PerWorkerTarget, SparseSelection, ThresholdState, SparsifierConfig
-//   sparsifier.hpp:49-76    select_by_threshold, micro_update_threshold,
-//                           hard_threshold_select, global/per_worker_target_count
-//   error_feedback.hpp:17-39 accumulate, compensate
+//   sparsifier.hpp:21-46    SparsifierKind, PerWorkerTarget, SparseSelection, ThresholdState,
+//                           SparsifierConfig
+//   sparsifier.hpp:49-84    select_by_threshold, select_topk, micro_update_threshold,
+//                           cltk_select, hard_threshold_select, select_all,
+//                           global/per_worker_target_count, to_string / parse_*
+//   error_feedback.hpp:17-48 accumulate, compensate, error_metric
 //   collectives.hpp:15-43   AggregatedSelection, all_gather_indices,
 //                           all_reduce_sparse(_values), buildup_factor,
 //                           redundant_traffic_factor
 //   metrics.cpp:7-10        actual_density
-//   harness.cpp:121-224     MicroEngine (the per-iteration MiCRO step)
+//   harness.cpp:121-224     MicroEngine (the per-iteration step for every SparsifierKind)
+//   metrics.hpp:15-29       IterationRecord via MicroEngine::records
 //
 // Vectors are any contiguous container of double with .data()/.size() (e.g.
 // Eigen::VectorXd or std::vector<double>); results are returned as
@@ -51,6 +54,7 @@ struct PartitionRange {
   bool operator==(const PartitionRange&) const = default;
 };
 
+enum class SparsifierKind { micro, topk, cltk, hard_threshold, dense };
 enum class PerWorkerTarget { split, full };
 
 struct SparseSelection {
@@ -64,6 +68,7 @@ struct ThresholdState {
 };
 
 struct SparsifierConfig {
+  SparsifierKind kind = SparsifierKind::micro;
   double density = 0.01;
   double initial_threshold = 0.01;
   double scaling_factor = 0.01;
@@ -189,6 +194,81 @@ SparseSelection select_by_threshold(const V& acc, const PartitionRange& range, d
   }
   out.indices.assign(ix.begin(), ix.end());
   return out;
+}
+
+// sparsifier.cpp:39-67 (device radix select; ties to the lower index)
+template <class V>
+SparseSelection select_topk(const V& acc, const PartitionRange& range, std::size_t k) {
+  const Index n_g = (Index)acc.size();
+  if (range.start < 0 || range.end < range.start || range.end > n_g)
+    b200::check(micro_select_topk(MICRO_F64, nullptr, n_g, range.start, range.end, 0, nullptr, nullptr, 0, nullptr,
+                                  nullptr));  // raises the range message
+  const Index m = range.end - range.start;
+  if ((Index)k > m)
+    throw std::invalid_argument("select_topk: k=" + std::to_string(k) + " exceeds range size " + std::to_string(m));
+  SparseSelection out;
+  if (k == 0) return out;
+  auto d_acc = b200::upload(acc);
+  b200::DeviceBuffer d_idx(sizeof(int32_t) * (k + 1)), d_val(sizeof(double) * (k + 1)), d_cnt(sizeof(int64_t));
+  b200::check(micro_select_topk(MICRO_F64, d_acc.get(), n_g, range.start, range.end, (int64_t)k,
+                                d_idx.as<int32_t>(), d_val.get(), (int64_t)k, d_cnt.as<int64_t>(), nullptr));
+  int64_t c = 0;
+  b200::d2h(&c, d_cnt.get(), sizeof c);
+  std::vector<int32_t> ix((std::size_t)c);
+  out.values.resize((std::size_t)c);
+  if (c) {
+    b200::d2h(ix.data(), d_idx.get(), sizeof(int32_t) * (std::size_t)c);
+    b200::d2h(out.values.data(), d_val.get(), sizeof(double) * (std::size_t)c);
+  }
+  out.indices.assign(ix.begin(), ix.end());
+  return out;
+}
+
+// sparsifier.cpp:85-97
+template <class V>
+SparseSelection cltk_select(const V& acc_leader, std::size_t k_total, int leader, std::int64_t t, int n) {
+  if (n < 1 || leader < 0 || leader >= n) throw std::invalid_argument("cltk_select: leader id out of range");
+  if (t < 0 || t % n != leader)
+    throw std::logic_error("cltk_select: worker " + std::to_string(leader) + " is not the leader at iteration " +
+                           std::to_string(t) + " (leader cycles as t mod n)");
+  if (k_total > (std::size_t)acc_leader.size()) throw std::invalid_argument("cltk_select: k exceeds gradient count");
+  return select_topk(acc_leader, PartitionRange{0, (Index)acc_leader.size(), leader}, k_total);
+}
+
+// sparsifier.cpp:103-108: every index with its value (a copy; no arithmetic)
+template <class V>
+SparseSelection select_all(const V& acc) {
+  SparseSelection out;
+  out.indices.resize((std::size_t)acc.size());
+  for (std::size_t j = 0; j < out.indices.size(); ++j) out.indices[j] = (Index)j;
+  out.values.assign(acc.data(), acc.data() + acc.size());
+  return out;
+}
+
+// sparsifier.cpp:127-160
+inline std::string to_string(SparsifierKind kind) {
+  switch (kind) {
+    case SparsifierKind::micro: return "micro";
+    case SparsifierKind::topk: return "topk";
+    case SparsifierKind::cltk: return "cltk";
+    case SparsifierKind::hard_threshold: return "hard";
+    case SparsifierKind::dense: return "dense";
+  }
+  throw std::invalid_argument("unknown sparsifier kind");
+}
+inline SparsifierKind parse_sparsifier_kind(const std::string& name) {
+  if (name == "micro") return SparsifierKind::micro;
+  if (name == "topk") return SparsifierKind::topk;
+  if (name == "cltk") return SparsifierKind::cltk;
+  if (name == "hard" || name == "hard_threshold") return SparsifierKind::hard_threshold;
+  if (name == "dense") return SparsifierKind::dense;
+  throw std::invalid_argument("unknown sparsifier '" + name + "' (expected micro|topk|cltk|hard|dense)");
+}
+inline std::string to_string(PerWorkerTarget target) { return target == PerWorkerTarget::split ? "split" : "full"; }
+inline PerWorkerTarget parse_per_worker_target(const std::string& name) {
+  if (name == "split") return PerWorkerTarget::split;
+  if (name == "full") return PerWorkerTarget::full;
+  throw std::invalid_argument("unknown per-worker target '" + name + "' (expected split|full)");
 }
 
 template <class V>
@@ -376,6 +456,7 @@ class MicroEngine {
     cfg.min_threshold = sc.min_threshold;
     cfg.target = sc.target == PerWorkerTarget::full ? MICRO_TARGET_FULL : MICRO_TARGET_SPLIT;
     cfg.error_feedback = error_feedback ? 1 : 0;
+    cfg.sparsifier = (int32_t)sc.kind;  // SparsifierKind order == MICRO_MICRO..MICRO_DENSE
     cfg.device = b200::device();
     b200::check(micro_ctx_create(&ctx_, &cfg, nullptr));
   }

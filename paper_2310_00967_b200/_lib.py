@@ -89,6 +89,7 @@ _SIGS = {
     "micro_accumulate": ([I32, VP, DBL, VP, VP, I64, VP], I32),
     "micro_select_by_threshold": ([I32, VP, I64, I64, I64, DBL, VP, VP, I64, VP, VP], I32),
     "micro_compensate": ([I32, VP, I64, VP, I64, VP], I32),
+    "micro_select_topk": ([I32, VP, I64, I64, I64, I64, VP, VP, I64, VP, VP], I32),
     "micro_all_reduce_sparse_values": ([I32, C.POINTER(VP), I32, I64, VP, I64, VP, VP], I32),
     "micro_all_reduce_sparse": ([I32, C.POINTER(VP), I32, I64, VP, I64, VP, VP], I32),
     "micro_all_gather_indices": ([I32, PI64, VP, VP, PI64, VP], I32),

@@ -1658,15 +1658,15 @@ int micro_accumulate(int dtype, const void* d_e, double eta, const void* d_g, vo
   return MICRO_OK;
 }
 
-int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end,
-                              double delta, int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count,
-                              void* stream) {
+// Ordered compaction of {j in [start, end) : |acc_j| > thr} (thr = *d_thr or
+// delta), plus, with d_tie, {|acc_j| == thr, j <= *d_tie} (top-k's ties).
+static int select_range(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end, double delta,
+                        const double* d_thr, const long long* d_tie, int32_t* d_idx, void* d_val, int64_t cap,
+                        int64_t* d_count, void* stream) {
   TRY(check_dtype(dtype));
   if (start < 0 || end < start || end > n_g)
     return fail(MICRO_EINVAL, "selection: range [%lld, %lld) invalid for vector of length %lld",
                 (long long)start, (long long)end, (long long)n_g);
-  if (!(delta >= 0.0) || !std::isfinite(delta))
-    return fail(MICRO_EINVAL, "selection: threshold must be finite and nonnegative");
   if (n_g >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "n_g must be < 2^31 (int32 indices)");
   if (!d_count) return fail(MICRO_EINVAL, "null count pointer");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1691,8 +1691,9 @@ int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t
   a.p_start = start;
   a.p_end = end;
   a.eta = 1.0;
-  a.delta = nullptr;
+  a.delta = d_thr;
   a.delta_value = delta;
+  a.tie_j = d_tie;
   a.sel_idx = d_idx;
   a.sel_val = d_val;
   a.cap = cap;
@@ -1711,6 +1712,85 @@ int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t
   CU(cudaGetLastError());
   CU(cudaFreeAsync(ws, s));
   return MICRO_OK;
+}
+
+int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end,
+                              double delta, int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count,
+                              void* stream) {
+  if (!(delta >= 0.0) || !std::isfinite(delta))
+    return fail(MICRO_EINVAL, "selection: threshold must be finite and nonnegative");
+  return select_range(dtype, d_acc, n_g, start, end, delta, nullptr, nullptr, d_idx, d_val, cap, d_count, stream);
+}
+
+}  // extern "C"
+
+template <typename T>
+static int topk_pivot(const T* acc, int64_t m, int64_t k, int64_t base, TopkState* st, unsigned* hist,
+                      unsigned* tie_counts, int dev, cudaStream_t s) {
+  k_topk_init<<<1, 1, 0, s>>>(st, k);
+  CU(cudaGetLastError());
+  const unsigned hgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 4 * (int64_t)num_sms(dev)));
+  for (int hi = KeyOf<T>::kBits; hi > 0; hi -= kDigitBits) {
+    const int width = std::min(kDigitBits, hi);
+    const int shift = hi - width;
+    k_topk_hist<T><<<hgrid, 256, 0, s>>>(acc, nullptr, 1.0, m, shift, width, st, hist);
+    CU(cudaGetLastError());
+    k_topk_digit<T><<<1, 1024, 0, s>>>(st, hist, shift, width, shift == 0, base + m);
+    CU(cudaGetLastError());
+  }
+  const int64_t chunk = (m + kTieChunks - 1) / kTieChunks;
+  const int nch = (int)((m + chunk - 1) / chunk);
+  k_tie_count<T><<<nch, 256, 0, s>>>(acc, nullptr, 1.0, m, chunk, st, tie_counts);
+  CU(cudaGetLastError());
+  k_tie_find<T><<<1, 1024, 0, s>>>(acc, nullptr, 1.0, m, chunk, nch, st, tie_counts, base);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+extern "C" {
+
+int micro_select_topk(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end, int64_t k,
+                      int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count, void* stream) {
+  TRY(check_dtype(dtype));
+  if (start < 0 || end < start || end > n_g)
+    return fail(MICRO_EINVAL, "selection: range [%lld, %lld) invalid for vector of length %lld",
+                (long long)start, (long long)end, (long long)n_g);
+  const int64_t m = end - start;
+  if (k < 0 || k > m)
+    return fail(MICRO_EINVAL, "select_topk: k=%lld exceeds range size %lld", (long long)k, (long long)m);
+  if (!d_count) return fail(MICRO_EINVAL, "null count pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (k == 0) {
+    CU(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+    return MICRO_OK;
+  }
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  // scratch: state, histogram, tie counts, the "everything" threshold
+  const size_t bytes = 256 + sizeof(unsigned) * (kBins + kTieChunks);
+  char* ws = nullptr;
+  CU(cudaMallocAsync((void**)&ws, bytes, s));
+  CU(cudaMemsetAsync(ws, 0, bytes, s));
+  auto* st = (TopkState*)ws;
+  auto* m1 = (double*)(ws + 128);
+  unsigned* hist = (unsigned*)(ws + 256);
+  unsigned* ties = hist + kBins;
+  int rc = MICRO_OK;
+  if (k == m) {  // every index of the range (sparsifier.cpp:56: no nth_element)
+    const double minus1 = -1.0;
+    CU(cudaMemcpyAsync(m1, &minus1, sizeof minus1, cudaMemcpyHostToDevice, s));
+    rc = select_range(dtype, d_acc, n_g, start, end, 0.0, m1, nullptr, d_idx, d_val, cap, d_count, stream);
+  } else {
+    if (dtype == MICRO_F32)
+      rc = topk_pivot<float>((const float*)d_acc + start, m, k, start, st, hist, ties, dev, s);
+    else
+      rc = topk_pivot<double>((const double*)d_acc + start, m, k, start, st, hist, ties, dev, s);
+    if (rc == MICRO_OK)
+      rc = select_range(dtype, d_acc, n_g, start, end, 0.0, &st->pivot, &st->tie_j, d_idx, d_val, cap, d_count,
+                        stream);
+  }
+  cudaFreeAsync(ws, s);
+  return rc;
 }
 
 int micro_compensate(int dtype, void* d_acc, int64_t n_g, const int32_t* d_idx, int64_t k, void* stream) {

@@ -49,6 +49,12 @@ template <> struct KeyOf<double> {
 };
 
 constexpr int kDigitBits = 11;
+
+// acc = e + eta*G (K1's arithmetic), or acc itself (g == NULL: the value API)
+template <typename T>
+__device__ __forceinline__ T acc_at(const T* e, const T* g, T eta, int64_t j) {
+  return g ? add_rn(e[j], mul_rn(eta, g[j])) : e[j];
+}
 constexpr int kBins = 1 << kDigitBits;
 
 __global__ void k_topk_init(TopkState* st, long long k) {
@@ -91,8 +97,19 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
   const unsigned long long prefix = st->prefix, mask = st->mask;
   const unsigned dmask = (1u << width) - 1u;
   const T eta = (T)eta_d;
-  const int64_t nv = n_g / VN;  // whole vectors (e, G are 16-byte aligned: K1 staging / caller)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (((uintptr_t)e % 16) || ((uintptr_t)g % 16)) {  // a range of the value API: scalar loads
+    for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n_g; j0 += stride) {
+      const int64_t j = j0 + threadIdx.x;
+      const bool ok = j < n_g;
+      hist_add<T>(s_hist, ok ? acc_at(e, g, eta, j) : (T)0, prefix, mask, shift, dmask, ok);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
+      if (s_hist[b]) atomicAdd(&hist[b], s_hist[b]);
+    return;
+  }
+  const int64_t nv = n_g / VN;  // whole vectors (e, G 16-byte aligned: K1 staging / cudaMalloc)
   for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * 2; v0 < nv; v0 += 2 * stride) {  // warp-uniform
     V ev[2], gv[2];
     bool ok[2];
@@ -102,14 +119,14 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
       ok[u] = v < nv;
       if (ok[u]) {
         ev[u] = reinterpret_cast<const V*>(e)[v];
-        gv[u] = ld_nc_stream(reinterpret_cast<const V*>(g) + v);
+        if (g) gv[u] = ld_nc_stream(reinterpret_cast<const V*>(g) + v);
       }
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int c = 0; c < VN; ++c) {
-        const T acc = ok[u] ? add_rn(comp(ev[u], c), mul_rn(eta, comp(gv[u], c))) : (T)0;
+        const T acc = !ok[u] ? (T)0 : g ? add_rn(comp(ev[u], c), mul_rn(eta, comp(gv[u], c))) : comp(ev[u], c);
         hist_add<T>(s_hist, acc, prefix, mask, shift, dmask, ok[u]);
       }
   }
@@ -117,7 +134,7 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const int64_t j = nv * VN + threadIdx.x;
     const bool ok = j < n_g;
-    hist_add<T>(s_hist, ok ? add_rn(e[j], mul_rn(eta, g[j])) : (T)0, prefix, mask, shift, dmask, ok);
+    hist_add<T>(s_hist, ok ? acc_at(e, g, eta, j) : (T)0, prefix, mask, shift, dmask, ok);
   }
   __syncthreads();
   for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
@@ -197,7 +214,7 @@ __global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, cons
   const T P = (T)st->pivot;
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(lo + chunk, n_g);
   unsigned c = 0;
-  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) c += absx(add_rn(e[j], mul_rn(eta, g[j]))) == P;
+  for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) c += absx(acc_at(e, g, eta, j)) == P;
   c = __reduce_add_sync(0xffffffffu, c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
   __syncthreads();
@@ -206,10 +223,11 @@ __global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, cons
 
 // One block of 1024: the chunk holding the k_rem-th tie, then that tie's
 // index (ties taken in index order).
+// base: added to the index written (the value API selects inside a range).
 template <typename T>
 __global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
                                                    int64_t n_g, int64_t chunk, int nchunks, TopkState* st,
-                                                   const unsigned* __restrict__ counts) {
+                                                   const unsigned* __restrict__ counts, int64_t base = 0) {
   if (!st->need_tie) return;
   __shared__ long long s_w[32];
   __shared__ long long s_rem;
@@ -260,7 +278,7 @@ __global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, cons
   __syncthreads();
   for (int64_t b = lo; b < hi; b += 1024) {
     const int64_t j = b + tid;
-    const bool tie = j < hi && absx(add_rn(e[j], mul_rn(eta, g[j]))) == P;
+    const bool tie = j < hi && absx(acc_at(e, g, eta, j)) == P;
     const unsigned bal = __ballot_sync(0xffffffffu, tie);
     if (lane == 0) s_w[w] = __popc(bal);
     __syncthreads();
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, cons
     rem -= total;
     __syncthreads();
   }
-  if (tid == 0) st->tie_j = s_j;
+  if (tid == 0) st->tie_j = base + s_j;
 }
 
 // acc = e + eta*G in place with the non-finite probe (workers that select

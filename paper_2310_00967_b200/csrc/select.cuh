@@ -64,6 +64,7 @@ struct SelectArgs {
   int64_t tile_lo;            // first tile of the grid
   int64_t num_tiles;          // tiles in the grid
   int* flags;                 // bit0 non-finite, bit1 capacity overflow
+  const long long* tie_j;     // top-k (value API): also |acc| == thr at j <= *tie_j (NULL: off)
 };
 
 // Warp 0 only.  Publishes this tile's aggregate, walks back over the
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 4) k1_fused_select(SelectArgs a) {
 
   const double delta = a.delta ? *a.delta : a.delta_value;
   const T thr = threshold_as(delta, (T*)nullptr);
+  const long long tie_limit = a.tie_j ? *a.tie_j : -1;
   const T eta = (T)a.eta;
   const T* __restrict__ G = (const T*)a.grad;
   T* __restrict__ E = (T*)a.resid;
@@ -174,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, 4) k1_fused_select(SelectArgs a) {
         acc = add_rn(acc, mul_rn(eta, gv));  // e + (eta*G): two roundings, no FMA
         set_comp(e[i], c, acc);
       }
-      const bool sel = (j >= p_start) && (j < p_end) && (absx(acc) > thr);
+      const bool sel = (j >= p_start) && (j < p_end) &&
+                       (absx(acc) > thr || (tie_limit >= 0 && absx(acc) == thr && j <= tie_limit));
       mask[i] |= (unsigned)sel << c;
     }
   }

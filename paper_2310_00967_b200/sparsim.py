@@ -145,6 +145,41 @@ def select_by_threshold(acc: torch.Tensor, rng: PartitionRange, delta: float) ->
     return SparseSelection(idx[:k], val[:k])
 
 
+def select_topk(acc: torch.Tensor, rng: PartitionRange, k: int) -> SparseSelection:
+    """sparsifier.cpp:39-67: the k largest |acc| in the range, ties to the lower index, ascending."""
+    acc = _vec(acc, "select_topk")
+    if acc.data_ptr() % 16:
+        acc = acc.clone()
+    m = max(rng.end - rng.start, 0)
+    idx = torch.empty(max(k, 1), dtype=torch.int32, device=acc.device)
+    val = torch.empty(max(k, 1), dtype=acc.dtype, device=acc.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=acc.device)
+    check(lib().micro_select_topk(_DT[acc.dtype], C.c_void_p(acc.data_ptr()), acc.numel(), rng.start, rng.end, k,
+                                  C.c_void_p(idx.data_ptr()), C.c_void_p(val.data_ptr()), max(k, 0),
+                                  C.c_void_p(cnt.data_ptr()), _stream(acc.device)))
+    n = int(cnt.item())
+    return SparseSelection(idx[:n], val[:n])
+
+
+def cltk_select(acc_leader: torch.Tensor, k_total: int, leader: int, t: int, n: int) -> SparseSelection:
+    """sparsifier.cpp:85-97: the cycling leader's global top-k."""
+    if n < 1 or leader < 0 or leader >= n:
+        raise InvalidArgument(_lib.MICRO_EINVAL, "cltk_select: leader id out of range")
+    if t < 0 or t % n != leader:
+        raise _lib.LogicError(_lib.MICRO_ELOGIC, f"cltk_select: worker {leader} is not the leader at iteration {t} "
+                                                 "(leader cycles as t mod n)")
+    acc_leader = _vec(acc_leader, "cltk_select")
+    if k_total > acc_leader.numel():
+        raise InvalidArgument(_lib.MICRO_EINVAL, "cltk_select: k exceeds gradient count")
+    return select_topk(acc_leader, PartitionRange(0, acc_leader.numel(), leader), k_total)
+
+
+def select_all(acc: torch.Tensor) -> SparseSelection:
+    """sparsifier.cpp:103-108: every index, including zeros."""
+    acc = _vec(acc, "select_all")
+    return SparseSelection(torch.arange(acc.numel(), dtype=torch.int32, device=acc.device), acc.clone())
+
+
 def hard_threshold_select(acc: torch.Tensor, delta_fixed: float) -> SparseSelection:
     """sparsifier.cpp:98-100 — the fixed-threshold baseline over the whole vector."""
     return select_by_threshold(acc, PartitionRange(0, acc.numel(), 0), delta_fixed)

@@ -2,6 +2,7 @@
 // drop-in (include/sparsim_b200.hpp) — the reference's own call sites compile
 // unchanged against it.  Built by __graft_entry__.build(), run on the GPU by
 // tests/test_gpu_cpp.py.  Exit code = number of failed checks.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -61,6 +62,42 @@ int main() {
     CHECK_THROWS_AS(select_by_threshold(five, PartitionRange{0, 9, 0}, 0.0), std::invalid_argument);
     CHECK_THROWS_AS(select_by_threshold(five, PartitionRange{0, 4, 0}, -1.0), std::invalid_argument);
     CHECK((hard_threshold_select(vec({0.1, 0.9, 0.5}), 0.4).indices == std::vector<Index>{1, 2}));
+  }
+  // test_sparsifier.cpp:71-98 top-k, CLT-k, select_all (ties to the lower index)
+  {
+    const GradientVector acc = vec({1, -3, 0.5, 2});
+    auto top = select_topk(acc, PartitionRange{0, 4, 0}, 2);
+    CHECK((top.indices == std::vector<Index>{1, 3}));
+    CHECK((top.values == std::vector<double>{-3, 2}));
+    const GradientVector tied = vec({1, -1, 1, 1});
+    CHECK((select_topk(tied, PartitionRange{0, 4, 0}, 2).indices == std::vector<Index>{0, 1}));
+    CHECK((select_topk(tied, PartitionRange{1, 4, 0}, 2).indices == std::vector<Index>{1, 2}));
+    CHECK(select_topk(acc, PartitionRange{0, 4, 0}, 4).count() == 4);
+    CHECK(select_topk(acc, PartitionRange{0, 4, 0}, 0).count() == 0);
+    CHECK_THROWS_AS(select_topk(acc, PartitionRange{0, 2, 0}, 3), std::invalid_argument);
+    CHECK((cltk_select(acc, 1, 1, 5, 4).indices == std::vector<Index>{1}));
+    CHECK_THROWS_AS(cltk_select(acc, 1, 0, 5, 4), std::logic_error);
+    CHECK_THROWS_AS(cltk_select(acc, 9, 1, 5, 4), std::invalid_argument);
+    CHECK(select_all(acc).count() == 4 && select_all(acc).values[1] == -3.0);
+    CHECK(parse_sparsifier_kind("hard") == SparsifierKind::hard_threshold && to_string(SparsifierKind::cltk) == "cltk");
+    CHECK_THROWS_AS(parse_sparsifier_kind("foo"), std::invalid_argument);
+    // randomized against a host sort (|acc| desc, index asc)
+    std::mt19937_64 r2(5);
+    for (int rep = 0; rep < 20; ++rep) {
+      const std::size_t n = 1 + r2() % 5000;
+      GradientVector a(n);
+      for (auto& v : a) v = (double)((int)(r2() % 9) - 4) * 0.25;  // many ties
+      const std::size_t k = r2() % (n + 1);
+      std::vector<Index> ord(n);
+      for (std::size_t j = 0; j < n; ++j) ord[j] = (Index)j;
+      std::sort(ord.begin(), ord.end(), [&](Index x, Index y) {
+        const double ax = std::fabs(a[(std::size_t)x]), ay = std::fabs(a[(std::size_t)y]);
+        return ax != ay ? ax > ay : x < y;
+      });
+      ord.resize(k);
+      std::sort(ord.begin(), ord.end());
+      CHECK(select_topk(a, PartitionRange{0, (Index)n, 0}, k).indices == ord);
+    }
   }
   // test_sparsifier.cpp:100-112, 217-227
   CHECK(micro_update_threshold({1.0}, 100, 150, 0.1).delta == 1.1000000000000001);

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 if torch.cuda.is_available():
     from paper_2310_00967_b200 import sparsim as S
-    from paper_2310_00967_b200._lib import InvalidArgument
+    from paper_2310_00967_b200._lib import InvalidArgument, LogicError
 
 
 def vec(xs, dtype=torch.float64):
@@ -162,3 +162,44 @@ def test_error_metric(dtype):
         S.error_metric([])
     with pytest.raises(InvalidArgument):
         S.error_metric([vec([1.0, 2.0]), vec([1.0])])
+
+
+# test_sparsifier.cpp:71-98 select_topk, sparsifier.cpp:85-108 cltk_select / select_all
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_select_topk_examples_and_oracle(dtype):
+    acc = vec([5, -7, 2, 7], dtype)
+    assert S.select_topk(acc, full(acc), 2).indices.tolist() == [1, 3]
+    assert S.select_topk(acc, full(acc), 0).count() == 0
+    assert S.select_topk(acc, full(acc), 4).indices.tolist() == [0, 1, 2, 3]
+    with pytest.raises(InvalidArgument):
+        S.select_topk(acc, full(acc), 5)
+    tie = vec([2, -2, 2], dtype)
+    assert S.select_topk(tie, full(tie), 2).indices.tolist() == [0, 1]
+    rng = np.random.default_rng(7)
+    for rep in range(150):
+        n = int(rng.integers(1, 401)) if rep < 140 else int(rng.integers(100_000, 300_000))
+        a = rng.standard_normal(n)
+        if n > 4:
+            a[1] = -a[0]
+            a[n // 2] = a[0]
+        if rep % 3 == 0:
+            a = np.round(a * 2) / 2  # many ties
+        start = int(rng.integers(0, n)) if rep % 4 == 0 else 0
+        k = int(rng.integers(0, n - start + 1))
+        t = torch.from_numpy(a).to("cuda", dtype)
+        av = np.abs(t.cpu().numpy()[start:]).astype(np.float64)
+        order = np.lexsort((np.arange(av.size), -av))[:k] + start  # |acc| desc, index asc
+        got = S.select_topk(t, S.PartitionRange(start, n, 0), k)
+        assert got.indices.cpu().numpy().tolist() == sorted(order.tolist()), (rep, n, k)
+        assert torch.equal(got.values, t[got.indices.long()])
+
+
+def test_cltk_and_select_all():
+    acc = vec([1, -3, 0.5, 2])
+    assert S.cltk_select(acc, 1, 1, 5, 4).indices.tolist() == [1]
+    with pytest.raises(LogicError):
+        S.cltk_select(acc, 1, 0, 5, 4)
+    with pytest.raises(InvalidArgument):
+        S.cltk_select(acc, 9, 1, 5, 4)
+    a = S.select_all(acc)
+    assert a.indices.tolist() == [0, 1, 2, 3] and a.values.tolist() == [1, -3, 0.5, 2]
