@@ -274,7 +274,7 @@ def our_arm(args, wl):
     # k_finalize; n > 1 ranks: K1 x2, gather_foreign, owner_reduce,
     # build_union, finalize (NCCL kernels not counted)
     launches_per_step = ((2 if W == 1 else 2 * W + 2) if world == 1
-                         else (4 if args.transport == "peer" else 6))  # peer: K1 x2, exchange, finalize
+                         else {"peer": 5, "peer_pull": 4, "nccl": 6}[args.transport])  # K1 x2 + exchange + finalize
     if args.sparsifier != "micro":  # baselines.cuh: per selecting worker, top-k = init + 2 per digit +
         # tie count/find + stream + gather (fp32: 11), hard = 2, else accumulate + count = 2; then
         # union marks (W) + popcount + scan (2) + emit + reduce + finalize (dense: iota + reduce + finalize)
@@ -380,7 +380,7 @@ def main():
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
     ap.add_argument("--sparsifier", choices=["micro", "topk", "cltk", "hard", "dense"], default="micro",
                     help="N = 1: a comparison sparsifier of the reference's harness instead of MiCRO")
-    ap.add_argument("--transport", choices=["peer", "nccl"], default="peer",
+    ap.add_argument("--transport", choices=["peer", "peer_pull", "nccl"], default="peer",
                     help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
     ap.add_argument("--error-norm", action="store_true",
                     help="also record the per-step error norm ||e_{t+1}|| (fused into k1_stream); off by "

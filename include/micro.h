@@ -285,11 +285,19 @@ int micro_dist_finalize(micro_ctx* ctx, const int32_t* d_all_idx, const void* d_
  *           micro_peer_finalize  (threshold, history, dense g/n, model)
  * The handle blob holds CUDA IPC handles of this rank's residual, counts,
  * union buffers and error-norm slot. */
-#define MICRO_PEER_HANDLE_BYTES 448
+#define MICRO_PEER_HANDLE_BYTES 640
 int micro_peer_export(micro_ctx* ctx, void* out);
 int micro_peer_import(micro_ctx* ctx, const void* all_handles);
 int micro_peer_exchange(micro_ctx* ctx);
 int micro_peer_finalize(micro_ctx* ctx);
+/* Bulk variant (every NVLink transfer contiguous; one more barrier):
+ *   micro_compress, barrier, micro_peer_contribute (gather own acc at every
+ *   other owner's indices — read from the owner, contiguous — zero them, write
+ *   the values into the owner's receive slab), barrier, micro_peer_reduce
+ *   (owner: rank-order sums from its slabs, push (j, s_j) to every rank),
+ *   barrier, micro_peer_finalize. */
+int micro_peer_contribute(micro_ctx* ctx);
+int micro_peer_reduce(micro_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ MICRO_OK, MICRO_EINVAL, MICRO_ELOGIC, MICRO_ENONFINITE = 0, 1, 2, 3
 MICRO_ECUDA, MICRO_ENCCL, MICRO_ECAPACITY, MICRO_ENOMEM = 4, 5, 6, 7
 MICRO_F32, MICRO_F64 = 0, 1
 MICRO_MAX_WORKERS = 64
-MICRO_PEER_HANDLE_BYTES = 448
+MICRO_PEER_HANDLE_BYTES = 640
 SPARSIFIERS = {"micro": 0, "topk": 1, "cltk": 2, "hard": 3, "dense": 4}  # sparsifier.hpp:21
 
 
@@ -130,6 +130,8 @@ _SIGS = {
     "micro_peer_import": ([VP, VP], I32),
     "micro_peer_exchange": ([VP], I32),
     "micro_peer_finalize": ([VP], I32),
+    "micro_peer_contribute": ([VP], I32),
+    "micro_peer_reduce": ([VP], I32),
 }
 
 EXPORTED = sorted(_SIGS)

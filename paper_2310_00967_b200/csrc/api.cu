@@ -241,12 +241,15 @@ struct micro_ctx {
   double* minus_one = nullptr;  // threshold that selects everything (k >= n_g)
   // peer-memory exchange (micro_peer_*): every rank's buffers mapped here
   bool peer_ready = false;
-  bool peer_exchanged = false;
   const long long* peer_counts[kMaxWorkers] = {};
   void* peer_resid[kMaxWorkers] = {};
   int32_t* peer_uidx[2][kMaxWorkers] = {};
   void* peer_usum[2][kMaxWorkers] = {};
   double* peer_corr[kMaxWorkers] = {};
+  const int32_t* peer_sel[2][kMaxWorkers] = {};
+  void* peer_recv[kMaxWorkers] = {};
+  void* recv = nullptr;          // bulk exchange: receive slabs [source rank][sel_cap] (lazy)
+  int peer_phase = 0;            // 0 idle, 1 contributed (bulk), 2 exchanged (ready to finalize)
   std::vector<void*> peer_opened;  // cudaIpcOpenMemHandle mappings to close
 
   int alloc(void** p, size_t bytes) {
@@ -1447,7 +1450,7 @@ int micro_dist_owner_reduce(micro_ctx* c, const void* d_recv, const int64_t* h_c
 
 // ---- peer-memory exchange (peer.cuh) ------------------------------------
 namespace {
-constexpr int kPeerBufs = 7;  // resid, counts, uidx x2, usum x2, norm corr
+constexpr int kPeerBufs = 10;  // resid, counts, uidx x2, usum x2, norm corr, sel_idx x2, recv
 static_assert(MICRO_PEER_HANDLE_BYTES == kPeerBufs * sizeof(cudaIpcMemHandle_t), "handle layout");
 
 void* peer_buf(micro_ctx* c, int b) {
@@ -1458,7 +1461,10 @@ void* peer_buf(micro_ctx* c, int b) {
     case 3: return c->uni_idx[1];
     case 4: return c->uni_sum[0];
     case 5: return c->uni_sum[1];
-    default: return c->norm ? c->norm_corr : nullptr;
+    case 6: return c->norm ? c->norm_corr : nullptr;
+    case 7: return c->sel_idx[0][0];
+    case 8: return c->sel_idx[1][0] != c->sel_idx[0][0] ? c->sel_idx[1][0] : nullptr;  // single-buffered
+    default: return c->recv;
   }
 }
 
@@ -1475,6 +1481,7 @@ int micro_peer_export(micro_ctx* c, void* out) {
   TRY(check_peer_ctx(c));
   if (!out) return fail(MICRO_EINVAL, "null handle buffer");
   DeviceGuard dg(c->dev);
+  if (!c->recv) TRY(c->alloc(&c->recv, (size_t)c->n * c->sel_cap * c->esz));
   auto* h = (cudaIpcMemHandle_t*)out;
   for (int b = 0; b < kPeerBufs; ++b) {
     std::memset(&h[b], 0, sizeof h[b]);
@@ -1503,7 +1510,8 @@ int micro_peer_import(micro_ctx* c, const void* all) {
       CU(cudaIpcOpenMemHandle(&p[b], hb, cudaIpcMemLazyEnablePeerAccess));
       c->peer_opened.push_back(p[b]);
     }
-    if (!p[0] || !p[1] || !p[2] || !p[3] || !p[4] || !p[5])
+    if (!p[8]) p[8] = p[7];  // the rank's selection is single-buffered
+    if (!p[0] || !p[1] || !p[2] || !p[3] || !p[4] || !p[5] || !p[7] || !p[9])
       return fail(MICRO_EINVAL, "rank %d exported incomplete handles", r);
     if (c->norm && !p[6]) return fail(MICRO_EINVAL, "rank %d does not record the error norm", r);
     c->peer_resid[r] = p[0];
@@ -1513,6 +1521,9 @@ int micro_peer_import(micro_ctx* c, const void* all) {
     c->peer_usum[0][r] = p[4];
     c->peer_usum[1][r] = p[5];
     c->peer_corr[r] = c->norm ? (double*)p[6] : nullptr;
+    c->peer_sel[0][r] = (const int32_t*)p[7];
+    c->peer_sel[1][r] = (const int32_t*)p[8];
+    c->peer_recv[r] = p[9];
   }
   c->peer_ready = true;
   return MICRO_OK;
@@ -1522,7 +1533,7 @@ int micro_peer_exchange(micro_ctx* c) {
   TRY(check_peer_ctx(c));
   if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_peer_import");
   if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_compress");
-  if (c->peer_exchanged) return fail(MICRO_ELOGIC, "micro_peer_exchange called twice");
+  if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_exchange called twice");
   DeviceGuard dg(c->dev);
   PeerPtrs pp{};
   for (int r = 0; r < c->n; ++r) {
@@ -1551,15 +1562,73 @@ int micro_peer_exchange(micro_ctx* c) {
                                                                       c->sel_idx[c->buf][0], v, Kout);
   }
   CU(cudaGetLastError());
-  c->peer_exchanged = true;
+  c->peer_phase = 2;
+  return MICRO_OK;
+}
+
+PeerBulkPtrs bulk_ptrs(micro_ctx* c) {
+  PeerBulkPtrs pb{};
+  for (int r = 0; r < c->n; ++r) {
+    pb.counts[r] = c->peer_counts[r];
+    pb.sel_idx[r] = c->peer_sel[c->buf][r];
+    pb.recv[r] = c->peer_recv[r];
+    pb.uidx[r] = c->peer_uidx[c->buf][r];
+    pb.usum[r] = c->peer_usum[c->buf][r];
+  }
+  return pb;
+}
+
+int micro_peer_contribute(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_contribute before micro_peer_import");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_contribute before micro_compress");
+  if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_contribute called twice");
+  DeviceGuard dg(c->dev);
+  const PeerBulkPtrs pb = bulk_ptrs(c);
+  const dim3 grid(grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev) / 2 + 1, c->n);
+  double* corr = c->norm ? c->norm_corr : nullptr;
+  const int me = c->cfg.rank;
+  if (c->esz == 4) {
+    if (c->cfg.error_feedback)
+      k_peer_contribute<float, true><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (float*)c->resid[0], corr);
+    else
+      k_peer_contribute<float, false><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (float*)c->resid[0], corr);
+  } else {
+    if (c->cfg.error_feedback)
+      k_peer_contribute<double, true><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (double*)c->resid[0], corr);
+    else
+      k_peer_contribute<double, false><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (double*)c->resid[0], corr);
+  }
+  CU(cudaGetLastError());
+  c->peer_phase = 1;
+  return MICRO_OK;
+}
+
+int micro_peer_reduce(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (c->peer_phase != 1) return fail(MICRO_ELOGIC, "micro_peer_reduce before micro_peer_contribute");
+  DeviceGuard dg(c->dev);
+  const PeerBulkPtrs pb = bulk_ptrs(c);
+  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
+  long long* Kout = c->Kbuf + c->buf;
+  if (c->esz == 4)
+    k_peer_reduce_push<float><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,
+                                                           c->sel_idx[c->buf][0],
+                                                           (const float*)c->sel_val[c->buf][0], Kout);
+  else
+    k_peer_reduce_push<double><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,
+                                                            c->sel_idx[c->buf][0],
+                                                            (const double*)c->sel_val[c->buf][0], Kout);
+  CU(cudaGetLastError());
+  c->peer_phase = 2;
   return MICRO_OK;
 }
 
 int micro_peer_finalize(micro_ctx* c) {
   TRY(check_peer_ctx(c));
-  if (!c->peer_exchanged) return fail(MICRO_ELOGIC, "micro_peer_finalize before micro_peer_exchange");
+  if (c->peer_phase != 2) return fail(MICRO_ELOGIC, "micro_peer_finalize before the exchange");
   DeviceGuard dg(c->dev);
-  c->peer_exchanged = false;
+  c->peer_phase = 0;
   if (c->esz == 4) return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
   return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
 }

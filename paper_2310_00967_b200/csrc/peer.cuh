@@ -112,3 +112,93 @@ __global__ void __launch_bounds__(256) k_peer_exchange(PeerPtrs p, int n, int me
 }
 
 }  // namespace micro
+
+namespace micro {
+
+// ---- bulk variant: every NVLink transfer contiguous --------------------------
+// Random 4-byte remote reads and stores (above) cost a whole NVLink request
+// each; here the only random accesses are local HBM ones:
+//   phase A (after barrier #1), every rank r for every other owner o: read
+//     o's selected index list (remote, contiguous), gather its own acc_r at
+//     those indices and zero them (local), write the values contiguously
+//     into o's receive slab r (remote, contiguous);
+//   phase B (after barrier #2), every owner: s = 0; s += contribution_r in
+//     rank order (local, contiguous), push (j, s_j) into every rank's union
+//     buffer (remote, contiguous);
+//   finalize after barrier #3.
+struct PeerBulkPtrs {
+  const long long* counts[kMaxWorkers];
+  const int32_t* sel_idx[kMaxWorkers];   // each owner's own selection (this step's parity)
+  void* recv[kMaxWorkers];               // each owner's receive slabs: [source rank][cap]
+  int32_t* uidx[kMaxWorkers];
+  void* usum[kMaxWorkers];
+};
+
+template <typename T, bool kZero>
+__global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me, long long cap, T* __restrict__ resid,
+                                                         double* corr) {
+  const int o = blockIdx.y;
+  if (o == me) return;  // block-uniform
+  __shared__ double s_q[8];
+  long long k = ld_volatile_i64(p.counts[o]);
+  k = k < cap ? k : cap;
+  const int32_t* __restrict__ idx = p.sel_idx[o];
+  T* __restrict__ out = (T*)p.recv[o] + (long long)me * cap;
+  double q = 0.0;
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
+    const int32_t j = idx[m];
+    const T v = ld_rand(resid + j);
+    out[m] = v;
+    if (kZero) {
+      resid[j] = (T)0;
+      q += (double)v * (double)v;
+    }
+  }
+  if (kZero && corr) {  // squares of the entries zeroed here (error norm)
+    q = warp_sum_f64(q);
+    if ((threadIdx.x & 31) == 0) s_q[threadIdx.x >> 5] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_q[w];
+      if (tot != 0.0) atomicAdd(corr, tot);
+    }
+  }
+  __threadfence_system();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_peer_reduce_push(PeerBulkPtrs p, int n, int me, int64_t t, long long cap,
+                                                          const int32_t* __restrict__ own_idx,
+                                                          const T* __restrict__ own_val, long long* K_out) {
+  __shared__ long long s_off, s_k;
+  if (threadIdx.x == 0) {
+    const int pme = (int)((t % n + me) % n);
+    long long off = 0, K = 0;
+    for (int q = 0; q < n; ++q) {
+      const long long kq = ld_volatile_i64(p.counts[partition_owner(q, n, t)]);
+      const long long kc = kq < cap ? kq : cap;
+      if (q < pme) off += kc;
+      K += kc;
+    }
+    const long long km = ld_volatile_i64(p.counts[me]);
+    s_off = off;
+    s_k = km < cap ? km : cap;
+    if (blockIdx.x == 0) *K_out = K;
+  }
+  __syncthreads();
+  const long long off = s_off, k = s_k;
+  const T* __restrict__ recv = (const T*)p.recv[me];
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
+    T s = (T)0;
+    for (int r = 0; r < n; ++r) s = add_rn(s, r == me ? own_val[m] : recv[(long long)r * cap + m]);
+    const int32_t j = own_idx[m];
+    for (int q = 0; q < n; ++q) {
+      p.uidx[q][off + m] = j;
+      ((T*)p.usum[q])[off + m] = s;
+    }
+  }
+  __threadfence_system();
+}
+
+}  // namespace micro

@@ -118,16 +118,18 @@ class DistMicro:
     """One rank's MiCRO engine; same calls as :class:`engine.Micro`.
 
     ``transport="nccl"``: the protocol above (NCCL moves the data).
-    ``transport="peer"``: one kernel per rank over peer memory
-    (micro_peer_*, csrc/peer.cuh) between two barriers — a 4-byte NCCL
-    all-reduce on the compute stream, or, with ``comm_device="cpu"`` (tests,
-    several ranks on one GPU), a host barrier after a stream sync, so no
-    kernel ever waits on another rank's kernel."""
+    ``transport="peer"``: two kernels per rank over peer memory with every
+    NVLink transfer contiguous (micro_peer_contribute / _reduce,
+    csrc/peer.cuh) between barriers; ``"peer_pull"``: one kernel whose owners
+    read the peers' entries remotely (micro_peer_exchange).  The barriers are
+    a 4-byte NCCL all-reduce on the compute stream, or, with
+    ``comm_device="cpu"`` (tests, several ranks on one GPU), a host barrier
+    after a stream sync, so no kernel ever waits on another rank's kernel."""
 
     def __init__(self, n_g: int, group=None, comm_device=None, transport: str = "nccl", **kw):
         if not dist.is_initialized():
             raise _lib.LogicError(_lib.MICRO_ELOGIC, "torch.distributed is not initialized")
-        if transport not in ("nccl", "peer"):
+        if transport not in ("nccl", "peer", "peer_pull"):
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unknown transport {transport!r}")
         self.group = group
         self.world = dist.get_world_size(group)
@@ -137,7 +139,7 @@ class DistMicro:
         self.n_g = n_g
         self.comm_device = comm_device
         self.transport = transport
-        if transport == "peer":
+        if transport in ("peer", "peer_pull"):
             blob = C.create_string_buffer(_lib.MICRO_PEER_HANDLE_BYTES)
             check(lib().micro_peer_export(self.m.handle, blob))
             blobs = [None] * self.world
@@ -160,7 +162,15 @@ class DistMicro:
     def aggregate(self) -> int | None:
         """NCCL transport: returns |union| (known on the host).  Peer
         transport: asynchronous, returns None (``query().K`` has it)."""
-        if self.transport == "peer":
+        if self.transport == "peer":  # bulk: every NVLink transfer contiguous
+            self._barrier()
+            check(lib().micro_peer_contribute(self.m.handle))
+            self._barrier()
+            check(lib().micro_peer_reduce(self.m.handle))
+            self._barrier()
+            check(lib().micro_peer_finalize(self.m.handle))
+            return None
+        if self.transport == "peer_pull":  # one kernel: owners read the peers' entries remotely
             self._barrier()
             check(lib().micro_peer_exchange(self.m.handle))
             self._barrier()

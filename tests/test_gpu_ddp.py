@@ -84,7 +84,7 @@ def _run(rank, world, port, iters, transport, q):
     q.put((rank, bad))
 
 
-@pytest.mark.parametrize("world,transport", [(1, "peer"), (2, "peer"), (2, "nccl")])
+@pytest.mark.parametrize("world,transport", [(1, "peer"), (2, "peer"), (2, "peer_pull"), (2, "nccl")])
 def test_ddp_hook(world, transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -81,7 +81,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("transport", ["nccl", "peer"])
+@pytest.mark.parametrize("transport", ["nccl", "peer", "peer_pull"])
 @pytest.mark.parametrize("world,n_g,ef", [(2, 100_003, True), (3, 50_000, True), (2, 20_000, False)])
 def test_dist_device_halves_one_gpu(world, n_g, ef, transport):
     """transport="nccl": the NCCL protocol's device halves (collectives staged
