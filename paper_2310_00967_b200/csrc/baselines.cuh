@@ -79,6 +79,8 @@ __device__ __forceinline__ void hist_add(unsigned* s_hist, T acc, unsigned long 
     const unsigned long long key = KO::key(absx(acc));
     if ((key & mask) == prefix) bin = (int)((key >> shift) & dmask);
   }
+  // after the first digit most lanes fall outside the prefix: skip the merge
+  if (!__any_sync(0xffffffffu, bin >= 0)) return;
   const unsigned peers = __match_any_sync(0xffffffffu, bin);
   if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[bin], __popc(peers));
 }
