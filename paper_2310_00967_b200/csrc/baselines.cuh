@@ -68,21 +68,20 @@ __global__ void k_topk_init(TopkState* st, long long k) {
 }
 
 // Histogram of the current digit over the elements whose higher digits match
-// the prefix.  Lanes hitting the same bin are merged with __match_any_sync
-// (the top digit holds the exponent: a handful of bins take everything).
+// the prefix, in kHistCopies interleaved shared-memory copies (the top digit
+// holds the exponent: a handful of bins take everything, so same-address
+// atomics are the cost to spread).
+constexpr int kHistCopies = 4;  // lane l counts into copy l % 4: at most 8 lanes share an address
+
 template <typename T>
 __device__ __forceinline__ void hist_add(unsigned* s_hist, T acc, unsigned long long prefix, unsigned long long mask,
                                          int shift, unsigned dmask, bool valid) {
   using KO = KeyOf<T>;
-  int bin = -1;
   if (valid) {
     const unsigned long long key = KO::key(absx(acc));
-    if ((key & mask) == prefix) bin = (int)((key >> shift) & dmask);
+    if ((key & mask) == prefix)
+      atomicAdd(&s_hist[((unsigned)(key >> shift) & dmask) * kHistCopies + (threadIdx.x & (kHistCopies - 1))], 1u);
   }
-  // after the first digit most lanes fall outside the prefix: skip the merge
-  if (!__any_sync(0xffffffffu, bin >= 0)) return;
-  const unsigned peers = __match_any_sync(0xffffffffu, bin);
-  if (bin >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_hist[bin], __popc(peers));
 }
 
 // 16-byte loads of e and G (the same acc = e + eta*G as K1), every lane
@@ -93,22 +92,29 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
                                                    unsigned* __restrict__ hist) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
-  __shared__ unsigned s_hist[kBins];
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) s_hist[b] = 0;
+  __shared__ unsigned s_hist[kBins * kHistCopies];
+  for (int b = threadIdx.x; b < kBins * kHistCopies; b += blockDim.x) s_hist[b] = 0;
   __syncthreads();
   const unsigned long long prefix = st->prefix, mask = st->mask;
   const unsigned dmask = (1u << width) - 1u;
   const T eta = (T)eta_d;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto flush = [&]() {
+    __syncthreads();
+    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x) {
+      unsigned c = 0;
+#pragma unroll
+      for (int q = 0; q < kHistCopies; ++q) c += s_hist[b * kHistCopies + q];
+      if (c) atomicAdd(&hist[b], c);
+    }
+  };
   if (((uintptr_t)e % 16) || ((uintptr_t)g % 16)) {  // a range of the value API: scalar loads
     for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n_g; j0 += stride) {
       const int64_t j = j0 + threadIdx.x;
       const bool ok = j < n_g;
       hist_add<T>(s_hist, ok ? acc_at(e, g, eta, j) : (T)0, prefix, mask, shift, dmask, ok);
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
-      if (s_hist[b]) atomicAdd(&hist[b], s_hist[b]);
+    flush();
     return;
   }
   const int64_t nv = n_g / VN;  // whole vectors (e, G 16-byte aligned: K1 staging / cudaMalloc)
@@ -138,9 +144,7 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
     const bool ok = j < n_g;
     hist_add<T>(s_hist, ok ? acc_at(e, g, eta, j) : (T)0, prefix, mask, shift, dmask, ok);
   }
-  __syncthreads();
-  for (int b = threadIdx.x; b <= (int)dmask; b += blockDim.x)
-    if (s_hist[b]) atomicAdd(&hist[b], s_hist[b]);
+  flush();
 }
 
 // One block of 1024: pick the bucket holding the k_rem-th largest key, fold
