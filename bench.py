@@ -173,6 +173,8 @@ def our_arm(args, wl):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dist_backend == "gloo":  # code-path check of N > 1 on one GPU: ranks share it, numbers are not valid
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n_g, d = wl["n_g"], wl["d"]
@@ -185,10 +187,14 @@ def our_arm(args, wl):
         import torch.distributed as tdist
 
         from paper_2310_00967_b200.dist import DistMicro
-        tdist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "gloo":
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
         m = DistMicro(n_g, transport=args.transport, density=d, initial_threshold=delta0, scaling_factor=ALPHA,
-                      dense_output=args.dense, record_error_norm=args.error_norm)
+                      dense_output=args.dense, record_error_norm=args.error_norm,
+                      comm_device="cpu" if args.dist_backend == "gloo" else None)
     else:
         m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
                          record_error_norm=args.error_norm, sparsifier=args.sparsifier)
@@ -250,7 +256,7 @@ def our_arm(args, wl):
     k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone
     m.kernel_timing(False)
     if dist:
-        v = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        v = torch.tensor([total_ms], device=dev if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         total_ms = float(v[0])
     ms_step = total_ms / args.steps
@@ -312,6 +318,40 @@ def our_arm(args, wl):
                "d2h_bytes_per_step": int(8 * statistics.mean(kk) + 8 + 4),
                "host_gradients": f"{nb - 1} distinct pinned buffers over {ke} steps",
                "density": float(statistics.mean(kk)) / n_g}
+    else:
+        # N ranks: each copies its own pinned host gradient in, steps through
+        # DistMicro, and reads the union back; the max over ranks is reported
+        ke = max(3, min(args.steps, 10))
+        nb = int(max(2, min(ke + 1, 4e9 // (4 * n_g))))
+        hGs = []
+        for b in range(nb):
+            engine.synth_gaussian(G[0], SEED, rank, t + 1 + b)
+            hGs.append(G[0].cpu().pin_memory())
+        dG = torch.empty(n_g, device=dev)
+        idx = torch.empty(n_g, dtype=torch.int32).pin_memory().numpy()
+        sums = torch.empty(n_g, dtype=torch.float32).pin_memory().numpy()
+        dG.copy_(hGs[-1], non_blocking=True)
+        m.step([dG], ETA, t)
+        m.union(idx, sums)
+        t += 1
+        kk = []
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(ke):
+            dG.copy_(hGs[s % (nb - 1)], non_blocking=True)
+            m.step([dG], ETA, t)
+            i_, _s = m.union(idx, sums)
+            kk.append(i_.size)
+            t += 1
+        torch.cuda.synchronize()
+        v = torch.tensor([(time.perf_counter() - t0) / ke], device=dev if args.dist_backend == "nccl" else "cpu",
+                         dtype=torch.float64)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(v[0]) * 1e6, "unit": "us/iter", "h2d_bytes_per_step": 4 * n_g,
+               "d2h_bytes_per_step": int(8 * statistics.mean(kk) + 8 + 4),
+               "host_gradients": f"{nb - 1} distinct pinned buffers per rank over {ke} steps",
+               "density": float(statistics.mean(kk)) / n_g, "per": "rank (max over ranks)"}
 
     # ---- CPU baseline: the reference's own code on this host (rank 0, N = 1) ----
     cpu = None
@@ -380,6 +420,8 @@ def main():
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
     ap.add_argument("--sparsifier", choices=["micro", "topk", "cltk", "hard", "dense"], default="micro",
                     help="N = 1: a comparison sparsifier of the reference's harness instead of MiCRO")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: exercise the N > 1 path with all ranks on one GPU (code check only)")
     ap.add_argument("--transport", choices=["peer", "peer_pull", "nccl"], default="peer",
                     help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
     ap.add_argument("--error-norm", action="store_true",

@@ -213,13 +213,20 @@ class Micro:
         check(lib().micro_kernel_times(self._h, out.ctypes.data, max_n, C.byref(w)))
         return out[: w.value].copy()
 
-    def union(self):
-        """(indices int32, sums) of the last step as host numpy arrays."""
-        idx = np.empty(self.n_g, np.int32)
-        sums = np.empty(self.n_g, _NP[self.dtype])
+    def union(self, out_idx: np.ndarray | None = None, out_sums: np.ndarray | None = None):
+        """(indices int32, sums) of the last step as host numpy arrays; with
+        caller buffers (e.g. pinned) the result views them without a copy."""
+        if out_idx is None or out_sums is None:
+            idx = np.empty(self.n_g, np.int32)
+            sums = np.empty(self.n_g, _NP[self.dtype])
+        else:
+            idx, sums = out_idx, out_sums
         K = C.c_int64()
-        check(lib().micro_copy_union(self._h, idx.ctypes.data, sums.ctypes.data, self.n_g, C.byref(K)))
-        return idx[: K.value].copy(), sums[: K.value].copy()
+        check(lib().micro_copy_union(self._h, idx.ctypes.data, sums.ctypes.data, min(idx.size, sums.size),
+                                     C.byref(K)))
+        if out_idx is None or out_sums is None:
+            return idx[: K.value].copy(), sums[: K.value].copy()
+        return idx[: K.value], sums[: K.value]
 
     def union_device(self):
         """Zero-copy device views (valid until the next step): idx, sums, K tensor."""
