@@ -227,6 +227,7 @@ struct micro_ctx {
   std::vector<void*> allocs;
   // comparison sparsifiers (micro_config.sparsifier, baselines.cuh)
   int kind = 0;                 // 0 MiCRO, 1 top-k, 2 CLT-k, 3 hard threshold, 4 dense
+  bool vectors_done = false;    // this step's model / dense g/n already written (dense kind)
   bool sel_is_union = false;    // n = 1 MiCRO: the union is worker 0's selection
   uint64_t k_global = 0;
   TopkState* topk = nullptr;    // n_local
@@ -633,6 +634,12 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   // n = 1 with the streaming K1: k1_gather applied the model update
   f.model = (c->sel_is_union && c->k1_kind == 0) ? nullptr : c->model;
   f.update_delta = c->kind == 0;
+  if (c->vectors_done) {  // k_dense_all wrote the model and the dense g/n
+    f.model = nullptr;
+    f.dense = nullptr;
+    f.prev_idx = nullptr;
+    c->vectors_done = false;
+  }
   f.slot = c->steps % kHistCap;
   f.hist_t = c->hist_t;
   f.hist_K = c->hist_K;
@@ -675,7 +682,7 @@ int finalize_blocks(micro_ctx* c) {
 // the (small, latency-bound) clear overlaps the HBM-bound K1.
 template <typename T>
 int fork_dense_clear(micro_ctx* c) {
-  if (!c->dense || c->dense_fused || !c->ever_stepped || !c->aux) return MICRO_OK;
+  if (!c->dense || c->dense_fused || !c->ever_stepped || !c->aux || c->kind == 4) return MICRO_OK;
   const int pb = c->buf ^ 1;
   const int32_t* prev = c->sel_is_union ? c->sel_idx[pb][0] : c->uni_idx[pb];
   CU(cudaEventRecord(c->ev_fork, c->stream));
@@ -695,9 +702,16 @@ int aggregate_baseline(micro_ctx* c) {
   int32_t* uidx = c->uni_idx[c->buf];
   long long* K = c->Kbuf + c->buf;
   const unsigned grid = grid_for(c->n_g, c->dev);
-  if (c->kind == 4) {
-    k_iota<<<grid, 256, 0, st>>>(uidx, c->n_g, K);
+  WorkerPtrs w{};
+  for (int i = 0; i < c->n_local; ++i) w.resid[i] = c->resid[i];
+  if (c->kind == 4) {  // one coalesced pass does the union, sums, model, dense g/n and zeroing
+    k_dense_all<T><<<grid, 256, 0, st>>>(w, c->n, c->n_g, (T*)c->model, (T*)c->dense, uidx,
+                                         (T*)c->uni_sum[c->buf], K);
     CU(cudaGetLastError());
+    if (c->norm)
+      for (int i = 0; i < c->n_local; ++i) TRY(launch_sumsq<T>(c, i));
+    c->vectors_done = true;
+    return launch_finalize<T>(c, uidx, c->uni_sum[c->buf], 0);
   } else {
     for (int i = 0; i < c->n_local; ++i) {
       k_union_mark<<<grid_for(std::min<int64_t>(c->sel_cap, 2 * (int64_t)c->k_global + 1024), c->dev), 256, 0, st>>>(
@@ -711,8 +725,6 @@ int aggregate_baseline(micro_ctx* c) {
     k_bitmap_emit<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_off, uidx, K);
     CU(cudaGetLastError());
   }
-  WorkerPtrs w{};
-  for (int i = 0; i < c->n_local; ++i) w.resid[i] = c->resid[i];
   if (c->cfg.error_feedback)
     k_union_reduce<T, true><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf]);
   else

@@ -388,3 +388,67 @@ __global__ void __launch_bounds__(256) k_union_reduce(WorkerPtrs w, int n, const
 }
 
 }  // namespace micro
+
+namespace micro {
+
+// Dense (select_all): the union is every index, so the whole step is one
+// coalesced pass — s_j = sum_r acc_r[j] in worker order, g/n = s_j / n into
+// the model and the dense output, the union written as (j, s_j), and every
+// residual zeroed (harness.cpp:210-224).
+template <typename T>
+__global__ void __launch_bounds__(256) k_dense_all(WorkerPtrs w, int n, int64_t n_g, T* __restrict__ x,
+                                                   T* __restrict__ dense, int32_t* __restrict__ uidx,
+                                                   T* __restrict__ usum, long long* K) {
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
+  const T nf = (T)n;
+  const int64_t nv = n_g / VN;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv + (n_g % VN ? 1 : 0); v += stride) {
+    if (v < nv) {
+      V s;
+#pragma unroll
+      for (int c = 0; c < VN; ++c) set_comp(s, c, (T)0);
+      for (int r = 0; r < n; ++r) {
+        V* e = reinterpret_cast<V*>(w.resid[r]) + v;
+        const V a = *e;
+#pragma unroll
+        for (int c = 0; c < VN; ++c) set_comp(s, c, add_rn(comp(s, c), comp(a, c)));
+        V z;
+#pragma unroll
+        for (int c = 0; c < VN; ++c) set_comp(z, c, (T)0);
+        *e = z;
+      }
+      reinterpret_cast<V*>(usum)[v] = s;
+      V avg;
+#pragma unroll
+      for (int c = 0; c < VN; ++c) set_comp(avg, c, div_rn(comp(s, c), nf));
+      if (x) {
+        V xv = reinterpret_cast<V*>(x)[v];
+#pragma unroll
+        for (int c = 0; c < VN; ++c) set_comp(xv, c, comp(xv, c) - comp(avg, c));
+        reinterpret_cast<V*>(x)[v] = xv;
+      }
+      if (dense) reinterpret_cast<V*>(dense)[v] = avg;
+#pragma unroll
+      for (int c = 0; c < VN; ++c) uidx[v * VN + c] = (int32_t)(v * VN + c);
+    } else {  // the tail
+      for (int64_t j = nv * VN; j < n_g; ++j) {
+        T s = (T)0;
+        for (int r = 0; r < n; ++r) {
+          T* e = (T*)w.resid[r] + j;
+          s = add_rn(s, *e);
+          *e = (T)0;
+        }
+        usum[j] = s;
+        const T avg = div_rn(s, nf);
+        if (x) x[j] = x[j] - avg;
+        if (dense) dense[j] = avg;
+        uidx[j] = (int32_t)j;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *K = n_g;
+}
+
+}  // namespace micro
