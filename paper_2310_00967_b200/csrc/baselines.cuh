@@ -369,21 +369,32 @@ template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_union_reduce(WorkerPtrs w, int n, const int32_t* __restrict__ uidx,
                                                       const long long* K, T* __restrict__ usum) {
   const long long k = *K;
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
-    const int32_t j = uidx[m];
-    T s = (T)0;
-    for (int r0 = 0; r0 < n; r0 += 8) {  // eight loads in flight, summed in worker order
-      T v[8];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // four union entries per thread in flight (random reads, 64-byte L2 fetches)
+  for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 4 * stride) {
+    int32_t j[4];
+    T s[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = r0 + u < n ? ld_rand((const T*)w.resid[r0 + u] + j) : (T)0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (r0 + u >= n) break;
-        s = add_rn(s, v[u]);
-        if (kZero) ((T*)w.resid[r0 + u])[j] = (T)0;
-      }
+    for (int q = 0; q < 4; ++q) {
+      s[q] = (T)0;
+      if (m0 + q * stride < k) j[q] = uidx[m0 + q * stride];
     }
-    usum[m] = s;
+    for (int r = 0; r < n; ++r) {  // worker order
+      T* e = (T*)w.resid[r];
+      T v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (m0 + q * stride < k) v[q] = ld_rand(e + j[q]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (m0 + q * stride < k) {
+          s[q] = add_rn(s[q], v[q]);
+          if (kZero) e[j[q]] = (T)0;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (m0 + q * stride < k) usum[m0 + q * stride] = s[q];
   }
 }
 
@@ -406,7 +417,8 @@ __global__ void __launch_bounds__(256) k_dense_all(WorkerPtrs w, int n, int64_t 
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv + (n_g % VN ? 1 : 0); v += stride) {
     if (v < nv) {
-      V s;
+      V s, xv;
+      if (x) xv = reinterpret_cast<const V*>(x)[v];  // issued before the residual stores
 #pragma unroll
       for (int c = 0; c < VN; ++c) set_comp(s, c, (T)0);
       for (int r = 0; r < n; ++r) {
@@ -424,14 +436,16 @@ __global__ void __launch_bounds__(256) k_dense_all(WorkerPtrs w, int n, int64_t 
 #pragma unroll
       for (int c = 0; c < VN; ++c) set_comp(avg, c, div_rn(comp(s, c), nf));
       if (x) {
-        V xv = reinterpret_cast<V*>(x)[v];
 #pragma unroll
         for (int c = 0; c < VN; ++c) set_comp(xv, c, comp(xv, c) - comp(avg, c));
         reinterpret_cast<V*>(x)[v] = xv;
       }
       if (dense) reinterpret_cast<V*>(dense)[v] = avg;
-#pragma unroll
-      for (int c = 0; c < VN; ++c) uidx[v * VN + c] = (int32_t)(v * VN + c);
+      if (VN == 4) {
+        reinterpret_cast<int4*>(uidx)[v] = make_int4((int)(v * 4), (int)(v * 4 + 1), (int)(v * 4 + 2), (int)(v * 4 + 3));
+      } else {
+        reinterpret_cast<int2*>(uidx)[v] = make_int2((int)(v * 2), (int)(v * 2 + 1));
+      }
     } else {  // the tail
       for (int64_t j = nv * VN; j < n_g; ++j) {
         T s = (T)0;

@@ -272,10 +272,19 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   const int32_t* cur = a.union_idx;
   const T nf = (T)a.n;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  if (x) {  // harness.cpp:212-215: x[j] -= s_j / n, one thread per union entry
-    for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < K; m += stride) {
-      const int32_t j = cur[m];
-      x[j] = ld_rand(x + j) - div_rn(sums[m], nf);  // one rounding after the division
+  if (x) {  // harness.cpp:212-215: x[j] -= s_j / n; four union entries per thread in flight
+    for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < K; m0 += 4 * stride) {
+      int32_t j[4];
+      T xv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (m0 + q * stride < K) {
+          j[q] = cur[m0 + q * stride];
+          xv[q] = ld_rand(x + j[q]);
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (m0 + q * stride < K) x[j[q]] = xv[q] - div_rn(sums[m0 + q * stride], nf);  // one rounding after /
     }
   }
   if (!dense) return;
