@@ -412,57 +412,74 @@ __global__ void __launch_bounds__(256) k_dense_all(WorkerPtrs w, int n, int64_t 
                                                    T* __restrict__ usum, long long* K) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
+  constexpr int U = 4;  // vectors per thread in flight (the pass is write-heavy: keep loads deep)
   const T nf = (T)n;
   const int64_t nv = n_g / VN;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv + (n_g % VN ? 1 : 0); v += stride) {
-    if (v < nv) {
-      V s, xv;
-      if (x) xv = reinterpret_cast<const V*>(x)[v];  // issued before the residual stores
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += U * stride) {
+    V s[U], xv[U];
+    bool ok[U];
 #pragma unroll
-      for (int c = 0; c < VN; ++c) set_comp(s, c, (T)0);
-      for (int r = 0; r < n; ++r) {
-        V* e = reinterpret_cast<V*>(w.resid[r]) + v;
-        const V a = *e;
+    for (int u = 0; u < U; ++u) {
+      ok[u] = v0 + u * stride < nv;
 #pragma unroll
-        for (int c = 0; c < VN; ++c) set_comp(s, c, add_rn(comp(s, c), comp(a, c)));
-        V z;
+      for (int c = 0; c < VN; ++c) set_comp(s[u], c, (T)0);
+      if (x && ok[u]) xv[u] = ld_stream(reinterpret_cast<const V*>(x) + v0 + u * stride);
+    }
+    for (int r = 0; r < n; ++r) {  // worker order
+      V a[U];
+      V* e = reinterpret_cast<V*>(w.resid[r]);
 #pragma unroll
-        for (int c = 0; c < VN; ++c) set_comp(z, c, (T)0);
-        *e = z;
-      }
-      reinterpret_cast<V*>(usum)[v] = s;
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) a[u] = ld_stream(e + v0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) {
+          V z;
+#pragma unroll
+          for (int c = 0; c < VN; ++c) {
+            set_comp(s[u], c, add_rn(comp(s[u], c), comp(a[u], c)));
+            set_comp(z, c, (T)0);
+          }
+          st_stream(e + v0 + u * stride, z);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      const int64_t v = v0 + u * stride;
+      st_stream(reinterpret_cast<V*>(usum) + v, s[u]);
       V avg;
 #pragma unroll
-      for (int c = 0; c < VN; ++c) set_comp(avg, c, div_rn(comp(s, c), nf));
+      for (int c = 0; c < VN; ++c) set_comp(avg, c, div_rn(comp(s[u], c), nf));
       if (x) {
 #pragma unroll
-        for (int c = 0; c < VN; ++c) set_comp(xv, c, comp(xv, c) - comp(avg, c));
-        reinterpret_cast<V*>(x)[v] = xv;
+        for (int c = 0; c < VN; ++c) set_comp(xv[u], c, comp(xv[u], c) - comp(avg, c));
+        st_stream(reinterpret_cast<V*>(x) + v, xv[u]);
       }
-      if (dense) reinterpret_cast<V*>(dense)[v] = avg;
-      if (VN == 4) {
-        reinterpret_cast<int4*>(uidx)[v] = make_int4((int)(v * 4), (int)(v * 4 + 1), (int)(v * 4 + 2), (int)(v * 4 + 3));
-      } else {
-        reinterpret_cast<int2*>(uidx)[v] = make_int2((int)(v * 2), (int)(v * 2 + 1));
-      }
-    } else {  // the tail
-      for (int64_t j = nv * VN; j < n_g; ++j) {
-        T s = (T)0;
-        for (int r = 0; r < n; ++r) {
-          T* e = (T*)w.resid[r] + j;
-          s = add_rn(s, *e);
-          *e = (T)0;
-        }
-        usum[j] = s;
-        const T avg = div_rn(s, nf);
-        if (x) x[j] = x[j] - avg;
-        if (dense) dense[j] = avg;
-        uidx[j] = (int32_t)j;
-      }
+      if (dense) st_stream(reinterpret_cast<V*>(dense) + v, avg);
+      if (VN == 4)
+        __stcs(reinterpret_cast<int4*>(uidx) + v, make_int4((int)(v * 4), (int)(v * 4 + 1), (int)(v * 4 + 2), (int)(v * 4 + 3)));
+      else
+        __stcs(reinterpret_cast<int2*>(uidx) + v, make_int2((int)(v * 2), (int)(v * 2 + 1)));
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *K = n_g;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the n_g % VN tail, and K
+    for (int64_t j = nv * VN; j < n_g; ++j) {
+      T s = (T)0;
+      for (int r = 0; r < n; ++r) {
+        T* e = (T*)w.resid[r] + j;
+        s = add_rn(s, *e);
+        *e = (T)0;
+      }
+      usum[j] = s;
+      const T avg = div_rn(s, nf);
+      if (x) x[j] = x[j] - avg;
+      if (dense) dense[j] = avg;
+      uidx[j] = (int32_t)j;
+    }
+    *K = n_g;
+  }
 }
 
 }  // namespace micro
