@@ -308,13 +308,37 @@ __global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, cons
 template <typename T>
 __global__ void __launch_bounds__(256) k_accumulate_probe(T* __restrict__ e, const T* __restrict__ g, double eta_d,
                                                           int64_t n_g, int* flags) {
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N;
+  constexpr int U = 4;  // vectors per thread in flight
   const T eta = (T)eta_d;
   T probe = (T)0;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_g; j += (int64_t)gridDim.x * blockDim.x) {
-    const T gv = g[j];
-    probe = probe + gv * (T)0;
-    e[j] = add_rn(e[j], mul_rn(eta, gv));
+  const int64_t nv = n_g / VN;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v0 < nv; v0 += U * stride) {
+    V ev[U], gv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v0 + u * stride < nv) {
+        ev[u] = ld_stream(reinterpret_cast<const V*>(e) + v0 + u * stride);
+        gv[u] = ld_nc_stream(reinterpret_cast<const V*>(g) + v0 + u * stride);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (v0 + u * stride < nv) {
+#pragma unroll
+        for (int c = 0; c < VN; ++c) {
+          probe = probe + comp(gv[u], c) * (T)0;
+          set_comp(ev[u], c, add_rn(comp(ev[u], c), mul_rn(eta, comp(gv[u], c))));
+        }
+        st_stream(reinterpret_cast<V*>(e) + v0 + u * stride, ev[u]);
+      }
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (int64_t j = nv * VN; j < n_g; ++j) {
+      probe = probe + g[j] * (T)0;
+      e[j] = add_rn(e[j], mul_rn(eta, g[j]));
+    }
   if (probe != probe) atomicOr(flags, 1);
 }
 

@@ -114,15 +114,25 @@ __global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_
   const int32_t* __restrict__ idx = all_idx + (int64_t)o * kmax;
   T* __restrict__ out = send + c.off[o];
   double q = 0.0;
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
-       m += (long long)gridDim.x * blockDim.x) {
-    const int32_t j = idx[m];
-    const T v = resid[j];
-    out[m] = v;
-    if (kZero) {
-      resid[j] = (T)0;
-      q += (double)v * (double)v;
-    }
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 4 * stride) {
+    int32_t j[4];
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (m0 + u * stride < k) j[u] = idx[m0 + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)  // four random reads in flight
+      if (m0 + u * stride < k) v[u] = ld_rand(resid + j[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (m0 + u * stride < k) {
+        out[m0 + u * stride] = v[u];
+        if (kZero) {
+          resid[j[u]] = (T)0;
+          q += (double)v[u] * (double)v[u];
+        }
+      }
   }
   if (kZero && sq_corr) {  // squares of the zeroed entries (error norm, see k_cluster_reduce)
     q = warp_sum_f64(q);

@@ -145,14 +145,25 @@ __global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me,
   const int32_t* __restrict__ idx = p.sel_idx[o];
   T* __restrict__ out = (T*)p.recv[o] + (long long)me * cap;
   double q = 0.0;
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
-    const int32_t j = idx[m];
-    const T v = ld_rand(resid + j);
-    out[m] = v;
-    if (kZero) {
-      resid[j] = (T)0;
-      q += (double)v * (double)v;
-    }
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 4 * stride) {
+    int32_t j[4];
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)  // four index reads (remote, coalesced) in flight
+      if (m0 + u * stride < k) j[u] = idx[m0 + u * stride];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)  // four local gathers in flight
+      if (m0 + u * stride < k) v[u] = ld_rand(resid + j[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (m0 + u * stride < k) {
+        out[m0 + u * stride] = v[u];
+        if (kZero) {
+          resid[j[u]] = (T)0;
+          q += (double)v[u] * (double)v[u];
+        }
+      }
   }
   if (kZero && corr) {  // squares of the entries zeroed here (error norm)
     q = warp_sum_f64(q);

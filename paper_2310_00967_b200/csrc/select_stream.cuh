@@ -414,14 +414,15 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   T* __restrict__ ov = (T*)a.sel_val + off;
   const long long room = a.cap - off;
   T* __restrict__ x = (T*)a.model;
-  // four entries per lane in flight: at high density a run holds hundreds of
+  // kG entries per lane in flight: at high density a run holds hundreds of
   // pairs and the model's random read-modify-write is latency bound
+  constexpr int kG = 8;
   const int lim = n < room ? n : (int)room;
-  for (int m0 = lane; m0 < lim; m0 += 128) {
-    int32_t j[4];
-    T v[4], xv[4];
+  for (int m0 = lane; m0 < lim; m0 += 32 * kG) {
+    int32_t j[kG];
+    T v[kG], xv[kG];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kG; ++q) {
       const int m = m0 + 32 * q;
       if (m < lim) {
         j[q] = si[m];
@@ -432,10 +433,10 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     }
     if (x) {  // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kG; ++q)
         if (m0 + 32 * q < lim) xv[q] = ld_rand(x + j[q]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kG; ++q)
         if (m0 + 32 * q < lim) x[j[q]] = xv[q] - v[q];
     }
   }
