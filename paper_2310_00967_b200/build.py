@@ -16,8 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmicro_b200.so")
-SOURCES = ["api.cu"]
-HEADERS = ["common.cuh", "norm.cuh", "select.cuh", "select_tma.cuh", "select_stream.cuh", "exchange.cuh", "peer.cuh"]
+SOURCES = ["api.cu", "dist_api.cu", "value_api.cu"]
+HEADERS = ["internal.cuh", "baselines.cuh", "common.cuh", "norm.cuh", "select.cuh", "select_tma.cuh", "select_stream.cuh", "exchange.cuh", "peer.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",

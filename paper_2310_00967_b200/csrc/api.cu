@@ -1,39 +1,18 @@
-// api.cu — the C ABI (include/micro.h): host-side engine around the sm_100a
-// kernels of select.cuh / exchange.cuh.  No CPU compute path exists: every
-// array operation below is a device kernel; the host only validates, sizes
-// launches and moves small scalars.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include "../../include/micro.h"
-#include "../../include/micro_synth.h"
-#include "exchange.cuh"
-#include "peer.cuh"
-#include "baselines.cuh"
-#include "select.cuh"
-#include "select_tma.cuh"
-#include "select_stream.cuh"
-
-using namespace micro;
+// api.cu — the C ABI's engine half (include/micro.h): the MiCRO context,
+// K1 launch plumbing, the single-device cluster, the comparison sparsifiers
+// and the host-side bookkeeping around the sm_100a kernels.  No CPU compute
+// path exists: every array operation is a device kernel; the host only
+// validates, sizes launches and moves small scalars.
+// (dist_api.cu: one rank of an n-GPU job; value_api.cu: stateless calls.)
+#include "internal.cuh"
 
 // ---------------------------------------------------------------- errors --
 
-namespace {
+namespace micro {
+namespace host {
 
 thread_local std::string g_err;
 
-int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -43,35 +22,6 @@ int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
-
-#define CU(call)                                                                           \
-  do {                                                                                     \
-    cudaError_t _e = (call);                                                               \
-    if (_e != cudaSuccess)                                                                 \
-      return fail(MICRO_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
-                  __LINE__);                                                               \
-  } while (0)
-
-#define TRY(call)                  \
-  do {                             \
-    int _rc = (call);              \
-    if (_rc != MICRO_OK) return _rc; \
-  } while (0)
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
-
-size_t dtype_size(int dtype) { return dtype == MICRO_F64 ? 8 : 4; }
 
 int check_dtype(int dtype) {
   if (dtype != MICRO_F32 && dtype != MICRO_F64) return fail(MICRO_EINVAL, "unknown dtype %d", dtype);
@@ -130,140 +80,101 @@ int h_update_threshold(double* delta, uint64_t k_target, uint64_t k_sel, double 
   return MICRO_OK;
 }
 
-constexpr int64_t kHistCap = 4096;
-constexpr int kTimingCap = 1024;
 
-template <typename T>
-int64_t p_max_for(int64_t range) {
-  return (range + tile_elems<T>() - 1) / tile_elems<T>() + 2;
+
+int read_flags(micro_ctx* c, int* flags) {
+  CU(cudaMemcpyAsync(flags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  if (*flags & 1) c->poisoned = true;
+  return MICRO_OK;
 }
 
-}  // namespace
+unsigned grid_for(int64_t work, int dev) {
+  const int64_t b = (work + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 8 * num_sms(dev)));
+}
 
-// ------------------------------------------------------------ the context --
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 
-struct micro_ctx {
-  micro_config cfg{};
-  int dev = 0;
-  cudaStream_t stream = nullptr;
-  int n = 1, n_local = 1;
-  int64_t n_g = 0;
-  size_t esz = 4;
-  uint64_t k_worker = 0;
-  int64_t sel_cap = 0, uni_cap = 0;
-  bool cluster = true;  // n_local == n
-  // per local worker
-  std::vector<void*> resid;
-  std::vector<int32_t*> sel_idx[2];
-  std::vector<void*> sel_val[2];
-  long long* counts = nullptr;    // n_local
-  double* delta = nullptr;        // n_local
-  // union (n > 1), double-buffered for the dense sparse-clear
-  int32_t* uni_idx[2] = {nullptr, nullptr};
-  void* uni_sum[2] = {nullptr, nullptr};
-  long long* Kbuf = nullptr;      // [2]
-  void* dense = nullptr;
-  void* model = nullptr;
-  // K1 workspace
-  unsigned long long* status = nullptr;
-  int64_t p_max = 0;
-  int64_t status_len = 0;       // allocated look-back words
-  int64_t status_hwm = 0;       // highest look-back index any launch has used
-  // K1 implementation (MICRO_K1_KERNEL): 0 "stream" k1_stream + k1_compact (default),
-  // 1 "tma" persistent k1_tma_select, 2 "tile" k1_fused_select (also the
-  // fallback for gradients that are not 16-byte aligned)
-  int k1_kind = 0;
-  bool use_tma = true;  // staging buffers allocated
-  int k1_cfg = 0;               // streaming configuration (MICRO_K1_CFG)
-  int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
-  void* stage_val = nullptr;
-  int* unit_counts = nullptr;    // selections per K1 unit / per k1_stream CTA run
-  // k1_stream -> k1_gather: selections per super block of super_runs CTA
-  // runs, two parities (a launch zeroes the other one for the next launch)
-  int* super_counts = nullptr;
-  int super_runs = 8;
-  int super_par = 0;
-  unsigned int* ticket = nullptr;
-  unsigned int epoch = 0;
-  int* flags = nullptr;
-  // history
-  long long *hist_t = nullptr, *hist_K = nullptr, *hist_counts = nullptr;
-  double* hist_delta = nullptr;
-  double* hist_err = nullptr;
-  // error norm (record_error_norm, EF on): ||e_{t+1}||^2 per worker, fused into K1
-  bool norm = false;
-  int64_t norm_ctas = 0;               // slots for the largest producing grid
-  double* norm_part = nullptr;
-  double* norm_group = nullptr;
-  unsigned* norm_ticket = nullptr;     // norm_groups + 1
-  double* norm_sq = nullptr;           // n_local
-  double* norm_corr = nullptr;         // n_local: squares of foreign entries zeroed by the exchange
-  // host-side step state
-  int64_t steps = 0;      // completed aggregations
-  int64_t t_cur = -1;     // iteration of the pending/last compress
-  int buf = 0;            // buffer parity of the pending/last step
-  bool compressed = false;
-  bool poisoned = false;
-  bool ever_stepped = false;
-  void* staging = nullptr;  // gradient staging (lazy): host inputs, unaligned device inputs
-  size_t staging_stride = 0;  // bytes per worker row (256-byte aligned)
-  // the previous union's dense clear runs on `aux`, overlapping K1 (fork at
-  // compress, join before finalize)
-  cudaStream_t aux = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  bool clear_pending = false;
-  // n = 1 with the streaming K1: the dense g/n is maintained inside K1
-  // (k1_stream<..., kDense>) with one dirty bit per 32-byte sector
-  bool dense_fused = false;
-  // micro_step on a one-worker cluster with the streaming K1: k1_gather's
-  // block 0 does the threshold update + history (no k_finalize launch)
-  bool fuse_step = false;   // set for the duration of micro_step
-  bool fin_done = false;    // this step's finalize already ran inside k1_gather
-  // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
-  bool timing = false;
-  int t_next = 0;
-  std::vector<cudaEvent_t> t_ev;
-  unsigned long long* dense_dirty = nullptr;
-  std::vector<void*> allocs;
-  // comparison sparsifiers (micro_config.sparsifier, baselines.cuh)
-  int kind = 0;                 // 0 MiCRO, 1 top-k, 2 CLT-k, 3 hard threshold, 4 dense
-  bool vectors_done = false;    // this step's model / dense g/n already written (dense kind)
-  bool sel_is_union = false;    // n = 1 MiCRO: the union is worker 0's selection
-  uint64_t k_global = 0;
-  TopkState* topk = nullptr;    // n_local
-  unsigned* topk_hist = nullptr;
-  unsigned* tie_counts = nullptr;
-  unsigned* bitmap = nullptr;   // union of overlapping selections
-  int* word_pc = nullptr;
-  int* word_off = nullptr;
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
-  int64_t nwords = 0;
-  double* minus_one = nullptr;  // threshold that selects everything (k >= n_g)
-  // peer-memory exchange (micro_peer_*): every rank's buffers mapped here
-  bool peer_ready = false;
-  const long long* peer_counts[kMaxWorkers] = {};
-  void* peer_resid[kMaxWorkers] = {};
-  int32_t* peer_uidx[2][kMaxWorkers] = {};
-  void* peer_usum[2][kMaxWorkers] = {};
-  double* peer_corr[kMaxWorkers] = {};
-  const int32_t* peer_sel[2][kMaxWorkers] = {};
-  void* peer_recv[kMaxWorkers] = {};
-  void* recv = nullptr;          // bulk exchange: receive slabs [source rank][sel_cap] (lazy)
-  int peer_phase = 0;            // 0 idle, 1 contributed (bulk), 2 exchanged (ready to finalize)
-  std::vector<void*> peer_opened;  // cudaIpcOpenMemHandle mappings to close
 
-  int alloc(void** p, size_t bytes) {
-    if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMalloc(p, bytes);
-    if (e != cudaSuccess)
-      return fail(MICRO_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
-    allocs.push_back(*p);
-    return MICRO_OK;
+int finalize_blocks(micro_ctx* c) {
+  const int64_t want = ((int64_t)c->k_worker * c->n * 3 / 2 + 255) / 256;
+  return (int)std::min<int64_t>(std::max<int64_t>(want, 1), 64 * num_sms(c->dev));
+}
+
+template <typename T>
+int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_from_counts) {
+  FinalizeArgs f{};
+  f.n = c->n;
+  f.n_local = c->n_local;
+  f.n_g = c->n_g;
+  f.t = c->t_cur;
+  f.counts = c->counts;
+  f.delta = c->delta;
+  f.k_target = c->k_worker;
+  f.alpha = c->cfg.scaling_factor;
+  f.min_threshold = c->cfg.min_threshold;
+  f.k_from_counts = k_from_counts;
+  f.cap = c->sel_cap;
+  f.K = c->Kbuf + c->buf;
+  f.union_idx = uidx;
+  f.union_sum = usum;
+  const int pb = c->buf ^ 1;
+  if (c->ever_stepped && c->dense && !c->dense_fused) {
+    f.prev_idx = c->sel_is_union ? c->sel_idx[pb][0] : c->uni_idx[pb];
+    f.prev_K = c->Kbuf + pb;
   }
-};
+  f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
+  // n = 1 with the streaming K1: k1_gather applied the model update
+  f.model = (c->sel_is_union && c->k1_kind == 0) ? nullptr : c->model;
+  f.update_delta = c->kind == 0;
+  if (c->vectors_done) {  // k_dense_all wrote the model and the dense g/n
+    f.model = nullptr;
+    f.dense = nullptr;
+    f.prev_idx = nullptr;
+    c->vectors_done = false;
+  }
+  f.slot = c->steps % kHistCap;
+  f.hist_t = c->hist_t;
+  f.hist_K = c->hist_K;
+  f.hist_counts = c->hist_counts;
+  f.hist_delta = c->hist_delta;
+  f.hist_err = c->hist_err;
+  f.norm_mode = norm_mode(c);
+  f.sq = c->norm_sq;
+  f.sq_corr = (c->n > 1 && c->kind == 0) ? c->norm_corr : nullptr;
+  const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
+  if (c->fin_done) {
+    // k1_gather already did the threshold update + history (n = 1, micro_step);
+    // dense (fused into K1) and model (k1_gather) are done too
+    c->fin_done = false;
+  } else {
+    if (c->clear_pending) {
+      CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+      c->clear_pending = false;
+    } else if (f.prev_idx) {
+      k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
+      CU(cudaGetLastError());
+    }
+    k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
+    CU(cudaGetLastError());
+  }
+  if (!c->cfg.error_feedback && c->n > 1)
+    for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
+  c->steps++;
+  c->ever_stepped = true;
+  c->compressed = false;
+  return MICRO_OK;
+}
 
-namespace {
+template int launch_finalize<float>(micro_ctx*, const int32_t*, const void*, int);
+template int launch_finalize<double>(micro_ctx*, const int32_t*, const void*, int);
+
+
 
 int check_ctx(micro_ctx* c) {
   if (!c) return fail(MICRO_EINVAL, "null context");
@@ -288,6 +199,11 @@ int check_poison(micro_ctx* c) {
                 (long long)c->t_cur);
   return MICRO_OK;
 }
+
+}  // namespace host
+}  // namespace micro
+
+namespace {
 
 // K1 streaming configurations (warps, stages, unit bytes); MICRO_K1_CFG picks one.
 using K1Cfg0 = WsCfg<8, 4, 2048>;
@@ -321,7 +237,6 @@ SumSqSlots norm_slots(micro_ctx* c, int i) {
   return q;
 }
 
-int norm_mode(const micro_ctx* c) { return !c->cfg.error_feedback ? 2 : c->norm ? 1 : 0; }
 
 // ||resid_i||^2 by a standalone pass (K1 variants without the fused sum).
 template <typename T>
@@ -507,8 +422,6 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   return MICRO_OK;
 }
 
-unsigned grid_for(int64_t work, int dev);
-constexpr int kTieChunks = 65536;
 
 // One worker of a comparison sparsifier (harness.cpp:152-181).
 template <typename T>
@@ -606,77 +519,7 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   return c->norm ? launch_sumsq<T>(c, i) : MICRO_OK;
 }
 
-int finalize_blocks(micro_ctx* c);
 
-template <typename T>
-int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_from_counts) {
-  FinalizeArgs f{};
-  f.n = c->n;
-  f.n_local = c->n_local;
-  f.n_g = c->n_g;
-  f.t = c->t_cur;
-  f.counts = c->counts;
-  f.delta = c->delta;
-  f.k_target = c->k_worker;
-  f.alpha = c->cfg.scaling_factor;
-  f.min_threshold = c->cfg.min_threshold;
-  f.k_from_counts = k_from_counts;
-  f.cap = c->sel_cap;
-  f.K = c->Kbuf + c->buf;
-  f.union_idx = uidx;
-  f.union_sum = usum;
-  const int pb = c->buf ^ 1;
-  if (c->ever_stepped && c->dense && !c->dense_fused) {
-    f.prev_idx = c->sel_is_union ? c->sel_idx[pb][0] : c->uni_idx[pb];
-    f.prev_K = c->Kbuf + pb;
-  }
-  f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
-  // n = 1 with the streaming K1: k1_gather applied the model update
-  f.model = (c->sel_is_union && c->k1_kind == 0) ? nullptr : c->model;
-  f.update_delta = c->kind == 0;
-  if (c->vectors_done) {  // k_dense_all wrote the model and the dense g/n
-    f.model = nullptr;
-    f.dense = nullptr;
-    f.prev_idx = nullptr;
-    c->vectors_done = false;
-  }
-  f.slot = c->steps % kHistCap;
-  f.hist_t = c->hist_t;
-  f.hist_K = c->hist_K;
-  f.hist_counts = c->hist_counts;
-  f.hist_delta = c->hist_delta;
-  f.hist_err = c->hist_err;
-  f.norm_mode = norm_mode(c);
-  f.sq = c->norm_sq;
-  f.sq_corr = (c->n > 1 && c->kind == 0) ? c->norm_corr : nullptr;
-  const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
-  if (c->fin_done) {
-    // k1_gather already did the threshold update + history (n = 1, micro_step);
-    // dense (fused into K1) and model (k1_gather) are done too
-    c->fin_done = false;
-  } else {
-    if (c->clear_pending) {
-      CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-      c->clear_pending = false;
-    } else if (f.prev_idx) {
-      k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
-      CU(cudaGetLastError());
-    }
-    k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
-    CU(cudaGetLastError());
-  }
-  if (!c->cfg.error_feedback && c->n > 1)
-    for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
-  c->steps++;
-  c->ever_stepped = true;
-  c->compressed = false;
-  return MICRO_OK;
-}
-
-int finalize_blocks(micro_ctx* c) {
-  const int64_t want = ((int64_t)c->k_worker * c->n * 3 / 2 + 255) / 256;
-  return (int)std::min<int64_t>(std::max<int64_t>(want, 1), 64 * num_sms(c->dev));
-}
 
 // Clear the previous union's sectors of the dense g/n on the aux stream, so
 // the (small, latency-bound) clear overlaps the HBM-bound K1.
@@ -828,65 +671,6 @@ int reset_state(micro_ctx* c) {
   return MICRO_OK;
 }
 
-int read_flags(micro_ctx* c, int* flags) {
-  CU(cudaMemcpyAsync(flags, c->flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  if (*flags & 1) c->poisoned = true;
-  return MICRO_OK;
-}
-
-template <typename T>
-__global__ void k_synth(uint64_t seed, uint32_t worker, uint64_t t, int64_t n, T* out) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q * 4 >= n) return;
-  float z[4];
-  ms_gaussian4(seed, worker, t, (uint64_t)q, z);
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-    if (q * 4 + c < n) out[q * 4 + c] = (T)z[c];
-}
-
-template <typename T>
-__global__ void k_accumulate(const T* e, T eta, const T* g, T* acc, int64_t n) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x)
-    acc[j] = add_rn(e[j], mul_rn(eta, g[j]));
-}
-
-template <typename T>
-__global__ void k_compensate(T* acc, int64_t n_g, const int32_t* idx, int64_t k, int* bad) {
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < k;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t j = idx[m];
-    if (j < 0 || j >= n_g) atomicOr(bad, 1);
-    else acc[j] = (T)0;
-  }
-}
-
-template <typename T>
-__global__ void k_reduce_values(WorkerPtrs w, int n, int64_t n_g, const int32_t* uidx, int64_t K,
-                                T* sums, T* dense, int* bad) {
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < K;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t j = uidx[m];
-    if (j < 0 || j >= n_g) { atomicOr(bad, 1); continue; }
-    T s = (T)0;
-    for (int r = 0; r < n; ++r) s = add_rn(s, ((const T*)w.sel_val[r])[j]);
-    if (sums) sums[m] = s;
-    if (dense) dense[j] = s;
-  }
-}
-
-unsigned grid_for(int64_t work, int dev) {
-  const int64_t b = (work + 255) / 256;
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, 8 * num_sms(dev)));
-}
-
-int current_device() {
-  int d = 0;
-  cudaGetDevice(&d);
-  return d;
-}
 
 }  // namespace
 
@@ -1391,623 +1175,5 @@ int micro_copy_dense(micro_ctx* c, void* h) {
 }
 
 // ---- one rank of a multi-GPU job ----
-
-static int dist_counts(micro_ctx* c, const int64_t* h_counts, Counts* out, bool own_segments) {
-  if (!h_counts) return fail(MICRO_EINVAL, "null counts");
-  long long off = 0;
-  const int me = c->cfg.rank;
-  for (int r = 0; r < c->n; ++r) {
-    if (h_counts[r] < 0) return fail(MICRO_EINVAL, "negative count");
-    out->k[r] = h_counts[r];
-    out->off[r] = off;
-    // send layout: segment o has k_o values (o != me); recv layout: segment r has k_me values
-    if (r != me) off += own_segments ? h_counts[me] : h_counts[r];
-  }
-  return MICRO_OK;
-}
-
-int micro_dist_gather_foreign(micro_ctx* c, const int32_t* d_all_idx, const int64_t* h_counts,
-                              int64_t kmax, void* d_send) {
-  TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
-  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_gather_foreign before micro_compress");
-  Counts cs{};
-  TRY(dist_counts(c, h_counts, &cs, false));
-  DeviceGuard dg(c->dev);
-  long long mx = 0;
-  for (int r = 0; r < c->n; ++r) mx = std::max<long long>(mx, cs.k[r]);
-  if (mx > kmax) return fail(MICRO_EINVAL, "kmax %lld smaller than a count %lld", (long long)kmax, mx);
-  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
-  double* corr = c->norm ? c->norm_corr : nullptr;
-  if (c->esz == 4) {
-    if (c->cfg.error_feedback)
-      k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                      (float*)c->resid[0], (float*)d_send, corr);
-    else
-      k_dist_gather_foreign<float, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                       (float*)c->resid[0], (float*)d_send, corr);
-  } else {
-    if (c->cfg.error_feedback)
-      k_dist_gather_foreign<double, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                       (double*)c->resid[0], (double*)d_send, corr);
-    else
-      k_dist_gather_foreign<double, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                        (double*)c->resid[0], (double*)d_send, corr);
-  }
-  CU(cudaGetLastError());
-  return MICRO_OK;
-}
-
-int micro_dist_owner_reduce(micro_ctx* c, const void* d_recv, const int64_t* h_counts, void* d_own_sums) {
-  TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
-  Counts cs{};
-  TRY(dist_counts(c, h_counts, &cs, true));
-  DeviceGuard dg(c->dev);
-  const int me = c->cfg.rank;
-  const long long k = cs.k[me];
-  const unsigned grid = grid_for(k, c->dev);
-  if (c->esz == 4)
-    k_dist_owner_reduce<float><<<grid, 256, 0, c->stream>>>((const float*)c->sel_val[c->buf][0], k,
-                                                            (const float*)d_recv, cs, c->n, me, (float*)d_own_sums);
-  else
-    k_dist_owner_reduce<double><<<grid, 256, 0, c->stream>>>((const double*)c->sel_val[c->buf][0], k,
-                                                             (const double*)d_recv, cs, c->n, me,
-                                                             (double*)d_own_sums);
-  CU(cudaGetLastError());
-  return MICRO_OK;
-}
-
-// ---- peer-memory exchange (peer.cuh) ------------------------------------
-namespace {
-constexpr int kPeerBufs = 10;  // resid, counts, uidx x2, usum x2, norm corr, sel_idx x2, recv
-static_assert(MICRO_PEER_HANDLE_BYTES == kPeerBufs * sizeof(cudaIpcMemHandle_t), "handle layout");
-
-void* peer_buf(micro_ctx* c, int b) {
-  switch (b) {
-    case 0: return c->resid[0];
-    case 1: return c->counts;
-    case 2: return c->uni_idx[0];
-    case 3: return c->uni_idx[1];
-    case 4: return c->uni_sum[0];
-    case 5: return c->uni_sum[1];
-    case 6: return c->norm ? c->norm_corr : nullptr;
-    case 7: return c->sel_idx[0][0];
-    case 8: return c->sel_idx[1][0] != c->sel_idx[0][0] ? c->sel_idx[1][0] : nullptr;  // single-buffered
-    default: return c->recv;
-  }
-}
-
-int check_peer_ctx(micro_ctx* c) {
-  TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster || c->n_local != 1 || c->n < 2)
-    return fail(MICRO_ELOGIC, "micro_peer_*: needs a rank context (n_local = 1 of n > 1 workers)");
-  return MICRO_OK;
-}
-}  // namespace
-
-int micro_peer_export(micro_ctx* c, void* out) {
-  TRY(check_peer_ctx(c));
-  if (!out) return fail(MICRO_EINVAL, "null handle buffer");
-  DeviceGuard dg(c->dev);
-  if (!c->recv) TRY(c->alloc(&c->recv, (size_t)c->n * c->sel_cap * c->esz));
-  auto* h = (cudaIpcMemHandle_t*)out;
-  for (int b = 0; b < kPeerBufs; ++b) {
-    std::memset(&h[b], 0, sizeof h[b]);
-    if (void* p = peer_buf(c, b)) CU(cudaIpcGetMemHandle(&h[b], p));
-  }
-  return MICRO_OK;
-}
-
-int micro_peer_import(micro_ctx* c, const void* all) {
-  TRY(check_peer_ctx(c));
-  if (!all) return fail(MICRO_EINVAL, "null handle array");
-  if (c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_import called twice");
-  DeviceGuard dg(c->dev);
-  const auto* h = (const cudaIpcMemHandle_t*)all;
-  const int me = c->cfg.rank;
-  static const cudaIpcMemHandle_t zero{};
-  for (int r = 0; r < c->n; ++r) {
-    void* p[kPeerBufs] = {};
-    for (int b = 0; b < kPeerBufs; ++b) {
-      if (r == me) {
-        p[b] = peer_buf(c, b);
-        continue;
-      }
-      const cudaIpcMemHandle_t& hb = h[(size_t)r * kPeerBufs + b];
-      if (std::memcmp(&hb, &zero, sizeof zero) == 0) continue;
-      CU(cudaIpcOpenMemHandle(&p[b], hb, cudaIpcMemLazyEnablePeerAccess));
-      c->peer_opened.push_back(p[b]);
-    }
-    if (!p[8]) p[8] = p[7];  // the rank's selection is single-buffered
-    if (!p[0] || !p[1] || !p[2] || !p[3] || !p[4] || !p[5] || !p[7] || !p[9])
-      return fail(MICRO_EINVAL, "rank %d exported incomplete handles", r);
-    if (c->norm && !p[6]) return fail(MICRO_EINVAL, "rank %d does not record the error norm", r);
-    c->peer_resid[r] = p[0];
-    c->peer_counts[r] = (const long long*)p[1];
-    c->peer_uidx[0][r] = (int32_t*)p[2];
-    c->peer_uidx[1][r] = (int32_t*)p[3];
-    c->peer_usum[0][r] = p[4];
-    c->peer_usum[1][r] = p[5];
-    c->peer_corr[r] = c->norm ? (double*)p[6] : nullptr;
-    c->peer_sel[0][r] = (const int32_t*)p[7];
-    c->peer_sel[1][r] = (const int32_t*)p[8];
-    c->peer_recv[r] = p[9];
-  }
-  c->peer_ready = true;
-  return MICRO_OK;
-}
-
-int micro_peer_exchange(micro_ctx* c) {
-  TRY(check_peer_ctx(c));
-  if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_peer_import");
-  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_compress");
-  if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_exchange called twice");
-  DeviceGuard dg(c->dev);
-  PeerPtrs pp{};
-  for (int r = 0; r < c->n; ++r) {
-    pp.counts[r] = c->peer_counts[r];
-    pp.resid[r] = c->peer_resid[r];
-    pp.uidx[r] = c->peer_uidx[c->buf][r];
-    pp.usum[r] = c->peer_usum[c->buf][r];
-    pp.corr[r] = c->peer_corr[r];
-  }
-  // sized for the expected selection (the kernel reads the actual count)
-  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
-  const int me = c->cfg.rank;
-  const bool ef = c->cfg.error_feedback != 0;
-  long long* Kout = c->Kbuf + c->buf;
-  if (c->esz == 4) {
-    const float* v = (const float*)c->sel_val[c->buf][0];
-    if (ef) k_peer_exchange<float, true><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
-                                                                      c->sel_idx[c->buf][0], v, Kout);
-    else k_peer_exchange<float, false><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
-                                                                     c->sel_idx[c->buf][0], v, Kout);
-  } else {
-    const double* v = (const double*)c->sel_val[c->buf][0];
-    if (ef) k_peer_exchange<double, true><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
-                                                                       c->sel_idx[c->buf][0], v, Kout);
-    else k_peer_exchange<double, false><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
-                                                                      c->sel_idx[c->buf][0], v, Kout);
-  }
-  CU(cudaGetLastError());
-  c->peer_phase = 2;
-  return MICRO_OK;
-}
-
-PeerBulkPtrs bulk_ptrs(micro_ctx* c) {
-  PeerBulkPtrs pb{};
-  for (int r = 0; r < c->n; ++r) {
-    pb.counts[r] = c->peer_counts[r];
-    pb.sel_idx[r] = c->peer_sel[c->buf][r];
-    pb.recv[r] = c->peer_recv[r];
-    pb.uidx[r] = c->peer_uidx[c->buf][r];
-    pb.usum[r] = c->peer_usum[c->buf][r];
-  }
-  return pb;
-}
-
-int micro_peer_contribute(micro_ctx* c) {
-  TRY(check_peer_ctx(c));
-  if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_contribute before micro_peer_import");
-  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_contribute before micro_compress");
-  if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_contribute called twice");
-  DeviceGuard dg(c->dev);
-  const PeerBulkPtrs pb = bulk_ptrs(c);
-  const dim3 grid(grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev) / 2 + 1, c->n);
-  double* corr = c->norm ? c->norm_corr : nullptr;
-  const int me = c->cfg.rank;
-  if (c->esz == 4) {
-    if (c->cfg.error_feedback)
-      k_peer_contribute<float, true><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (float*)c->resid[0], corr);
-    else
-      k_peer_contribute<float, false><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (float*)c->resid[0], corr);
-  } else {
-    if (c->cfg.error_feedback)
-      k_peer_contribute<double, true><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (double*)c->resid[0], corr);
-    else
-      k_peer_contribute<double, false><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (double*)c->resid[0], corr);
-  }
-  CU(cudaGetLastError());
-  c->peer_phase = 1;
-  return MICRO_OK;
-}
-
-int micro_peer_reduce(micro_ctx* c) {
-  TRY(check_peer_ctx(c));
-  if (c->peer_phase != 1) return fail(MICRO_ELOGIC, "micro_peer_reduce before micro_peer_contribute");
-  DeviceGuard dg(c->dev);
-  const PeerBulkPtrs pb = bulk_ptrs(c);
-  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
-  long long* Kout = c->Kbuf + c->buf;
-  if (c->esz == 4)
-    k_peer_reduce_push<float><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,
-                                                           c->sel_idx[c->buf][0],
-                                                           (const float*)c->sel_val[c->buf][0], Kout);
-  else
-    k_peer_reduce_push<double><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,
-                                                            c->sel_idx[c->buf][0],
-                                                            (const double*)c->sel_val[c->buf][0], Kout);
-  CU(cudaGetLastError());
-  c->peer_phase = 2;
-  return MICRO_OK;
-}
-
-int micro_peer_finalize(micro_ctx* c) {
-  TRY(check_peer_ctx(c));
-  if (c->peer_phase != 2) return fail(MICRO_ELOGIC, "micro_peer_finalize before the exchange");
-  DeviceGuard dg(c->dev);
-  c->peer_phase = 0;
-  if (c->esz == 4) return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-}
-
-int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_all_sums,
-                        const int64_t* h_counts, int64_t kmax) {
-  TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
-  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_finalize before micro_compress");
-  Counts cs{};
-  TRY(dist_counts(c, h_counts, &cs, false));
-  long long K = 0, mx = 0;
-  for (int r = 0; r < c->n; ++r) {
-    K += cs.k[r];
-    mx = std::max<long long>(mx, cs.k[r]);
-  }
-  if (K > c->uni_cap) return fail(MICRO_ECAPACITY, "union %lld exceeds capacity %lld", K, (long long)c->uni_cap);
-  DeviceGuard dg(c->dev);
-  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
-  if (c->esz == 4) {
-    k_dist_build_union<float><<<grid, 256, 0, c->stream>>>(d_all_idx, (const float*)d_all_sums, kmax, cs, c->n,
-                                                           c->t_cur, c->uni_idx[c->buf],
-                                                           (float*)c->uni_sum[c->buf], c->Kbuf + c->buf);
-    CU(cudaGetLastError());
-    return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-  }
-  k_dist_build_union<double><<<grid, 256, 0, c->stream>>>(d_all_idx, (const double*)d_all_sums, kmax, cs, c->n,
-                                                          c->t_cur, c->uni_idx[c->buf],
-                                                          (double*)c->uni_sum[c->buf], c->Kbuf + c->buf);
-  CU(cudaGetLastError());
-  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-}
-
-// ---- device memory plumbing ----
-
-int micro_device_count(int* count) {
-  if (!count) return fail(MICRO_EINVAL, "null count");
-  CU(cudaGetDeviceCount(count));
-  return MICRO_OK;
-}
-
-int micro_device_malloc(void** d, int64_t bytes, int device) {
-  if (!d || bytes < 0) return fail(MICRO_EINVAL, "bad allocation request");
-  *d = nullptr;
-  DeviceGuard dg(device);
-  cudaError_t e = cudaMalloc(d, bytes ? (size_t)bytes : 16);
-  if (e != cudaSuccess) return fail(MICRO_ENOMEM, "cudaMalloc(%lld): %s", (long long)bytes, cudaGetErrorString(e));
-  return MICRO_OK;
-}
-
-int micro_device_free(void* d) {
-  if (d) CU(cudaFree(d));
-  return MICRO_OK;
-}
-
-int micro_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
-  if (bytes < 0 || kind < 0 || kind > 2) return fail(MICRO_EINVAL, "bad copy request");
-  if (!bytes) return MICRO_OK;
-  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost
-                                                                          : cudaMemcpyDeviceToDevice;
-  CU(cudaMemcpyAsync(dst, src, (size_t)bytes, k, (cudaStream_t)stream));
-  CU(cudaStreamSynchronize((cudaStream_t)stream));
-  return MICRO_OK;
-}
-
-// ---- stateless value-level operations ----
-
-int micro_synth_gaussian(int dtype, uint64_t seed, uint32_t worker, uint64_t t, int64_t n, void* d_out,
-                         void* stream) {
-  TRY(check_dtype(dtype));
-  if (n < 0 || (n && !d_out)) return fail(MICRO_EINVAL, "bad output");
-  if (!n) return MICRO_OK;
-  const int64_t q = (n + 3) / 4;
-  const unsigned grid = (unsigned)((q + 255) / 256);
-  if (dtype == MICRO_F32) k_synth<float><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, worker, t, n, (float*)d_out);
-  else k_synth<double><<<grid, 256, 0, (cudaStream_t)stream>>>(seed, worker, t, n, (double*)d_out);
-  CU(cudaGetLastError());
-  return MICRO_OK;
-}
-
-int micro_accumulate(int dtype, const void* d_e, double eta, const void* d_g, void* d_acc, int64_t n,
-                     void* stream) {
-  TRY(check_dtype(dtype));
-  if (!(eta > 0.0)) return fail(MICRO_EINVAL, "accumulate: eta must be positive");
-  if (n < 0) return fail(MICRO_EINVAL, "accumulate: negative length");
-  if (!n) return MICRO_OK;
-  const unsigned grid = grid_for(n, current_device());
-  if (dtype == MICRO_F32)
-    k_accumulate<float><<<grid, 256, 0, (cudaStream_t)stream>>>((const float*)d_e, (float)eta, (const float*)d_g,
-                                                                (float*)d_acc, n);
-  else
-    k_accumulate<double><<<grid, 256, 0, (cudaStream_t)stream>>>((const double*)d_e, eta, (const double*)d_g,
-                                                                 (double*)d_acc, n);
-  CU(cudaGetLastError());
-  return MICRO_OK;
-}
-
-// Ordered compaction of {j in [start, end) : |acc_j| > thr} (thr = *d_thr or
-// delta), plus, with d_tie, {|acc_j| == thr, j <= *d_tie} (top-k's ties).
-static int select_range(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end, double delta,
-                        const double* d_thr, const long long* d_tie, int32_t* d_idx, void* d_val, int64_t cap,
-                        int64_t* d_count, void* stream) {
-  TRY(check_dtype(dtype));
-  if (start < 0 || end < start || end > n_g)
-    return fail(MICRO_EINVAL, "selection: range [%lld, %lld) invalid for vector of length %lld",
-                (long long)start, (long long)end, (long long)n_g);
-  if (n_g >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "n_g must be < 2^31 (int32 indices)");
-  if (!d_count) return fail(MICRO_EINVAL, "null count pointer");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (end == start) {
-    CU(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
-    return MICRO_OK;
-  }
-  if ((uintptr_t)d_acc % 16) return fail(MICRO_EINVAL, "acc not 16-byte aligned");
-  const int TILE = dtype == MICRO_F32 ? tile_elems<float>() : tile_elems<double>();
-  const int64_t tlo = start / TILE, thi = (end - 1) / TILE;
-  const int64_t ntiles = thi - tlo + 1;
-  const int64_t pmax = ntiles + 2;
-  // scratch: status words, ticket, flags (stream-ordered allocator)
-  char* ws = nullptr;
-  const size_t wbytes = sizeof(unsigned long long) * pmax + 16;
-  CU(cudaMallocAsync((void**)&ws, wbytes, s));
-  CU(cudaMemsetAsync(ws, 0, wbytes, s));
-  SelectArgs a{};
-  a.grad = nullptr;
-  a.resid = const_cast<void*>(d_acc);
-  a.n_g = n_g;
-  a.p_start = start;
-  a.p_end = end;
-  a.eta = 1.0;
-  a.delta = d_thr;
-  a.delta_value = delta;
-  a.tie_j = d_tie;
-  a.sel_idx = d_idx;
-  a.sel_val = d_val;
-  a.cap = cap;
-  a.count = (long long*)d_count;
-  a.status = (unsigned long long*)ws;
-  a.p_max = pmax;
-  a.ticket = (unsigned int*)(ws + sizeof(unsigned long long) * pmax);
-  a.flags = (int*)(ws + sizeof(unsigned long long) * pmax + 8);
-  a.epoch = 1;
-  a.tile_lo = tlo;
-  a.num_tiles = ntiles;
-  if (dtype == MICRO_F32)
-    k1_fused_select<float, false, kWriteNone><<<(unsigned)ntiles, kThreads, 0, s>>>(a);
-  else
-    k1_fused_select<double, false, kWriteNone><<<(unsigned)ntiles, kThreads, 0, s>>>(a);
-  CU(cudaGetLastError());
-  CU(cudaFreeAsync(ws, s));
-  return MICRO_OK;
-}
-
-int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end,
-                              double delta, int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count,
-                              void* stream) {
-  if (!(delta >= 0.0) || !std::isfinite(delta))
-    return fail(MICRO_EINVAL, "selection: threshold must be finite and nonnegative");
-  return select_range(dtype, d_acc, n_g, start, end, delta, nullptr, nullptr, d_idx, d_val, cap, d_count, stream);
-}
-
-}  // extern "C"
-
-template <typename T>
-static int topk_pivot(const T* acc, int64_t m, int64_t k, int64_t base, TopkState* st, unsigned* hist,
-                      unsigned* tie_counts, int dev, cudaStream_t s) {
-  k_topk_init<<<1, 1, 0, s>>>(st, k);
-  CU(cudaGetLastError());
-  const unsigned hgrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 4 * (int64_t)num_sms(dev)));
-  for (int hi = KeyOf<T>::kBits; hi > 0; hi -= kDigitBits) {
-    const int width = std::min(kDigitBits, hi);
-    const int shift = hi - width;
-    k_topk_hist<T><<<hgrid, 256, 0, s>>>(acc, nullptr, 1.0, m, shift, width, st, hist);
-    CU(cudaGetLastError());
-    k_topk_digit<T><<<1, 1024, 0, s>>>(st, hist, shift, width, shift == 0, base + m);
-    CU(cudaGetLastError());
-  }
-  const int64_t chunk = (m + kTieChunks - 1) / kTieChunks;
-  const int nch = (int)((m + chunk - 1) / chunk);
-  k_tie_count<T><<<nch, 256, 0, s>>>(acc, nullptr, 1.0, m, chunk, st, tie_counts);
-  CU(cudaGetLastError());
-  k_tie_find<T><<<1, 1024, 0, s>>>(acc, nullptr, 1.0, m, chunk, nch, st, tie_counts, base);
-  CU(cudaGetLastError());
-  return MICRO_OK;
-}
-
-extern "C" {
-
-int micro_select_topk(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end, int64_t k,
-                      int32_t* d_idx, void* d_val, int64_t cap, int64_t* d_count, void* stream) {
-  TRY(check_dtype(dtype));
-  if (start < 0 || end < start || end > n_g)
-    return fail(MICRO_EINVAL, "selection: range [%lld, %lld) invalid for vector of length %lld",
-                (long long)start, (long long)end, (long long)n_g);
-  const int64_t m = end - start;
-  if (k < 0 || k > m)
-    return fail(MICRO_EINVAL, "select_topk: k=%lld exceeds range size %lld", (long long)k, (long long)m);
-  if (!d_count) return fail(MICRO_EINVAL, "null count pointer");
-  cudaStream_t s = (cudaStream_t)stream;
-  if (k == 0) {
-    CU(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
-    return MICRO_OK;
-  }
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  // scratch: state, histogram, tie counts, the "everything" threshold
-  const size_t bytes = 256 + sizeof(unsigned) * (kBins + kTieChunks);
-  char* ws = nullptr;
-  CU(cudaMallocAsync((void**)&ws, bytes, s));
-  CU(cudaMemsetAsync(ws, 0, bytes, s));
-  auto* st = (TopkState*)ws;
-  auto* m1 = (double*)(ws + 128);
-  unsigned* hist = (unsigned*)(ws + 256);
-  unsigned* ties = hist + kBins;
-  int rc = MICRO_OK;
-  if (k == m) {  // every index of the range (sparsifier.cpp:56: no nth_element)
-    const double minus1 = -1.0;
-    CU(cudaMemcpyAsync(m1, &minus1, sizeof minus1, cudaMemcpyHostToDevice, s));
-    rc = select_range(dtype, d_acc, n_g, start, end, 0.0, m1, nullptr, d_idx, d_val, cap, d_count, stream);
-  } else {
-    if (dtype == MICRO_F32)
-      rc = topk_pivot<float>((const float*)d_acc + start, m, k, start, st, hist, ties, dev, s);
-    else
-      rc = topk_pivot<double>((const double*)d_acc + start, m, k, start, st, hist, ties, dev, s);
-    if (rc == MICRO_OK)
-      rc = select_range(dtype, d_acc, n_g, start, end, 0.0, &st->pivot, &st->tie_j, d_idx, d_val, cap, d_count,
-                        stream);
-  }
-  cudaFreeAsync(ws, s);
-  return rc;
-}
-
-int micro_compensate(int dtype, void* d_acc, int64_t n_g, const int32_t* d_idx, int64_t k, void* stream) {
-  TRY(check_dtype(dtype));
-  if (k < 0) return fail(MICRO_EINVAL, "compensate: negative count");
-  if (!k) return MICRO_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  int* bad = nullptr;
-  CU(cudaMallocAsync((void**)&bad, sizeof(int), s));
-  CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  const unsigned grid = grid_for(k, current_device());
-  if (dtype == MICRO_F32) k_compensate<float><<<grid, 256, 0, s>>>((float*)d_acc, n_g, d_idx, k, bad);
-  else k_compensate<double><<<grid, 256, 0, s>>>((double*)d_acc, n_g, d_idx, k, bad);
-  CU(cudaGetLastError());
-  int hbad = 0;
-  CU(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CU(cudaFreeAsync(bad, s));
-  CU(cudaStreamSynchronize(s));
-  if (hbad) return fail(MICRO_EINVAL, "compensate: index out of range");
-  return MICRO_OK;
-}
-
-static int reduce_values(int dtype, const void* const* h_accs, int n, int64_t n_g, const int32_t* d_union,
-                         int64_t K, void* d_sums, void* d_dense, void* stream) {
-  TRY(check_dtype(dtype));
-  if (n < 1 || !h_accs) return fail(MICRO_EINVAL, "all_reduce_sparse: no workers");
-  if (n > kMaxWorkers) return fail(MICRO_EINVAL, "all_reduce_sparse: at most %d workers", kMaxWorkers);
-  if (K < 0) return fail(MICRO_EINVAL, "all_reduce_sparse: negative union size");
-  cudaStream_t s = (cudaStream_t)stream;
-  const size_t esz = dtype_size(dtype);
-  if (d_dense) CU(cudaMemsetAsync(d_dense, 0, n_g * esz, s));
-  if (!K) return MICRO_OK;
-  WorkerPtrs w{};
-  for (int r = 0; r < n; ++r) w.sel_val[r] = h_accs[r];
-  int* bad = nullptr;
-  CU(cudaMallocAsync((void**)&bad, sizeof(int), s));
-  CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
-  const unsigned grid = grid_for(K, current_device());
-  if (dtype == MICRO_F32)
-    k_reduce_values<float><<<grid, 256, 0, s>>>(w, n, n_g, d_union, K, (float*)d_sums, (float*)d_dense, bad);
-  else
-    k_reduce_values<double><<<grid, 256, 0, s>>>(w, n, n_g, d_union, K, (double*)d_sums, (double*)d_dense, bad);
-  CU(cudaGetLastError());
-  int hbad = 0;
-  CU(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CU(cudaFreeAsync(bad, s));
-  CU(cudaStreamSynchronize(s));
-  if (hbad) return fail(MICRO_EINVAL, "all_reduce_sparse: index out of range");
-  return MICRO_OK;
-}
-
-int micro_all_reduce_sparse_values(int dtype, const void* const* h_accs, int n, int64_t n_g,
-                                   const int32_t* d_union, int64_t K, void* d_sums, void* stream) {
-  return reduce_values(dtype, h_accs, n, n_g, d_union, K, d_sums, nullptr, stream);
-}
-
-int micro_all_reduce_sparse(int dtype, const void* const* h_accs, int n, int64_t n_g,
-                            const int32_t* d_union, int64_t K, void* d_dense, void* stream) {
-  if (!d_dense) return fail(MICRO_EINVAL, "null dense output");
-  return reduce_values(dtype, h_accs, n, n_g, d_union, K, nullptr, d_dense, stream);
-}
-
-int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_concat, int32_t* d_union,
-                             int64_t* K, void* stream) {
-  if (n < 0 || (n && !h_counts)) return fail(MICRO_EINVAL, "bad selection list");
-  if (!K) return fail(MICRO_EINVAL, "null K");
-  int64_t total = 0;
-  for (int i = 0; i < n; ++i) {
-    if (h_counts[i] < 0) return fail(MICRO_EINVAL, "negative count");
-    total += h_counts[i];
-  }
-  *K = 0;
-  if (!total) return MICRO_OK;
-  if (total >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "too many indices");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int items = (int)total;
-  int32_t* sorted = nullptr;
-  int* d_num = nullptr;
-  void* tmp = nullptr;
-  size_t b1 = 0, b2 = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, b1, d_concat, (int32_t*)nullptr, items, 0, 32, s);
-  cub::DeviceSelect::Unique(nullptr, b2, (const int32_t*)nullptr, (int32_t*)nullptr, (int*)nullptr, items, s);
-  const size_t tb = std::max(b1, b2);
-  CU(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * items, s));
-  CU(cudaMallocAsync((void**)&d_num, sizeof(int), s));
-  CU(cudaMallocAsync(&tmp, tb, s));
-  size_t tb1 = tb, tb2 = tb;
-  CU(cub::DeviceRadixSort::SortKeys(tmp, tb1, d_concat, sorted, items, 0, 32, s));
-  CU(cub::DeviceSelect::Unique(tmp, tb2, (const int32_t*)sorted, d_union, d_num, items, s));
-  int hn = 0;
-  CU(cudaMemcpyAsync(&hn, d_num, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CU(cudaFreeAsync(sorted, s));
-  CU(cudaFreeAsync(d_num, s));
-  CU(cudaFreeAsync(tmp, s));
-  CU(cudaStreamSynchronize(s));
-  *K = hn;
-  return MICRO_OK;
-}
-
-int micro_error_metric(int dtype, const void* const* h_res, int n, int64_t n_g, double* out, void* stream) {
-  TRY(check_dtype(dtype));
-  if (n < 1 || !h_res) return fail(MICRO_EINVAL, "error_metric: no workers");
-  if (n_g < 0 || !out) return fail(MICRO_EINVAL, "error_metric: bad arguments");
-  cudaStream_t s = (cudaStream_t)stream;
-  int dev = 0;
-  CU(cudaGetDevice(&dev));
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n_g + 255) / 256, 4 * (int64_t)num_sms(dev)));
-  const int64_t groups = sumsq_groups(grid);
-  // one scratch block: per-worker slots (part, group, ticket) + n totals
-  const size_t bytes = sizeof(double) * (size_t)n * (grid + groups + 1) + sizeof(unsigned) * (size_t)n * (groups + 1);
-  char* scratch = nullptr;
-  CU(cudaMallocAsync((void**)&scratch, bytes, s));
-  CU(cudaMemsetAsync(scratch, 0, bytes, s));
-  double* part = (double*)scratch;
-  double* grp = part + (size_t)n * grid;
-  double* tot = grp + (size_t)n * groups;
-  unsigned* tick = (unsigned*)(tot + n);
-  for (int i = 0; i < n; ++i) {
-    if (n_g && !h_res[i]) {
-      cudaFreeAsync(scratch, s);
-      return fail(MICRO_EINVAL, "error_metric: null residual %d", i);
-    }
-    SumSqSlots q{part + (size_t)i * grid, grp + (size_t)i * groups, tick + (size_t)i * (groups + 1), tot + i};
-    if (n_g == 0) continue;
-    if (dtype == MICRO_F32) k_sumsq<float><<<(unsigned)grid, 256, 0, s>>>((const float*)h_res[i], n_g, q);
-    else k_sumsq<double><<<(unsigned)grid, 256, 0, s>>>((const double*)h_res[i], n_g, q);
-    CU(cudaGetLastError());
-  }
-  std::vector<double> h(n);
-  CU(cudaMemcpyAsync(h.data(), tot, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-  CU(cudaFreeAsync(scratch, s));
-  CU(cudaStreamSynchronize(s));
-  double sum = 0.0;  // error_feedback.hpp:44-47: norms summed in worker order, then / n
-  for (int i = 0; i < n; ++i) sum += std::sqrt(h[i]);
-  *out = sum / (double)n;
-  return MICRO_OK;
-}
 
 }  // extern "C"

@@ -21,6 +21,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "exchange.cuh"  // WorkerPtrs
 
 namespace micro {
 
@@ -49,6 +50,7 @@ template <> struct KeyOf<double> {
 };
 
 constexpr int kDigitBits = 11;
+constexpr int kTieChunks = 65536;  // tie counting granularity (k_tie_count / k_tie_find)
 
 // acc = e + eta*G (K1's arithmetic), or acc itself (g == NULL: the value API)
 template <typename T>
@@ -57,7 +59,7 @@ __device__ __forceinline__ T acc_at(const T* e, const T* g, T eta, int64_t j) {
 }
 constexpr int kBins = 1 << kDigitBits;
 
-__global__ void k_topk_init(TopkState* st, long long k) {
+static __global__ void k_topk_init(TopkState* st, long long k) {
   st->prefix = 0;
   st->mask = 0;
   st->k_rem = k;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) k_accumulate_probe(T* __restrict__ e, con
 }
 
 // ---- union of overlapping selections: bitmap, then ordered emission ----
-__global__ void __launch_bounds__(256) k_union_mark(const int32_t* __restrict__ idx, const long long* count,
+static __global__ void __launch_bounds__(256) k_union_mark(const int32_t* __restrict__ idx, const long long* count,
                                                     long long cap, unsigned* __restrict__ bitmap) {
   const long long k = min(*count, cap);
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(256) k_union_mark(const int32_t* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(256) k_word_popc(const unsigned* __restrict__ bitmap, int64_t nwords,
+static __global__ void __launch_bounds__(256) k_word_popc(const unsigned* __restrict__ bitmap, int64_t nwords,
                                                    int* __restrict__ pc) {
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x)
     pc[w] = __popc(bitmap[w]);
@@ -360,7 +362,7 @@ __global__ void __launch_bounds__(256) k_word_popc(const unsigned* __restrict__ 
 
 // off: exclusive prefix of the popcounts.  Writes the union in index order,
 // K, and clears the bitmap for the next step.
-__global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict__ bitmap, int64_t nwords,
+static __global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict__ bitmap, int64_t nwords,
                                                      const int* __restrict__ off, int32_t* __restrict__ uidx,
                                                      long long* K) {
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
@@ -377,13 +379,13 @@ __global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict__ bitm
   }
 }
 
-__global__ void k_iota(int32_t* u, int64_t n, long long* K) {
+static __global__ void k_iota(int32_t* u, int64_t n, long long* K) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
     u[j] = (int32_t)j;
   if (blockIdx.x == 0 && threadIdx.x == 0) *K = n;
 }
 
-__global__ void k_fill_i64(long long* p, int n, long long v) {
+static __global__ void k_fill_i64(long long* p, int n, long long v) {
   if ((int)threadIdx.x < n) p[threadIdx.x] = v;
 }
 

@@ -1,0 +1,293 @@
+// dist_api.cu — one rank of an n-GPU job (include/micro.h micro_dist_* and
+// micro_peer_*): the device halves of the NCCL protocol (dist.py) and the
+// exchange over peer memory (peer.cuh).
+#include "internal.cuh"
+
+extern "C" {
+
+static int dist_counts(micro_ctx* c, const int64_t* h_counts, Counts* out, bool own_segments) {
+  if (!h_counts) return fail(MICRO_EINVAL, "null counts");
+  long long off = 0;
+  const int me = c->cfg.rank;
+  for (int r = 0; r < c->n; ++r) {
+    if (h_counts[r] < 0) return fail(MICRO_EINVAL, "negative count");
+    out->k[r] = h_counts[r];
+    out->off[r] = off;
+    // send layout: segment o has k_o values (o != me); recv layout: segment r has k_me values
+    if (r != me) off += own_segments ? h_counts[me] : h_counts[r];
+  }
+  return MICRO_OK;
+}
+
+int micro_dist_gather_foreign(micro_ctx* c, const int32_t* d_all_idx, const int64_t* h_counts,
+                              int64_t kmax, void* d_send) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_gather_foreign before micro_compress");
+  Counts cs{};
+  TRY(dist_counts(c, h_counts, &cs, false));
+  DeviceGuard dg(c->dev);
+  long long mx = 0;
+  for (int r = 0; r < c->n; ++r) mx = std::max<long long>(mx, cs.k[r]);
+  if (mx > kmax) return fail(MICRO_EINVAL, "kmax %lld smaller than a count %lld", (long long)kmax, mx);
+  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
+  double* corr = c->norm ? c->norm_corr : nullptr;
+  if (c->esz == 4) {
+    if (c->cfg.error_feedback)
+      k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                      (float*)c->resid[0], (float*)d_send, corr);
+    else
+      k_dist_gather_foreign<float, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                       (float*)c->resid[0], (float*)d_send, corr);
+  } else {
+    if (c->cfg.error_feedback)
+      k_dist_gather_foreign<double, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                       (double*)c->resid[0], (double*)d_send, corr);
+    else
+      k_dist_gather_foreign<double, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
+                                                                        (double*)c->resid[0], (double*)d_send, corr);
+  }
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+int micro_dist_owner_reduce(micro_ctx* c, const void* d_recv, const int64_t* h_counts, void* d_own_sums) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
+  Counts cs{};
+  TRY(dist_counts(c, h_counts, &cs, true));
+  DeviceGuard dg(c->dev);
+  const int me = c->cfg.rank;
+  const long long k = cs.k[me];
+  const unsigned grid = grid_for(k, c->dev);
+  if (c->esz == 4)
+    k_dist_owner_reduce<float><<<grid, 256, 0, c->stream>>>((const float*)c->sel_val[c->buf][0], k,
+                                                            (const float*)d_recv, cs, c->n, me, (float*)d_own_sums);
+  else
+    k_dist_owner_reduce<double><<<grid, 256, 0, c->stream>>>((const double*)c->sel_val[c->buf][0], k,
+                                                             (const double*)d_recv, cs, c->n, me,
+                                                             (double*)d_own_sums);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
+
+// ---- peer-memory exchange (peer.cuh) ------------------------------------
+namespace {
+constexpr int kPeerBufs = 10;  // resid, counts, uidx x2, usum x2, norm corr, sel_idx x2, recv
+static_assert(MICRO_PEER_HANDLE_BYTES == kPeerBufs * sizeof(cudaIpcMemHandle_t), "handle layout");
+
+void* peer_buf(micro_ctx* c, int b) {
+  switch (b) {
+    case 0: return c->resid[0];
+    case 1: return c->counts;
+    case 2: return c->uni_idx[0];
+    case 3: return c->uni_idx[1];
+    case 4: return c->uni_sum[0];
+    case 5: return c->uni_sum[1];
+    case 6: return c->norm ? c->norm_corr : nullptr;
+    case 7: return c->sel_idx[0][0];
+    case 8: return c->sel_idx[1][0] != c->sel_idx[0][0] ? c->sel_idx[1][0] : nullptr;  // single-buffered
+    default: return c->recv;
+  }
+}
+
+int check_peer_ctx(micro_ctx* c) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster || c->n_local != 1 || c->n < 2)
+    return fail(MICRO_ELOGIC, "micro_peer_*: needs a rank context (n_local = 1 of n > 1 workers)");
+  return MICRO_OK;
+}
+}  // namespace
+
+int micro_peer_export(micro_ctx* c, void* out) {
+  TRY(check_peer_ctx(c));
+  if (!out) return fail(MICRO_EINVAL, "null handle buffer");
+  DeviceGuard dg(c->dev);
+  if (!c->recv) TRY(c->alloc(&c->recv, (size_t)c->n * c->sel_cap * c->esz));
+  auto* h = (cudaIpcMemHandle_t*)out;
+  for (int b = 0; b < kPeerBufs; ++b) {
+    std::memset(&h[b], 0, sizeof h[b]);
+    if (void* p = peer_buf(c, b)) CU(cudaIpcGetMemHandle(&h[b], p));
+  }
+  return MICRO_OK;
+}
+
+int micro_peer_import(micro_ctx* c, const void* all) {
+  TRY(check_peer_ctx(c));
+  if (!all) return fail(MICRO_EINVAL, "null handle array");
+  if (c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_import called twice");
+  DeviceGuard dg(c->dev);
+  const auto* h = (const cudaIpcMemHandle_t*)all;
+  const int me = c->cfg.rank;
+  static const cudaIpcMemHandle_t zero{};
+  for (int r = 0; r < c->n; ++r) {
+    void* p[kPeerBufs] = {};
+    for (int b = 0; b < kPeerBufs; ++b) {
+      if (r == me) {
+        p[b] = peer_buf(c, b);
+        continue;
+      }
+      const cudaIpcMemHandle_t& hb = h[(size_t)r * kPeerBufs + b];
+      if (std::memcmp(&hb, &zero, sizeof zero) == 0) continue;
+      CU(cudaIpcOpenMemHandle(&p[b], hb, cudaIpcMemLazyEnablePeerAccess));
+      c->peer_opened.push_back(p[b]);
+    }
+    if (!p[8]) p[8] = p[7];  // the rank's selection is single-buffered
+    if (!p[0] || !p[1] || !p[2] || !p[3] || !p[4] || !p[5] || !p[7] || !p[9])
+      return fail(MICRO_EINVAL, "rank %d exported incomplete handles", r);
+    if (c->norm && !p[6]) return fail(MICRO_EINVAL, "rank %d does not record the error norm", r);
+    c->peer_resid[r] = p[0];
+    c->peer_counts[r] = (const long long*)p[1];
+    c->peer_uidx[0][r] = (int32_t*)p[2];
+    c->peer_uidx[1][r] = (int32_t*)p[3];
+    c->peer_usum[0][r] = p[4];
+    c->peer_usum[1][r] = p[5];
+    c->peer_corr[r] = c->norm ? (double*)p[6] : nullptr;
+    c->peer_sel[0][r] = (const int32_t*)p[7];
+    c->peer_sel[1][r] = (const int32_t*)p[8];
+    c->peer_recv[r] = p[9];
+  }
+  c->peer_ready = true;
+  return MICRO_OK;
+}
+
+int micro_peer_exchange(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_peer_import");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_exchange before micro_compress");
+  if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_exchange called twice");
+  DeviceGuard dg(c->dev);
+  PeerPtrs pp{};
+  for (int r = 0; r < c->n; ++r) {
+    pp.counts[r] = c->peer_counts[r];
+    pp.resid[r] = c->peer_resid[r];
+    pp.uidx[r] = c->peer_uidx[c->buf][r];
+    pp.usum[r] = c->peer_usum[c->buf][r];
+    pp.corr[r] = c->peer_corr[r];
+  }
+  // sized for the expected selection (the kernel reads the actual count)
+  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
+  const int me = c->cfg.rank;
+  const bool ef = c->cfg.error_feedback != 0;
+  long long* Kout = c->Kbuf + c->buf;
+  if (c->esz == 4) {
+    const float* v = (const float*)c->sel_val[c->buf][0];
+    if (ef) k_peer_exchange<float, true><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                      c->sel_idx[c->buf][0], v, Kout);
+    else k_peer_exchange<float, false><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                     c->sel_idx[c->buf][0], v, Kout);
+  } else {
+    const double* v = (const double*)c->sel_val[c->buf][0];
+    if (ef) k_peer_exchange<double, true><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                       c->sel_idx[c->buf][0], v, Kout);
+    else k_peer_exchange<double, false><<<grid, 256, 0, c->stream>>>(pp, c->n, me, c->t_cur, c->sel_cap,
+                                                                      c->sel_idx[c->buf][0], v, Kout);
+  }
+  CU(cudaGetLastError());
+  c->peer_phase = 2;
+  return MICRO_OK;
+}
+
+PeerBulkPtrs bulk_ptrs(micro_ctx* c) {
+  PeerBulkPtrs pb{};
+  for (int r = 0; r < c->n; ++r) {
+    pb.counts[r] = c->peer_counts[r];
+    pb.sel_idx[r] = c->peer_sel[c->buf][r];
+    pb.recv[r] = c->peer_recv[r];
+    pb.uidx[r] = c->peer_uidx[c->buf][r];
+    pb.usum[r] = c->peer_usum[c->buf][r];
+  }
+  return pb;
+}
+
+int micro_peer_contribute(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (!c->peer_ready) return fail(MICRO_ELOGIC, "micro_peer_contribute before micro_peer_import");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_peer_contribute before micro_compress");
+  if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_contribute called twice");
+  DeviceGuard dg(c->dev);
+  const PeerBulkPtrs pb = bulk_ptrs(c);
+  const dim3 grid(grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev) / 2 + 1, c->n);
+  double* corr = c->norm ? c->norm_corr : nullptr;
+  const int me = c->cfg.rank;
+  if (c->esz == 4) {
+    if (c->cfg.error_feedback)
+      k_peer_contribute<float, true><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (float*)c->resid[0], corr);
+    else
+      k_peer_contribute<float, false><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (float*)c->resid[0], corr);
+  } else {
+    if (c->cfg.error_feedback)
+      k_peer_contribute<double, true><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (double*)c->resid[0], corr);
+    else
+      k_peer_contribute<double, false><<<grid, 256, 0, c->stream>>>(pb, me, c->sel_cap, (double*)c->resid[0], corr);
+  }
+  CU(cudaGetLastError());
+  c->peer_phase = 1;
+  return MICRO_OK;
+}
+
+int micro_peer_reduce(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (c->peer_phase != 1) return fail(MICRO_ELOGIC, "micro_peer_reduce before micro_peer_contribute");
+  DeviceGuard dg(c->dev);
+  const PeerBulkPtrs pb = bulk_ptrs(c);
+  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
+  long long* Kout = c->Kbuf + c->buf;
+  if (c->esz == 4)
+    k_peer_reduce_push<float><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,
+                                                           c->sel_idx[c->buf][0],
+                                                           (const float*)c->sel_val[c->buf][0], Kout);
+  else
+    k_peer_reduce_push<double><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,
+                                                            c->sel_idx[c->buf][0],
+                                                            (const double*)c->sel_val[c->buf][0], Kout);
+  CU(cudaGetLastError());
+  c->peer_phase = 2;
+  return MICRO_OK;
+}
+
+int micro_peer_finalize(micro_ctx* c) {
+  TRY(check_peer_ctx(c));
+  if (c->peer_phase != 2) return fail(MICRO_ELOGIC, "micro_peer_finalize before the exchange");
+  DeviceGuard dg(c->dev);
+  c->peer_phase = 0;
+  if (c->esz == 4) return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+}
+
+int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_all_sums,
+                        const int64_t* h_counts, int64_t kmax) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
+  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_finalize before micro_compress");
+  Counts cs{};
+  TRY(dist_counts(c, h_counts, &cs, false));
+  long long K = 0, mx = 0;
+  for (int r = 0; r < c->n; ++r) {
+    K += cs.k[r];
+    mx = std::max<long long>(mx, cs.k[r]);
+  }
+  if (K > c->uni_cap) return fail(MICRO_ECAPACITY, "union %lld exceeds capacity %lld", K, (long long)c->uni_cap);
+  DeviceGuard dg(c->dev);
+  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
+  if (c->esz == 4) {
+    k_dist_build_union<float><<<grid, 256, 0, c->stream>>>(d_all_idx, (const float*)d_all_sums, kmax, cs, c->n,
+                                                           c->t_cur, c->uni_idx[c->buf],
+                                                           (float*)c->uni_sum[c->buf], c->Kbuf + c->buf);
+    CU(cudaGetLastError());
+    return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+  }
+  k_dist_build_union<double><<<grid, 256, 0, c->stream>>>(d_all_idx, (const double*)d_all_sums, kmax, cs, c->n,
+                                                          c->t_cur, c->uni_idx[c->buf],
+                                                          (double*)c->uni_sum[c->buf], c->Kbuf + c->buf);
+  CU(cudaGetLastError());
+  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+}
+
+// ---- device memory plumbing ----
+
+}  // extern "C"
