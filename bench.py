@@ -243,6 +243,8 @@ def our_arm(args, wl):
     torch.cuda.synchronize()
     t_first = t
     m.kernel_timing(True)  # CUDA events around K1's streaming pass, inside the library
+    if dist:
+        m.exchange_timing(True)
     with ClockSampler(local) as clk:
         start.record(stream)
         for s in range(args.steps):
@@ -255,6 +257,14 @@ def our_arm(args, wl):
     total_ms = start.elapsed_time(end)
     k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone
     m.kernel_timing(False)
+    xchg_ms = None
+    if dist:
+        xt = m.exchange_times()
+        m.exchange_timing(False)
+        v = torch.tensor([statistics.mean(xt) if xt else 0.0],
+                         device=dev if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        xchg_ms = float(v[0])
     if dist:
         v = torch.tensor([total_ms], device=dev if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
@@ -364,6 +374,19 @@ def our_arm(args, wl):
         except Exception as ex:  # the checker is optional at run time; the GPU number stands
             cpu = {"value": None, "unit": "us/iter", "cores": 1, "kind": "reference", "sample": f"failed: {ex}"}
 
+    # the exchange against the NVLink roofline (N > 1): bytes received per GPU,
+    # 4(K-k) foreign indices + 4k(n-1) contributions + 4(K-k) sums
+    exchange_line = None
+    if dist and xchg_ms:
+        Km, km = float(K.mean()), float(k_own.mean())
+        b_net = 4.0 * (Km - km) + 4.0 * km * (world - 1) + 4.0 * (Km - km)
+        exchange_line = {"bound": "nvlink", "achieved": b_net / (xchg_ms * 1e-3) / 1e9, "peak": 900.0,
+                         "unit": "GB/s", "frac": b_net / (xchg_ms * 1e-3) / 1e9 / 900.0,
+                         "bytes_per_gpu": b_net, "avg_ms": xchg_ms, "transport": args.transport,
+                         "peak_source": "NVLink 5 per direction per GPU (nominal)",
+                         "timed": "exchange kernels, barriers excluded" if args.transport != "nccl"
+                         else "the whole NCCL protocol"}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_step * 1e3, "unit": "us/iter", "n_gpus": world, "steps": args.steps,
@@ -392,6 +415,7 @@ def our_arm(args, wl):
                          "kernel": "k1_stream", "algorithmic_bytes_per_launch": k1_bytes,
                          "avg_launch_ms": k1a_avg_ms, "peak_source": peak_kind,
                          "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
+            "exchange": exchange_line,
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,

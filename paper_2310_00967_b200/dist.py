@@ -159,24 +159,50 @@ class DistMicro:
     def compress(self, grads, eta: float, t: int):
         self.m.compress(grads, eta, t)
 
+    def exchange_timing(self, enable: bool = True):
+        """Record CUDA events around the exchange's data movement each step
+        (peer: the exchange kernels, barriers excluded; nccl: the whole
+        protocol) — the NVLink roofline's denominator in bench.py."""
+        self._xt = [] if enable else None
+
+    def exchange_times(self) -> list[float]:
+        out = []
+        for parts in getattr(self, "_xt", None) or []:
+            out.append(sum(a.elapsed_time(b) for a, b in parts))
+        return out
+
+    def _timed(self, parts, fn):
+        if getattr(self, "_xt", None) is None:
+            return fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(self.m.stream)
+        r = fn()
+        b.record(self.m.stream)
+        parts.append((a, b))
+        return r
+
     def aggregate(self) -> int | None:
         """NCCL transport: returns |union| (known on the host).  Peer
         transport: asynchronous, returns None (``query().K`` has it)."""
+        parts = []
+        if getattr(self, "_xt", None) is not None:
+            self._xt.append(parts)
+        h = self.m.handle
         if self.transport == "peer":  # bulk: every NVLink transfer contiguous
             self._barrier()
-            check(lib().micro_peer_contribute(self.m.handle))
+            self._timed(parts, lambda: check(lib().micro_peer_contribute(h)))
             self._barrier()
-            check(lib().micro_peer_reduce(self.m.handle))
+            self._timed(parts, lambda: check(lib().micro_peer_reduce(h)))
             self._barrier()
-            check(lib().micro_peer_finalize(self.m.handle))
+            check(lib().micro_peer_finalize(h))
             return None
         if self.transport == "peer_pull":  # one kernel: owners read the peers' entries remotely
             self._barrier()
-            check(lib().micro_peer_exchange(self.m.handle))
+            self._timed(parts, lambda: check(lib().micro_peer_exchange(h)))
             self._barrier()
-            check(lib().micro_peer_finalize(self.m.handle))
+            check(lib().micro_peer_finalize(h))
             return None
-        return exchange(self.ops, self.group, self.comm_device)
+        return self._timed(parts, lambda: exchange(self.ops, self.group, self.comm_device))
 
     def step(self, grads, eta: float, t: int) -> int | None:
         self.compress(grads, eta, t)

@@ -40,4 +40,5 @@ def test_bench_n2_code_path(transport):
     assert r.returncode == 0, r.stderr[-2000:]
     d = _line(r.stdout)
     assert d["n_gpus"] == 2 and d["e2e"]["per"].startswith("rank")
+    assert d["exchange"]["bound"] == "nvlink" and d["exchange"]["avg_ms"] > 0
     assert transport in d["config"]["parallelism"]
