@@ -1,0 +1,146 @@
+"""The reference's acceptance criteria (proj/tests/acceptance.cpp) that
+concern this path, restated on synthetic N(0,1) gradients instead of the
+simulator's tasks (which are out of scope).  GPU only.
+
+  C1  no build-up: |union| == sum k_i every iteration (acceptance.cpp:93-118)
+  C2  CLT-k exact: |union| == k every iteration (:121-132)
+  C3  build-up reproduction: top-k density > d and redundant factor in
+      (1, n]; MiCRO exactly 1.0 (:135-171)
+  C4  threshold tracking: MiCRO last-half density within +/-25 % of d, the
+      fixed threshold deviates more (:174-220)
+  C7  error-feedback conservation, bitwise: e_{t+1} + sent == e_t + eta*G (:279-306)
+  C8  d = 1, delta0 = 0: every sparsifier's model equals dense SGD bitwise (:309-340)
+  C9  records' error norm == error_metric(residuals) to 1e-12; dense: 0 (:343-363)
+  C11 identical runs -> identical CSV records (:390-414)
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2310_00967_b200 import engine, report, sparsim
+
+
+def _run(n_g, n, iters, seed=1, eta=0.01, **kw):
+    m = engine.Micro(n_g, n, **kw)
+    x = torch.zeros(n_g, device="cuda", dtype=kw.get("dtype", torch.float32))
+    m.set_model(x)
+    g = [torch.empty(n_g, device="cuda") for _ in range(n)]
+    for t in range(iters):
+        for i in range(n):
+            engine.synth_gaussian(g[i], seed, i, t)
+        m.step(g, eta, t)
+    torch.cuda.synchronize()
+    return m, x
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+@pytest.mark.parametrize("d", [0.01, 0.001])
+def test_c1_no_buildup(n, d):
+    m, _ = _run(65_536, n, 300, density=d, initial_threshold=0.02)
+    recs = m.records(300)
+    assert len(recs) == 300
+    assert all(r["K"] == r["total_selected"] for r in recs)
+    assert all(r["redundant_traffic_factor"] == (1.0 if r["K"] else 0.0) for r in recs)
+    m.close()
+
+
+def test_c2_cltk_exact():
+    m, _ = _run(50_000, 4, 200, density=0.01, sparsifier="cltk")
+    k = sparsim.global_target_count(0.01, 50_000)
+    assert all(r["K"] == k for r in m.records(200))
+    m.close()
+
+
+def test_c3_buildup_reproduction():
+    n = 16
+    topk, _ = _run(40_000, n, 100, density=0.01, sparsifier="topk")
+    micro, _ = _run(40_000, n, 100, density=0.01, initial_threshold=0.02)
+    rt, rm = topk.records(100), micro.records(100)
+    assert np.mean([r["actual_density"] for r in rt]) > 0.01
+    red = np.mean([r["redundant_traffic_factor"] for r in rt])
+    assert 1.0 < red <= n
+    active = [r for r in rm if r["total_selected"] > 0]
+    assert len(active) >= 90 and all(r["redundant_traffic_factor"] == 1.0 for r in active)
+    topk.close()
+    micro.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_c4_threshold_tracking(seed):
+    d, iters = 0.01, 2000
+    micro, _ = _run(100_000, 8, iters, seed=seed, density=d, initial_threshold=0.01)
+    hard, _ = _run(100_000, 8, iters, seed=seed, density=d, initial_threshold=0.01, sparsifier="hard")
+    last = lambda m: np.mean([r["actual_density"] for r in m.records(iters)[iters // 2:]])  # noqa: E731
+    dm, dh = last(micro), last(hard)
+    assert abs(dm - d) <= 0.25 * d, dm
+    assert abs(dh - d) > abs(dm - d), (dm, dh)
+    micro.close()
+    hard.close()
+
+
+@pytest.mark.parametrize("kind", ["micro", "topk", "hard"])
+def test_c7_error_feedback_conservation(kind):
+    """e_{t+1} + sent == accumulate(e_t, eta, G) bitwise, per worker."""
+    n_g, n = 4096, 4
+    m = engine.Micro(n_g, n, density=0.01, initial_threshold=0.02, sparsifier=kind)
+    g = [torch.empty(n_g, device="cuda") for _ in range(n)]
+    checked = 0
+    for t in range(60):
+        e_t = [m.residual_device(i).clone() for i in range(n)]
+        for i in range(n):
+            engine.synth_gaussian(g[i], 3, i, t)
+        m.step(g, 0.01, t)
+        idx, _ = m.union()
+        idx = torch.from_numpy(idx).long().cuda()
+        for i in range(n):
+            acc = sparsim.accumulate(e_t[i], 0.01, g[i])  # the same two-rounding accumulate
+            sent = torch.zeros_like(acc)
+            sent[idx] = acc[idx]
+            lhs = m.residual_device(i) + sent
+            assert torch.equal(lhs, acc), (t, i)
+            checked += 1
+    assert checked >= 100
+    m.close()
+
+
+def test_c8_dense_equivalence():
+    """d = 1 and delta0 = 0: every sparsifier selects everything — the final
+    model equals dense SGD's bit for bit."""
+    models = {}
+    for kind in ["dense", "micro", "topk", "cltk", "hard"]:
+        m, x = _run(4096, 4, 100, density=1.0, initial_threshold=0.0, sparsifier=kind)
+        models[kind] = x.cpu().numpy()
+        m.close()
+    for kind in ["micro", "topk", "cltk", "hard"]:
+        assert np.array_equal(models[kind], models["dense"]), kind
+
+
+def test_c9_error_metric():
+    n_g, n = 8192, 4
+    m = engine.Micro(n_g, n, density=0.01, initial_threshold=0.02)
+    g = [torch.empty(n_g, device="cuda") for _ in range(n)]
+    for t in range(100):
+        for i in range(n):
+            engine.synth_gaussian(g[i], 7, i, t)
+        m.step(g, 0.01, t)
+        rec = m.records(1)[0]
+        want = sparsim.error_metric([m.residual_device(i) for i in range(n)])
+        assert abs(rec["error_norm"] - want) <= 1e-12, (t, rec["error_norm"], want)
+    m.close()
+    d, _ = _run(2048, 2, 20, density=1.0, initial_threshold=0.0, sparsifier="dense")
+    assert all(r["error_norm"] == 0.0 for r in d.records(20))
+    d.close()
+
+
+def test_c11_determinism(tmp_path):
+    outs = []
+    for rep in range(2):
+        m, _ = _run(20_000, 4, 200, seed=11, density=0.02, initial_threshold=0.02)
+        p = tmp_path / f"run{rep}.csv"
+        report.emit(report.config_for(m, lr=0.01, iterations=200, seed=11), m.records(200), "csv", str(p))
+        outs.append(p.read_bytes())
+        m.close()
+    assert outs[0] == outs[1]
