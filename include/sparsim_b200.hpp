@@ -393,6 +393,20 @@ inline double actual_density(const AggregatedSelection& agg, Index n_g) {
   return static_cast<double>(agg.indices.size()) / static_cast<double>(n_g);
 }
 
+// harness.hpp:25-32 / harness.cpp:61-63, 109-110: the step-decay learning
+// rate that run_iteration hands to each step (host arithmetic).
+struct LrSchedule {
+  double initial = 0.01;
+  double decay_factor = 0.1;
+  std::int64_t decay_at = -1;  // -1: resolved to 3/4 of the run
+};
+inline std::int64_t resolve_decay_at(const LrSchedule& lr, std::int64_t iterations) {
+  return lr.decay_at >= 0 ? lr.decay_at : (3 * iterations) / 4;
+}
+inline double learning_rate_at(const LrSchedule& lr, std::int64_t decay_at, std::int64_t t) {
+  return lr.initial * (t >= decay_at ? lr.decay_factor : 1.0);
+}
+
 // error_feedback.hpp:41-48: mean of the per-worker residual norms (each
 // ||e_i||^2 a deterministic fp64 tree sum on the device; the reference's
 // Eigen summation order is not pinned, so agreement is to ~1e-15 relative).

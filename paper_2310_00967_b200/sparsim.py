@@ -272,3 +272,21 @@ def error_metric(residuals) -> float:
     check(lib().micro_error_metric(_DT[res[0].dtype], arr, len(res), res[0].numel(), C.byref(out),
                                    _stream(res[0].device)))
     return out.value
+
+
+@dataclass(frozen=True)
+class LrSchedule:
+    """harness.hpp:25-32: step decay of the learning rate eta(t)."""
+    initial: float = 0.01
+    decay_factor: float = 0.1
+    decay_at: int = -1  # -1: 3/4 of the run
+
+
+def resolve_decay_at(lr: LrSchedule, iterations: int) -> int:
+    """harness.cpp:109-110."""
+    return lr.decay_at if lr.decay_at >= 0 else (3 * iterations) // 4
+
+
+def learning_rate_at(lr: LrSchedule, decay_at: int, t: int) -> float:
+    """harness.cpp:61-63: the eta handed to each MiCRO step (host arithmetic)."""
+    return lr.initial * (lr.decay_factor if t >= decay_at else 1.0)

@@ -219,3 +219,12 @@ def test_all_reduce_equals_dense_then_mask(ref, orc):
         for i in range(n):
             d32 = d32 + f[i]
         assert np.array_equal(orc.all_reduce_sparse_values(f, u), d32[u])
+
+
+def test_learning_rate_schedule():
+    """harness.cpp:61-63, 109-110 (host arithmetic of the Python face)."""
+    from paper_2310_00967_b200.sparsim import LrSchedule, learning_rate_at, resolve_decay_at
+    lr = LrSchedule(initial=0.1, decay_factor=0.5, decay_at=-1)
+    assert resolve_decay_at(lr, 200) == 150
+    assert learning_rate_at(lr, 150, 149) == 0.1 and learning_rate_at(lr, 150, 150) == 0.05
+    assert resolve_decay_at(LrSchedule(decay_at=7), 200) == 7
