@@ -115,7 +115,7 @@ struct micro_ctx {
   int64_t p_max = 0;
   int64_t status_len = 0;       // allocated look-back words
   int64_t status_hwm = 0;       // highest look-back index any launch has used
-  // K1 implementation (MICRO_K1_KERNEL): 0 "stream" k1_stream + k1_compact (default),
+  // K1 implementation (MICRO_K1_KERNEL): 0 "stream" k1_stream + k1_gather (default),
   // 1 "tma" persistent k1_tma_select, 2 "tile" k1_fused_select (also the
   // fallback for gradients that are not 16-byte aligned)
   int k1_kind = 0;
