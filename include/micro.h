@@ -233,9 +233,9 @@ typedef struct micro_record {
 int micro_records(micro_ctx* ctx, int64_t max, micro_record* out, int64_t* written);
 
 /* Diagnostics: CUDA-event timing of K1's streaming pass (k1_stream) inside
- * the library.  micro_kernel_timing(1) starts recording (up to 1024 launches,
- * restarting the count); micro_kernel_times synchronises and returns the
- * per-launch durations in ms. */
+ * the library.  micro_kernel_timing(p), p >= 1, starts recording every p-th
+ * launch (up to 1024 recorded, restarting the count; 0 stops);
+ * micro_kernel_times synchronises and returns the per-launch durations in ms. */
 int micro_kernel_timing(micro_ctx* ctx, int enable);
 int micro_kernel_times(micro_ctx* ctx, float* ms, int max, int* written);
 

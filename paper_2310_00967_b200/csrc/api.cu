@@ -347,7 +347,9 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
   cudaStream_t st = c->stream;
-  const bool timed = c->timing && c->t_next < kTimingCap;
+  // every timing_period-th launch (event records between kernels cost the step
+  // a few µs at small sizes, so long runs sample)
+  const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
 #define K1S(MODE, D) k1_stream<T, MODE, D, false><<<grid, kStreamThreads, 0, st>>>(a)
 #define K1N(D)                                                                       \
@@ -1007,7 +1009,10 @@ int micro_kernel_timing(micro_ctx* c, int enable) {
     c->t_ev.resize(2 * kTimingCap);
     for (auto& ev : c->t_ev) CU(cudaEventCreate(&ev));
   }
+  if (enable < 0) return fail(MICRO_EINVAL, "timing period must be >= 0");
   c->timing = enable != 0;
+  c->timing_period = enable > 0 ? enable : 1;
+  c->t_seen = 0;
   c->t_next = 0;
   return MICRO_OK;
 }

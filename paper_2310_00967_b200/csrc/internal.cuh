@@ -167,6 +167,8 @@ struct micro_ctx {
   bool fin_done = false;    // this step's finalize already ran inside k1_gather
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
   bool timing = false;
+  int timing_period = 1;   // record every timing_period-th k1_stream launch
+  int64_t t_seen = 0;
   int t_next = 0;
   std::vector<cudaEvent_t> t_ev;
   unsigned long long* dense_dirty = nullptr;

@@ -203,9 +203,10 @@ class Micro:
         check(lib().micro_records(self._h, n, buf, C.byref(w)))
         return [{f: getattr(buf[i], f) for f, _ in _lib.micro_record._fields_} for i in range(w.value)]
 
-    def kernel_timing(self, enable: bool = True):
-        """Record CUDA-event durations of K1's streaming pass (diagnostics)."""
-        check(lib().micro_kernel_timing(self._h, int(enable)))
+    def kernel_timing(self, enable: bool = True, every: int = 1):
+        """Record CUDA-event durations of K1's streaming pass (diagnostics),
+        every `every`-th launch."""
+        check(lib().micro_kernel_timing(self._h, every if enable else 0))
 
     def kernel_times(self, max_n: int = 1024) -> np.ndarray:
         out = np.empty(max_n, np.float32)
