@@ -351,11 +351,11 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   // a few µs at small sizes, so long runs sample)
   const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
-#define K1S(MODE, D) k1_stream<T, MODE, D, false><<<grid, kStreamThreads, 0, st>>>(a)
-#define K1N(D)                                                                       \
-  do {                                                                               \
-    if (c->norm) k1_stream<T, kWriteZeroSel, D, true><<<grid, kStreamThreads, 0, st>>>(a); \
-    else K1S(kWriteZeroSel, D);                                                      \
+#define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(grid), dim3(kStreamThreads), st, a))
+#define K1N(D)                                                                                              \
+  do {                                                                                                      \
+    if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(grid), dim3(kStreamThreads), st, a)); \
+    else K1S(kWriteZeroSel, D);                                                                             \
   } while (0)
   if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
   if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
@@ -419,8 +419,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.fin_slot = c->steps % kHistCap;
     gblocks += 1;
   }
-  k1_gather<T><<<gblocks, kGatherWarps * 32, 0, c->stream>>>(b);
-  CU(cudaGetLastError());
+  CU(launch_maybe_pdl(c->pdl, k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
   return MICRO_OK;
 }
 
@@ -766,6 +765,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     const char* k = std::getenv("MICRO_K1_KERNEL");
     c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
     if (c->kind) c->k1_kind = 0;  // the baselines compact with the streaming K1
+    if (const char* p = std::getenv("MICRO_PDL")) c->pdl = std::atoi(p) != 0;
     c->dense_fused = c->sel_is_union && cfg->dense_output && c->k1_kind == 0;
     c->use_tma = c->k1_kind != 2;
     const char* cf = std::getenv("MICRO_K1_CFG");

@@ -141,6 +141,13 @@ __device__ __forceinline__ double ld_rand(const double* p) {
   return v;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic
+// stream serialization may start while its predecessor drains; it must wait
+// for the predecessor's completion (and memory) before touching its results.
+// Both are no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Drop a 128-byte L2 line without writing it back (its content is dead).
 __device__ __forceinline__ void discard_l2_line(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");

@@ -75,6 +75,23 @@ int h_update_threshold(double* delta, uint64_t k_target, uint64_t k_sel, double 
 constexpr int64_t kHistCap = 4096;
 constexpr int kTimingCap = 1024;
 
+// Launch with programmatic stream serialization (PDL) when `pdl`: the kernel
+// may begin while its predecessor drains and waits in pdl_wait().
+template <typename... P, typename... A>
+cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(P...), dim3 grid, dim3 block, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+
 template <typename T>
 int64_t p_max_for(int64_t range) {
   return (range + tile_elems<T>() - 1) / tile_elems<T>() + 2;
@@ -166,6 +183,7 @@ struct micro_ctx {
   bool fuse_step = false;   // set for the duration of micro_step
   bool fin_done = false;    // this step's finalize already ran inside k1_gather
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
+  bool pdl = true;          // programmatic dependent launch between the step's kernels (MICRO_PDL=0: off)
   bool timing = false;
   int timing_period = 1;   // record every timing_period-th k1_stream launch
   int64_t t_seen = 0;

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   __shared__ int s_cnt[kStreamWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int u = blockIdx.x * kStreamWarps + w;
+  pdl_wait();  // the previous step's gather / finalize (staging, counts, delta) is done
   const int base = u * UE;
   // warps past the vector's end idle but still meet the CTA barrier below
   const int elems = base >= a.n_g ? 0 : (a.n_g - base < UE ? a.n_g - base : UE);
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     }
   }
   if (probe != probe) atomicOr(a.flags, 1);
+  pdl_trigger();  // this CTA's results are written: k1_gather may start launching
   if (kNorm) {  // the stored e_{t+1}: acc with the own selections zeroed (EF on)
     double sq = 0.0;
 #pragma unroll
@@ -364,6 +366,8 @@ template <typename T>
 __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   __shared__ long long s_part[kGatherWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  pdl_wait();  // k1_stream's runs and counts are complete and visible
+  pdl_trigger();
   // norm on: CTA 0 (scheduled first, overlapping the copies) reduces
   // ||e_{t+1}||^2 in a fixed order; the copy CTAs are 1..
   if (a.sq_part && blockIdx.x == 0) {
