@@ -153,15 +153,17 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
     // dense (fused into K1) and model (k1_gather) are done too
     c->fin_done = false;
   } else {
+    bool waited = false;  // an event wait or a clear kernel sits between: launch normally
     if (c->clear_pending) {
       CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
       c->clear_pending = false;
+      waited = true;
     } else if (f.prev_idx) {
+      waited = true;
       k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
       CU(cudaGetLastError());
     }
-    k_finalize<T><<<blocks, 256, 0, c->stream>>>(f);
-    CU(cudaGetLastError());
+    CU(launch_maybe_pdl(c->pdl && !waited, k_finalize<T>, dim3(blocks), dim3(256), c->stream, f));
   }
   if (!c->cfg.error_feedback && c->n > 1)
     for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
@@ -595,13 +597,13 @@ int aggregate_cluster(micro_ctx* c) {
   const unsigned gx = (unsigned)std::min<int64_t>((expect + 255) / 256, 2048);
   const dim3 grid(gx, (unsigned)c->n);
   if (c->cfg.error_feedback)
-    k_cluster_reduce<T, true><<<grid, 256, 0, c->stream>>>(w, c->counts, c->sel_cap, c->n, c->t_cur,
-                                                            c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
-                                                            c->norm ? c->norm_corr : nullptr);
+    CU(launch_maybe_pdl(c->pdl, k_cluster_reduce<T, true>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
+                        (long long)c->sel_cap, c->n, (int64_t)c->t_cur, c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
+                        c->norm ? c->norm_corr : (double*)nullptr));
   else
-    k_cluster_reduce<T, false><<<grid, 256, 0, c->stream>>>(w, c->counts, c->sel_cap, c->n, c->t_cur,
-                                                             c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
-                                                             nullptr);
+    CU(launch_maybe_pdl(c->pdl, k_cluster_reduce<T, false>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
+                        (long long)c->sel_cap, c->n, (int64_t)c->t_cur, c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
+                        (double*)nullptr));
   CU(cudaGetLastError());
   return launch_finalize<T>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 1);
 }

@@ -43,6 +43,8 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
   // ||e||^2 by k_finalize.  Lane r of each warp accumulates worker r
   // (r + 32 in a second register); one global atomic per block and worker.
   __shared__ double s_corr[8][kMaxWorkers];
+  pdl_wait();  // the workers' K1 results are complete
+  pdl_trigger();
   const int p = blockIdx.y;
   const int owner = partition_owner(p, n, t);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -234,6 +236,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
   constexpr int SEC = 32 / (int)sizeof(T);  // elements per 32-byte sector
   __shared__ long long s_K;
+  pdl_wait();  // the union and counts are complete
+  pdl_trigger();
   if (threadIdx.x == 0) {
     long long K;
     if (a.k_from_counts) {
