@@ -144,3 +144,22 @@ def test_c11_determinism(tmp_path):
         outs.append(p.read_bytes())
         m.close()
     assert outs[0] == outs[1]
+
+
+def test_harness_single_worker_and_exclusivity():
+    """test_harness.cpp:78-103: one worker's union is its own selection; four
+    workers: exclusive, build-up free, density exactly sum(k_i) / n_g."""
+    m, _ = _run(10_000, 1, 50, density=0.02, initial_threshold=0.02)
+    for r in m.records(50):
+        assert r["K"] == r["total_selected"]
+    st = m.query()
+    idx, _ = m.union()
+    pi, pv, pc = m.selection_device(0)
+    assert int(pc.item()) == st.counts[0] == idx.size
+    m.close()
+    m, _ = _run(1024, 4, 50, density=0.02, initial_threshold=0.02)
+    for r in m.records(50):
+        assert r["K"] == r["total_selected"]
+        assert r["actual_density"] == r["total_selected"] / 1024
+        assert r["redundant_traffic_factor"] == (1.0 if r["total_selected"] else 0.0)
+    m.close()

@@ -203,3 +203,19 @@ def test_cltk_and_select_all():
         S.cltk_select(acc, 9, 1, 5, 4)
     a = S.select_all(acc)
     assert a.indices.tolist() == [0, 1, 2, 3] and a.values.tolist() == [1, -3, 0.5, 2]
+
+
+def test_spec_examples_error_metric_accumulate():
+    """SPEC.md:200-220 (error_metric, accumulate examples)."""
+    assert S.error_metric([torch.zeros(5, dtype=torch.float64, device="cuda")]) == 0.0
+    e0 = vec([3.0, 0.0])  # ||e0|| = 3
+    e1 = vec([3.0, 4.0])  # ||e1|| = 5
+    assert S.error_metric([e0, e1]) == 4.0
+    assert S.error_metric([e1]) == 5.0
+    g = vec([1.0, 2.0, -0.5])
+    e = torch.zeros(3, dtype=torch.float64, device="cuda")
+    norms = []
+    for _ in range(5):  # no selection, fixed-sign gradient: ||e|| grows monotonically
+        e = S.accumulate(e, 0.5, g)
+        norms.append(S.error_metric([e]))
+    assert all(b > a for a, b in zip(norms, norms[1:]))
