@@ -179,6 +179,8 @@ def our_arm(args, wl):
     dev = torch.device("cuda", local)
     n_g, d = wl["n_g"], wl["d"]
     delta0 = warm_delta0(d)
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    esz = 8 if args.dtype == "f64" else 4
     # W workers per process: 1 (one per GPU), or --cluster-workers W at N = 1:
     # the reference's own in-process cluster (harness.cpp:121-224) on one GPU
     W = args.cluster_workers if (world == 1 and args.cluster_workers > 1) else 1
@@ -193,16 +195,16 @@ def our_arm(args, wl):
             tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
         m = DistMicro(n_g, transport=args.transport, density=d, initial_threshold=delta0, scaling_factor=ALPHA,
-                      dense_output=args.dense, record_error_norm=args.error_norm,
+                      dense_output=args.dense, record_error_norm=args.error_norm, dtype=tdt,
                       comm_device="cpu" if args.dist_backend == "gloo" else None)
     else:
         m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
-                         record_error_norm=args.error_norm, sparsifier=args.sparsifier)
+                         record_error_norm=args.error_norm, sparsifier=args.sparsifier, dtype=tdt)
     stream = torch.cuda.current_stream(dev)
     # the model update x -= g/n at the union is part of the reference's
     # iteration (harness.cpp:212-215); a dense g/n is not (run_iteration uses
     # the sparse sums), so it is materialised only with --dense
-    model = torch.zeros(n_g, device=dev)
+    model = torch.zeros(n_g, device=dev, dtype=tdt)
     if args.model:
         m.set_model(model)
 
@@ -213,7 +215,7 @@ def our_arm(args, wl):
     # per step when memory allows (same statistics as the prime phase),
     # otherwise R buffers rotated.
     t = 0
-    gen = [torch.empty(n_g, device=dev) for _ in range(W)]
+    gen = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(W)]
     for _ in range(args.prime):
         for i in range(W):
             engine.synth_gaussian(gen[i], SEED, rank + i, t)
@@ -222,8 +224,8 @@ def our_arm(args, wl):
     del gen
     torch.cuda.synchronize()
     need = (args.warmup + args.steps) * W
-    R = max(W + 1, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (4 * n_g))))
-    G = [torch.empty(n_g, device=dev) for _ in range(R)]
+    R = max(W + 1, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (esz * n_g))))
+    G = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(R)]
     for r in range(R):
         engine.synth_gaussian(G[r], SEED, rank + r % W, t + r)
     t0_bufs = t
@@ -280,14 +282,14 @@ def our_arm(args, wl):
     # (dense has no selection pass: the whole step stands in for the kernel)
     k1a_avg_ms = statistics.mean(k1a_ms) if k1a_ms else ms_step
     # algorithmic bytes of the dominant kernel, k1_stream: read e and G, write
-    # e (all n_g) + one (int32, fp32) pair per selection
-    k1_bytes = 12.0 * n_g + 8.0 * float(k_own.mean())
+    # e (all n_g) + one (int32, value) pair per selection
+    k1_bytes = 3.0 * esz * n_g + (4.0 + esz) * float(k_own.mean())
     achieved = k1_bytes / (k1a_avg_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     # whole step vs the same roofline: K1 bytes + union (8 B) and, with the
     # model update, x read+write (8 B) per union entry
-    step_bytes = (W * k1_bytes + 8.0 * float(K.mean()) * (2 if args.model else 1)
-                  + (8.0 * float(K.mean()) * W if W > 1 else 0.0))  # cluster reduce: W reads + zeroing
+    step_bytes = (W * k1_bytes + (4.0 + esz) * float(K.mean()) + (2.0 * esz * float(K.mean()) if args.model else 0.0)
+                  + (2.0 * esz * float(K.mean()) * W if W > 1 else 0.0))  # cluster reduce: W reads + zeroing
     # our kernels per step: k1_stream, k1_gather (+ threshold update + model
     # update) at n = 1; a W-worker cluster: 2 per worker + k_cluster_reduce +
     # k_finalize; n > 1 ranks: K1 x2, gather_foreign, owner_reduce,
@@ -308,16 +310,16 @@ def our_arm(args, wl):
         # as the timed steps; re-feeding one gradient would make the residual
         # grow coherently and inflate the selection)
         ke = max(3, min(args.steps, 10))
-        nb = int(max(2, min(ke + 1, 8e9 // (4 * n_g * W))))  # <= 8 GB of pinned host gradients
+        nb = int(max(2, min(ke + 1, 8e9 // (esz * n_g * W))))  # <= 8 GB of pinned host gradients
         hGs = []
         for b in range(nb):
-            hG = torch.empty(W * n_g, dtype=torch.float32).pin_memory()
+            hG = torch.empty(W * n_g, dtype=tdt).pin_memory()
             for i in range(W):
                 engine.synth_gaussian(G[i], SEED, rank + i, t + 1 + b)  # fresh: steps t+1 .. t+nb
                 hG[i * n_g:(i + 1) * n_g].copy_(G[i].cpu())
             hGs.append(hG)
         idx = torch.empty(n_g, dtype=torch.int32).pin_memory().numpy()  # pinned result buffers
-        sums = torch.empty(n_g, dtype=torch.float32).pin_memory().numpy()
+        sums = torch.empty(n_g, dtype=tdt).pin_memory().numpy()
         m.step_host(hGs[-1], ETA, t, idx, sums)  # warm (staging allocation); its gradient is not reused
         t += 1
         kk = []
@@ -327,22 +329,22 @@ def our_arm(args, wl):
             kk.append(i_.size)
             t += 1
         e2e_s = (time.perf_counter() - t0) / ke
-        e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": 4 * n_g * W,
-               "d2h_bytes_per_step": int(8 * statistics.mean(kk) + 8 + 4),
+        e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g * W,
+               "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
                "host_gradients": f"{nb - 1} distinct pinned buffers over {ke} steps",
                "density": float(statistics.mean(kk)) / n_g}
     else:
         # N ranks: each copies its own pinned host gradient in, steps through
         # DistMicro, and reads the union back; the max over ranks is reported
         ke = max(3, min(args.steps, 10))
-        nb = int(max(2, min(ke + 1, 4e9 // (4 * n_g))))
+        nb = int(max(2, min(ke + 1, 4e9 // (esz * n_g))))
         hGs = []
         for b in range(nb):
             engine.synth_gaussian(G[0], SEED, rank, t + 1 + b)
             hGs.append(G[0].cpu().pin_memory())
-        dG = torch.empty(n_g, device=dev)
+        dG = torch.empty(n_g, device=dev, dtype=tdt)
         idx = torch.empty(n_g, dtype=torch.int32).pin_memory().numpy()
-        sums = torch.empty(n_g, dtype=torch.float32).pin_memory().numpy()
+        sums = torch.empty(n_g, dtype=tdt).pin_memory().numpy()
         dG.copy_(hGs[-1], non_blocking=True)
         m.step([dG], ETA, t)
         m.union(idx, sums)
@@ -361,8 +363,8 @@ def our_arm(args, wl):
         v = torch.tensor([(time.perf_counter() - t0) / ke], device=dev if args.dist_backend == "nccl" else "cpu",
                          dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(v[0]) * 1e6, "unit": "us/iter", "h2d_bytes_per_step": 4 * n_g,
-               "d2h_bytes_per_step": int(8 * statistics.mean(kk) + 8 + 4),
+        e2e = {"value": float(v[0]) * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g,
+               "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
                "host_gradients": f"{nb - 1} distinct pinned buffers per rank over {ke} steps",
                "density": float(statistics.mean(kk)) / n_g, "per": "rank (max over ranks)"}
 
@@ -394,7 +396,8 @@ def our_arm(args, wl):
         line = {
             "metric": METRIC, "value": ms_step * 1e3, "unit": "us/iter", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) fp32 gradients (include/micro_synth.h)",
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": f"synthetic N(0,1) {args.dtype} gradients (include/micro_synth.h)",
             "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world * W,
                        "one_worker_per_gpu": W == 1, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
@@ -403,8 +406,8 @@ def our_arm(args, wl):
                        "sparsifier": args.sparsifier,
                        "inputs": (f"{R} resident N(0,1) gradients ("
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
-                                  + "); each 4*n_g bytes > L2 (no flush needed)")
-                       if 4 * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
+                                  + f"); each {esz}*n_g bytes > L2 (no flush needed)")
+                       if esz * n_g > 126e6 else "resident gradients; L2 not flushed (smaller than L2)",
                        "parallelism": (f"dp{world} (exclusive cyclic partitions"
                                        + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
                                        f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
@@ -452,6 +455,8 @@ def main():
                     help="gloo: exercise the N > 1 path with all ranks on one GPU (code check only)")
     ap.add_argument("--transport", choices=["peer", "peer_pull", "nccl"], default="peer",
                     help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
+    ap.add_argument("--dtype", choices=["f32", "f64"], default="f32",
+                    help="f64: the reference's own arithmetic (bit-exact with its code)")
     ap.add_argument("--error-norm", action="store_true",
                     help="also record the per-step error norm ||e_{t+1}|| (fused into k1_stream); off by "
                          "default, like the reference arm's timed step")
