@@ -323,7 +323,7 @@ int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps,
 
 template <typename T>
 int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe,
-                     const double* thr = nullptr, const long long* tie = nullptr) {
+                     const double* thr = nullptr, const long long* tie = nullptr, bool acc_in_e = false) {
   constexpr int UE = stream_unit_elems<T>();
   StreamArgs a{};
   a.grad = grad;
@@ -361,7 +361,11 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   } while (0)
   if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
   if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
-    if (tie) k1_stream<T, kWriteAcc, false, false, true><<<grid, kStreamThreads, 0, st>>>(a);
+    if (acc_in_e)  // top-k: e holds acc already; compact only
+      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(grid),
+                          dim3(kStreamThreads), st, a));
+    else if (tie)
+      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(grid), dim3(kStreamThreads), st, a));
     else K1S(kWriteAcc, false);
   } else if (c->n > 1) {
     if (c->cfg.error_feedback) K1N(false);
@@ -452,22 +456,26 @@ int launch_baseline(micro_ctx* c, int i, const void* grad, double eta, int64_t t
   CU(cudaGetLastError());
   const int bits = KeyOf<T>::kBits;
   const unsigned hgrid = (unsigned)std::min<int64_t>((n_g + 255) / 256, 4 * (int64_t)num_sms(c->dev));
+  T* acc = (T*)c->resid[i];
   for (int hi = bits; hi > 0; hi -= kDigitBits) {  // MSB-first digits of <= 11 bits
     const int width = std::min(kDigitBits, hi);
     const int shift = hi - width;
-    k_topk_hist<T><<<hgrid, 256, 0, st>>>((const T*)c->resid[i], (const T*)grad, eta, n_g, shift, width, ts,
-                                          c->topk_hist);
+    if (hi == bits)  // the first pass forms acc = e + eta*G once and keeps it in e
+      k_topk_hist<T><<<hgrid, 256, 0, st>>>(acc, (const T*)grad, eta, n_g, shift, width, ts, c->topk_hist, acc,
+                                            c->flags);
+    else  // later passes, ties and the compaction read acc alone
+      k_topk_hist<T><<<hgrid, 256, 0, st>>>(acc, nullptr, eta, n_g, shift, width, ts, c->topk_hist);
     CU(cudaGetLastError());
     k_topk_digit<T><<<1, 1024, 0, st>>>(ts, c->topk_hist, shift, width, shift == 0, n_g);
     CU(cudaGetLastError());
   }
   const int64_t chunk = (n_g + kTieChunks - 1) / kTieChunks;
   const int nch = (int)((n_g + chunk - 1) / chunk);
-  k_tie_count<T><<<nch, 256, 0, st>>>((const T*)c->resid[i], (const T*)grad, eta, n_g, chunk, ts, c->tie_counts);
+  k_tie_count<T><<<nch, 256, 0, st>>>(acc, nullptr, eta, n_g, chunk, ts, c->tie_counts);
   CU(cudaGetLastError());
-  k_tie_find<T><<<1, 1024, 0, st>>>((const T*)c->resid[i], (const T*)grad, eta, n_g, chunk, nch, ts, c->tie_counts);
+  k_tie_find<T><<<1, 1024, 0, st>>>(acc, nullptr, eta, n_g, chunk, nch, ts, c->tie_counts);
   CU(cudaGetLastError());
-  return launch_k1_stream<T>(c, i, grad, eta, 0, n_g, &ts->pivot, &ts->tie_j);
+  return launch_k1_stream<T>(c, i, grad, eta, 0, n_g, &ts->pivot, &ts->tie_j, /*acc_in_e=*/true);
 }
 
 template <typename T>

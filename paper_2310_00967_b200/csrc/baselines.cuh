@@ -87,11 +87,15 @@ __device__ __forceinline__ void hist_add(unsigned* s_hist, T acc, unsigned long 
 }
 
 // 16-byte loads of e and G (the same acc = e + eta*G as K1), every lane
-// keeping two vectors of each in flight.
+// keeping two vectors of each in flight.  With acc_out (the first digit of
+// the engine's top-k) acc is also written back in place and G probed for
+// non-finite values, so the later passes and the compaction read acc alone
+// (4 instead of 8 bytes per element).
 template <typename T>
-__global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
-                                                   int64_t n_g, int shift, int width, const TopkState* st,
-                                                   unsigned* __restrict__ hist) {
+__global__ void __launch_bounds__(256) k_topk_hist(const T* e, const T* __restrict__ g, double eta_d, int64_t n_g,
+                                                   int shift, int width, const TopkState* st,
+                                                   unsigned* __restrict__ hist, T* acc_out = nullptr,
+                                                   int* flags = nullptr) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
   __shared__ unsigned s_hist[kBins * kHistCopies];
@@ -110,12 +114,19 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
       if (c) atomicAdd(&hist[b], c);
     }
   };
+  T probe = (T)0;  // NaN iff some G is Inf/NaN (acc_out passes only)
   if (((uintptr_t)e % 16) || ((uintptr_t)g % 16)) {  // a range of the value API: scalar loads
     for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n_g; j0 += stride) {
       const int64_t j = j0 + threadIdx.x;
       const bool ok = j < n_g;
-      hist_add<T>(s_hist, ok ? acc_at(e, g, eta, j) : (T)0, prefix, mask, shift, dmask, ok);
+      const T acc = ok ? acc_at(e, g, eta, j) : (T)0;
+      if (ok && acc_out) {
+        probe = probe + g[j] * (T)0;
+        acc_out[j] = acc;
+      }
+      hist_add<T>(s_hist, acc, prefix, mask, shift, dmask, ok);
     }
+    if (flags && probe != probe) atomicOr(flags, 1);
     flush();
     return;
   }
@@ -133,19 +144,30 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* __restrict__ e, cons
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+    for (int u = 0; u < 2; ++u) {
+      V av;
 #pragma unroll
       for (int c = 0; c < VN; ++c) {
         const T acc = !ok[u] ? (T)0 : g ? add_rn(comp(ev[u], c), mul_rn(eta, comp(gv[u], c))) : comp(ev[u], c);
+        set_comp(av, c, acc);
+        if (acc_out && ok[u]) probe = probe + comp(gv[u], c) * (T)0;
         hist_add<T>(s_hist, acc, prefix, mask, shift, dmask, ok[u]);
       }
+      if (acc_out && ok[u]) st_stream(reinterpret_cast<V*>(acc_out) + v0 + u * blockDim.x + threadIdx.x, av);
+    }
   }
   // the tail (n_g % VN elements)
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const int64_t j = nv * VN + threadIdx.x;
     const bool ok = j < n_g;
-    hist_add<T>(s_hist, ok ? acc_at(e, g, eta, j) : (T)0, prefix, mask, shift, dmask, ok);
+    const T acc = ok ? acc_at(e, g, eta, j) : (T)0;
+    if (ok && acc_out) {
+      probe = probe + g[j] * (T)0;
+      acc_out[j] = acc;
+    }
+    hist_add<T>(s_hist, acc, prefix, mask, shift, dmask, ok);
   }
+  if (flags && probe != probe) atomicOr(flags, 1);
   flush();
 }
 

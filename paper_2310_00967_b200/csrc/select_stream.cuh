@@ -84,7 +84,9 @@ __device__ __forceinline__ unsigned even_bits(unsigned x) {
 __device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
 
-template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false>
+// kNoG (top-k baseline): e already holds acc (written by the first histogram
+// pass), G is not read.
+template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false>
 __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       e[i] = ld_hint(reinterpret_cast<const V*>(E) + i * 32 + lane, pol_stream);
-      g[i] = ld_nc_hint(reinterpret_cast<const V*>(Gp) + i * 32 + lane, pol_stream);
+      if (!kNoG) g[i] = ld_nc_hint(reinterpret_cast<const V*>(Gp) + i * 32 + lane, pol_stream);
     }
   } else {  // the vector's last, partial unit
 #pragma unroll
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
       for (int c = 0; c < VN; ++c) {
         const int off = (i * 32 + lane) * VN + c;
         set_comp(e[i], c, off < elems ? E[off] : (T)0);
-        set_comp(g[i], c, off < elems ? Gp[off] : (T)0);
+        set_comp(g[i], c, (!kNoG && off < elems) ? Gp[off] : (T)0);
       }
   }
 
@@ -136,9 +138,14 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
     mask[i] = 0;
 #pragma unroll
     for (int c = 0; c < VN; ++c) {
-      const T gv = comp(g[i], c);
-      probe = nan_probe_s(gv, probe);
-      const T acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
+      T acc;
+      if (kNoG) {
+        acc = comp(e[i], c);
+      } else {
+        const T gv = comp(g[i], c);
+        probe = nan_probe_s(gv, probe);
+        acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
+      }
       set_comp(e[i], c, acc);
       bool sel = sel_unit && absx(acc) > thr;
       if (kTie && sel_unit && absx(acc) == thr)  // top-k: ties at the pivot up to index J
