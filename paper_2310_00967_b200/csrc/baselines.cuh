@@ -131,6 +131,22 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* e, const T* __restri
     return;
   }
   const int64_t nv = n_g / VN;  // whole vectors (e, G 16-byte aligned: K1 staging / cudaMalloc)
+  if (!g) {  // acc alone: four vectors per thread in flight
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * 4; v0 < nv; v0 += 4 * stride) {  // warp-uniform
+      V ev[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t v = v0 + u * blockDim.x + threadIdx.x;
+        ok[u] = v < nv;
+        if (ok[u]) ev[u] = ld_stream(reinterpret_cast<const V*>(e) + v);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < VN; ++c) hist_add<T>(s_hist, ok[u] ? comp(ev[u], c) : (T)0, prefix, mask, shift, dmask, ok[u]);
+    }
+  } else
   for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * 2; v0 < nv; v0 += 2 * stride) {  // warp-uniform
     V ev[2], gv[2];
     bool ok[2];
