@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl"):
+def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl", f64=False):
     import sys
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Oracle, OracleCluster
@@ -28,18 +28,19 @@ def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl"):
     torch.cuda.set_device(0)
     o = Oracle()
     d, delta0, eta = 0.02, 0.015, 0.01
+    tdt, ndt = (torch.float64, np.float64) if f64 else (torch.float32, np.float32)
     m = DistMicro(n_g, comm_device="cpu", transport=transport, density=d, initial_threshold=delta0,
-                  error_feedback=ef)
-    x = torch.zeros(n_g, device="cuda")
+                  error_feedback=ef, dtype=tdt)
+    x = torch.zeros(n_g, device="cuda", dtype=tdt)
     m.set_model(x)
-    ref = OracleCluster(n_g, world, density=d, delta0=delta0, error_feedback=ef, model=True)
+    ref = OracleCluster(n_g, world, density=d, delta0=delta0, error_feedback=ef, model=True, dtype=ndt)
     bad = []
     want = []
     for t in range(iters):
         thr = 0.0
         for dl in ref.delta:
             thr += float(dl)
-        G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)])
+        G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)]).astype(ndt)
         K = m.step([torch.from_numpy(G[rank]).cuda()], eta, t)
         r = ref.step(G, eta, t)
         idx, sums = m.union()
@@ -56,8 +57,8 @@ def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl"):
             bad.append((t, "residual"))
         if st.deltas[0] != r["delta_next"][rank]:
             bad.append((t, "delta"))
-        dw = np.zeros(n_g, np.float32)
-        dw[r["union_idx"]] = r["union_sum"] / np.float32(world)
+        dw = np.zeros(n_g, ndt)
+        dw[r["union_idx"]] = r["union_sum"].astype(ndt) / ndt(world)
         if not np.array_equal(m.dense(), dw):
             bad.append((t, "dense"))
         if not np.array_equal(x.cpu().numpy(), ref.x):
@@ -95,6 +96,22 @@ def test_dist_device_halves_one_gpu(world, n_g, ef, transport):
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, bad in res:
+        assert not bad, (rank, bad[:5])
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_dist_f64_one_gpu(transport):
+    """fp64 ranks (the reference's arithmetic) through both exchanges."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 30_000, 8, True, q, transport, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
     for p in procs:
         p.join(timeout=60)
     for rank, bad in res:
