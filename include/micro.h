@@ -299,6 +299,14 @@ int micro_peer_finalize(micro_ctx* ctx);
 int micro_peer_contribute(micro_ctx* ctx);
 int micro_peer_reduce(micro_ctx* ctx);
 
+/* One process driving all n ranks (SURVEY.md 8b "micro_aggregate_all"):
+ * ctxs[r] is rank r's context (n_local = 1, on any device); attach maps the
+ * buffers directly (peer access between distinct devices, no IPC), and
+ * micro_group_step runs compress -> contribute -> reduce -> finalize on every
+ * rank's stream with event barriers between the phases (no host sync). */
+int micro_group_attach(micro_ctx* const* ctxs, int n);
+int micro_group_step(micro_ctx* const* ctxs, int n, const void* const* d_grads, double eta, int64_t t);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,6 +132,8 @@ _SIGS = {
     "micro_peer_finalize": ([VP], I32),
     "micro_peer_contribute": ([VP], I32),
     "micro_peer_reduce": ([VP], I32),
+    "micro_group_attach": ([C.POINTER(VP), I32], I32),
+    "micro_group_step": ([C.POINTER(VP), I32, C.POINTER(VP), DBL, I64], I32),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -885,6 +885,7 @@ int micro_ctx_destroy(micro_ctx* c) {
   if (c->staging) cudaFree(c->staging);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->group_ev) cudaEventDestroy(c->group_ev);
 
   if (c->aux) cudaStreamDestroy(c->aux);
   delete c;

@@ -290,4 +290,83 @@ int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_al
 
 // ---- device memory plumbing ----
 
+
+// ---- one process driving all n ranks (peer access instead of CUDA IPC) ----
+
+int micro_group_attach(micro_ctx* const* ctxs, int n) {
+  if (!ctxs || n < 2 || n > MICRO_MAX_WORKERS) return fail(MICRO_EINVAL, "micro_group_attach: need 2..64 contexts");
+  for (int r = 0; r < n; ++r) {
+    TRY(check_peer_ctx(ctxs[r]));
+    if (ctxs[r]->n != n || ctxs[r]->cfg.rank != r)
+      return fail(MICRO_EINVAL, "micro_group_attach: context %d is not rank %d of %d", r, r, n);
+    if (ctxs[r]->peer_ready) return fail(MICRO_ELOGIC, "micro_group_attach: context %d already attached", r);
+    if (ctxs[r]->n_g != ctxs[0]->n_g || ctxs[r]->esz != ctxs[0]->esz || ctxs[r]->norm != ctxs[0]->norm)
+      return fail(MICRO_EINVAL, "micro_group_attach: contexts disagree on n_g / dtype / error norm");
+  }
+  for (int r = 0; r < n; ++r) {  // peer access between distinct devices, receive slabs
+    micro_ctx* c = ctxs[r];
+    DeviceGuard dg(c->dev);
+    for (int q = 0; q < n; ++q) {
+      const int d = ctxs[q]->dev;
+      if (d == c->dev) continue;
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, c->dev, d));
+      if (!can) return fail(MICRO_ECUDA, "device %d cannot access device %d", c->dev, d);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(MICRO_ECUDA, "cudaDeviceEnablePeerAccess(%d): %s", d, cudaGetErrorString(e));
+      cudaGetLastError();  // clear "already enabled"
+    }
+    if (!c->recv) TRY(c->alloc(&c->recv, (size_t)c->n * c->sel_cap * c->esz));
+    if (!c->group_ev) CU(cudaEventCreateWithFlags(&c->group_ev, cudaEventDisableTiming));
+  }
+  for (int r = 0; r < n; ++r) {
+    micro_ctx* c = ctxs[r];
+    for (int q = 0; q < n; ++q) {
+      micro_ctx* o = ctxs[q];
+      c->peer_resid[q] = o->resid[0];
+      c->peer_counts[q] = o->counts;
+      c->peer_uidx[0][q] = o->uni_idx[0];
+      c->peer_uidx[1][q] = o->uni_idx[1];
+      c->peer_usum[0][q] = o->uni_sum[0];
+      c->peer_usum[1][q] = o->uni_sum[1];
+      c->peer_corr[q] = c->norm ? o->norm_corr : nullptr;
+      c->peer_sel[0][q] = o->sel_idx[0][0];
+      c->peer_sel[1][q] = o->sel_idx[1][0];
+      c->peer_recv[q] = o->recv;
+    }
+    c->peer_ready = true;
+  }
+  return MICRO_OK;
+}
+
+// every context's stream waits for every other's work so far (a device-side
+// barrier built from events: the host never blocks)
+static int group_barrier(micro_ctx* const* ctxs, int n) {
+  for (int r = 0; r < n; ++r) {
+    DeviceGuard dg(ctxs[r]->dev);
+    CU(cudaEventRecord(ctxs[r]->group_ev, ctxs[r]->stream));
+  }
+  for (int r = 0; r < n; ++r) {
+    DeviceGuard dg(ctxs[r]->dev);
+    for (int q = 0; q < n; ++q)
+      if (q != r) CU(cudaStreamWaitEvent(ctxs[r]->stream, ctxs[q]->group_ev, 0));
+  }
+  return MICRO_OK;
+}
+
+int micro_group_step(micro_ctx* const* ctxs, int n, const void* const* d_grads, double eta, int64_t t) {
+  if (!ctxs || !d_grads || n < 2) return fail(MICRO_EINVAL, "micro_group_step: bad arguments");
+  for (int r = 0; r < n; ++r)
+    if (!ctxs[r] || !ctxs[r]->peer_ready) return fail(MICRO_ELOGIC, "micro_group_step before micro_group_attach");
+  for (int r = 0; r < n; ++r) TRY(micro_compress(ctxs[r], d_grads + r, eta, t));
+  TRY(group_barrier(ctxs, n));
+  for (int r = 0; r < n; ++r) TRY(micro_peer_contribute(ctxs[r]));
+  TRY(group_barrier(ctxs, n));
+  for (int r = 0; r < n; ++r) TRY(micro_peer_reduce(ctxs[r]));
+  TRY(group_barrier(ctxs, n));
+  for (int r = 0; r < n; ++r) TRY(micro_peer_finalize(ctxs[r]));
+  return MICRO_OK;
+}
+
 }  // extern "C"

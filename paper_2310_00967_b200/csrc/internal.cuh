@@ -217,6 +217,7 @@ struct micro_ctx {
   void* peer_recv[kMaxWorkers] = {};
   void* recv = nullptr;          // bulk exchange: receive slabs [source rank][sel_cap] (lazy)
   int peer_phase = 0;            // 0 idle, 1 contributed (bulk), 2 exchanged (ready to finalize)
+  cudaEvent_t group_ev = nullptr;  // micro_group_step barriers (one process, all ranks)
   std::vector<void*> peer_opened;  // cudaIpcOpenMemHandle mappings to close
 
   int alloc(void** p, size_t bytes) {

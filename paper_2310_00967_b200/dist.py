@@ -230,3 +230,38 @@ class DistMicro:
 
     def __getattr__(self, name):  # query, history, union, residual, dense, set_model, sync ...
         return getattr(self.m, name)
+
+
+class GroupMicro:
+    """One process driving all n ranks (micro_group_*): rank r's context on
+    ``devices[r]`` with its own stream; the exchange runs over direct peer
+    pointers with event barriers, so one host thread enqueues the whole
+    n-GPU step without blocking."""
+
+    def __init__(self, n_g: int, n: int, devices=None, **kw):
+        devices = list(devices) if devices is not None else list(range(n))
+        if len(devices) != n:
+            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, "one device per rank")
+        self.n, self.n_g = n, n_g
+        self.streams = [torch.cuda.Stream(device=d) for d in devices]
+        self.ranks = [Micro(n_g, n, n_local=1, rank=r, device=devices[r], stream=self.streams[r], **kw)
+                      for r in range(n)]
+        self._arr = (C.c_void_p * n)(*[m.handle.value for m in self.ranks])
+        check(lib().micro_group_attach(self._arr, n))
+
+    def step(self, grads, eta: float, t: int) -> None:
+        if len(grads) != self.n:
+            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"expected {self.n} gradients")
+        for m, g in zip(self.ranks, grads):
+            m._grads([g])
+        self._keep = grads
+        ptrs = (C.c_void_p * self.n)(*[g.data_ptr() for g in grads])
+        check(lib().micro_group_step(self._arr, self.n, ptrs, eta, t))
+
+    def synchronize(self):
+        for s in self.streams:
+            s.synchronize()
+
+    def close(self):
+        for m in self.ranks:
+            m.close()
