@@ -546,4 +546,55 @@ class MicroEngine {
   std::size_t esz_;
 };
 
+// The same step with one GPU per worker, driven from one process
+// (micro_group_*): rank r's context lives on devices[r]; the exchange reads
+// the peers' buffers directly (NVLink) between event barriers.  step() takes
+// one device gradient pointer per rank (on that rank's device) and enqueues
+// the whole iteration without blocking; sync() waits for it.
+class MicroGroup {
+ public:
+  MicroGroup(Index n_g, const std::vector<int>& devices, const SparsifierConfig& sc, bool error_feedback = true,
+             int dtype = MICRO_F32)
+      : n_((int)devices.size()) {
+    if (n_ < 2) throw std::invalid_argument("MicroGroup: need at least two ranks");
+    ctxs_.assign((std::size_t)n_, nullptr);
+    for (int r = 0; r < n_; ++r) {
+      micro_config cfg;
+      micro_config_default(&cfg);
+      cfg.n_g = n_g;
+      cfg.n_workers = n_;
+      cfg.n_local = 1;
+      cfg.rank = r;
+      cfg.dtype = dtype;
+      cfg.density = sc.density;
+      cfg.initial_threshold = sc.initial_threshold;
+      cfg.scaling_factor = sc.scaling_factor;
+      cfg.min_threshold = sc.min_threshold;
+      cfg.target = sc.target == PerWorkerTarget::full ? MICRO_TARGET_FULL : MICRO_TARGET_SPLIT;
+      cfg.error_feedback = error_feedback ? 1 : 0;
+      cfg.device = devices[(std::size_t)r];
+      b200::check(micro_ctx_create(&ctxs_[(std::size_t)r], &cfg, nullptr));
+    }
+    b200::check(micro_group_attach(ctxs_.data(), n_));
+  }
+  MicroGroup(const MicroGroup&) = delete;
+  MicroGroup& operator=(const MicroGroup&) = delete;
+  ~MicroGroup() {
+    for (auto* c : ctxs_) micro_ctx_destroy(c);
+  }
+
+  void step(const std::vector<const void*>& d_grads, double eta, std::int64_t t) {
+    if ((int)d_grads.size() != n_) throw std::invalid_argument("MicroGroup::step: one gradient per rank");
+    b200::check(micro_group_step(ctxs_.data(), n_, d_grads.data(), eta, t));
+  }
+  void sync() {
+    for (auto* c : ctxs_) b200::check(micro_sync(c));
+  }
+  micro_ctx* rank(int r) const { return ctxs_.at((std::size_t)r); }
+
+ private:
+  int n_;
+  std::vector<micro_ctx*> ctxs_;
+};
+
 }  // namespace sparsim

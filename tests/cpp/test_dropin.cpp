@@ -225,6 +225,42 @@ int main() {
       CHECK(std::fabs(recs[s].error_norm - want_norm[s]) <= 1e-12 * want_norm[s]);
     }
   }
+  // MicroGroup (one process, one context per rank; here all on device 0)
+  // == MicroEngine (single-device cluster), bit for bit
+  {
+    const Index n_g = 50001;
+    const int n = 3;
+    SparsifierConfig sc;
+    sc.density = 0.02;
+    sc.initial_threshold = 0.02;
+    MicroEngine eng(n_g, n, sc, true, MICRO_F32);
+    MicroGroup grp(n_g, std::vector<int>(n, 0), sc, true, MICRO_F32);
+    std::mt19937_64 rng(9);
+    std::normal_distribution<float> unit(0.0f, 1.0f);
+    std::vector<float> G((std::size_t)(n * n_g));
+    std::vector<void*> d(n);
+    for (int r = 0; r < n; ++r) b200::check(micro_device_malloc(&d[r], (int64_t)n_g * 4, 0));
+    for (int t = 0; t < 8; ++t) {
+      for (auto& v : G) v = unit(rng);
+      std::vector<double> summed;
+      const auto agg = eng.step(G.data(), 0.01, t, &summed);
+      for (int r = 0; r < n; ++r) b200::h2d(d[r], G.data() + (std::size_t)r * n_g, (std::size_t)n_g * 4);
+      grp.step(std::vector<const void*>(d.begin(), d.end()), 0.01, t);
+      grp.sync();
+      for (int r = 0; r < n; ++r) {
+        std::vector<int32_t> idx((std::size_t)n_g);
+        std::vector<float> sums((std::size_t)n_g);
+        int64_t K = 0;
+        b200::check(micro_copy_union(grp.rank(r), idx.data(), sums.data(), n_g, &K));
+        CHECK((std::size_t)K == agg.indices.size());
+        bool same = (std::size_t)K == agg.indices.size();
+        for (int64_t k = 0; same && k < K; ++k)
+          same = idx[(std::size_t)k] == agg.indices[(std::size_t)k] && (double)sums[(std::size_t)k] == summed[(std::size_t)k];
+        CHECK(same);
+      }
+    }
+    for (int r = 0; r < n; ++r) micro_device_free(d[r]);
+  }
   std::printf("%s: %d failed checks\n", g_fail ? "FAIL" : "OK", g_fail);
   return g_fail;
 }
