@@ -87,7 +87,7 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 // kNoG (top-k baseline): e already holds acc (written by the first histogram
 // pass), G is not read.
 template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false>
-__global__ void __launch_bounds__(kStreamThreads, 4) k1_stream(StreamArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(StreamArgs a) {  // acc-only: 51 regs, 5 CTAs/SM
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
   constexpr int UE = stream_unit_elems<T>();
