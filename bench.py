@@ -420,7 +420,8 @@ def our_arm(args, wl):
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
                                   + (f"); L2 flushed between timed steps (256 MB write outside the per-step "
                                      f"events: the working set {3 * esz * n_g / 1e6:.0f} MB would fit L2)"
-                                     if flush else f"); each {esz}*n_g bytes > L2 (no flush needed)")),
+                                     if flush else f"); each {esz}*n_g bytes > L2 (no flush needed)"
+                                     if esz * n_g > 126e6 else "); L2 NOT flushed (--flush-l2 off)")),
                        "parallelism": (f"dp{world} (exclusive cyclic partitions"
                                        + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
                                        f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
