@@ -6,6 +6,9 @@
 // (dist_api.cu: one rank of an n-GPU job; value_api.cu: stateless calls.)
 #include "internal.cuh"
 
+using namespace micro;
+using namespace micro::host;
+
 // ---------------------------------------------------------------- errors --
 
 namespace micro {

@@ -3,6 +3,9 @@
 // exchange over peer memory (peer.cuh).
 #include "internal.cuh"
 
+using namespace micro;
+using namespace micro::host;
+
 extern "C" {
 
 static int dist_counts(micro_ctx* c, const int64_t* h_counts, Counts* out, bool own_segments) {

@@ -100,8 +100,12 @@ int64_t p_max_for(int64_t range) {
 }  // namespace host
 }  // namespace micro
 
-using namespace micro;
-using namespace micro::host;
+// (the translation units bring micro:: and micro::host:: into scope themselves)
+namespace micro {
+namespace host {
+using namespace ::micro;
+}  // namespace host
+}  // namespace micro
 
 // ------------------------------------------------------------ the context --
 
@@ -196,7 +200,7 @@ struct micro_ctx {
   bool vectors_done = false;    // this step's model / dense g/n already written (dense kind)
   bool sel_is_union = false;    // n = 1 MiCRO: the union is worker 0's selection
   uint64_t k_global = 0;
-  TopkState* topk = nullptr;    // n_local
+  micro::TopkState* topk = nullptr;    // n_local
   unsigned* topk_hist = nullptr;
   unsigned* tie_counts = nullptr;
   unsigned* bitmap = nullptr;   // union of overlapping selections
@@ -208,13 +212,13 @@ struct micro_ctx {
   double* minus_one = nullptr;  // threshold that selects everything (k >= n_g)
   // peer-memory exchange (micro_peer_*): every rank's buffers mapped here
   bool peer_ready = false;
-  const long long* peer_counts[kMaxWorkers] = {};
-  void* peer_resid[kMaxWorkers] = {};
-  int32_t* peer_uidx[2][kMaxWorkers] = {};
-  void* peer_usum[2][kMaxWorkers] = {};
-  double* peer_corr[kMaxWorkers] = {};
-  const int32_t* peer_sel[2][kMaxWorkers] = {};
-  void* peer_recv[kMaxWorkers] = {};
+  const long long* peer_counts[micro::kMaxWorkers] = {};
+  void* peer_resid[micro::kMaxWorkers] = {};
+  int32_t* peer_uidx[2][micro::kMaxWorkers] = {};
+  void* peer_usum[2][micro::kMaxWorkers] = {};
+  double* peer_corr[micro::kMaxWorkers] = {};
+  const int32_t* peer_sel[2][micro::kMaxWorkers] = {};
+  void* peer_recv[micro::kMaxWorkers] = {};
   void* recv = nullptr;          // bulk exchange: receive slabs [source rank][sel_cap] (lazy)
   int peer_phase = 0;            // 0 idle, 1 contributed (bulk), 2 exchanged (ready to finalize)
   cudaEvent_t group_ev = nullptr;  // micro_group_step barriers (one process, all ranks)
@@ -224,7 +228,7 @@ struct micro_ctx {
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess)
-      return fail(MICRO_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+      return micro::host::fail(MICRO_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
     allocs.push_back(*p);
     return MICRO_OK;
   }

@@ -3,6 +3,9 @@
 // plumbing for hosts without the CUDA runtime, and the synthetic inputs.
 #include "internal.cuh"
 
+using namespace micro;
+using namespace micro::host;
+
 namespace {
 
 template <typename T>
