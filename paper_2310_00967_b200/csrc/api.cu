@@ -352,56 +352,37 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
   cudaStream_t st = c->stream;
-  // n = 1 MiCRO: split the pass in two halves so the first half's gather
-  // (ordered copy + the model's random read-modify-write) runs on the side
-  // stream while the second half streams — the offsets of a run only depend
-  // on the runs before it (MICRO_SPLIT=1 turns it off)
-  const unsigned ga = (unsigned)(grid / 2 / kGatherWarps * kGatherWarps);
-  const bool split = c->split > 1 && c->side && c->sel_is_union && c->kind == 0 && ga >= kGatherWarps;
   // every timing_period-th launch (event records between kernels cost the step
   // a few µs at small sizes, so long runs sample)
   const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
-  if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
-  auto dispatch = [&](unsigned g) -> int {
-#define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(g), dim3(kStreamThreads), st, a))
-#define K1N(D)                                                                                           \
-  do {                                                                                                   \
-    if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
-    else K1S(kWriteZeroSel, D);                                                                          \
+#define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(grid), dim3(kStreamThreads), st, a))
+#define K1N(D)                                                                                              \
+  do {                                                                                                      \
+    if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(grid), dim3(kStreamThreads), st, a)); \
+    else K1S(kWriteZeroSel, D);                                                                             \
   } while (0)
-    if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
-      if (acc_in_e)  // top-k: e holds acc already; compact only
-        CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
-                            dim3(kStreamThreads), st, a));
-      else if (tie)
-        CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
-      else K1S(kWriteAcc, false);
-    } else if (c->n > 1) {
-      if (c->cfg.error_feedback) K1N(false);
-      else K1S(kWriteAcc, false);
-    } else if (c->cfg.error_feedback) {
-      if (fd) K1N(true);
-      else K1N(false);
-    } else {
-      if (fd) K1S(kWriteNone, true);
-      else K1S(kWriteNone, false);
-    }
+  if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
+  if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
+    if (acc_in_e)  // top-k: e holds acc already; compact only
+      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(grid),
+                          dim3(kStreamThreads), st, a));
+    else if (tie)
+      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(grid), dim3(kStreamThreads), st, a));
+    else K1S(kWriteAcc, false);
+  } else if (c->n > 1) {
+    if (c->cfg.error_feedback) K1N(false);
+    else K1S(kWriteAcc, false);
+  } else if (c->cfg.error_feedback) {
+    if (fd) K1N(true);
+    else K1N(false);
+  } else {
+    if (fd) K1S(kWriteNone, true);
+    else K1S(kWriteNone, false);
+  }
 #undef K1S
 #undef K1N
-    CU(cudaGetLastError());
-    return MICRO_OK;
-  };
-  if (split) {
-    a.cta_offset = 0;
-    TRY(dispatch(ga));
-    CU(cudaEventRecord(c->ev_half, st));
-    a.cta_offset = (int)ga;
-    a.skip_pdl_wait = 1;  // independent of the first half
-    TRY(dispatch(grid - ga));
-  } else {
-    TRY(dispatch(grid));
-  }
+  CU(cudaGetLastError());
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next++ + 1], st));
   CompactArgs b{};
   b.stage_idx = c->stage_idx;
@@ -422,18 +403,6 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.model = c->sel_is_union ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
   if ((b.num_runs + b.super_runs - 1) / b.super_runs > kMaxSupers)
     return fail(MICRO_ECAPACITY, "super-block workspace too small");
-  if (split) {  // the first half's runs, on the side stream, while the second half streams
-    CU(cudaStreamWaitEvent(c->side, c->ev_half, 0));
-    CompactArgs h = b;
-    h.num_runs = (int)ga;
-    h.run_base = 0;
-    h.lead = 0;
-    CU(launch_maybe_pdl(false, k1_gather<T>, dim3(ga / kGatherWarps), dim3(kGatherWarps * 32), c->side, h));
-    CU(cudaEventRecord(c->ev_full, st));
-    CU(cudaStreamWaitEvent(c->side, c->ev_full, 0));
-    b.run_base = (int)ga;
-  }
-  b.lead = 1;
   if (c->fuse_step) {
     b.fin_delta = c->delta + i;
     b.k_target = c->k_worker;
@@ -450,7 +419,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.norm_mode = norm_mode(c);
     c->fin_done = true;
   }
-  unsigned gblocks = (unsigned)((b.num_runs - b.run_base + kGatherWarps - 1) / kGatherWarps);
+  unsigned gblocks = (unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps);
   if (c->norm && c->kind == 0) {  // one more CTA reduces k1_stream's per-CTA partials
     b.sq_part = c->norm_part;
     b.sq_parts = (int)grid;
@@ -459,13 +428,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.fin_slot = c->steps % kHistCap;
     gblocks += 1;
   }
-  if (split) {
-    CU(launch_maybe_pdl(false, k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), c->side, b));
-    CU(cudaEventRecord(c->ev_side, c->side));
-    CU(cudaStreamWaitEvent(st, c->ev_side, 0));  // the step ends on the caller's stream
-  } else {
-    CU(launch_maybe_pdl(c->pdl, k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), st, b));
-  }
+  CU(launch_maybe_pdl(c->pdl, k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
   return MICRO_OK;
 }
 
@@ -816,7 +779,6 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
     if (c->kind) c->k1_kind = 0;  // the baselines compact with the streaming K1
     if (const char* p = std::getenv("MICRO_PDL")) c->pdl = std::atoi(p) != 0;
-    if (const char* p = std::getenv("MICRO_SPLIT")) c->split = std::atoi(p);
     c->dense_fused = c->sel_is_union && cfg->dense_output && c->k1_kind == 0;
     c->use_tma = c->k1_kind != 2;
     const char* cf = std::getenv("MICRO_K1_CFG");
@@ -904,13 +866,6 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
     return cleanup(fail(MICRO_ECUDA, "memset: %s", cudaGetErrorString(e)));
-  if (c->sel_is_union && c->k1_kind == 0 && c->split > 1) {
-    if ((e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_half, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_full, cudaEventDisableTiming)) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming)) != cudaSuccess)
-      return cleanup(fail(MICRO_ECUDA, "side stream: %s", cudaGetErrorString(e)));
-  }
   if (c->dense && !c->dense_fused) {
     if ((e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
@@ -927,7 +882,6 @@ int micro_ctx_destroy(micro_ctx* c) {
   DeviceGuard dg(c->dev);
   cudaStreamSynchronize(c->stream);
   if (c->aux) cudaStreamSynchronize(c->aux);
-  if (c->side) cudaStreamSynchronize(c->side);
   for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocs) cudaFree(p);
   for (cudaEvent_t ev : c->t_ev) cudaEventDestroy(ev);
@@ -935,9 +889,6 @@ int micro_ctx_destroy(micro_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->group_ev) cudaEventDestroy(c->group_ev);
-  for (cudaEvent_t ev : {c->ev_half, c->ev_full, c->ev_side})
-    if (ev) cudaEventDestroy(ev);
-  if (c->side) cudaStreamDestroy(c->side);
 
   if (c->aux) cudaStreamDestroy(c->aux);
   delete c;

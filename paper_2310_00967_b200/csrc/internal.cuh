@@ -188,11 +188,6 @@ struct micro_ctx {
   bool fin_done = false;    // this step's finalize already ran inside k1_gather
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
   bool pdl = true;          // programmatic dependent launch between the step's kernels (MICRO_PDL=0: off)
-  // n = 1: the K1 pass in two halves, the first half's gather on `side`
-  // overlapping the second half's streaming (MICRO_SPLIT=1: off)
-  int split = 2;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_half = nullptr, ev_full = nullptr, ev_side = nullptr;
   bool timing = false;
   int timing_period = 1;   // record every timing_period-th k1_stream launch
   int64_t t_seen = 0;

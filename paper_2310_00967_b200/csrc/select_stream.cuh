@@ -65,8 +65,6 @@ struct StreamArgs {
   int super_runs;
   double* sq_part;         // kNorm: per CTA, sum of e_{t+1}^2 (own selections zeroed); reduced by k1_gather
   const long long* tie_j;  // kTie (top-k baseline): also select |acc| == thr at j <= *tie_j
-  int cta_offset;          // this launch covers CTAs [cta_offset, cta_offset + gridDim.x) of the vector
-  int skip_pdl_wait;       // the second half of a split pass: independent of the first
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -98,9 +96,8 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
 
   __shared__ int s_cnt[kStreamWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int bx = (int)blockIdx.x + a.cta_offset;
-  const int u = bx * kStreamWarps + w;
-  if (!a.skip_pdl_wait) pdl_wait();  // the previous step's gather / finalize (staging, counts, delta) is done
+  const int u = blockIdx.x * kStreamWarps + w;
+  pdl_wait();  // the previous step's gather / finalize (staging, counts, delta) is done
   const int base = u * UE;
   // warps past the vector's end idle but still meet the CTA barrier below
   const int elems = base >= a.n_g ? 0 : (a.n_g - base < UE ? a.n_g - base : UE);
@@ -221,7 +218,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   // counts are packed as 8-bit fields (warp totals <= 128); units in warp
   // order inside the CTA.  Runs live at staging slot (CTA - cta_lo) * 8 * UE.
   const int cta_lo = a.unit_lo / kStreamWarps, cta_hi = a.unit_hi / kStreamWarps;
-  const bool sel_cta = bx >= cta_lo && bx <= cta_hi;  // CTA-uniform
+  const bool sel_cta = (int)blockIdx.x >= cta_lo && (int)blockIdx.x <= cta_hi;  // CTA-uniform
   if (sel_cta) {
     unsigned packed = 0;
 #pragma unroll
@@ -245,7 +242,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       woff += q < w ? x : 0;
       cta_count += x;
     }
-    const int slot = bx - cta_lo;
+    const int slot = (int)blockIdx.x - cta_lo;
     if (threadIdx.x == 0) {
       a.unit_counts[slot] = cta_count;
       if (cta_count) atomicAdd(a.super_counts + slot / a.super_runs, cta_count);
@@ -295,7 +292,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       double t = 0.0;
 #pragma unroll
       for (int q = 0; q < kStreamWarps; ++q) t += s_sq[q];
-      a.sq_part[bx] = t;
+      a.sq_part[blockIdx.x] = t;
     }
   }
 }
@@ -310,8 +307,6 @@ struct CompactArgs {
   int num_runs;
   int super_runs;
   int run_stride;          // staging elements per run slot
-  int run_base;            // first run of this launch (a multiple of kGatherWarps; split passes)
-  int lead;                // this launch forms k_i, the threshold update and clears the other parity
   int32_t* sel_idx;
   void* sel_val;
   long long cap;
@@ -382,7 +377,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   pdl_trigger();
   // norm on: CTA 0 (scheduled first, overlapping the copies) reduces
   // ||e_{t+1}||^2 in a fixed order; the copy CTAs are 1..
-  if (a.sq_part && blockIdx.x == 0) {  // (only set on the lead launch)
+  if (a.sq_part && blockIdx.x == 0) {
     __shared__ double s_sq[kGatherWarps];
     double v = 0.0;
 #pragma unroll 8
@@ -399,14 +394,13 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     }
     return;
   }
-  const int gb0 = (int)blockIdx.x - (a.sq_part ? 1 : 0);
-  const int gb = gb0 + a.run_base / kGatherWarps;
+  const int gb = (int)blockIdx.x - (a.sq_part ? 1 : 0);
   const int r0 = gb * kGatherWarps;
   const int sb = r0 / a.super_runs;
   // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0)
   long long base = block_sum_range(a.super_counts, 0, sb, s_part) +
                    block_sum_range(a.run_counts, sb * a.super_runs, r0, s_part);
-  if (a.lead && gb0 == 0) {
+  if (gb == 0) {
     const int nsup = (a.num_runs + a.super_runs - 1) / a.super_runs;
     const long long total = block_sum_range(a.super_counts, 0, nsup, s_part);
     if (threadIdx.x == 0) {
