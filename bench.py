@@ -218,7 +218,7 @@ def our_arm(args, wl):
     gen = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(W)]
     for _ in range(args.prime):
         for i in range(W):
-            engine.synth_gaussian(gen[i], SEED, rank + i, t)
+            engine.synth_gaussian(gen[i], args.seed, rank + i, t)
         m.step(gen, ETA, t)
         t += 1
     del gen
@@ -227,7 +227,7 @@ def our_arm(args, wl):
     R = max(W + 1, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (esz * n_g))))
     G = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(R)]
     for r in range(R):
-        engine.synth_gaussian(G[r], SEED, rank + r % W, t + r)
+        engine.synth_gaussian(G[r], args.seed, rank + r % W, t + r)
     t0_bufs = t
 
     def grads(t):
@@ -271,7 +271,8 @@ def our_arm(args, wl):
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    total_ms = sum(a.elapsed_time(b) for a, b in step_ev) if flush else start.elapsed_time(end)
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    total_ms = sum(step_ms) if flush else start.elapsed_time(end)
     k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone (sampled launches)
     m.kernel_timing(False)
     xchg_ms = None
@@ -327,7 +328,7 @@ def our_arm(args, wl):
         for b in range(nb):
             hG = torch.empty(W * n_g, dtype=tdt).pin_memory()
             for i in range(W):
-                engine.synth_gaussian(G[i], SEED, rank + i, t + 1 + b)  # fresh: steps t+1 .. t+nb
+                engine.synth_gaussian(G[i], args.seed, rank + i, t + 1 + b)  # fresh: steps t+1 .. t+nb
                 hG[i * n_g:(i + 1) * n_g].copy_(G[i].cpu())
             hGs.append(hG)
         idx = torch.empty(n_g, dtype=torch.int32).pin_memory().numpy()  # pinned result buffers
@@ -352,7 +353,7 @@ def our_arm(args, wl):
         nb = int(max(2, min(ke + 1, 4e9 // (esz * n_g))))
         hGs = []
         for b in range(nb):
-            engine.synth_gaussian(G[0], SEED, rank, t + 1 + b)
+            engine.synth_gaussian(G[0], args.seed, rank, t + 1 + b)
             hGs.append(G[0].cpu().pin_memory())
         dG = torch.empty(n_g, device=dev, dtype=tdt)
         idx = torch.empty(n_g, dtype=torch.int32).pin_memory().numpy()
@@ -414,7 +415,7 @@ def our_arm(args, wl):
                        "one_worker_per_gpu": W == 1, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
                        "adaptation_iterations": args.prime, "first_timed_t": t_first,
                        "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
-                       "error_norm_recorded": bool(args.error_norm),
+                       "error_norm_recorded": bool(args.error_norm), "seed": args.seed,
                        "sparsifier": args.sparsifier,
                        "inputs": (f"{R} resident N(0,1) gradients ("
                                   + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
@@ -425,6 +426,7 @@ def our_arm(args, wl):
                        "parallelism": (f"dp{world} (exclusive cyclic partitions"
                                        + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
                                        f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
+            "median_us_per_step": (float(np.median(step_ms)) * 1e3 if step_ms else None),
             "density": density, "density_rel_err": density / d - 1.0,
             "density_window": {"first_quarter": float(K[: max(1, len(K) // 4)].mean() / n_g),
                                "last_quarter": float(K[-max(1, len(K) // 4):].mean() / n_g),
@@ -469,6 +471,7 @@ def main():
                     help="gloo: exercise the N > 1 path with all ranks on one GPU (code check only)")
     ap.add_argument("--transport", choices=["peer", "peer_pull", "nccl"], default="peer",
                     help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
+    ap.add_argument("--seed", type=int, default=SEED, help="synthetic gradient stream (SURVEY.md 8d: 1, 2, 3)")
     ap.add_argument("--flush-l2", choices=["auto", "on", "off"], default="auto",
                     help="flush L2 between timed steps (auto: when e, G and x would fit in L2)")
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32",
