@@ -345,7 +345,9 @@ def our_arm(args, wl):
         e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g * W,
                "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
                "host_gradients": f"{nb - 1} distinct pinned buffers over {ke} steps",
-               "density": float(statistics.mean(kk)) / n_g}
+               "density": float(statistics.mean(kk)) / n_g,
+               # what bounds it: the H2D of the gradient over PCIe (Gen5 x16: ~64 GB/s nominal)
+               "h2d_gbs_effective": esz * n_g * W / e2e_s / 1e9}
     else:
         # N ranks: each copies its own pinned host gradient in, steps through
         # DistMicro, and reads the union back; the max over ranks is reported
