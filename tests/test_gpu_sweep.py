@@ -14,7 +14,7 @@ if torch.cuda.is_available():
     from paper_2310_00967_b200 import engine
 
 
-def _cases(count=40, seed=2024):
+def _cases(count=150, seed=2024):
     rng = np.random.default_rng(seed)
     out = []
     for c in range(count):
