@@ -290,3 +290,21 @@ def resolve_decay_at(lr: LrSchedule, iterations: int) -> int:
 def learning_rate_at(lr: LrSchedule, decay_at: int, t: int) -> float:
     """harness.cpp:61-63: the eta handed to each MiCRO step (host arithmetic)."""
     return lr.initial * (lr.decay_factor if t >= decay_at else 1.0)
+
+
+# sparsifier.cpp:127-160: the kind / target names of the reference's CLI and records
+SPARSIFIER_KINDS = ("micro", "topk", "cltk", "hard", "dense")
+
+
+def parse_sparsifier_kind(name: str) -> str:
+    if name == "hard_threshold":
+        return "hard"
+    if name not in SPARSIFIER_KINDS:
+        raise InvalidArgument(_lib.MICRO_EINVAL, f"unknown sparsifier '{name}' (expected micro|topk|cltk|hard|dense)")
+    return name
+
+
+def parse_per_worker_target(name: str) -> str:
+    if name not in ("split", "full"):
+        raise InvalidArgument(_lib.MICRO_EINVAL, f"unknown per-worker target '{name}' (expected split|full)")
+    return name

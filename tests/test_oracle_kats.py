@@ -228,3 +228,15 @@ def test_learning_rate_schedule():
     assert resolve_decay_at(lr, 200) == 150
     assert learning_rate_at(lr, 150, 149) == 0.1 and learning_rate_at(lr, 150, 150) == 0.05
     assert resolve_decay_at(LrSchedule(decay_at=7), 200) == 7
+
+
+def test_kind_names():
+    """sparsifier.cpp:136-160."""
+    from paper_2310_00967_b200._lib import InvalidArgument
+    from paper_2310_00967_b200.sparsim import parse_per_worker_target, parse_sparsifier_kind
+    assert parse_sparsifier_kind("hard_threshold") == "hard" and parse_sparsifier_kind("topk") == "topk"
+    assert parse_per_worker_target("full") == "full"
+    with pytest.raises(InvalidArgument):
+        parse_sparsifier_kind("foo")
+    with pytest.raises(InvalidArgument):
+        parse_per_worker_target("half")
