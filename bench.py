@@ -308,7 +308,7 @@ def our_arm(args, wl):
     # k_finalize; n > 1 ranks: K1 x2, gather_foreign, owner_reduce,
     # build_union, finalize (NCCL kernels not counted)
     launches_per_step = ((2 if W == 1 else 2 * W + 2) if world == 1
-                         else {"peer": 5, "peer_pull": 4, "nccl": 6}[args.transport])  # K1 x2 + exchange + finalize
+                         else {"peer": 5, "peer_pull": 4, "nccl": 6}[m.transport])  # K1 x2 + exchange + finalize
     if args.sparsifier != "micro":  # baselines.cuh: per selecting worker, top-k = init + 2 per digit +
         # tie count/find + stream + gather (fp32: 11), hard = 2, else accumulate + count = 2; then
         # union marks (W) + popcount + scan (2) + emit + reduce + finalize (dense: iota + reduce + finalize)
@@ -402,9 +402,9 @@ def our_arm(args, wl):
         b_net = 4.0 * (Km - km) + 4.0 * km * (world - 1) + 4.0 * (Km - km)
         exchange_line = {"bound": "nvlink", "achieved": b_net / (xchg_ms * 1e-3) / 1e9, "peak": 900.0,
                          "unit": "GB/s", "frac": b_net / (xchg_ms * 1e-3) / 1e9 / 900.0,
-                         "bytes_per_gpu": b_net, "avg_ms": xchg_ms, "transport": args.transport,
+                         "bytes_per_gpu": b_net, "avg_ms": xchg_ms, "transport": m.transport,
                          "peak_source": "NVLink 5 per direction per GPU (nominal)",
-                         "timed": "exchange kernels, barriers excluded" if args.transport != "nccl"
+                         "timed": "exchange kernels, barriers excluded" if m.transport != "nccl"
                          else "the whole NCCL protocol"}
 
     if rank == 0:
@@ -426,7 +426,7 @@ def our_arm(args, wl):
                                      if flush else f"); each {esz}*n_g bytes > L2 (no flush needed)"
                                      if esz * n_g > 126e6 else "); L2 NOT flushed (--flush-l2 off)")),
                        "parallelism": (f"dp{world} (exclusive cyclic partitions"
-                                       + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
+                                       + (f", {m.transport} exchange)" if world > 1 else ")") if W == 1 else
                                        f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
             "median_us_per_step": (float(np.median(step_ms)) * 1e3 if step_ms else None),
             "density": density, "density_rel_err": density / d - 1.0,

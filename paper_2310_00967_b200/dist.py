@@ -140,13 +140,25 @@ class DistMicro:
         self.comm_device = comm_device
         self.transport = transport
         if transport in ("peer", "peer_pull"):
-            blob = C.create_string_buffer(_lib.MICRO_PEER_HANDLE_BYTES)
-            check(lib().micro_peer_export(self.m.handle, blob))
-            blobs = [None] * self.world
-            dist.all_gather_object(blobs, blob.raw, group=group)
-            allb = C.create_string_buffer(b"".join(blobs), _lib.MICRO_PEER_HANDLE_BYTES * self.world)
-            check(lib().micro_peer_import(self.m.handle, allb))
             self._bar = torch.zeros(1, dtype=torch.int32, device=self.m.device)
+            ok, why = True, ""
+            try:
+                blob = C.create_string_buffer(_lib.MICRO_PEER_HANDLE_BYTES)
+                check(lib().micro_peer_export(self.m.handle, blob))
+                blobs = [None] * self.world
+                dist.all_gather_object(blobs, blob.raw, group=group)
+                allb = C.create_string_buffer(b"".join(blobs), _lib.MICRO_PEER_HANDLE_BYTES * self.world)
+                check(lib().micro_peer_import(self.m.handle, allb))
+            except _lib.MicroError as ex:  # e.g. no peer access between these devices
+                ok, why = False, str(ex)
+            # every rank must agree on the transport, or the barriers deadlock
+            flags = [None] * self.world
+            dist.all_gather_object(flags, ok, group=group)
+            if not all(flags):
+                import warnings
+                warnings.warn(f"peer-memory exchange unavailable on some rank ({why or 'remote failure'}); "
+                              "falling back to the NCCL protocol")
+                self.transport = "nccl"
 
     def _barrier(self):
         if self.comm_device is not None:  # host barrier (gloo): the stream's work is done first
