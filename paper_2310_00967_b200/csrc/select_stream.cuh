@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   T* __restrict__ E = (T*)a.resid + base;
 
   const unsigned long long pol_stream = policy_evict_first();
+  // kDense: last step's sector bits, loaded with e and G so the latency overlaps
+  const unsigned long long dirty_prev = (kDense && live) ? a.dirty[u] : 0ull;
   V e[VPL], g[VPL];
   if (elems == UE) {  // (elems == 0 for dead warps: the guarded path below loads nothing)
 #pragma unroll
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
     // holds a selection now or held one last step; lanes 2k and 2k+1 own its
     // two 16-byte halves (sector k + 16 i of the unit).
     static_assert(VPL * 16 == 64, "64 sectors per unit");
-    const unsigned long long prev = a.dirty[u];
+    const unsigned long long prev = dirty_prev;
     unsigned long long now = 0;
     T* D = (T*)a.dense + base;
 #pragma unroll
