@@ -38,6 +38,12 @@ namespace micro {
 constexpr int kStreamWarps = 8;                  // units per CTA
 constexpr int kStreamThreads = kStreamWarps * 32;
 constexpr int kStreamUnitBytes = 2048;            // per operand
+// dense g/n write granularity: a chunk of kDenseLanes lanes (16 B each) is
+// rewritten whole when any of its entries is (or was) selected
+#ifndef MICRO_DENSE_LANES
+#define MICRO_DENSE_LANES 2
+#endif
+constexpr int kDenseLanes = MICRO_DENSE_LANES;
 
 
 template <typename T>
@@ -193,8 +199,12 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const bool half = mask[i] != 0;
-      const bool other = __shfl_xor_sync(0xffffffffu, half, 1);  // every lane: no short-circuit
-      const bool sec = half || other;
+      bool sec = half;  // the lanes of one kDenseLanes * 16-byte chunk agree (every lane shuffles)
+#pragma unroll
+      for (int o = 1; o < kDenseLanes; o <<= 1) {
+        const bool peer = __shfl_xor_sync(0xffffffffu, sec, o);  // unconditional: no short-circuit
+        sec = sec || peer;
+      }
       const unsigned secbits = even_bits(__ballot_sync(0xffffffffu, sec));
       now |= (unsigned long long)secbits << (16 * i);
       if (sec || ((prev >> (16 * i + (lane >> 1))) & 1ull)) {
