@@ -3,6 +3,7 @@ N = 2 path (both ranks on one GPU over gloo: a code-path check, the numbers
 are not valid) for each exchange transport.  GPU only."""
 import json
 import os
+import socket
 import subprocess
 import sys
 
@@ -12,6 +13,12 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
         "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"}
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def _line(out: str) -> dict:
@@ -33,7 +40,7 @@ def test_bench_line_n1():
 @pytest.mark.parametrize("transport", ["peer", "peer_pull", "nccl"])
 def test_bench_n2_code_path(transport):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", str(29600 + len(transport)), "bench.py",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
                         "--gpus", "2", "--dist-backend", "gloo", "--transport", transport, "--workload", "c1",
                         "--steps", "3", "--warmup", "3", "--prime", "20"],
                        cwd=ROOT, capture_output=True, text=True, timeout=600)
