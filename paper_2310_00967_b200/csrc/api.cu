@@ -356,19 +356,20 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   // a few µs at small sizes, so long runs sample)
   const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
-#define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(grid), dim3(kStreamThreads), st, a))
+auto dispatch = [&](unsigned g) -> int {
+#define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(g), dim3(kStreamThreads), st, a))
 #define K1N(D)                                                                                              \
   do {                                                                                                      \
-    if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(grid), dim3(kStreamThreads), st, a)); \
+    if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
     else K1S(kWriteZeroSel, D);                                                                             \
   } while (0)
   if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
   if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
     if (acc_in_e)  // top-k: e holds acc already; compact only
-      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(grid),
+      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
                           dim3(kStreamThreads), st, a));
     else if (tie)
-      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(grid), dim3(kStreamThreads), st, a));
+      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
     else K1S(kWriteAcc, false);
   } else if (c->n > 1) {
     if (c->cfg.error_feedback) K1N(false);
@@ -383,6 +384,23 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
 #undef K1S
 #undef K1N
   CU(cudaGetLastError());
+    return MICRO_OK;
+  };
+  if (c->h2d_chunks > 1 && c->sel_is_union && c->kind == 0) {
+    // step_host: chunk k of the gradient landed on the copy stream -> stream
+    // its CTAs while the next chunk is still in flight over PCIe
+    const unsigned per = (grid + c->h2d_chunks - 1) / c->h2d_chunks;
+    for (int k = 0; k < c->h2d_chunks; ++k) {
+      const unsigned lo = std::min(grid, per * k), hi = std::min(grid, per * (k + 1));
+      if (lo >= hi) break;
+      CU(cudaStreamWaitEvent(st, c->h2d_ev[k], 0));
+      a.cta_offset = (int)lo;
+      TRY(dispatch(hi - lo));
+    }
+    a.cta_offset = 0;
+  } else {
+    TRY(dispatch(grid));
+  }
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next++ + 1], st));
   CompactArgs b{};
   b.stage_idx = c->stage_idx;
@@ -779,6 +797,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
     if (c->kind) c->k1_kind = 0;  // the baselines compact with the streaming K1
     if (const char* p = std::getenv("MICRO_PDL")) c->pdl = std::atoi(p) != 0;
+    if (const char* p = std::getenv("MICRO_H2D_PIPELINE")) c->h2d_pipeline = std::atoi(p) != 0;
     c->dense_fused = c->sel_is_union && cfg->dense_output && c->k1_kind == 0;
     c->use_tma = c->k1_kind != 2;
     const char* cf = std::getenv("MICRO_K1_CFG");
@@ -889,6 +908,13 @@ int micro_ctx_destroy(micro_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->group_ev) cudaEventDestroy(c->group_ev);
+  if (c->h2d_stream) {
+    cudaStreamSynchronize(c->h2d_stream);
+    for (cudaEvent_t ev : c->h2d_ev)
+      if (ev) cudaEventDestroy(ev);
+    if (c->h2d_free) cudaEventDestroy(c->h2d_free);
+    cudaStreamDestroy(c->h2d_stream);
+  }
 
   if (c->aux) cudaStreamDestroy(c->aux);
   delete c;
@@ -980,11 +1006,38 @@ int micro_step_host(micro_ctx* c, const void* h_grads, double eta, int64_t t, in
   DeviceGuard dg(c->dev);
   TRY(ensure_staging(c));
   const size_t row = (size_t)c->n_g * c->esz;
-  CU(cudaMemcpy2DAsync(c->staging, c->staging_stride, h_grads, row, row, c->n_local, cudaMemcpyHostToDevice,
-                       c->stream));
   std::vector<const void*> g(c->n_local);
   for (int i = 0; i < c->n_local; ++i) g[i] = (const char*)c->staging + (size_t)i * c->staging_stride;
-  TRY(micro_step(c, g.data(), eta, t));
+  if (c->sel_is_union && c->kind == 0 && c->k1_kind == 0 && c->h2d_pipeline) {
+    // copy/compute overlap: the gradient crosses PCIe in chunks of whole K1
+    // CTAs on a copy stream; K1 streams each chunk as it lands
+    if (!c->h2d_stream) {
+      CU(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+      for (auto& ev : c->h2d_ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&c->h2d_free, cudaEventDisableTiming));
+    }
+    const int64_t cta_elems = (c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>()) * kStreamWarps;
+    const int64_t ctas = (c->n_g + cta_elems - 1) / cta_elems;
+    const int64_t per = (ctas + micro_ctx::kH2DChunks - 1) / micro_ctx::kH2DChunks;
+    CU(cudaEventRecord(c->h2d_free, c->stream));  // the last step's K1 has read the staging
+    CU(cudaStreamWaitEvent(c->h2d_stream, c->h2d_free, 0));
+    for (int k = 0; k < micro_ctx::kH2DChunks; ++k) {
+      const int64_t lo = std::min<int64_t>(c->n_g, per * k * cta_elems);
+      const int64_t hi = std::min<int64_t>(c->n_g, per * (k + 1) * cta_elems);
+      if (hi > lo)
+        CU(cudaMemcpyAsync((char*)c->staging + lo * c->esz, (const char*)h_grads + lo * c->esz,
+                           (size_t)(hi - lo) * c->esz, cudaMemcpyHostToDevice, c->h2d_stream));
+      CU(cudaEventRecord(c->h2d_ev[k], c->h2d_stream));
+    }
+    c->h2d_chunks = micro_ctx::kH2DChunks;
+    const int rc = micro_step(c, g.data(), eta, t);
+    c->h2d_chunks = 0;
+    TRY(rc);
+  } else {
+    CU(cudaMemcpy2DAsync(c->staging, c->staging_stride, h_grads, row, row, c->n_local, cudaMemcpyHostToDevice,
+                         c->stream));
+    TRY(micro_step(c, g.data(), eta, t));
+  }
   return micro_copy_union(c, h_idx, h_sums, cap, K);
 }
 

@@ -188,6 +188,14 @@ struct micro_ctx {
   bool fin_done = false;    // this step's finalize already ran inside k1_gather
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
   bool pdl = true;          // programmatic dependent launch between the step's kernels (MICRO_PDL=0: off)
+  // micro_step_host (n = 1): the gradient arrives in kH2DChunks pieces on
+  // h2d_stream; K1 streams each piece's CTAs as soon as it has landed
+  static constexpr int kH2DChunks = 4;
+  int h2d_chunks = 0;        // > 1 only while micro_step_host runs
+  bool h2d_pipeline = true;  // MICRO_H2D_PIPELINE=0: one copy, then the step
+  cudaStream_t h2d_stream = nullptr;
+  cudaEvent_t h2d_ev[kH2DChunks] = {};
+  cudaEvent_t h2d_free = nullptr;  // the previous step is done with the staging buffer
   bool timing = false;
   int timing_period = 1;   // record every timing_period-th k1_stream launch
   int64_t t_seen = 0;

@@ -71,6 +71,7 @@ struct StreamArgs {
   int super_runs;
   double* sq_part;         // kNorm: per CTA, sum of e_{t+1}^2 (own selections zeroed); reduced by k1_gather
   const long long* tie_j;  // kTie (top-k baseline): also select |acc| == thr at j <= *tie_j
+  int cta_offset;          // this launch covers CTAs [cta_offset, cta_offset + gridDim.x) (chunked H2D)
 };
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
 
   __shared__ int s_cnt[kStreamWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int u = blockIdx.x * kStreamWarps + w;
+  const int bx = (int)blockIdx.x + a.cta_offset;
+  const int u = bx * kStreamWarps + w;
   pdl_wait();  // the previous step's gather / finalize (staging, counts, delta) is done
   const int base = u * UE;
   // warps past the vector's end idle but still meet the CTA barrier below
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   // counts are packed as 8-bit fields (warp totals <= 128); units in warp
   // order inside the CTA.  Runs live at staging slot (CTA - cta_lo) * 8 * UE.
   const int cta_lo = a.unit_lo / kStreamWarps, cta_hi = a.unit_hi / kStreamWarps;
-  const bool sel_cta = (int)blockIdx.x >= cta_lo && (int)blockIdx.x <= cta_hi;  // CTA-uniform
+  const bool sel_cta = bx >= cta_lo && bx <= cta_hi;  // CTA-uniform
   if (sel_cta) {
     unsigned packed = 0;
 #pragma unroll
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       woff += q < w ? x : 0;
       cta_count += x;
     }
-    const int slot = (int)blockIdx.x - cta_lo;
+    const int slot = bx - cta_lo;
     if (threadIdx.x == 0) {
       a.unit_counts[slot] = cta_count;
       if (cta_count) atomicAdd(a.super_counts + slot / a.super_runs, cta_count);
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       double t = 0.0;
 #pragma unroll
       for (int q = 0; q < kStreamWarps; ++q) t += s_sq[q];
-      a.sq_part[blockIdx.x] = t;
+      a.sq_part[bx] = t;
     }
   }
 }

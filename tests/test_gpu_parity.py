@@ -305,3 +305,27 @@ def test_gpu_records_to_reference_format(tmp_path):
     assert [r["error_norm"] for r in back["records"]] == [r["error_norm"] for r in recs]
     assert back["config"]["workers"] == 2 and back["config"]["density"] == 0.01
     m.close()
+
+
+@pytest.mark.parametrize("n_g", [1_000_003, 65_536 * 3 + 17])
+def test_gpu_step_host_pipelined_matches_device_step(n_g):
+    """micro_step_host (gradient copied in chunks on a copy stream, K1
+    streaming each chunk as it lands) == micro_step on device gradients."""
+    o = Oracle()
+    a = engine.Micro(n_g, 1, density=0.01, initial_threshold=0.02)
+    b = engine.Micro(n_g, 1, density=0.01, initial_threshold=0.02)
+    xa = torch.zeros(n_g, device="cuda")
+    xb = torch.zeros(n_g, device="cuda")
+    a.set_model(xa)
+    b.set_model(xb)
+    for t in range(6):
+        G = o.gaussian(SEED, 0, t, n_g)
+        hG = torch.from_numpy(G).pin_memory()
+        ia, sa = a.step_host(hG, ETA, t)
+        b.step([torch.from_numpy(G).cuda()], ETA, t)
+        ib, sb = b.union()
+        assert np.array_equal(ia, ib) and np.array_equal(sa, sb), t
+        assert np.array_equal(a.residual(0), b.residual(0)), t
+        assert torch.equal(xa, xb), t
+    a.close()
+    b.close()
