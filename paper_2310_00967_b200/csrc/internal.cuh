@@ -190,7 +190,7 @@ struct micro_ctx {
   bool pdl = true;          // programmatic dependent launch between the step's kernels (MICRO_PDL=0: off)
   // micro_step_host (n = 1): the gradient arrives in kH2DChunks pieces on
   // h2d_stream; K1 streams each piece's CTAs as soon as it has landed
-  static constexpr int kH2DChunks = 4;
+  static constexpr int kH2DChunks = 8;
   int h2d_chunks = 0;        // > 1 only while micro_step_host runs
   bool h2d_pipeline = true;  // MICRO_H2D_PIPELINE=0: one copy, then the step
   cudaStream_t h2d_stream = nullptr;
