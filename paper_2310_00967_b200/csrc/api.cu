@@ -356,34 +356,34 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   // a few µs at small sizes, so long runs sample)
   const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
-auto dispatch = [&](unsigned g) -> int {
+  auto dispatch = [&](unsigned g) -> int {
 #define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(g), dim3(kStreamThreads), st, a))
 #define K1N(D)                                                                                              \
-  do {                                                                                                      \
-    if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
-    else K1S(kWriteZeroSel, D);                                                                             \
-  } while (0)
-  if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
-  if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
-    if (acc_in_e)  // top-k: e holds acc already; compact only
-      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
-                          dim3(kStreamThreads), st, a));
-    else if (tie)
-      CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
-    else K1S(kWriteAcc, false);
-  } else if (c->n > 1) {
-    if (c->cfg.error_feedback) K1N(false);
-    else K1S(kWriteAcc, false);
-  } else if (c->cfg.error_feedback) {
-    if (fd) K1N(true);
-    else K1N(false);
-  } else {
-    if (fd) K1S(kWriteNone, true);
-    else K1S(kWriteNone, false);
-  }
+    do {                                                                                                      \
+      if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
+      else K1S(kWriteZeroSel, D);                                                                             \
+    } while (0)
+    if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
+    if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
+      if (acc_in_e)  // top-k: e holds acc already; compact only
+        CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
+                            dim3(kStreamThreads), st, a));
+      else if (tie)
+        CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
+      else K1S(kWriteAcc, false);
+    } else if (c->n > 1) {
+      if (c->cfg.error_feedback) K1N(false);
+      else K1S(kWriteAcc, false);
+    } else if (c->cfg.error_feedback) {
+      if (fd) K1N(true);
+      else K1N(false);
+    } else {
+      if (fd) K1S(kWriteNone, true);
+      else K1S(kWriteNone, false);
+    }
 #undef K1S
 #undef K1N
-  CU(cudaGetLastError());
+    CU(cudaGetLastError());
     return MICRO_OK;
   };
   if (c->h2d_chunks > 1 && c->sel_is_union && c->kind == 0) {
