@@ -112,6 +112,9 @@ int micro_error_metric(int dtype, const void* const* h_res, int n, int64_t n_g, 
  * 2 device->device.  micro_memcpy synchronises `stream`. */
 int micro_device_malloc(void** d_ptr, int64_t bytes, int device);
 int micro_device_free(void* d_ptr);
+/* Pinned (page-locked) host memory: full-bandwidth H2D/D2H for step_host. */
+int micro_host_malloc(void** h_ptr, int64_t bytes);
+int micro_host_free(void* h_ptr);
 int micro_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 int micro_device_count(int* count);
 

@@ -476,24 +476,31 @@ class MicroEngine {
   }
   MicroEngine(const MicroEngine&) = delete;
   MicroEngine& operator=(const MicroEngine&) = delete;
-  ~MicroEngine() { micro_ctx_destroy(ctx_); }
+  ~MicroEngine() {
+    micro_ctx_destroy(ctx_);
+    micro_host_free(h_idx_);
+    micro_host_free(h_sums_);
+  }
 
   // h_grads: workers * n_g elements of the engine's dtype (double for MICRO_F64).
   AggregatedSelection step(const void* h_grads, double eta, std::int64_t t, std::vector<double>* summed = nullptr) {
-    std::vector<int32_t> idx((std::size_t)n_g_);
-    std::vector<unsigned char> sums((std::size_t)n_g_ * esz_);
+    if (!h_idx_) {  // pinned result buffers, allocated once (full-bandwidth D2H, no per-step zeroing)
+      b200::check(micro_host_malloc(reinterpret_cast<void**>(&h_idx_), (int64_t)n_g_ * 4));
+      b200::check(micro_host_malloc(&h_sums_, (int64_t)n_g_ * (int64_t)esz_));
+    }
     int64_t K = 0;
-    b200::check(micro_step_host(ctx_, h_grads, eta, t, idx.data(), sums.data(), n_g_, &K));
+    b200::check(micro_step_host(ctx_, h_grads, eta, t, h_idx_, h_sums_, n_g_, &K));
+    const unsigned char* sums = static_cast<const unsigned char*>(h_sums_);
     AggregatedSelection agg;
-    agg.indices.assign(idx.begin(), idx.begin() + K);
+    agg.indices.assign(h_idx_, h_idx_ + K);
     std::vector<int64_t> counts((std::size_t)n_);
     b200::check(micro_query(ctx_, nullptr, counts.data(), nullptr));
     for (auto c : counts) agg.per_worker_counts.push_back((std::size_t)c);
     if (summed) {
       summed->resize((std::size_t)K);
       for (int64_t k = 0; k < K; ++k)
-        (*summed)[(std::size_t)k] = esz_ == 8 ? reinterpret_cast<const double*>(sums.data())[k]
-                                              : reinterpret_cast<const float*>(sums.data())[k];
+        (*summed)[(std::size_t)k] = esz_ == 8 ? reinterpret_cast<const double*>(sums)[k]
+                                              : reinterpret_cast<const float*>(sums)[k];
     }
     return agg;
   }
@@ -544,6 +551,8 @@ class MicroEngine {
   Index n_g_;
   int n_;
   std::size_t esz_;
+  int32_t* h_idx_ = nullptr;  // pinned step results (lazily allocated)
+  void* h_sums_ = nullptr;
 };
 
 // The same step with one GPU per worker, driven from one process

@@ -97,6 +97,8 @@ _SIGS = {
     "micro_synth_gaussian": ([I32, U64, U32, U64, I64, VP, VP], I32),
     "micro_device_malloc": ([C.POINTER(VP), I64, I32], I32),
     "micro_device_free": ([VP], I32),
+    "micro_host_malloc": ([C.POINTER(VP), I64], I32),
+    "micro_host_free": ([VP], I32),
     "micro_memcpy": ([VP, VP, I64, I32, VP], I32),
     "micro_device_count": ([C.POINTER(I32)], I32),
     "micro_config_default": ([C.POINTER(micro_config)], None),

@@ -69,6 +69,18 @@ int micro_device_malloc(void** d, int64_t bytes, int device) {
   return MICRO_OK;
 }
 
+int micro_host_malloc(void** h, int64_t bytes) {
+  if (!h || bytes < 0) return fail(MICRO_EINVAL, "micro_host_malloc: bad arguments");
+  *h = nullptr;
+  CU(cudaMallocHost(h, bytes ? (size_t)bytes : 16));
+  return MICRO_OK;
+}
+
+int micro_host_free(void* h) {
+  if (h) CU(cudaFreeHost(h));
+  return MICRO_OK;
+}
+
 int micro_device_free(void* d) {
   if (d) CU(cudaFree(d));
   return MICRO_OK;

@@ -158,15 +158,27 @@ class Micro:
                   out_sums: np.ndarray | None = None):
         """End-to-end call with host buffers (pinned CPU tensor of n_local*n_g)."""
         assert not h_grads.is_cuda and h_grads.dtype == self.dtype and h_grads.is_contiguous()
-        cap = self.n_g
-        if out_idx is None:
-            out_idx = np.empty(cap, np.int32)
-        if out_sums is None:
-            out_sums = np.empty(cap, _NP[self.dtype])
+        own = out_idx is None or out_sums is None
+        if own:
+            out_idx, out_sums = self._host_out()
         K = C.c_int64()
         check(lib().micro_step_host(self._h, C.c_void_p(h_grads.data_ptr()), eta, t,
-                                    out_idx.ctypes.data, out_sums.ctypes.data, out_idx.size, C.byref(K)))
+                                    out_idx.ctypes.data, out_sums.ctypes.data, min(out_idx.size, out_sums.size),
+                                    C.byref(K)))
+        if own:  # the internal buffers are reused by the next call
+            return out_idx[: K.value].copy(), out_sums[: K.value].copy()
         return out_idx[: K.value], out_sums[: K.value]
+
+    def _host_out(self):
+        """Pinned result buffers (n_g entries), allocated once per context:
+        full-bandwidth D2H; results are copied out of them (K entries)."""
+        if getattr(self, "_hout", None) is None:
+            pin = torch.cuda.is_available()
+            ti = torch.empty(self.n_g, dtype=torch.int32, pin_memory=pin)
+            ts = torch.empty(self.n_g, dtype=self.dtype, pin_memory=pin)
+            self._hout = (ti, ts)
+        ti, ts = self._hout
+        return ti.numpy(), ts.numpy()
 
     def sync(self):
         check(lib().micro_sync(self._h))
@@ -218,8 +230,7 @@ class Micro:
         """(indices int32, sums) of the last step as host numpy arrays; with
         caller buffers (e.g. pinned) the result views them without a copy."""
         if out_idx is None or out_sums is None:
-            idx = np.empty(self.n_g, np.int32)
-            sums = np.empty(self.n_g, _NP[self.dtype])
+            idx, sums = self._host_out()
         else:
             idx, sums = out_idx, out_sums
         K = C.c_int64()
