@@ -1,11 +1,13 @@
 // cpp_e2e.cpp — end-to-end time of the C++ drop-in (sparsim_b200.hpp
 // MicroEngine::step: host gradient in, aggregated selection + sums out) at
-// BASELINE C3 size, fp32, pinned host gradients.
+// BASELINE C3 size, fp32.  Every step gets a fresh N(0,1) gradient (made on
+// the device by micro_synth_gaussian and copied into pinned host memory
+// outside the timed call); the threshold adapts for `prime` steps first.
 //   g++ -std=c++20 -O2 -I include tools/cpp_e2e.cpp -L paper_2310_00967_b200/lib -lmicro_b200 \
-//       -Wl,-rpath,$PWD/paper_2310_00967_b200/lib -o tools/build/cpp_e2e
+//       -Wl,-rpath,'$ORIGIN/../../paper_2310_00967_b200/lib' -o tools/build/cpp_e2e
 #include <chrono>
 #include <cstdio>
-#include <random>
+#include <cstdlib>
 #include <vector>
 
 #include "sparsim_b200.hpp"
@@ -13,26 +15,32 @@
 int main(int argc, char** argv) {
   const sparsim::Index n_g = argc > 1 ? std::atoll(argv[1]) : 138000000;
   const int steps = argc > 2 ? std::atoi(argv[2]) : 10;
+  const int prime = argc > 3 ? std::atoi(argv[3]) : 300;
   sparsim::SparsifierConfig sc;
   sc.density = 0.01;
   sc.initial_threshold = 0.025758293035489;
   sparsim::MicroEngine eng(n_g, 1, sc, true, MICRO_F32);
-  const int nbuf = 4;
-  std::vector<float*> G(nbuf);
-  std::mt19937_64 rng(1);
-  std::normal_distribution<float> unit(0.0f, 1.0f);
-  for (auto& g : G) {
-    sparsim::b200::check(micro_host_malloc(reinterpret_cast<void**>(&g), (int64_t)n_g * 4));
-    for (sparsim::Index j = 0; j < n_g; ++j) g[j] = unit(rng);
-  }
+  float* h = nullptr;
+  void* d = nullptr;
+  sparsim::b200::check(micro_host_malloc(reinterpret_cast<void**>(&h), (int64_t)n_g * 4));
+  sparsim::b200::check(micro_device_malloc(&d, (int64_t)n_g * 4, 0));
   std::vector<double> summed;
-  for (int t = 0; t < 3; ++t) eng.step(G[t % nbuf], 0.01, t, &summed);  // warm
-  const auto t0 = std::chrono::steady_clock::now();
-  std::size_t K = 0;
-  for (int t = 3; t < 3 + steps; ++t) K += eng.step(G[t % nbuf], 0.01, t, &summed).indices.size();
-  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / steps;
+  double total_us = 0.0, K = 0.0;
+  for (int t = 0; t < prime + steps; ++t) {
+    sparsim::b200::check(micro_synth_gaussian(MICRO_F32, 1, 0, (uint64_t)t, n_g, d, nullptr));
+    sparsim::b200::d2h(h, d, (std::size_t)n_g * 4);  // a fresh host gradient (untimed)
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto agg = eng.step(h, 0.01, t, &summed);
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    if (t >= prime) {
+      total_us += us;
+      K += (double)agg.indices.size();
+    }
+  }
   std::printf("{\"what\": \"C++ MicroEngine::step e2e (pinned host fp32 gradient in, indices + sums out)\", "
-              "\"n_g\": %lld, \"us_per_step\": %.1f, \"mean_K\": %.0f}\n", (long long)n_g, us, (double)K / steps);
-  for (auto* g : G) micro_host_free(g);
+              "\"n_g\": %lld, \"prime\": %d, \"steps\": %d, \"us_per_step\": %.1f, \"density\": %.5f}\n",
+              (long long)n_g, prime, steps, total_us / steps, K / steps / (double)n_g);
+  micro_host_free(h);
+  micro_device_free(d);
   return 0;
 }
