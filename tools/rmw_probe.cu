@@ -3,6 +3,8 @@
 //   0: one thread per index, plain RMW        1: 0 with ld.global.L2::64B
 //   2: 4 indices per thread (ILP), 64B hint   3: write only x[j] = v
 //   4: read only (sum x[j])                   5: 2 with ld.global.L2::128B
+//   6: whole 32-byte sector writes at a random subset of sectors (the dense
+//      g/n pattern), 7: the same sectors with streaming (.cs) stores
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o rmw_probe tools/rmw_probe.cu
 #include <algorithm>
 #include <cstdio>
@@ -52,6 +54,42 @@ __global__ void __launch_bounds__(256) rmw(float* x, const int* idx, const float
     const float y = x[j];
     if (y == 12345.f) sink[0] = y;
   }
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) secw(float* x, const int* sec, long K) {
+  const long tid = blockIdx.x * 256L + threadIdx.x;
+  if (tid >= K) return;
+  float4* p = reinterpret_cast<float4*>(x) + 2L * sec[tid];
+  const float4 z = make_float4(0.5f, 0.f, 0.f, 0.25f);
+  if (V == 6) {
+    p[0] = z;
+    p[1] = z;
+  } else {
+    __stcs(p, z);
+    __stcs(p + 1, z);
+  }
+}
+
+template <int V>
+float run_sec(float* x, const int* sec, long K, float* flush, size_t fbytes) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e9f;
+  for (int r = 0; r < 12; ++r) {
+    cudaMemsetAsync(flush, r, fbytes);
+    cudaEventRecord(a);
+    secw<V><<<(unsigned)((K + 255) / 256), 256>>>(x, sec, K);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (r >= 2) best = ms < best ? ms : best;
+  }
+  printf("  variant %d: %ld sectors, best %.1f us (%.0f GB/s of 32-byte writes)\n", V, K, best * 1e3,
+         K * 32.0 / (best * 1e-3) / 1e9);
+  return best;
 }
 
 template <int V>
@@ -110,6 +148,18 @@ int main(int argc, char** argv) {
   run<5>(x, idx, val, K, sink, flush, fbytes);
   run<3>(x, idx, val, K, sink, flush, fbytes);
   run<4>(x, idx, val, K, sink, flush, fbytes);
+  {  // the dense g/n pattern: ~2 x 8.5 % of the sectors, whole 32-byte writes
+    std::bernoulli_distribution pick_s(argc > 3 ? atof(argv[3]) : 0.17);
+    std::vector<int> hs;
+    for (long s = 0; s < n / 8; ++s)
+      if (pick_s(rng)) hs.push_back((int)s);
+    int* dsec;
+    cudaMalloc(&dsec, hs.size() * 4);
+    cudaMemcpy(dsec, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice);
+    run_sec<6>(x, dsec, (long)hs.size(), flush, fbytes);
+    run_sec<7>(x, dsec, (long)hs.size(), flush, fbytes);
+    cudaFree(dsec);
+  }
   const cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
   return 0;
