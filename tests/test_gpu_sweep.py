@@ -52,3 +52,27 @@ def test_sweep(case, n_g, n, d, ef, kind, dense, delta0):
             dw[r["union_idx"]] = r["union_sum"].astype(np.float32) / np.float32(n)
             assert np.array_equal(m.dense(), dw), t
     m.close()
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("case,n_g,n,d,ef,kind,dense,delta0", _cases(count=40, seed=99))
+def test_sweep_f64_reference_code(case, n_g, n, d, ef, kind, dense, delta0):
+    """The same sweep in fp64 against the reference's own compiled code."""
+    from oracle import RefCluster
+    o = Oracle()
+    m = engine.Micro(n_g, n, dtype=torch.float64, density=d, initial_threshold=delta0, error_feedback=ef,
+                     sparsifier=kind, dense_output=dense)
+    x = torch.zeros(n_g, device="cuda", dtype=torch.float64)
+    m.set_model(x)
+    ref = RefCluster(n_g, n, d, delta0, 0.01, 1e-12, False, ef, model=True)
+    for t in range(3):
+        G = np.stack([o.gaussian(case, i, t, n_g) for i in range(n)]).astype(np.float64)
+        m.step(list(torch.from_numpy(G).cuda()), 0.01, t)
+        r = ref.step(G, 0.01, t, kind=kind)
+        idx, sums = m.union()
+        assert np.array_equal(m.query().counts, r["counts"]), t
+        assert np.array_equal(idx.astype(np.int64), r["union_idx"]), t
+        assert np.array_equal(sums, r["union_sum"]), t
+        assert np.array_equal(np.stack([m.residual(i) for i in range(n)]), ref.residuals()), t
+        assert np.array_equal(x.cpu().numpy(), ref.x), t
+    m.close()
