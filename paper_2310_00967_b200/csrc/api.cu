@@ -437,7 +437,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.norm_mode = norm_mode(c);
     c->fin_done = true;
   }
-  unsigned gblocks = (unsigned)((b.num_runs + kGatherRuns - 1) / kGatherRuns);
+  unsigned gblocks = (unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps);
   if (c->norm && c->kind == 0) {  // one more CTA reduces k1_stream's per-CTA partials
     b.sq_part = c->norm_part;
     b.sq_parts = (int)grid;
@@ -843,7 +843,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
       const int64_t ue = c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>();
       const int64_t runs = max_range / (kStreamWarps * ue) + 2;
       const int64_t S = (runs + kMaxSupers - 1) / kMaxSupers;
-      c->super_runs = (int)std::max<int64_t>(kGatherRuns, (S + kGatherRuns - 1) / kGatherRuns * kGatherRuns);
+      c->super_runs = (int)std::max<int64_t>(kGatherWarps, (S + kGatherWarps - 1) / kGatherWarps * kGatherWarps);
     }
   }
   if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);

@@ -362,8 +362,7 @@ __device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long 
   *a.fin_delta = d;
 }
 
-constexpr int kGatherWarps = 8;   // warps per k1_gather CTA
-constexpr int kGatherRuns = 16;   // runs per k1_gather CTA (two per warp; divides super_runs)
+constexpr int kGatherWarps = 8;   // runs per k1_gather CTA (divides super_runs)
 constexpr int kMaxSupers = 1024;  // super blocks per launch
 
 // CTA-wide sum of an int range [lo, hi) (256 threads).
@@ -410,7 +409,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     return;
   }
   const int gb = (int)blockIdx.x - (a.sq_part ? 1 : 0);
-  const int r0 = gb * kGatherRuns;
+  const int r0 = gb * kGatherWarps;
   const int sb = r0 / a.super_runs;
   // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0)
   long long base = block_sum_range(a.super_counts, 0, sb, s_part) +
@@ -425,57 +424,51 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     }
     for (int q = threadIdx.x; q < a.super_len; q += kGatherWarps * 32) a.super_clear[q] = 0;
   }
-  __shared__ int s_rc[kGatherRuns];  // this CTA's run counts
-  if (threadIdx.x < kGatherRuns)
-    s_rc[threadIdx.x] = r0 + (int)threadIdx.x < a.num_runs ? a.run_counts[r0 + threadIdx.x] : 0;
-  __syncthreads();
+  const int r = r0 + w;
+  // runs of this CTA before r (<= 7 L2 hits)
+  const int mine = (r0 + lane < a.num_runs && lane < w) ? a.run_counts[r0 + lane] : 0;
+  base += (long long)__reduce_add_sync(0xffffffffu, (unsigned)mine);
+  if (r >= a.num_runs) return;
+  const int n = a.run_counts[r];
+  if (!n) return;
+  const long long off = base < a.cap ? base : a.cap;
+  const long long src = (long long)r * a.run_stride;
+  const int32_t* __restrict__ si = a.stage_idx + src;
+  const T* __restrict__ sv = (const T*)a.stage_val + src;
+  int32_t* __restrict__ oi = a.sel_idx + off;
+  T* __restrict__ ov = (T*)a.sel_val + off;
+  const long long room = a.cap - off;
   T* __restrict__ x = (T*)a.model;
-  for (int h = 0; h < kGatherRuns / kGatherWarps; ++h) {  // warp w: runs w and w + 8 of the CTA
-    const int q = h * kGatherWarps + w;
-    const int r = r0 + q;
-    if (r >= a.num_runs) break;
-    const int n = s_rc[q];
-    if (!n) continue;
-    long long pre = base;
-    for (int p = 0; p < q; ++p) pre += s_rc[p];
-    const long long off = pre < a.cap ? pre : a.cap;
-    const long long src = (long long)r * a.run_stride;
-    const int32_t* __restrict__ si = a.stage_idx + src;
-    const T* __restrict__ sv = (const T*)a.stage_val + src;
-    int32_t* __restrict__ oi = a.sel_idx + off;
-    T* __restrict__ ov = (T*)a.sel_val + off;
-    const long long room = a.cap - off;
-    // kG entries per lane in flight: at high density a run holds hundreds of
-    // pairs and the model's random read-modify-write is latency bound
-    constexpr int kG = 8;
-    const int lim = n < room ? n : (int)room;
-    for (int m0 = lane; m0 < lim; m0 += 32 * kG) {
-      int32_t j[kG];
-      T v[kG], xv[kG];
+  // kG entries per lane in flight: at high density a run holds hundreds of
+  // pairs and the model's random read-modify-write is latency bound
+  constexpr int kG = 8;
+  const int lim = n < room ? n : (int)room;
+  for (int m0 = lane; m0 < lim; m0 += 32 * kG) {
+    int32_t j[kG];
+    T v[kG], xv[kG];
 #pragma unroll
-      for (int u = 0; u < kG; ++u) {
-        const int m = m0 + 32 * u;
-        if (m < lim) {
-          j[u] = si[m];
-          v[u] = sv[m];
-          oi[m] = j[u];
-          ov[m] = v[u];
-        }
-      }
-      if (x) {  // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
-#pragma unroll
-        for (int u = 0; u < kG; ++u)
-          if (m0 + 32 * u < lim) xv[u] = ld_rand(x + j[u]);
-#pragma unroll
-        for (int u = 0; u < kG; ++u)
-          if (m0 + 32 * u < lim) x[j[u]] = xv[u] - v[u];
+    for (int q = 0; q < kG; ++q) {
+      const int m = m0 + 32 * q;
+      if (m < lim) {
+        j[q] = si[m];
+        v[q] = sv[m];
+        oi[m] = j[q];
+        ov[m] = v[q];
       }
     }
-    __syncwarp();
-    for (int o = lane * 128; o < n * 4; o += 32 * 128) discard_l2_line(reinterpret_cast<const char*>(si) + o);
-    for (int o = lane * 128; o < n * (int)sizeof(T); o += 32 * 128)
-      discard_l2_line(reinterpret_cast<const char*>(sv) + o);
+    if (x) {  // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
+#pragma unroll
+      for (int q = 0; q < kG; ++q)
+        if (m0 + 32 * q < lim) xv[q] = ld_rand(x + j[q]);
+#pragma unroll
+      for (int q = 0; q < kG; ++q)
+        if (m0 + 32 * q < lim) x[j[q]] = xv[q] - v[q];
+    }
   }
+  __syncwarp();
+  for (int o = lane * 128; o < n * 4; o += 32 * 128) discard_l2_line(reinterpret_cast<const char*>(si) + o);
+  for (int o = lane * 128; o < n * (int)sizeof(T); o += 32 * 128)
+    discard_l2_line(reinterpret_cast<const char*>(sv) + o);
 }
 
 }  // namespace micro
