@@ -82,3 +82,33 @@ def test_device_calls_fail_loudly_without_gpu(L):
     rc = L.micro_ctx_create(C.byref(h), C.byref(cfg), None)
     assert rc == _lib.MICRO_ECUDA and not h.value
     assert L.micro_last_error()
+
+
+@pytest.mark.ref
+def test_host_error_messages_match_the_reference(L):
+    """The C ABI's status codes and messages are the reference's exceptions
+    (tensor.hpp:49-55, sparsifier.cpp:73-75, :112-122), word for word."""
+    from oracle import OracleError, Reference
+    from paper_2310_00967_b200 import sparsim
+    from paper_2310_00967_b200._lib import InvalidArgument
+    ref = Reference()
+    cases = [
+        (lambda: sparsim.partition(3, 4, 0, 0), lambda: ref.partition(3, 4, 0, 0)),
+        (lambda: sparsim.partition(8, 4, 0, 4), lambda: ref.partition(8, 4, 0, 4)),
+        (lambda: sparsim.partition(8, 0, 0, 0), lambda: ref.partition(8, 0, 0, 0)),
+        (lambda: sparsim.partition(8, 4, -1, 0), lambda: ref.partition(8, 4, -1, 0)),
+        (lambda: sparsim.global_target_count(1.5, 100), lambda: ref.global_target_count(1.5, 100)),
+        (lambda: sparsim.global_target_count(0.01, 0), lambda: ref.global_target_count(0.01, 0)),
+        (lambda: sparsim.per_worker_target_count(0.01, 100, 0), lambda: ref.per_worker_target_count(0.01, 100, 0)),
+        (lambda: sparsim.micro_update_threshold(sparsim.ThresholdState(1.0), 10, 5, 0.0),
+         lambda: ref.update_threshold(1.0, 10, 5, 0.0)),
+        (lambda: sparsim.micro_update_threshold(sparsim.ThresholdState(-1.0), 10, 5, 0.1),
+         lambda: ref.update_threshold(-1.0, 10, 5, 0.1)),
+    ]
+    for ours, theirs in cases:
+        with pytest.raises(InvalidArgument) as a:
+            ours()
+        with pytest.raises(OracleError) as b:
+            theirs()
+        theirs_msg = str(b.value).split("] ", 1)[-1]  # OracleError prefixes "[code] "
+        assert str(a.value) == theirs_msg, (str(a.value), theirs_msg)
