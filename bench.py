@@ -296,7 +296,11 @@ def our_arm(args, wl):
     k1a_avg_ms = statistics.mean(k1a_ms) if k1a_ms else ms_step
     # algorithmic bytes of the dominant kernel, k1_stream: read e and G, write
     # e (all n_g) + one (int32, value) pair per selection
-    k1_bytes = 3.0 * esz * n_g + (4.0 + esz) * float(k_own.mean())
+    # (top-k's compaction pass reads acc only, 1 element read per entry: the
+    # histogram passes already wrote acc into e; CLT-k's leader is top-k, its
+    # other workers select by threshold — the timed launches average over both)
+    acc_only = {"topk": W, "cltk": 1}.get(args.sparsifier, 0)
+    k1_bytes = (esz * n_g * (acc_only + 3.0 * (W - acc_only)) / W) + (4.0 + esz) * float(k_own.mean())
     achieved = k1_bytes / (k1a_avg_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
     # whole step vs the same roofline: K1 bytes + union (8 B) and, with the

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   const T eta = (T)a.eta;
   T probe = (T)0;  // becomes NaN iff some G is Inf/NaN
   unsigned mask[VPL];
+  bool tie_seen = false;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     mask[i] = 0;
@@ -158,14 +159,26 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       }
       set_comp(e[i], c, acc);
       bool sel = sel_unit && absx(acc) > thr;
-      if (kTie && sel_unit && absx(acc) == thr)  // top-k: ties at the pivot up to index J
-        sel = (long long)(base + (i * 32 + lane) * VN + c) <= tie_limit;
+      if (kTie) tie_seen |= sel_unit && absx(acc) == thr;
       if (!all_in) {
         const int j = base + (i * 32 + lane) * VN + c;
         sel = sel && j >= a.p_start && j < a.p_end;
       }
       mask[i] |= (unsigned)sel << c;
     }
+  }
+  // top-k: ties at the pivot are selected up to index J.  They are rare, so
+  // the index comparisons run only in the warps that hold one.
+  if (kTie && __any_sync(0xffffffffu, tie_seen)) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        const int j = base + (i * 32 + lane) * VN + c;
+        const bool tie = sel_unit && absx(comp(e[i], c)) == thr && (long long)j <= tie_limit &&
+                         (all_in || (j >= a.p_start && j < a.p_end));
+        mask[i] |= (unsigned)tie << c;
+      }
   }
 
   if (kMode != kWriteNone) {
