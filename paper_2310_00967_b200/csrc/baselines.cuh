@@ -91,8 +91,17 @@ __device__ __forceinline__ void hist_add(unsigned* s_hist, T acc, unsigned long 
 // the engine's top-k) acc is also written back in place and G probed for
 // non-finite values, so the later passes and the compaction read acc alone
 // (4 instead of 8 bytes per element).
+// vectors per thread in flight (warp-uniform grid-stride loops)
+#ifndef MICRO_HIST_VECS
+#define MICRO_HIST_VECS 8
+#endif
+#ifndef MICRO_HIST_VECS_G
+#define MICRO_HIST_VECS_G 2
+#endif
+constexpr int kHistVecs = MICRO_HIST_VECS, kHistVecsG = MICRO_HIST_VECS_G;
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_topk_hist(const T* e, const T* __restrict__ g, double eta_d, int64_t n_g,
+__global__ void __launch_bounds__(256, 4) k_topk_hist(const T* e, const T* __restrict__ g, double eta_d, int64_t n_g,
                                                    int shift, int width, const TopkState* st,
                                                    unsigned* __restrict__ hist, T* acc_out = nullptr,
                                                    int* flags = nullptr) {
@@ -131,27 +140,27 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* e, const T* __restri
     return;
   }
   const int64_t nv = n_g / VN;  // whole vectors (e, G 16-byte aligned: K1 staging / cudaMalloc)
-  if (!g) {  // acc alone: four vectors per thread in flight
-    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * 4; v0 < nv; v0 += 4 * stride) {  // warp-uniform
-      V ev[4];
-      bool ok[4];
+  if (!g) {  // acc alone: kHistVecs vectors per thread in flight
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * kHistVecs; v0 < nv; v0 += kHistVecs * stride) {
+      V ev[kHistVecs];
+      bool ok[kHistVecs];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kHistVecs; ++u) {
         const int64_t v = v0 + u * blockDim.x + threadIdx.x;
         ok[u] = v < nv;
         if (ok[u]) ev[u] = ld_stream(reinterpret_cast<const V*>(e) + v);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kHistVecs; ++u)
 #pragma unroll
         for (int c = 0; c < VN; ++c) hist_add<T>(s_hist, ok[u] ? comp(ev[u], c) : (T)0, prefix, mask, shift, dmask, ok[u]);
     }
   } else
-  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * 2; v0 < nv; v0 += 2 * stride) {  // warp-uniform
-    V ev[2], gv[2];
-    bool ok[2];
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * kHistVecsG; v0 < nv; v0 += kHistVecsG * stride) {
+    V ev[kHistVecsG], gv[kHistVecsG];
+    bool ok[kHistVecsG];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kHistVecsG; ++u) {
       const int64_t v = v0 + u * blockDim.x + threadIdx.x;
       ok[u] = v < nv;
       if (ok[u]) {
@@ -160,7 +169,7 @@ __global__ void __launch_bounds__(256) k_topk_hist(const T* e, const T* __restri
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kHistVecsG; ++u) {
       V av;
 #pragma unroll
       for (int c = 0; c < VN; ++c) {
