@@ -691,7 +691,7 @@ int reset_state(micro_ctx* c) {
   if (c->norm) {
     CU(cudaMemsetAsync(c->norm_ticket, 0, sizeof(unsigned) * (sumsq_groups(c->norm_ctas) + 1), c->stream));
     CU(cudaMemsetAsync(c->norm_sq, 0, sizeof(double) * c->n_local, c->stream));
-    CU(cudaMemsetAsync(c->norm_corr, 0, sizeof(double) * c->n_local, c->stream));
+    CU(cudaMemsetAsync(c->norm_corr, 0, 2 * sizeof(double) * c->n_local, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   c->steps = 0;
@@ -879,7 +879,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     if ((rc = c->alloc((void**)&c->norm_group, sizeof(double) * groups))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->norm_ticket, sizeof(unsigned) * (groups + 1)))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->norm_sq, sizeof(double) * c->n_local))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->norm_corr, sizeof(double) * c->n_local))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->norm_corr, 2 * sizeof(double) * c->n_local))) return cleanup(rc);
   }
   cudaError_t e;
   if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||

@@ -41,7 +41,8 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
   // sq_corr (kZero, error norm on): per worker, the squares of the residual
   // entries zeroed here (foreign union indices), subtracted from K1's
   // ||e||^2 by k_finalize.  Lane r of each warp accumulates worker r
-  // (r + 32 in a second register); one global atomic per block and worker.
+  // (r + 32 in a second register); one order-independent fixed-point add
+  // (norm.cuh fx_add) per block and worker.
   __shared__ double s_corr[8][kMaxWorkers];
   pdl_wait();  // the workers' K1 results are complete
   pdl_trigger();
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
     if ((int)threadIdx.x < n) {
       double tot = 0.0;
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += s_corr[q][threadIdx.x];
-      if (tot != 0.0) atomicAdd(sq_corr + threadIdx.x, tot);
+      if (tot != 0.0) fx_add(sq_corr + 2 * threadIdx.x, tot);
     }
   }
 }
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_
     if (threadIdx.x == 0) {
       double tot = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_corr[w];
-      if (tot != 0.0) atomicAdd(sq_corr, tot);
+      if (tot != 0.0) fx_add(sq_corr, tot);
     }
   }
 }
@@ -213,7 +214,7 @@ struct FinalizeArgs {
   int norm_mode;              // 0: not recorded (NaN), 1: sqrt(sq - sq_corr), 2: residual is zero (EF off)
   int update_delta;           // 0: comparison sparsifiers (no threshold estimate, harness.cpp:201)
   const double* sq;           // per worker ||e||^2 after K1 (own selections zeroed)
-  double* sq_corr;            // per worker squares of the foreign entries zeroed by the exchange (reset here)
+  double* sq_corr;            // per worker 16-byte fixed-point slots (fx_add): squares of the foreign entries zeroed by the exchange (cleared here)
 };
 
 __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long n, int64_t key) {
@@ -264,9 +265,8 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
       a.hist_delta[a.slot * a.n_local + i] = d;
       double err = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not recorded
       if (a.norm_mode == 1) {
-        const double sq = a.sq[i] - (a.sq_corr ? a.sq_corr[i] : 0.0);
+        const double sq = a.sq[i] - (a.sq_corr ? fx_take(a.sq_corr + 2 * i) : 0.0);
         err = sqrt(sq > 0.0 ? sq : 0.0);
-        if (a.sq_corr) a.sq_corr[i] = 0.0;
       } else if (a.norm_mode == 2) {
         err = 0.0;
       }

@@ -164,7 +164,7 @@ struct micro_ctx {
   double* norm_group = nullptr;
   unsigned* norm_ticket = nullptr;     // norm_groups + 1
   double* norm_sq = nullptr;           // n_local
-  double* norm_corr = nullptr;         // n_local: squares of foreign entries zeroed by the exchange
+  double* norm_corr = nullptr;         // n_local 16-byte fixed-point slots (norm.cuh fx_add): squares of foreign entries zeroed by the exchange
   // host-side step state
   int64_t steps = 0;      // completed aggregations
   int64_t t_cur = -1;     // iteration of the pending/last compress

@@ -31,6 +31,36 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
+// Exchange-side corrections (squares of the foreign entries a worker's
+// residual loses in the exchange) come from many CTAs, and over peer memory
+// from several GPUs, in no fixed order.  fp64 atomicAdd would make the
+// recorded norm depend on CTA timing (acceptance C11: identical runs give
+// identical records), so each CTA's (deterministic) non-negative partial is
+// rounded once to 64.64 fixed point and added with integer atomics, which
+// are exact and order-independent.  A slot is two u64 words {frac, int}
+// (16 bytes); a non-finite partial saturates the slot to +inf.
+__device__ __forceinline__ void fx_add(double* slot, double v) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(slot);
+  if (!(v < 1.8e19)) {  // non-finite or out of range
+    atomicExch(a + 1, ~0ull);
+    return;
+  }
+  const double h = floor(v);
+  const unsigned long long lo = __double2ull_rz((v - h) * 18446744073709551616.0);
+  const unsigned long long old = atomicAdd(a, lo);
+  atomicAdd(a + 1, (unsigned long long)h + (old + lo < old ? 1ull : 0ull));
+}
+
+// Reads a slot and clears it for the next step (single reader).
+__device__ __forceinline__ double fx_take(double* slot) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(slot);
+  const unsigned long long lo = a[0], hi = a[1];
+  a[0] = 0ull;
+  a[1] = 0ull;
+  if (hi == ~0ull) return __longlong_as_double(0x7ff0000000000000ll);
+  return (double)hi + (double)lo * 0x1p-64;
+}
+
 // Called by every thread of the CTA (contains a __syncthreads) at the end of
 // the kernel: after it returns, only warp 0 of the finishing CTAs has done
 // anything further.

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) k_peer_exchange(PeerPtrs p, int n, int me
     if ((int)threadIdx.x < n && (int)threadIdx.x != me) {
       double tot = 0.0;
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += s_corr[q][threadIdx.x];
-      if (tot != 0.0) atomicAdd(p.corr[threadIdx.x], tot);
+      if (tot != 0.0) fx_add(p.corr[threadIdx.x], tot);
     }
   }
   __threadfence_system();  // peer stores visible before the caller's barrier
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me,
     if (threadIdx.x == 0) {
       double tot = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_q[w];
-      if (tot != 0.0) atomicAdd(corr, tot);
+      if (tot != 0.0) fx_add(corr, tot);
     }
   }
   __threadfence_system();
