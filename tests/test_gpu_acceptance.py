@@ -163,3 +163,17 @@ def test_harness_single_worker_and_exclusivity():
         assert r["actual_density"] == r["total_selected"] / 1024
         assert r["redundant_traffic_factor"] == (1.0 if r["total_selected"] else 0.0)
     m.close()
+
+
+@pytest.mark.parametrize("n", [2, 8])
+def test_c11_error_norm_bitwise_many_ctas(n):
+    """C11 at a size where the exchange runs hundreds of CTAs per worker: the
+    error norm's exchange corrections arrive in CTA-timing order, so they are
+    accumulated in fixed point (norm.cuh fx_add); repeated runs must give the
+    same records bit for bit."""
+    runs = []
+    for _ in range(3):
+        m, _ = _run(2_000_000, n, 30, seed=5, density=0.05, initial_threshold=0.5)
+        runs.append([(r["K"], r["error_norm"].hex()) for r in m.records(30)])
+        m.close()
+    assert runs[0] == runs[1] == runs[2]
