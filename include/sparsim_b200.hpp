@@ -505,6 +505,12 @@ class MicroEngine {
     return agg;
   }
 
+  // Back to t = 0 (residuals 0, thresholds delta_0).  Needed after a
+  // non-finite gradient: the reference throws before its accumulator replaces
+  // the residual (harness.cpp:128-130, :223); here K1 has already streamed the
+  // NaN/Inf into e_{t+1}, so the engine refuses to step until reset.
+  void reset() { b200::check(micro_ctx_reset(ctx_)); }
+
   std::vector<ThresholdState> thresholds() const {
     std::vector<double> d((std::size_t)n_);
     b200::check(micro_query(ctx_, nullptr, nullptr, d.data()));

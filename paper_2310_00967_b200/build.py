@@ -17,10 +17,11 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmicro_b200.so")
 SOURCES = ["api.cu", "dist_api.cu", "value_api.cu"]
-HEADERS = ["internal.cuh", "baselines.cuh", "common.cuh", "norm.cuh", "select.cuh", "select_tma.cuh", "select_stream.cuh", "exchange.cuh", "peer.cuh"]
+HEADERS = ["internal.cuh", "baselines.cuh", "common.cuh", "norm.cuh", "scan.cuh", "select.cuh", "select_stream.cuh",
+           "exchange.cuh", "peer.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
          "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
          "-I", os.path.join(ROOT, "include")]
 
@@ -38,9 +39,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []),
-           "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES]]
-    subprocess.run(cmd, check=True)
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    # one nvcc per translation unit, in parallel, then one shared-library link
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        procs.append(subprocess.Popen([NVCC, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []),
+                                       "-c", "-o", obj, os.path.join(CSRC, src)]))
+    if any(p.wait() != 0 for p in procs):
+        raise subprocess.CalledProcessError(1, "nvcc")
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], check=True)
     return LIB
 
 

@@ -133,7 +133,7 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   }
   f.dense = c->dense_fused ? nullptr : c->dense;  // fused: K1 maintained it
   // n = 1 with the streaming K1: k1_gather applied the model update
-  f.model = (c->sel_is_union && c->k1_kind == 0) ? nullptr : c->model;
+  f.model = c->sel_is_union ? nullptr : c->model;
   f.update_delta = c->kind == 0;
   if (c->vectors_done) {  // k_dense_all wrote the model and the dense g/n
     f.model = nullptr;
@@ -148,8 +148,8 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
   f.hist_delta = c->hist_delta;
   f.hist_err = c->hist_err;
   f.norm_mode = norm_mode(c);
-  f.sq = c->norm_sq;
-  f.sq_corr = (c->n > 1 && c->kind == 0) ? c->norm_corr : nullptr;
+  f.slots = c->norm_slot;
+  f.corr = c->n > 1 && c->kind == 0;
   const int blocks = (f.dense || f.model) ? finalize_blocks(c) : 1;  // grid-stride over the union
   if (c->fin_done) {
     // k1_gather already did the threshold update + history (n = 1, micro_step);
@@ -166,7 +166,7 @@ int launch_finalize(micro_ctx* c, const int32_t* uidx, const void* usum, int k_f
       k_dense_clear<T><<<blocks, 256, 0, c->stream>>>(f.prev_idx, f.prev_K, (T*)c->dense, c->n_g);
       CU(cudaGetLastError());
     }
-    CU(launch_maybe_pdl(c->pdl && !waited, k_finalize<T>, dim3(blocks), dim3(256), c->stream, f));
+    CU(launch_maybe_pdl(!waited, k_finalize<T>, dim3(blocks), dim3(256), c->stream, f));
   }
   if (!c->cfg.error_feedback && c->n > 1)
     for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, c->stream));
@@ -180,6 +180,17 @@ template int launch_finalize<float>(micro_ctx*, const int32_t*, const void*, int
 template int launch_finalize<double>(micro_ctx*, const int32_t*, const void*, int);
 
 
+
+int bitmap_offsets(const unsigned* bitmap, int64_t nwords, int* off, int* tiles, cudaStream_t st) {
+  const int64_t nt = scan_tiles(nwords);
+  k_scan_totals<true><<<(unsigned)nt, kScanThreads, 0, st>>>(bitmap, nwords, tiles);
+  CU(cudaGetLastError());
+  k_scan_top<<<1, kScanThreads, 0, st>>>(tiles, nt, nullptr);
+  CU(cudaGetLastError());
+  k_scan_apply<true><<<(unsigned)nt, kScanThreads, 0, st>>>(bitmap, nwords, tiles, off);
+  CU(cudaGetLastError());
+  return MICRO_OK;
+}
 
 int check_ctx(micro_ctx* c) {
   if (!c) return fail(MICRO_EINVAL, "null context");
@@ -210,35 +221,12 @@ int check_poison(micro_ctx* c) {
 
 namespace {
 
-// K1 streaming configurations (warps, stages, unit bytes); MICRO_K1_CFG picks one.
-using K1Cfg0 = WsCfg<8, 4, 2048>;
-using K1Cfg1 = WsCfg<16, 4, 1024>;
-using K1Cfg2 = WsCfg<16, 2, 2048>;
-using K1Cfg3 = WsCfg<12, 3, 2048>;
-using K1Cfg4 = WsCfg<32, 2, 1024>;
-using K1Cfg5 = WsCfg<8, 6, 2048>;
-using K1Cfg6 = WsCfg<16, 3, 2048>;
-using K1Cfg7 = WsCfg<8, 1, 1024, false, 6>;   // LDG streaming, 48 warps/SM
-using K1Cfg8 = WsCfg<8, 1, 2048, false, 4>;   // LDG streaming, 32 warps/SM, 4 vectors/lane
-using K1Cfg9 = WsCfg<8, 1, 1024, false, 8>;   // LDG streaming, 64 warps/SM
-constexpr int kNumK1Cfg = 10;
-
-// Look-back words are shared by every ordered launch of a context: a launch
-// with G CTAs stamps [0, G) through its chain and its last CTA stamps
-// [G, hwm) with the same epoch, so when the next launch starts every word it
-// can read carries a different epoch (epochs are 24-bit and skip 0, the
-// memset value of never-used words).
-unsigned int next_epoch(micro_ctx* c) {
-  unsigned int e = ++c->epoch;
-  if ((e & 0xFFFFFFu) == 0) e = ++c->epoch;
-  return e;
-}
 SumSqSlots norm_slots(micro_ctx* c, int i) {
   SumSqSlots q{};
   q.part = c->norm_part;
   q.group = c->norm_group;
   q.ticket = c->norm_ticket;
-  q.out = c->norm_sq + i;
+  q.out = &c->norm_slot[i].sq;
   return q;
 }
 
@@ -250,78 +238,6 @@ int launch_sumsq(micro_ctx* c, int i) {
   k_sumsq<T><<<(unsigned)grid, 256, 0, c->stream>>>((const T*)c->resid[i], c->n_g, norm_slots(c, i));
   CU(cudaGetLastError());
   return MICRO_OK;
-}
-
-int64_t status_span(micro_ctx* c, int64_t G) {
-  c->status_hwm = std::max(c->status_hwm, G);
-  return c->status_hwm;
-}
-
-template <typename T, int kMode, class Cfg>
-int launch_k1_tma_cfg(micro_ctx* c, TmaSelectArgs a) {
-  static int resident[64] = {0};  // CTAs per SM, per instantiation and device
-  if (c->dev >= 64 || !resident[c->dev]) {
-    if (Cfg::SMEM)
-      CU(cudaFuncSetAttribute(k1_tma_select<T, kMode, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg::SMEM));
-    int occ = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1_tma_select<T, kMode, Cfg>, Cfg::THREADS, Cfg::SMEM));
-    if (occ < 1) return fail(MICRO_ECUDA, "K1 configuration does not fit on an SM");
-    if (c->dev < 64) resident[c->dev] = std::min(occ, Cfg::MINB);
-  }
-  const int per_sm = c->dev < 64 ? resident[c->dev] : 1;
-  constexpr int UNIT = Cfg::UNIT_BYTES / (int)sizeof(T);
-  a.num_units = (c->n_g + UNIT - 1) / UNIT;
-  a.unit_lo = a.p_start / UNIT;
-  a.unit_hi = (a.p_end - 1) / UNIT;
-  // persistent: every CTA resident (the look-back waits only on earlier CTAs)
-  const int64_t grid = (int64_t)num_sms(c->dev) * per_sm;
-  if (grid > c->status_len) return fail(MICRO_ECAPACITY, "look-back workspace too small");
-  a.status_len = status_span(c, grid);
-  k1_tma_select<T, kMode, Cfg><<<(unsigned)grid, Cfg::THREADS, Cfg::SMEM, c->stream>>>(a);
-  CU(cudaGetLastError());
-  return MICRO_OK;
-}
-
-template <typename T, int kMode>
-int launch_k1_tma_mode(micro_ctx* c, const TmaSelectArgs& a) {
-  switch (c->k1_cfg) {
-    case 1: return launch_k1_tma_cfg<T, kMode, K1Cfg1>(c, a);
-    case 2: return launch_k1_tma_cfg<T, kMode, K1Cfg2>(c, a);
-    case 3: return launch_k1_tma_cfg<T, kMode, K1Cfg3>(c, a);
-    case 4: return launch_k1_tma_cfg<T, kMode, K1Cfg4>(c, a);
-    case 5: return launch_k1_tma_cfg<T, kMode, K1Cfg5>(c, a);
-    case 6: return launch_k1_tma_cfg<T, kMode, K1Cfg6>(c, a);
-    case 7: return launch_k1_tma_cfg<T, kMode, K1Cfg7>(c, a);
-    case 8: return launch_k1_tma_cfg<T, kMode, K1Cfg8>(c, a);
-    case 9: return launch_k1_tma_cfg<T, kMode, K1Cfg9>(c, a);
-    default: return launch_k1_tma_cfg<T, kMode, K1Cfg0>(c, a);
-  }
-}
-
-template <typename T>
-int launch_k1_tma(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe) {
-  TmaSelectArgs a{};
-  a.grad = grad;
-  a.resid = c->resid[i];
-  a.n_g = c->n_g;
-  a.p_start = ps;
-  a.p_end = pe;
-  a.eta = eta;
-  a.delta = c->delta + i;
-  a.sel_idx = c->sel_idx[c->buf][i];
-  a.sel_val = c->sel_val[c->buf][i];
-  a.cap = c->sel_cap;
-  a.count = c->counts + i;
-  a.stage_idx = c->stage_idx;
-  a.stage_val = c->stage_val;
-  a.unit_counts = c->unit_counts;
-  a.status = c->status;
-  a.epoch = next_epoch(c);
-  a.flags = c->flags;
-  if (c->cfg.error_feedback) return launch_k1_tma_mode<T, kWriteZeroSel>(c, a);
-  if (c->n > 1) return launch_k1_tma_mode<T, kWriteAcc>(c, a);
-  return launch_k1_tma_mode<T, kWriteNone>(c, a);
 }
 
 template <typename T>
@@ -357,19 +273,19 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
   auto dispatch = [&](unsigned g) -> int {
-#define K1S(MODE, D) CU(launch_maybe_pdl(c->pdl, k1_stream<T, MODE, D, false>, dim3(g), dim3(kStreamThreads), st, a))
+#define K1S(MODE, D) CU(launch_pdl(k1_stream<T, MODE, D, false>, dim3(g), dim3(kStreamThreads), st, a))
 #define K1N(D)                                                                                              \
     do {                                                                                                      \
-      if (c->norm) CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
+      if (c->norm) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
       else K1S(kWriteZeroSel, D);                                                                             \
     } while (0)
     if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
     if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
       if (acc_in_e)  // top-k: e holds acc already; compact only
-        CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
+        CU(launch_pdl(k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
                             dim3(kStreamThreads), st, a));
       else if (tie)
-        CU(launch_maybe_pdl(c->pdl, k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
+        CU(launch_pdl(k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
       else K1S(kWriteAcc, false);
     } else if (c->n > 1) {
       if (c->cfg.error_feedback) K1N(false);
@@ -441,12 +357,12 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   if (c->norm && c->kind == 0) {  // one more CTA reduces k1_stream's per-CTA partials
     b.sq_part = c->norm_part;
     b.sq_parts = (int)grid;
-    b.sq_out = c->norm_sq + i;
+    b.sq_out = &c->norm_slot[i].sq;
     b.hist_err = c->hist_err;
     b.fin_slot = c->steps % kHistCap;
     gblocks += 1;
   }
-  CU(launch_maybe_pdl(c->pdl, k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
+  CU(launch_pdl(k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
   return MICRO_OK;
 }
 
@@ -501,57 +417,11 @@ int launch_baseline(micro_ctx* c, int i, const void* grad, double eta, int64_t t
 
 template <typename T>
 int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
+  if (c->kind) return launch_baseline<T>(c, i, grad, eta, t);  // grad realigned by micro_compress
   int64_t ps, pe;
   partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
-  const bool aligned = ((uintptr_t)grad % 16) == 0;
-  if (c->kind) return launch_baseline<T>(c, i, grad, eta, t);  // grad realigned by micro_compress
-  if (c->k1_kind == 0 && aligned) return launch_k1_stream<T>(c, i, grad, eta, ps, pe);
-  if (c->k1_kind == 1 && aligned) {
-    TRY(launch_k1_tma<T>(c, i, grad, eta, ps, pe));
-    return c->norm ? launch_sumsq<T>(c, i) : MICRO_OK;
-  }
-  SelectArgs a{};
-  a.grad = grad;
-  a.resid = c->resid[i];
-  a.n_g = c->n_g;
-  a.p_start = ps;
-  a.p_end = pe;
-  a.eta = eta;
-  a.delta = c->delta + i;
-  a.sel_idx = c->sel_idx[c->buf][i];
-  a.sel_val = c->sel_val[c->buf][i];
-  a.cap = c->sel_cap;
-  a.count = c->counts + i;
-  a.status = c->status;
-  {
-    const int64_t P_cur = (pe - 1) / tile_elems<T>() - ps / tile_elems<T>() + 1;
-    a.p_max = status_span(c, P_cur);
-  }
-  a.ticket = c->ticket;
-  a.epoch = next_epoch(c);
-  a.tile_lo = 0;
-  a.num_tiles = (c->n_g + tile_elems<T>() - 1) / tile_elems<T>();
-  a.flags = c->flags;
-  const dim3 grid((unsigned)a.num_tiles);
-  const bool ef = c->cfg.error_feedback != 0;
-  const bool al = ((uintptr_t)grad % 16) == 0;
-  if (ef && al)
-    k1_fused_select<T, true, kWriteZeroSel, true><<<grid, kThreads, 0, c->stream>>>(a);
-  else if (ef)
-    k1_fused_select<T, true, kWriteZeroSel, false><<<grid, kThreads, 0, c->stream>>>(a);
-  else if (c->n > 1 && al)
-    k1_fused_select<T, true, kWriteAcc, true><<<grid, kThreads, 0, c->stream>>>(a);
-  else if (c->n > 1)
-    k1_fused_select<T, true, kWriteAcc, false><<<grid, kThreads, 0, c->stream>>>(a);
-  else if (al)
-    k1_fused_select<T, true, kWriteNone, true><<<grid, kThreads, 0, c->stream>>>(a);
-  else
-    k1_fused_select<T, true, kWriteNone, false><<<grid, kThreads, 0, c->stream>>>(a);
-  CU(cudaGetLastError());
-  return c->norm ? launch_sumsq<T>(c, i) : MICRO_OK;
+  return launch_k1_stream<T>(c, i, grad, eta, ps, pe);
 }
-
-
 
 // Clear the previous union's sectors of the dense g/n on the aux stream, so
 // the (small, latency-bound) clear overlaps the HBM-bound K1.
@@ -593,10 +463,7 @@ int aggregate_baseline(micro_ctx* c) {
           c->sel_idx[c->buf][i], c->counts + i, c->sel_cap, c->bitmap);
       CU(cudaGetLastError());
     }
-    k_word_popc<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_pc);
-    CU(cudaGetLastError());
-    size_t tb = c->cub_bytes;
-    CU(cub::DeviceScan::ExclusiveSum(c->cub_tmp, tb, c->word_pc, c->word_off, (int)c->nwords, st));
+    TRY(bitmap_offsets(c->bitmap, c->nwords, c->word_off, c->scan_tmp, st));
     k_bitmap_emit<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_off, uidx, K);
     CU(cudaGetLastError());
   }
@@ -626,13 +493,13 @@ int aggregate_cluster(micro_ctx* c) {
   const unsigned gx = (unsigned)std::min<int64_t>((expect + 255) / 256, 2048);
   const dim3 grid(gx, (unsigned)c->n);
   if (c->cfg.error_feedback)
-    CU(launch_maybe_pdl(c->pdl, k_cluster_reduce<T, true>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
+    CU(launch_pdl(k_cluster_reduce<T, true>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
                         (long long)c->sel_cap, c->n, (int64_t)c->t_cur, c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
-                        c->norm ? c->norm_corr : (double*)nullptr));
+                        c->norm ? c->norm_slot : (NormSlot*)nullptr));
   else
-    CU(launch_maybe_pdl(c->pdl, k_cluster_reduce<T, false>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
+    CU(launch_pdl(k_cluster_reduce<T, false>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
                         (long long)c->sel_cap, c->n, (int64_t)c->t_cur, c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
-                        (double*)nullptr));
+                        (NormSlot*)nullptr));
   CU(cudaGetLastError());
   return launch_finalize<T>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 1);
 }
@@ -690,8 +557,7 @@ int reset_state(micro_ctx* c) {
   }
   if (c->norm) {
     CU(cudaMemsetAsync(c->norm_ticket, 0, sizeof(unsigned) * (sumsq_groups(c->norm_ctas) + 1), c->stream));
-    CU(cudaMemsetAsync(c->norm_sq, 0, sizeof(double) * c->n_local, c->stream));
-    CU(cudaMemsetAsync(c->norm_corr, 0, 2 * sizeof(double) * c->n_local, c->stream));
+    CU(cudaMemsetAsync(c->norm_slot, 0, sizeof(NormSlot) * c->n_local, c->stream));
   }
   CU(cudaStreamSynchronize(c->stream));
   c->steps = 0;
@@ -790,20 +656,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   const int64_t max_range = c->kind ? c->n_g : (c->n_g + c->n - 1) / c->n;
   c->sel_cap = cfg->selection_capacity ? std::min<int64_t>(cfg->selection_capacity, max_range) : max_range;
   c->uni_cap = std::min<int64_t>(c->n_g, (int64_t)c->n * c->sel_cap);
-  c->p_max = c->esz == 4 ? p_max_for<float>(max_range) : p_max_for<double>(max_range);
-  c->status_len = std::max<int64_t>(c->p_max, 16 * num_sms(c->dev));  // >= K1 CTAs
-  {
-    const char* k = std::getenv("MICRO_K1_KERNEL");
-    c->k1_kind = !k ? 0 : std::strcmp(k, "tma") == 0 ? 1 : std::strcmp(k, "tile") == 0 ? 2 : 0;
-    if (c->kind) c->k1_kind = 0;  // the baselines compact with the streaming K1
-    if (const char* p = std::getenv("MICRO_PDL")) c->pdl = std::atoi(p) != 0;
-    if (const char* p = std::getenv("MICRO_H2D_PIPELINE")) c->h2d_pipeline = std::atoi(p) != 0;
-    c->dense_fused = c->sel_is_union && cfg->dense_output && c->k1_kind == 0;
-    c->use_tma = c->k1_kind != 2;
-    const char* cf = std::getenv("MICRO_K1_CFG");
-    c->k1_cfg = cf ? std::atoi(cf) : 0;
-    if (c->k1_cfg < 0 || c->k1_cfg >= kNumK1Cfg) c->k1_cfg = 0;
-  }
+  c->dense_fused = c->sel_is_union && cfg->dense_output;
   const int nbuf = c->n == 1 ? 2 : 1;
   c->resid.assign(c->n_local, nullptr);
   for (int b = 0; b < 2; ++b) {
@@ -831,22 +684,21 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   if ((rc = c->alloc((void**)&c->Kbuf, sizeof(long long) * 2))) return cleanup(rc);
   if (cfg->dense_output && (rc = c->alloc(&c->dense, c->n_g * c->esz))) return cleanup(rc);
   if (c->dense_fused && (rc = c->alloc((void**)&c->dense_dirty, (c->n_g / 256 + 8) * 8))) return cleanup(rc);
-  if ((rc = c->alloc((void**)&c->status, sizeof(unsigned long long) * c->status_len))) return cleanup(rc);
-  if (c->use_tma) {
-    const int64_t stage = c->p_max * (int64_t)tile_elems<float>() * 4 / (int64_t)c->esz;  // >= units(partition) * unit
+  {
+    // K1 staging: one run slot of kStreamWarps units per k1_stream CTA that meets the range
+    const int64_t ue = c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>();
+    const int64_t stage = (max_range / (kStreamWarps * ue) + 2) * kStreamWarps * ue;
     if ((rc = c->alloc((void**)&c->stage_idx, stage * 4))) return cleanup(rc);
     if ((rc = c->alloc(&c->stage_val, stage * c->esz))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->unit_counts, (max_range / 128 + 8) * sizeof(int)))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->super_counts, 2 * kMaxSupers * sizeof(int)))) return cleanup(rc);
     {
       // super blocks of S runs (S a multiple of the gather CTA's 8 runs), <= kMaxSupers of them
-      const int64_t ue = c->esz == 4 ? stream_unit_elems<float>() : stream_unit_elems<double>();
       const int64_t runs = max_range / (kStreamWarps * ue) + 2;
       const int64_t S = (runs + kMaxSupers - 1) / kMaxSupers;
       c->super_runs = (int)std::max<int64_t>(kGatherWarps, (S + kGatherWarps - 1) / kGatherWarps * kGatherWarps);
     }
   }
-  if ((rc = c->alloc((void**)&c->ticket, sizeof(unsigned int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->flags, sizeof(int)))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_t, sizeof(long long) * kHistCap))) return cleanup(rc);
   if ((rc = c->alloc((void**)&c->hist_K, sizeof(long long) * kHistCap))) return cleanup(rc);
@@ -861,13 +713,9 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     if ((rc = c->alloc((void**)&c->topk_hist, sizeof(unsigned) * kBins))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->tie_counts, sizeof(unsigned) * kTieChunks))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->bitmap, sizeof(unsigned) * c->nwords))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->word_pc, sizeof(int) * c->nwords))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->scan_tmp, sizeof(int) * scan_tiles(c->nwords)))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->word_off, sizeof(int) * c->nwords))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->minus_one, sizeof(double)))) return cleanup(rc);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, c->word_pc, c->word_off, (int)c->nwords, c->stream);
-    c->cub_bytes = std::max<size_t>(tb, 16);
-    if ((rc = c->alloc(&c->cub_tmp, c->cub_bytes))) return cleanup(rc);
   }
   if (c->norm) {
     // producing grids: k1_stream (one CTA per 8 units) or k_sumsq (4 per SM)
@@ -878,13 +726,9 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     if ((rc = c->alloc((void**)&c->norm_part, sizeof(double) * c->norm_ctas))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->norm_group, sizeof(double) * groups))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->norm_ticket, sizeof(unsigned) * (groups + 1)))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->norm_sq, sizeof(double) * c->n_local))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->norm_corr, 2 * sizeof(double) * c->n_local))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->norm_slot, sizeof(NormSlot) * c->n_local))) return cleanup(rc);
   }
   cudaError_t e;
-  if ((e = cudaMemsetAsync(c->status, 0, sizeof(unsigned long long) * c->status_len, c->stream)) != cudaSuccess ||
-      (e = cudaMemsetAsync(c->ticket, 0, sizeof(unsigned int), c->stream)) != cudaSuccess)
-    return cleanup(fail(MICRO_ECUDA, "memset: %s", cudaGetErrorString(e)));
   if (c->dense && !c->dense_fused) {
     if ((e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
@@ -952,7 +796,7 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
   TRY(c->esz == 4 ? fork_dense_clear<float>(c) : fork_dense_clear<double>(c));
   for (int i = 0; i < c->n_local; ++i) {
     const void* g = d_grads[i];
-    if (c->k1_kind == 0 && (uintptr_t)g % 16) {
+    if ((uintptr_t)g % 16) {
       // the streaming K1 reads 16-byte vectors: realign once (8 B/elem copy)
       TRY(ensure_staging(c));
       void* dst = (char*)c->staging + (size_t)i * c->staging_stride;
@@ -979,7 +823,7 @@ int micro_aggregate(micro_ctx* c) {
 int micro_step(micro_ctx* c, const void* const* d_grads, double eta, int64_t t) {
   TRY(check_ctx(c));
   // one-worker cluster, streaming K1: fold k_finalize into k1_gather
-  c->fuse_step = c->cluster && c->sel_is_union && c->k1_kind == 0 && (!c->dense || c->dense_fused);
+  c->fuse_step = c->cluster && c->sel_is_union && (!c->dense || c->dense_fused);
   const int rc = micro_compress(c, d_grads, eta, t);
   c->fuse_step = false;
   if (rc != MICRO_OK) {
@@ -1008,7 +852,7 @@ int micro_step_host(micro_ctx* c, const void* h_grads, double eta, int64_t t, in
   const size_t row = (size_t)c->n_g * c->esz;
   std::vector<const void*> g(c->n_local);
   for (int i = 0; i < c->n_local; ++i) g[i] = (const char*)c->staging + (size_t)i * c->staging_stride;
-  if (c->sel_is_union && c->kind == 0 && c->k1_kind == 0 && c->h2d_pipeline) {
+  if (c->sel_is_union && c->kind == 0) {
     // copy/compute overlap: the gradient crosses PCIe in chunks of whole K1
     // CTAs on a copy stream; K1 streams each chunk as it lands
     if (!c->h2d_stream) {

@@ -401,12 +401,6 @@ static __global__ void __launch_bounds__(256) k_union_mark(const int32_t* __rest
   }
 }
 
-static __global__ void __launch_bounds__(256) k_word_popc(const unsigned* __restrict__ bitmap, int64_t nwords,
-                                                   int* __restrict__ pc) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x)
-    pc[w] = __popc(bitmap[w]);
-}
-
 // off: exclusive prefix of the popcounts.  Writes the union in index order,
 // K, and clears the bitmap for the next step.
 static __global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict__ bitmap, int64_t nwords,

@@ -35,7 +35,7 @@ int micro_dist_gather_foreign(micro_ctx* c, const int32_t* d_all_idx, const int6
   for (int r = 0; r < c->n; ++r) mx = std::max<long long>(mx, cs.k[r]);
   if (mx > kmax) return fail(MICRO_EINVAL, "kmax %lld smaller than a count %lld", (long long)kmax, mx);
   const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
-  double* corr = c->norm ? c->norm_corr : nullptr;
+  NormSlot* corr = c->norm ? c->norm_slot : nullptr;
   if (c->esz == 4) {
     if (c->cfg.error_feedback)
       k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
@@ -89,7 +89,7 @@ void* peer_buf(micro_ctx* c, int b) {
     case 3: return c->uni_idx[1];
     case 4: return c->uni_sum[0];
     case 5: return c->uni_sum[1];
-    case 6: return c->norm ? c->norm_corr : nullptr;
+    case 6: return c->norm ? c->norm_slot : nullptr;
     case 7: return c->sel_idx[0][0];
     case 8: return c->sel_idx[1][0] != c->sel_idx[0][0] ? c->sel_idx[1][0] : nullptr;  // single-buffered
     default: return c->recv;
@@ -148,7 +148,7 @@ int micro_peer_import(micro_ctx* c, const void* all) {
     c->peer_uidx[1][r] = (int32_t*)p[3];
     c->peer_usum[0][r] = p[4];
     c->peer_usum[1][r] = p[5];
-    c->peer_corr[r] = c->norm ? (double*)p[6] : nullptr;
+    c->peer_corr[r] = c->norm ? (NormSlot*)p[6] : nullptr;
     c->peer_sel[0][r] = (const int32_t*)p[7];
     c->peer_sel[1][r] = (const int32_t*)p[8];
     c->peer_recv[r] = p[9];
@@ -214,7 +214,7 @@ int micro_peer_contribute(micro_ctx* c) {
   DeviceGuard dg(c->dev);
   const PeerBulkPtrs pb = bulk_ptrs(c);
   const dim3 grid(grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev) / 2 + 1, c->n);
-  double* corr = c->norm ? c->norm_corr : nullptr;
+  NormSlot* corr = c->norm ? c->norm_slot : nullptr;
   const int me = c->cfg.rank;
   if (c->esz == 4) {
     if (c->cfg.error_feedback)
@@ -333,7 +333,7 @@ int micro_group_attach(micro_ctx* const* ctxs, int n) {
       c->peer_uidx[1][q] = o->uni_idx[1];
       c->peer_usum[0][q] = o->uni_sum[0];
       c->peer_usum[1][q] = o->uni_sum[1];
-      c->peer_corr[q] = c->norm ? o->norm_corr : nullptr;
+      c->peer_corr[q] = c->norm ? o->norm_slot : nullptr;
       c->peer_sel[0][q] = o->sel_idx[0][0];
       c->peer_sel[1][q] = o->sel_idx[1][0];
       c->peer_recv[q] = o->recv;

@@ -37,7 +37,7 @@ template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long long* counts,
                                                         long long cap, int n, int64_t t,
                                                         int32_t* union_idx, T* union_sum,
-                                                        double* sq_corr) {
+                                                        NormSlot* sq_corr) {
   // sq_corr (kZero, error norm on): per worker, the squares of the residual
   // entries zeroed here (foreign union indices), subtracted from K1's
   // ||e||^2 by k_finalize.  Lane r of each warp accumulates worker r
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
     if ((int)threadIdx.x < n) {
       double tot = 0.0;
       for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += s_corr[q][threadIdx.x];
-      if (tot != 0.0) fx_add(sq_corr + 2 * threadIdx.x, tot);
+      if (tot != 0.0) fx_add(sq_corr + threadIdx.x, tot);
     }
   }
 }
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_idx, int64_t kmax,
                                                              Counts c, int me, T* resid, T* send,
-                                                             double* sq_corr) {
+                                                             NormSlot* sq_corr) {
   __shared__ double s_corr[8];
   const int o = blockIdx.y;
   if (o == me) return;  // block-uniform
@@ -211,10 +211,10 @@ struct FinalizeArgs {
   long long* hist_counts;
   double* hist_delta;
   double* hist_err;           // per worker ||e_{t+1}||_2 (error_norm record)
-  int norm_mode;              // 0: not recorded (NaN), 1: sqrt(sq - sq_corr), 2: residual is zero (EF off)
+  int norm_mode;              // 0: not recorded (NaN), 1: sqrt(sq - corrections), 2: residual is zero (EF off)
   int update_delta;           // 0: comparison sparsifiers (no threshold estimate, harness.cpp:201)
-  const double* sq;           // per worker ||e||^2 after K1 (own selections zeroed)
-  double* sq_corr;            // per worker 16-byte fixed-point slots (fx_add): squares of the foreign entries zeroed by the exchange (cleared here)
+  NormSlot* slots;            // per worker: ||e||^2 after K1 (own selections zeroed) + the exchange's corrections
+  int corr;                   // 1: subtract (and clear) the corrections (n > 1 MiCRO)
 };
 
 __device__ __forceinline__ long long lower_bound_i32(const int32_t* a, long long n, int64_t key) {
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(256) k_finalize(FinalizeArgs a) {
       a.hist_delta[a.slot * a.n_local + i] = d;
       double err = __longlong_as_double(0x7ff8000000000000ll);  // NaN: not recorded
       if (a.norm_mode == 1) {
-        const double sq = a.sq[i] - (a.sq_corr ? fx_take(a.sq_corr + 2 * i) : 0.0);
+        const double sq = a.slots[i].sq - (a.corr ? fx_take(a.slots + i) : 0.0);
         err = sqrt(sq > 0.0 ? sq : 0.0);
       } else if (a.norm_mode == 2) {
         err = 0.0;

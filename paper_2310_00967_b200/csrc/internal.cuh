@@ -3,9 +3,6 @@
 // value-level calls).  Not part of the ABI.
 #pragma once
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cub/device/device_select.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,9 +19,9 @@
 #include "baselines.cuh"
 #include "exchange.cuh"
 #include "peer.cuh"
+#include "scan.cuh"
 #include "select.cuh"
 #include "select_stream.cuh"
-#include "select_tma.cuh"
 
 namespace micro {
 namespace host {
@@ -92,9 +89,9 @@ cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(P...), dim3 grid, dim3 block
   return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
 }
 
-template <typename T>
-int64_t p_max_for(int64_t range) {
-  return (range + tile_elems<T>() - 1) / tile_elems<T>() + 2;
+template <typename... P, typename... A>
+cudaError_t launch_pdl(void (*kern)(P...), dim3 grid, dim3 block, cudaStream_t st, A&&... args) {
+  return launch_maybe_pdl(true, kern, grid, block, st, std::forward<A>(args)...);
 }
 
 }  // namespace host
@@ -131,18 +128,8 @@ struct micro_ctx {
   long long* Kbuf = nullptr;      // [2]
   void* dense = nullptr;
   void* model = nullptr;
-  // K1 workspace
-  unsigned long long* status = nullptr;
-  int64_t p_max = 0;
-  int64_t status_len = 0;       // allocated look-back words
-  int64_t status_hwm = 0;       // highest look-back index any launch has used
-  // K1 implementation (MICRO_K1_KERNEL): 0 "stream" k1_stream + k1_gather (default),
-  // 1 "tma" persistent k1_tma_select, 2 "tile" k1_fused_select (also the
-  // fallback for gradients that are not 16-byte aligned)
-  int k1_kind = 0;
-  bool use_tma = true;  // staging buffers allocated
-  int k1_cfg = 0;               // streaming configuration (MICRO_K1_CFG)
-  int32_t* stage_idx = nullptr;  // K1 staging runs (TMA kernel)
+  // K1 workspace (k1_stream -> k1_gather)
+  int32_t* stage_idx = nullptr;  // per-CTA staging runs
   void* stage_val = nullptr;
   int* unit_counts = nullptr;    // selections per K1 unit / per k1_stream CTA run
   // k1_stream -> k1_gather: selections per super block of super_runs CTA
@@ -150,8 +137,6 @@ struct micro_ctx {
   int* super_counts = nullptr;
   int super_runs = 8;
   int super_par = 0;
-  unsigned int* ticket = nullptr;
-  unsigned int epoch = 0;
   int* flags = nullptr;
   // history
   long long *hist_t = nullptr, *hist_K = nullptr, *hist_counts = nullptr;
@@ -163,8 +148,7 @@ struct micro_ctx {
   double* norm_part = nullptr;
   double* norm_group = nullptr;
   unsigned* norm_ticket = nullptr;     // norm_groups + 1
-  double* norm_sq = nullptr;           // n_local
-  double* norm_corr = nullptr;         // n_local 16-byte fixed-point slots (norm.cuh fx_add): squares of foreign entries zeroed by the exchange
+  micro::NormSlot* norm_slot = nullptr;  // n_local: ||e||^2 after K1 + the exchange's corrections (norm.cuh)
   // host-side step state
   int64_t steps = 0;      // completed aggregations
   int64_t t_cur = -1;     // iteration of the pending/last compress
@@ -187,12 +171,10 @@ struct micro_ctx {
   bool fuse_step = false;   // set for the duration of micro_step
   bool fin_done = false;    // this step's finalize already ran inside k1_gather
   // optional in-library kernel timing of K1's streaming pass (micro_kernel_times)
-  bool pdl = true;          // programmatic dependent launch between the step's kernels (MICRO_PDL=0: off)
   // micro_step_host (n = 1): the gradient arrives in kH2DChunks pieces on
   // h2d_stream; K1 streams each piece's CTAs as soon as it has landed
   static constexpr int kH2DChunks = 8;
   int h2d_chunks = 0;        // > 1 only while micro_step_host runs
-  bool h2d_pipeline = true;  // MICRO_H2D_PIPELINE=0: one copy, then the step
   cudaStream_t h2d_stream = nullptr;
   cudaEvent_t h2d_ev[kH2DChunks] = {};
   cudaEvent_t h2d_free = nullptr;  // the previous step is done with the staging buffer
@@ -212,10 +194,8 @@ struct micro_ctx {
   unsigned* topk_hist = nullptr;
   unsigned* tie_counts = nullptr;
   unsigned* bitmap = nullptr;   // union of overlapping selections
-  int* word_pc = nullptr;
   int* word_off = nullptr;
-  void* cub_tmp = nullptr;
-  size_t cub_bytes = 0;
+  int* scan_tmp = nullptr;      // block totals of the hand-written scan (scan.cuh)
   int64_t nwords = 0;
   double* minus_one = nullptr;  // threshold that selects everything (k >= n_g)
   // peer-memory exchange (micro_peer_*): every rank's buffers mapped here
@@ -224,7 +204,7 @@ struct micro_ctx {
   void* peer_resid[micro::kMaxWorkers] = {};
   int32_t* peer_uidx[2][micro::kMaxWorkers] = {};
   void* peer_usum[2][micro::kMaxWorkers] = {};
-  double* peer_corr[micro::kMaxWorkers] = {};
+  micro::NormSlot* peer_corr[micro::kMaxWorkers] = {};
   const int32_t* peer_sel[2][micro::kMaxWorkers] = {};
   void* peer_recv[micro::kMaxWorkers] = {};
   void* recv = nullptr;          // bulk exchange: receive slabs [source rank][sel_cap] (lazy)
@@ -251,6 +231,9 @@ int check_ctx(micro_ctx* c);
 int check_poison(micro_ctx* c);
 int ensure_staging(micro_ctx* c);
 int read_flags(micro_ctx* c, int* flags);
+// word offsets of a union bitmap: off[w] = popcount of words [0, w) (scan.cuh);
+// `tiles` holds scan_tiles(nwords) ints of scratch
+int bitmap_offsets(const unsigned* bitmap, int64_t nwords, int* off, int* tiles, cudaStream_t st);
 // threshold update, history, dense g/n and model after the union is formed
 // (instantiated for float and double in api.cu)
 template <typename T>

@@ -31,34 +31,49 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
   return v;
 }
 
-// Exchange-side corrections (squares of the foreign entries a worker's
-// residual loses in the exchange) come from many CTAs, and over peer memory
-// from several GPUs, in no fixed order.  fp64 atomicAdd would make the
-// recorded norm depend on CTA timing (acceptance C11: identical runs give
-// identical records), so each CTA's (deterministic) non-negative partial is
-// rounded once to 64.64 fixed point and added with integer atomics, which
-// are exact and order-independent.  A slot is two u64 words {frac, int}
-// (16 bytes); a non-finite partial saturates the slot to +inf.
-__device__ __forceinline__ void fx_add(double* slot, double v) {
-  unsigned long long* a = reinterpret_cast<unsigned long long*>(slot);
-  if (!(v < 1.8e19)) {  // non-finite or out of range
-    atomicExch(a + 1, ~0ull);
+// Per-worker error-norm slot.  K1 leaves ||e_{t+1}||^2 (own selections
+// zeroed) in `sq`; the exchange then zeroes the foreign union entries of the
+// residual and subtracts their squares, which arrive from many CTAs — over
+// peer memory from several GPUs — in no fixed order.  fp64 atomics would make
+// the record depend on CTA timing (acceptance C11: identical runs, identical
+// records), so each CTA's (deterministic) partial is added exactly and
+// order-independently as a 128-bit fixed-point integer.  The fixed point is
+// scaled by the power of two just above `sq` (every correction is a part of
+// sq), so its resolution is relative to the norm — 2^-128 of it — whatever
+// the residuals' magnitude, and the sum cannot overflow.  A partial outside
+// that range (non-finite, or larger than sq) sets a sticky flag and the record
+// reads NaN.  Slots that other GPUs update use system-scope atomics.
+struct NormSlot {
+  unsigned long long lo, hi;  // sum of corrections * 2^(64 - E) as hi + lo * 2^-64, E = ilogb(sq) + 2
+  double sq;                  // ||e||^2 after K1
+  unsigned long long bad;     // sticky
+};
+
+__device__ __forceinline__ void fx_add(NormSlot* s, double v) {
+  if (v == 0.0) return;
+  const double sq = *reinterpret_cast<volatile double*>(&s->sq);
+  const double x = (sq > 0.0 && sq < INFINITY) ? ldexp(v, 64 - (ilogb(sq) + 2)) : -1.0;
+  if (!(x >= 0.0 && x < 1.8e19)) {  // also NaN / inf partials
+    atomicOr_system(&s->bad, 1ull);
     return;
   }
-  const double h = floor(v);
-  const unsigned long long lo = __double2ull_rz((v - h) * 18446744073709551616.0);
-  const unsigned long long old = atomicAdd(a, lo);
-  atomicAdd(a + 1, (unsigned long long)h + (old + lo < old ? 1ull : 0ull));
+  const double h = floor(x);
+  const unsigned long long hi = (unsigned long long)h;
+  const unsigned long long lo = __double2ull_rz((x - h) * 18446744073709551616.0);
+  const unsigned long long old = atomicAdd_system(&s->lo, lo);
+  atomicAdd_system(&s->hi, hi + (old + lo < old ? 1ull : 0ull));
 }
 
-// Reads a slot and clears it for the next step (single reader).
-__device__ __forceinline__ double fx_take(double* slot) {
-  unsigned long long* a = reinterpret_cast<unsigned long long*>(slot);
-  const unsigned long long lo = a[0], hi = a[1];
-  a[0] = 0ull;
-  a[1] = 0ull;
-  if (hi == ~0ull) return __longlong_as_double(0x7ff0000000000000ll);
-  return (double)hi + (double)lo * 0x1p-64;
+// The corrections' sum; clears it for the next step (single reader, after
+// every contributor is done).
+__device__ __forceinline__ double fx_take(NormSlot* s) {
+  const unsigned long long lo = s->lo, hi = s->hi, bad = s->bad;
+  s->lo = 0ull;
+  s->hi = 0ull;
+  s->bad = 0ull;
+  if (bad) return __longlong_as_double(0x7ff8000000000000ll);
+  if (!(s->sq > 0.0)) return 0.0;
+  return ldexp((double)hi + (double)lo * 0x1p-64, (ilogb(s->sq) + 2) - 64);
 }
 
 // Called by every thread of the CTA (contains a __syncthreads) at the end of

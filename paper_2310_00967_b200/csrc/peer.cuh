@@ -30,7 +30,7 @@ struct PeerPtrs {
   void* resid[kMaxWorkers];
   int32_t* uidx[kMaxWorkers];            // union buffers of this step's parity
   void* usum[kMaxWorkers];
-  double* corr[kMaxWorkers];             // error-norm corrections (NULL: not recorded)
+  NormSlot* corr[kMaxWorkers];           // error-norm slots (NULL: not recorded)
 };
 
 __device__ __forceinline__ long long ld_volatile_i64(const long long* p) {
@@ -136,7 +136,7 @@ struct PeerBulkPtrs {
 
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me, long long cap, T* __restrict__ resid,
-                                                         double* corr) {
+                                                         NormSlot* corr) {
   const int o = blockIdx.y;
   if (o == me) return;  // block-uniform
   __shared__ double s_q[8];

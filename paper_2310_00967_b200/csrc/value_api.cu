@@ -50,6 +50,32 @@ __global__ void k_reduce_values(WorkerPtrs w, int n, int64_t n_g, const int32_t*
   }
 }
 
+// min / max of a concatenated index list (the bitmap's extent)
+__global__ void k_index_extent(const int32_t* idx, int64_t n, int* mm) {
+  int lo = INT32_MAX, hi = -1;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
+    const int j = idx[m];
+    lo = min(lo, j);
+    hi = max(hi, j);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
+  }
+}
+
+__global__ void k_mark_indices(const int32_t* idx, int64_t n, unsigned* bitmap) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = idx[m];
+    atomicOr(&bitmap[j >> 5], 1u << (j & 31));
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -335,28 +361,42 @@ int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_co
   *K = 0;
   if (!total) return MICRO_OK;
   if (total >= (int64_t)INT32_MAX) return fail(MICRO_EINVAL, "too many indices");
+  // sort + unique (collectives.cpp:25-26) as a bitmap over the index extent:
+  // mark, popcount prefix (scan.cuh), emit in index order — the same sorted
+  // unique union for any input order, duplicates included
   cudaStream_t s = (cudaStream_t)stream;
-  const int items = (int)total;
-  int32_t* sorted = nullptr;
-  int* d_num = nullptr;
-  void* tmp = nullptr;
-  size_t b1 = 0, b2 = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, b1, d_concat, (int32_t*)nullptr, items, 0, 32, s);
-  cub::DeviceSelect::Unique(nullptr, b2, (const int32_t*)nullptr, (int32_t*)nullptr, (int*)nullptr, items, s);
-  const size_t tb = std::max(b1, b2);
-  CU(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * items, s));
-  CU(cudaMallocAsync((void**)&d_num, sizeof(int), s));
-  CU(cudaMallocAsync(&tmp, tb, s));
-  size_t tb1 = tb, tb2 = tb;
-  CU(cub::DeviceRadixSort::SortKeys(tmp, tb1, d_concat, sorted, items, 0, 32, s));
-  CU(cub::DeviceSelect::Unique(tmp, tb2, (const int32_t*)sorted, d_union, d_num, items, s));
-  int hn = 0;
-  CU(cudaMemcpyAsync(&hn, d_num, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CU(cudaFreeAsync(sorted, s));
-  CU(cudaFreeAsync(d_num, s));
-  CU(cudaFreeAsync(tmp, s));
+  const int dev = current_device();
+  int* mm = nullptr;
+  CU(cudaMallocAsync((void**)&mm, 2 * sizeof(int), s));
+  const int init[2] = {INT32_MAX, -1};
+  CU(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
+  k_index_extent<<<grid_for(total, dev), 256, 0, s>>>(d_concat, total, mm);
+  CU(cudaGetLastError());
+  int hmm[2] = {0, 0};
+  CU(cudaMemcpyAsync(hmm, mm, sizeof hmm, cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(mm, s));
   CU(cudaStreamSynchronize(s));
-  *K = hn;
+  if (hmm[0] < 0) return fail(MICRO_EINVAL, "all_gather_indices: negative index %d", hmm[0]);
+  const int64_t nwords = (int64_t)hmm[1] / 32 + 1;
+  const int64_t nt = scan_tiles(nwords);
+  char* ws = nullptr;
+  const size_t bm = sizeof(unsigned) * nwords, ob = sizeof(int) * nwords, tb = sizeof(int) * nt;
+  CU(cudaMallocAsync((void**)&ws, bm + ob + tb + 16, s));
+  unsigned* bitmap = (unsigned*)ws;
+  int* off = (int*)(ws + bm);
+  int* tiles = (int*)(ws + bm + ob);
+  long long* dK = (long long*)(ws + ((bm + ob + tb + 7) / 8 * 8));
+  CU(cudaMemsetAsync(bitmap, 0, bm, s));
+  k_mark_indices<<<grid_for(total, dev), 256, 0, s>>>(d_concat, total, bitmap);
+  CU(cudaGetLastError());
+  TRY(bitmap_offsets(bitmap, nwords, off, tiles, s));
+  k_bitmap_emit<<<grid_for(nwords, dev), 256, 0, s>>>(bitmap, nwords, off, d_union, dK);
+  CU(cudaGetLastError());
+  long long hk = 0;
+  CU(cudaMemcpyAsync(&hk, dK, sizeof hk, cudaMemcpyDeviceToHost, s));
+  CU(cudaFreeAsync(ws, s));
+  CU(cudaStreamSynchronize(s));
+  *K = hk;
   return MICRO_OK;
 }
 

@@ -225,6 +225,33 @@ int main() {
       CHECK(std::fabs(recs[s].error_norm - want_norm[s]) <= 1e-12 * want_norm[s]);
     }
   }
+  // non-finite gradient (harness.cpp:128-130): MicroEngine::step throws
+  // std::runtime_error, keeps refusing until reset(), then steps again
+  {
+    const Index n_g = 4099;
+    const int n = 2;
+    SparsifierConfig sc;
+    MicroEngine eng(n_g, n, sc);
+    std::vector<double> G((std::size_t)(n * n_g), 0.5);
+    eng.step(G.data(), 0.01, 0);
+    G[(std::size_t)n_g + 7] = std::nan("");
+    CHECK_THROWS_AS(eng.step(G.data(), 0.01, 1), std::runtime_error);
+    G[(std::size_t)n_g + 7] = 0.5;
+    CHECK_THROWS_AS(eng.step(G.data(), 0.01, 2), std::runtime_error);  // poisoned until reset
+    eng.reset();
+    const auto agg = eng.step(G.data(), 0.01, 0);
+    CHECK(agg.per_worker_counts.size() == 2);
+    G[3] = INFINITY;
+    CHECK_THROWS_AS(eng.step(G.data(), 0.01, 1), std::runtime_error);
+    bool is_logic = false;  // runtime_error, not invalid_argument / logic_error
+    try {
+      eng.step(G.data(), 0.01, 2);
+    } catch (const std::logic_error&) {
+      is_logic = true;
+    } catch (const std::runtime_error&) {
+    }
+    CHECK(!is_logic);
+  }
   // MicroGroup (one process, one context per rank; here all on device 0)
   // == MicroEngine (single-device cluster), bit for bit
   {

@@ -36,7 +36,7 @@ def gen(o, n, n_g, t, dtype):
 
 
 def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, oracle="restatement",
-             check_every=1, split=False):
+             check_every=1, split=False, unaligned=False):
     o = Oracle()
     tdt = torch.float32 if dtype == np.float32 else torch.float64
     m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, target="full" if full else "split",
@@ -57,12 +57,17 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         e_now = ref.residuals() if oracle == "reference" else ref.e
         acc = e_now.astype(dtype) + dtype(ETA) * G
         energy = float(np.sqrt((acc.astype(np.float64) ** 2).sum(axis=1)).max())
-        Gd = torch.from_numpy(G).cuda()
+        Gd = list(torch.from_numpy(G).cuda())
+        if unaligned:  # gradients off the 16-byte grid: the library realigns them (staging copy)
+            buf = torch.empty((n, n_g + 1), dtype=tdt, device="cuda")
+            buf[:, 1:] = torch.stack(Gd)
+            Gd = [buf[i, 1:] for i in range(n)]
+            assert Gd[0].data_ptr() % 16
         if split:  # micro_compress + micro_aggregate (k_finalize launched separately)
-            m.compress(list(Gd), ETA, t)
+            m.compress(Gd, ETA, t)
             m.aggregate()
         else:      # micro_step (n = 1: threshold update folded into k1_gather)
-            m.step(list(Gd), ETA, t)
+            m.step(Gd, ETA, t)
         r = ref.step(G, ETA, t)
         E = ref.residuals() if oracle == "reference" else ref.e
         norms = np.sqrt((E.astype(np.float64) ** 2).sum(axis=1))
@@ -102,13 +107,11 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     m.close()
 
 
-@pytest.fixture(params=["stream", "tma", "tile"])
-def k1_kernel(request, monkeypatch):
-    """K1 implementation: streaming pass + ordered compaction (default), the
-    persistent TMA kernel, or the per-tile look-back kernel (fallback for
-    unaligned gradients)."""
-    monkeypatch.setenv("MICRO_K1_KERNEL", request.param)
-    return request.param
+@pytest.fixture(params=["aligned", "unaligned"])
+def k1_kernel(request):
+    """Gradient placement: 16-byte aligned (K1 streams it directly) or not
+    (the library realigns it into its staging buffer first)."""
+    return request.param == "unaligned"
 
 
 @pytest.mark.parametrize("n_g,n,d,delta0", [
@@ -123,13 +126,13 @@ def k1_kernel(request, monkeypatch):
     (123_457, 7, 0.001, 0.03),
 ])
 def test_gpu_f32_matches_restatement(n_g, n, d, delta0, k1_kernel):
-    run_pair(n_g, n, d, delta0, iters=25)
+    run_pair(n_g, n, d, delta0, iters=25, unaligned=k1_kernel)
 
 
 @pytest.mark.parametrize("full,ef", [(True, True), (False, False), (True, False)])
 def test_gpu_f32_modes(full, ef, k1_kernel):
-    run_pair(20_000, 4, 0.01, 0.01, iters=15, full=full, ef=ef)
-    run_pair(20_000, 1, 0.01, 0.01, iters=15, full=full, ef=ef)
+    run_pair(20_000, 4, 0.01, 0.01, iters=15, full=full, ef=ef, unaligned=k1_kernel)
+    run_pair(20_000, 1, 0.01, 0.01, iters=15, full=full, ef=ef, unaligned=k1_kernel)
 
 
 @pytest.mark.parametrize("n_g,n", [(10_000, 1), (65_537, 1), (10_007, 2)])
@@ -154,7 +157,7 @@ def test_gpu_density_one_threshold_zero():
 @pytest.mark.parametrize("n_g,n,d,delta0", [(10_000, 1, 0.01, 0.01), (10_007, 2, 0.01, 0.02),
                                              (12_345, 8, 0.02, 0.01), (3_001, 3, 0.1, 0.05)])
 def test_gpu_f64_matches_reference_code(n_g, n, d, delta0, k1_kernel):
-    run_pair(n_g, n, d, delta0, iters=20, dtype=np.float64, oracle="reference")
+    run_pair(n_g, n, d, delta0, iters=20, dtype=np.float64, oracle="reference", unaligned=k1_kernel)
 
 
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "micro_ref64_*.npz")))
@@ -255,8 +258,7 @@ def test_step_host_end_to_end():
 
 
 def test_full_size_properties_138M():
-    """BASELINE C3 size at n = 1 (and one n = 8 step): size-independent
-    properties — ordered unique indices inside the partition, |acc| > delta,
+    """BASELINE C3 size at n = 1: size-independent properties — ordered unique indices inside the partition, |acc| > delta,
     conservation e_{t+1} + sent == e_t + eta*G elementwise, count == the
     torch-computed count, dense == sums at the union."""
     n_g = 138_000_000
