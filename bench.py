@@ -113,25 +113,94 @@ def traffic_from_profiles(workload: str):
 # ---------------------------------------------------------------- reference
 
 
-def run_reference_cluster(n_g: int, n: int, d: float, steps: int, warmup: int, seed: int = SEED):
-    """The reference's own hot-path code (oracle/_ref) driven in run_iteration
-    order: fp64, one host thread, all n workers serially.  Returns per-step
-    seconds."""
+def host_info(threads: int) -> dict:
+    """The host the CPU numbers were taken on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": len(os.sched_getaffinity(0)), "cpu_model": model, "threads_used": threads}
+
+
+def _fresh_normal(rng_pool, out: np.ndarray):
+    """Fill `out` (float64) with fresh N(0,1) draws, one numpy Generator per
+    host thread (they release the GIL), outside any timed region."""
+    from concurrent.futures import ThreadPoolExecutor
+    flat = out.reshape(-1)
+    k = len(rng_pool)
+    step = (flat.size + k - 1) // k
+    with ThreadPoolExecutor(k) as ex:
+        list(ex.map(lambda i: rng_pool[i].standard_normal(out=flat[i * step:(i + 1) * step]), range(k)))
+
+
+def run_reference_converged(n_g: int, n: int, d: float, steps: int, warmup: int, adapt_iters: int = 1000,
+                            adapt_n: int = 1 << 20, dense: bool = True, model: bool = True, threads: int = 1,
+                            seed: int = SEED):
+    """The reference's own hot-path code (oracle/_ref: its sparsifier and
+    collectives TUs compiled verbatim, re-driven in run_iteration's order),
+    fp64, timed in the STATIONARY regime:
+
+      1. adapt_iters iterations from the warm delta_0 at a sampled
+         n_s = min(n_g, adapt_n) with fresh N(0,1) gradients (the threshold and
+         residual reach their stationary law; both are scale-free in n_g);
+      2. the converged state is transplanted into a full-size cluster: each
+         worker's threshold, and its residual tiled to n_g (the coordinates
+         are i.i.d. at stationarity, so the tiled residual has the stationary
+         marginal law);
+      3. `warmup` + `steps` iterations at the full n_g, a fresh gradient per
+         step generated outside the timed region; each step is timed alone.
+
+    Returns per-step seconds, the realised density of each timed step, the
+    first timed iteration and a description."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle import RefCluster
 
-    rng = np.random.default_rng(seed)
-    ref = RefCluster(n_g, n, density=d, delta0=warm_delta0(d), alpha=ALPHA)
-    G = [rng.standard_normal((n, n_g)) for _ in range(2)]
-    times = []
+    pool = [np.random.default_rng([seed, 7, i]) for i in range(max(1, min(16, len(os.sched_getaffinity(0)))))]
+    delta0 = warm_delta0(d)
+    n_s = min(n_g, max(adapt_n, n))
+    small = RefCluster(n_s, n, density=d, delta0=delta0, alpha=ALPHA)
+    small.set_options(dense=False, threads=threads)
+    Gs = np.empty((n, n_s))
+    for t in range(adapt_iters):
+        _fresh_normal(pool, Gs)
+        small.step(Gs, ETA, t)
+    res = [small.residual(i) for i in range(n)]
+    thr = np.empty(n)
+    small.r.lib.ref_cluster_thresholds(small.h, thr)
+    del small, Gs
+    ref = RefCluster(n_g, n, density=d, delta0=delta0, alpha=ALPHA, model=model)
+    ref.set_options(dense=dense, threads=threads)
+    if n_s != n_g:
+        for i in range(n):
+            ref.set_state(i, np.resize(res[i], n_g), thr[i])
+    else:
+        for i in range(n):
+            ref.set_state(i, res[i], thr[i])
+    del res
+    G = np.empty((n, n_g))
+    times, dens = [], []
+    t = adapt_iters
     for s in range(warmup + steps):
+        _fresh_normal(pool, G)
         t0 = time.perf_counter()
-        ref.step(G[s % 2], ETA, s)
+        r = ref.step(G, ETA, t)
         dt = time.perf_counter() - t0
+        t += 1
         if s >= warmup:
             times.append(dt)
-    del ref, G
-    return times
+            dens.append(r["union_idx"].size / n_g)
+    sample = (f"{steps} timed iterations (after {warmup} warm-up) at the full n_g={n_g}, n={n} workers "
+              f"({'serially on 1 thread' if threads == 1 else f'per-worker loops on {threads} threads'}), fp64, "
+              f"the reference's sparsifier/collectives TUs compiled verbatim (oracle/_ref) driven in "
+              f"run_iteration order with the model update{' and the dense all_reduce_sparse / n' if dense else ''}; "
+              f"stationary start: {adapt_iters} adaptation iterations at n_s={n_s} (fresh N(0,1) gradients), "
+              f"state transplanted (threshold; residual tiled to n_g); a fresh gradient per step")
+    return dict(times=times, density=dens, first_timed_t=adapt_iters + warmup, sample=sample)
 
 
 def reference_arm(args, wl):
@@ -139,22 +208,24 @@ def reference_arm(args, wl):
     if rank != 0:
         return 0
     n = args.gpus
-    n_g = wl["n_g"]
-    # bounded sample: keep (warmup + steps) * n * n_g * ~8 ns under ~150 s
-    frac = min(1.0, 150.0 / max(1e-9, (args.warmup + args.steps) * n * n_g * 8e-9))
-    n_s = max(n * 1024, int(n_g * frac))
-    times = run_reference_cluster(n_s, n, wl["d"], args.steps, args.warmup)
-    per = statistics.mean(times) * (n_g / n_s)
+    threads = max(1, min(n, len(os.sched_getaffinity(0))))
+    r = run_reference_converged(wl["n_g"], n, wl["d"], args.steps, args.warmup, adapt_iters=args.prime,
+                                dense=args.dense, model=args.model, threads=threads, seed=args.seed)
+    per = statistics.mean(r["times"])
     us = per * 1e6
-    sample = (f"{args.steps} timed iterations (after {args.warmup} warm-up) of the reference's MiCRO iteration "
-              f"(sparsifier/collectives TUs compiled verbatim, fp64, n={n} workers serially on 1 thread) at "
-              f"n_g={n_s}" + (f", scaled x{n_g / n_s:.2f} to n_g={n_g}" if n_s != n_g else ""))
+    dens = float(np.mean(r["density"]))
     line = {"metric": METRIC, "value": us, "unit": "us/iter", "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic N(0,1) gradients",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic N(0,1) gradients (numpy, fresh per step)",
             "impl": "reference",
-            "config": {"workload": wl["desc"], "n_g": n_g, "density": wl["d"], "workers": n},
-            "cpu_baseline": {"value": us, "unit": "us/iter", "cores": 1, "kind": "reference", "sample": sample},
+            "config": bench_config(args, wl, n),
+            "protocol": {"adaptation_iterations": args.prime, "first_timed_t": r["first_timed_t"],
+                         "median_us_per_step": float(np.median(r["times"])) * 1e6},
+            "density": dens, "density_rel_err": dens / wl["d"] - 1.0,
+            "host": host_info(threads),
+            "cpu_baseline": {"value": us, "unit": "us/iter", "cores": threads, "kind": "reference",
+                             "sample": r["sample"]},
             "e2e": {"value": us, "unit": "us/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -163,37 +234,53 @@ def reference_arm(args, wl):
 # ---------------------------------------------------------------- our arm
 
 
-def our_arm(args, wl):
+def bench_config(args, wl, world: int) -> dict:
+    """The workload both arms run (identical dicts: the ratio is like for like)."""
+    W = args.cluster_workers if (world == 1 and args.cluster_workers > 1) else 1
+    n = world * W
+    label = wl["desc"]
+    if args.workload == "c3" and n == 1:
+        label = "C3 per-GPU slice (n=1): " + wl["desc"] + " — configs[2] runs n=8, one worker per GPU"
+    return {"workload": label, "n_g": wl["n_g"], "density_target": wl["d"], "workers": n,
+            "one_worker_per_gpu": W == 1, "eta": ETA, "alpha": ALPHA, "delta0": warm_delta0(wl["d"]),
+            "error_feedback": True, "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
+            "error_norm_recorded": bool(args.error_norm), "sparsifier": args.sparsifier,
+            "arithmetic": "f64 (the reference's own, bit-exact with its code)" if args.dtype == "f64"
+            else "f32 (the north star's gradient type)",
+            "parallelism": (f"dp{world} (exclusive cyclic partitions"
+                            + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
+                            f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)"),
+            "timing": "stationary regime: threshold and residual adapted before the timed steps; "
+                      "a fresh N(0,1) gradient per step"}
+
+
+def traffic_from_profiles(key: str):
+    """DRAM bytes per launch of the dominant kernel from the ncu --set full
+    capture of the same command (profiles/k1_dram_bytes.json)."""
+    p = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        v = j.get(key)
+        if isinstance(v, dict):
+            return v.get("bytes"), v.get("source")
+        return v, "profiles/k1_dram_bytes.json"
+    return None, None
+
+
+def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
+    """Adapt, warm up and time K steps of the device path at dtype tdt.
+    Returns the measurement dict (and the engine + buffers when keep)."""
     import torch
 
     from paper_2310_00967_b200 import engine
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if args.dist_backend == "gloo":  # code-path check of N > 1 on one GPU: ranks share it, numbers are not valid
-        local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     n_g, d = wl["n_g"], wl["d"]
     delta0 = warm_delta0(d)
-    tdt = torch.float64 if args.dtype == "f64" else torch.float32
-    esz = 8 if args.dtype == "f64" else 4
-    # W workers per process: 1 (one per GPU), or --cluster-workers W at N = 1:
-    # the reference's own in-process cluster (harness.cpp:121-224) on one GPU
+    esz = 8 if tdt == torch.float64 else 4
     W = args.cluster_workers if (world == 1 and args.cluster_workers > 1) else 1
-    dist = None
-    if world > 1:
-        import torch.distributed as tdist
-
+    if dist is not None:
         from paper_2310_00967_b200.dist import DistMicro
-        if args.dist_backend == "gloo":
-            tdist.init_process_group("gloo")
-        else:
-            tdist.init_process_group("nccl", device_id=dev)
-        dist = tdist
         m = DistMicro(n_g, transport=args.transport, density=d, initial_threshold=delta0, scaling_factor=ALPHA,
                       dense_output=args.dense, record_error_norm=args.error_norm, dtype=tdt,
                       comm_device="cpu" if args.dist_backend == "gloo" else None)
@@ -202,8 +289,7 @@ def our_arm(args, wl):
                          record_error_norm=args.error_norm, sparsifier=args.sparsifier, dtype=tdt)
     stream = torch.cuda.current_stream(dev)
     # the model update x -= g/n at the union is part of the reference's
-    # iteration (harness.cpp:212-215); a dense g/n is not (run_iteration uses
-    # the sparse sums), so it is materialised only with --dense
+    # iteration (harness.cpp:212-215)
     model = torch.zeros(n_g, device=dev, dtype=tdt)
     if args.model:
         m.set_model(model)
@@ -211,9 +297,9 @@ def our_arm(args, wl):
     # The threshold adapts for `prime` untimed iterations on fresh N(0,1)
     # gradients (generated between steps), reaching the stationary regime the
     # density target refers to.  The warm-up and timed steps
-    # then read gradients that are already resident in HBM: one fresh buffer
-    # per step when memory allows (same statistics as the prime phase),
-    # otherwise R buffers rotated.
+    # then read gradients already resident in HBM: one fresh buffer per step
+    # when memory allows (same statistics as the prime phase), otherwise R
+    # buffers rotated.
     t = 0
     gen = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(W)]
     for _ in range(args.prime):
@@ -224,7 +310,7 @@ def our_arm(args, wl):
     del gen
     torch.cuda.synchronize()
     need = (args.warmup + args.steps) * W
-    R = max(W + 1, min(need, args.buffers, int(0.6 * torch.cuda.mem_get_info(dev)[0] // (esz * n_g))))
+    R = max(W + 1, min(need, args.buffers, int(0.5 * torch.cuda.mem_get_info(dev)[0] // (esz * n_g))))
     G = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(R)]
     for r in range(R):
         engine.synth_gaussian(G[r], args.seed, rank + r % W, t + r)
@@ -245,16 +331,18 @@ def our_arm(args, wl):
     torch.cuda.synchronize()
     t_first = t
     # CUDA events around K1's streaming pass, inside the library, on every
-    # 4th step of the timed region (an event pair between kernels costs the
-    # step ~5 µs at c1 size; sampled, the step time stays the step's)
+    # 4th step of the timed region (sampled, so the step time stays the step's)
     m.kernel_timing(True, every=4)
     if dist:
         m.exchange_timing(True)
     # the step's working set (e, G, x) fits in L2 at the small workloads:
-    # there, flush L2 between timed steps (a 256 MB write, outside the per-step
-    # event windows); at C3 and up the inputs are larger than L2
+    # there, flush L2 between timed steps, outside the per-step event windows:
+    # a 256 MB write (evicts the step's lines) then a 256 MB read (so the
+    # flush's own dirty lines are written back inside the flush, not charged
+    # to the next step).  At C3 and up the inputs are larger than L2.
     flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and 3 * esz * n_g < 2 * 126e6)
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    scratch2 = torch.empty(64 << 20, dtype=torch.float32, device=dev) if flush else None
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)] if flush else []
     with ClockSampler(local) as clk:
@@ -262,6 +350,7 @@ def our_arm(args, wl):
         for s in range(args.steps):
             if flush:
                 scratch.fill_(s & 0xFF)
+                scratch2.sum()
                 step_ev[s][0].record(stream)
             m.step(grads(t), ETA, t)  # the whole iteration, one library call
             if flush:
@@ -276,58 +365,114 @@ def our_arm(args, wl):
     k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone (sampled launches)
     m.kernel_timing(False)
     xchg_ms = None
+    cdev = dev if args.dist_backend == "nccl" else "cpu"
     if dist:
         xt = m.exchange_times()
         m.exchange_timing(False)
-        v = torch.tensor([statistics.mean(xt) if xt else 0.0],
-                         device=dev if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
+        v = torch.tensor([statistics.mean(xt) if xt else 0.0], device=cdev, dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         xchg_ms = float(v[0])
-    if dist:
-        v = torch.tensor([total_ms], device=dev if args.dist_backend == "nccl" else "cpu", dtype=torch.float64)
+        v = torch.tensor([total_ms], device=cdev, dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         total_ms = float(v[0])
     ms_step = total_ms / args.steps
     hist = m.history(args.steps)
     K = hist["K"].astype(np.float64)
     k_own = hist["counts"][:, 0].astype(np.float64)
-    density = float(K.mean() / n_g)
-    # (dense has no selection pass: the whole step stands in for the kernel)
-    k1a_avg_ms = statistics.mean(k1a_ms) if k1a_ms else ms_step
-    # algorithmic bytes of the dominant kernel, k1_stream: read e and G, write
-    # e (all n_g) + one (int32, value) pair per selection
-    # (top-k's compaction pass reads acc only, 1 element read per entry: the
-    # histogram passes already wrote acc into e; CLT-k's leader is top-k, its
-    # other workers select by threshold — the timed launches average over both)
+    out = dict(ms_step=ms_step, step_ms=step_ms, k1a_ms=k1a_ms, xchg_ms=xchg_ms, K=K, k_own=k_own, R=R,
+               flush=flush, t_first=t_first, t_next=t, W=W, esz=esz, clocks=clk.summary(),
+               transport=getattr(m, "transport", None))
+    if keep:
+        out.update(m=m, G=G)
+    else:
+        m.close()
+        del G
+        torch.cuda.empty_cache()
+    return out
+
+
+def roofline_of(args, r, wl, world, peak, peak_kind):
+    """Algorithmic bytes of the dominant kernel (k1_stream) and of the step."""
+    n_g, W, esz = wl["n_g"], r["W"], r["esz"]
+    K, k_own = r["K"], r["k_own"]
+    # k1_stream: read e and G, write e (all n_g, SURVEY.md P4) + one (int32,
+    # value) pair per selection; with the dense g/n (fused at n = 1) the
+    # current union's values and the previous union's zeros (2 values per
+    # entry).  top-k's compaction reads acc only (the histogram passes formed
+    # it); CLT-k's leader is top-k, its other workers select by threshold.
     acc_only = {"topk": W, "cltk": 1}.get(args.sparsifier, 0)
-    k1_bytes = (esz * n_g * (acc_only + 3.0 * (W - acc_only)) / W) + (4.0 + esz) * float(k_own.mean())
+    dense_fused = args.dense and world == 1 and W == 1 and args.sparsifier == "micro"
+    k1_bytes = ((esz * n_g * (acc_only + 3.0 * (W - acc_only)) / W) + (4.0 + esz) * float(k_own.mean())
+                + (2.0 * esz * float(K.mean()) if dense_fused else 0.0))
+    k1a_avg_ms = statistics.mean(r["k1a_ms"]) if r["k1a_ms"] else r["ms_step"]
     achieved = k1_bytes / (k1a_avg_ms * 1e-3) / 1e9
+    # whole step vs the same roofline: K1 + the union (8 B at n = 1: written by
+    # the gather) + the model's read-modify-write (2 values per union entry) +
+    # the dense g/n when not fused + the cluster reduce (W reads + zeroing)
+    step_bytes = (W * k1_bytes + (4.0 + esz) * float(K.mean())
+                  + (2.0 * esz * float(K.mean()) if args.model else 0.0)
+                  + (2.0 * esz * float(K.mean()) if (args.dense and not dense_fused) else 0.0)
+                  + (2.0 * esz * float(K.mean()) * W if W > 1 else 0.0))
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "kernel": "k1_stream", "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1a_avg_ms,
+            "peak_source": peak_kind,
+            "timed_launches": f"{len(r['k1a_ms'])} of {args.steps} (every 4th, CUDA events on the launch stream)",
+            "step_frac": step_bytes / (r["ms_step"] * 1e-3) / 1e9 / peak}
+
+
+def our_arm(args, wl):
+    import torch
+
+    from paper_2310_00967_b200 import engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dist_backend == "gloo":  # code-path check of N > 1 on one GPU: ranks share it, numbers are not valid
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n_g, d = wl["n_g"], wl["d"]
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        if args.dist_backend == "gloo":
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
+        dist = tdist
+    r = device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=True)
+    m, G, W, esz = r["m"], r["G"], r["W"], r["esz"]
+    t = r["t_next"]
+    ms_step, K, k_own = r["ms_step"], r["K"], r["k_own"]
+    density = float(K.mean() / n_g)
     peak, peak_kind = peaks()
-    # whole step vs the same roofline: K1 bytes + union (8 B) and, with the
-    # model update, x read+write (8 B) per union entry
-    step_bytes = (W * k1_bytes + (4.0 + esz) * float(K.mean()) + (2.0 * esz * float(K.mean()) if args.model else 0.0)
-                  + (2.0 * esz * float(K.mean()) * W if W > 1 else 0.0))  # cluster reduce: W reads + zeroing
+    roof = roofline_of(args, r, wl, world, peak, peak_kind)
+    tkey = f"{args.workload}_{args.dtype}{'_dense' if args.dense else ''}"
+    roof["traffic"], roof["traffic_source"] = traffic_from_profiles(tkey)
     # our kernels per step: k1_stream, k1_gather (+ threshold update + model
-    # update) at n = 1; a W-worker cluster: 2 per worker + k_cluster_reduce +
-    # k_finalize; n > 1 ranks: K1 x2, gather_foreign, owner_reduce,
-    # build_union, finalize (NCCL kernels not counted)
-    launches_per_step = ((2 if W == 1 else 2 * W + 2) if world == 1
-                         else {"peer": 5, "peer_pull": 4, "nccl": 6}[m.transport])  # K1 x2 + exchange + finalize
+    # update + dense g/n) at n = 1; a W-worker cluster: 2 per worker +
+    # k_cluster_reduce + k_finalize (+ k_dense_clear); n > 1 ranks: K1 x2 +
+    # the exchange + finalize (NCCL kernels not counted)
+    launches_per_step = ((2 if W == 1 else 2 * W + 2 + (1 if args.dense else 0)) if world == 1
+                         else {"peer": 5, "peer_pull": 4, "nccl": 6}[r["transport"]])
     if args.sparsifier != "micro":  # baselines.cuh: per selecting worker, top-k = init + 2 per digit +
         # tie count/find + stream + gather (fp32: 11), hard = 2, else accumulate + count = 2; then
-        # union marks (W) + popcount + scan (2) + emit + reduce + finalize (dense: iota + reduce + finalize)
+        # union marks (W) + 3 scan passes + emit + reduce + finalize (dense: dense_all + finalize)
         per = {"topk": 11 * W, "cltk": 11 + 2 * (W - 1), "hard": 2 * W, "dense": 2 * W}[args.sparsifier]
-        launches_per_step = per + (3 if args.sparsifier == "dense" else W + 6)
-    clocks = clk.summary()
+        launches_per_step = per + (2 if args.sparsifier == "dense" else W + 6)
 
-    # ---- end to end through the public API with host buffers (N = 1) ----
-    e2e = None
+    # ---- end to end through the public API with host buffers ----
+    cdev = dev if args.dist_backend == "nccl" else "cpu"
     if world == 1:
         # one distinct pinned host gradient per e2e step (the same statistics
         # as the timed steps; re-feeding one gradient would make the residual
         # grow coherently and inflate the selection)
         ke = max(3, min(args.steps, 10))
-        nb = int(max(2, min(ke + 1, 8e9 // (esz * n_g * W))))  # <= 8 GB of pinned host gradients
+        nb = int(max(2, min(ke + 1, 16e9 // (esz * n_g * W))))  # <= 16 GB of pinned host gradients
         hGs = []
         for b in range(nb):
             hG = torch.empty(W * n_g, dtype=tdt).pin_memory()
@@ -348,10 +493,12 @@ def our_arm(args, wl):
         e2e_s = (time.perf_counter() - t0) / ke
         e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g * W,
                "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
+               "api": "micro_step_host (include/micro.h)",
                "host_gradients": f"{nb - 1} distinct pinned buffers over {ke} steps",
                "density": float(statistics.mean(kk)) / n_g,
                # what bounds it: the H2D of the gradient over PCIe (Gen5 x16: ~64 GB/s nominal)
                "h2d_gbs_effective": esz * n_g * W / e2e_s / 1e9}
+        del hGs
     else:
         # N ranks: each copies its own pinned host gradient in, steps through
         # DistMicro, and reads the union back; the max over ranks is reported
@@ -379,73 +526,82 @@ def our_arm(args, wl):
             kk.append(i_.size)
             t += 1
         torch.cuda.synchronize()
-        v = torch.tensor([(time.perf_counter() - t0) / ke], device=dev if args.dist_backend == "nccl" else "cpu",
-                         dtype=torch.float64)
+        v = torch.tensor([(time.perf_counter() - t0) / ke], device=cdev, dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         e2e = {"value": float(v[0]) * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g,
                "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
+               "api": "DistMicro.step + union (paper_2310_00967_b200/dist.py)",
                "host_gradients": f"{nb - 1} distinct pinned buffers per rank over {ke} steps",
                "density": float(statistics.mean(kk)) / n_g, "per": "rank (max over ranks)"}
+        del hGs
+    m.close()
+    del G, m
+    torch.cuda.empty_cache()
+
+    # ---- the same measurement in the other arithmetic (N = 1, MiCRO) ----
+    other = None
+    if world == 1 and args.sparsifier == "micro" and not args.no_other_dtype:
+        otdt = torch.float32 if tdt == torch.float64 else torch.float64
+        ro = device_measure(args, wl, otdt, None, world, rank, local, dev)
+        rf = roofline_of(args, ro, wl, world, peak, peak_kind)
+        other = {"dtype": "f32" if otdt == torch.float32 else "f64", "value": ro["ms_step"] * 1e3,
+                 "unit": "us/iter", "density": float(ro["K"].mean() / n_g),
+                 "roofline": {k: rf[k] for k in ("achieved", "peak", "frac", "algorithmic_bytes_per_launch",
+                                                 "avg_launch_ms", "step_frac")}}
 
     # ---- CPU baseline: the reference's own code on this host (rank 0, N = 1) ----
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            times = run_reference_cluster(n_g, W, d, steps=args.cpu_steps, warmup=1)
-            cpu = {"value": statistics.mean(times) * 1e6, "unit": "us/iter", "cores": 1, "kind": "reference",
-                   "sample": f"{args.cpu_steps} iterations (after 1 warm-up) of the full workload (n_g={n_g}, n={W}) "
-                             "through the reference's sparsifier/collectives TUs compiled verbatim (fp64, 1 thread)"}
+            cr = run_reference_converged(n_g, W, d, steps=args.cpu_steps, warmup=1, adapt_iters=args.prime,
+                                         dense=args.dense, model=args.model, threads=1, seed=args.seed)
+            cd = float(np.mean(cr["density"]))
+            cpu = {"value": statistics.mean(cr["times"]) * 1e6, "unit": "us/iter", "cores": 1, "kind": "reference",
+                   "sample": cr["sample"], "density": cd, "first_timed_t": cr["first_timed_t"],
+                   "density_vs_ours": cd / density - 1.0, "host": host_info(1)}
         except Exception as ex:  # the checker is optional at run time; the GPU number stands
             cpu = {"value": None, "unit": "us/iter", "cores": 1, "kind": "reference", "sample": f"failed: {ex}"}
 
     # the exchange against the NVLink roofline (N > 1): bytes received per GPU,
     # 4(K-k) foreign indices + 4k(n-1) contributions + 4(K-k) sums
     exchange_line = None
-    if dist and xchg_ms:
+    if dist and r["xchg_ms"]:
         Km, km = float(K.mean()), float(k_own.mean())
         b_net = 4.0 * (Km - km) + 4.0 * km * (world - 1) + 4.0 * (Km - km)
-        exchange_line = {"bound": "nvlink", "achieved": b_net / (xchg_ms * 1e-3) / 1e9, "peak": 900.0,
-                         "unit": "GB/s", "frac": b_net / (xchg_ms * 1e-3) / 1e9 / 900.0,
-                         "bytes_per_gpu": b_net, "avg_ms": xchg_ms, "transport": m.transport,
+        xms = r["xchg_ms"]
+        exchange_line = {"bound": "nvlink", "achieved": b_net / (xms * 1e-3) / 1e9, "peak": 900.0,
+                         "unit": "GB/s", "frac": b_net / (xms * 1e-3) / 1e9 / 900.0,
+                         "bytes_per_gpu": b_net, "avg_ms": xms, "transport": r["transport"],
                          "peak_source": "NVLink 5 per direction per GPU (nominal)",
-                         "timed": "exchange kernels, barriers excluded" if m.transport != "nccl"
+                         "timed": "exchange kernels, barriers excluded" if r["transport"] != "nccl"
                          else "the whole NCCL protocol"}
 
     if rank == 0:
+        R = r["R"]
         line = {
             "metric": METRIC, "value": ms_step * 1e3, "unit": "us/iter", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype,
             "data": f"synthetic N(0,1) {args.dtype} gradients (include/micro_synth.h)",
-            "config": {"workload": wl["desc"], "n_g": n_g, "density_target": d, "workers": world * W,
-                       "one_worker_per_gpu": W == 1, "eta": ETA, "alpha": ALPHA, "delta0": delta0,
-                       "adaptation_iterations": args.prime, "first_timed_t": t_first,
-                       "model_update": bool(args.model), "dense_g_over_n": bool(args.dense),
-                       "error_norm_recorded": bool(args.error_norm), "seed": args.seed,
-                       "sparsifier": args.sparsifier,
-                       "inputs": (f"{R} resident N(0,1) gradients ("
-                                  + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
-                                  + (f"); L2 flushed between timed steps (256 MB write outside the per-step "
-                                     f"events: the working set {3 * esz * n_g / 1e6:.0f} MB would fit L2)"
-                                     if flush else f"); each {esz}*n_g bytes > L2 (no flush needed)"
-                                     if esz * n_g > 126e6 else "); L2 NOT flushed (--flush-l2 off)")),
-                       "parallelism": (f"dp{world} (exclusive cyclic partitions"
-                                       + (f", {m.transport} exchange)" if world > 1 else ")") if W == 1 else
-                                       f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)")},
-            "median_us_per_step": (float(np.median(step_ms)) * 1e3 if step_ms else None),
+            "config": bench_config(args, wl, world),
+            "protocol": {"adaptation_iterations": args.prime, "first_timed_t": r["t_first"], "seed": args.seed,
+                         "inputs": (f"{R} resident N(0,1) gradients ("
+                                    + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
+                                    + (f"); L2 flushed between timed steps (256 MB write + 256 MB read outside "
+                                       f"the per-step events: the working set {3 * esz * n_g / 1e6:.0f} MB would "
+                                       f"fit L2)" if r["flush"] else f"); each {esz}*n_g bytes > L2 (no flush "
+                                       f"needed)" if esz * n_g > 126e6 else "); L2 NOT flushed (--flush-l2 off)")),
+                         "median_us_per_step": (float(np.median(r["step_ms"])) * 1e3 if r["step_ms"] else None)},
             "density": density, "density_rel_err": density / d - 1.0,
+            "density_reference": (cpu or {}).get("density"),
             "density_window": {"first_quarter": float(K[: max(1, len(K) // 4)].mean() / n_g),
                                "last_quarter": float(K[-max(1, len(K) // 4):].mean() / n_g),
                                "median": float(np.median(K) / n_g)},
-            "select_gbs": achieved,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic_from_profiles(args.workload),
-                         "kernel": "k1_stream", "algorithmic_bytes_per_launch": k1_bytes,
-                         "avg_launch_ms": k1a_avg_ms, "peak_source": peak_kind,
-                         "timed_launches": f"{len(k1a_ms)} of {args.steps} (every 4th, CUDA events on the launch stream)",
-                         "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / peak},
+            "select_gbs": roof["achieved"],
+            "roofline": roof,
             "exchange": exchange_line,
-            "clocks": clocks,
+            "other_dtype": other,
+            "clocks": r["clocks"],
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
@@ -467,7 +623,8 @@ def main():
     ap.add_argument("--buffers", type=int, default=256, help="max resident gradient buffers")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--dense", action="store_true", help="also maintain the dense g/n vector")
+    ap.add_argument("--no-dense", dest="dense", action="store_false",
+                    help="skip the dense averaged gradient g/n (all_reduce_sparse / n, collectives.cpp:51-57)")
     ap.add_argument("--cluster-workers", type=int, default=1,
                     help="N = 1 only: W in-process workers on the GPU (the reference's in-process cluster)")
     ap.add_argument("--no-model", dest="model", action="store_false", help="skip the model update x -= g/n")
@@ -480,8 +637,10 @@ def main():
     ap.add_argument("--seed", type=int, default=SEED, help="synthetic gradient stream (SURVEY.md 8d: 1, 2, 3)")
     ap.add_argument("--flush-l2", choices=["auto", "on", "off"], default="auto",
                     help="flush L2 between timed steps (auto: when e, G and x would fit in L2)")
-    ap.add_argument("--dtype", choices=["f32", "f64"], default="f32",
-                    help="f64: the reference's own arithmetic (bit-exact with its code)")
+    ap.add_argument("--dtype", choices=["f32", "f64"], default="f64",
+                    help="f64 (default): the reference's own arithmetic (bit-exact with its code); f32: the "
+                         "north star's gradient type (reported beside the f64 line as other_dtype)")
+    ap.add_argument("--no-other-dtype", action="store_true", help="skip the other-dtype measurement")
     ap.add_argument("--error-norm", action="store_true",
                     help="also record the per-step error norm ||e_{t+1}|| (fused into k1_stream); off by "
                          "default, like the reference arm's timed step")

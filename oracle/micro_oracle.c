@@ -103,26 +103,44 @@ void orc_gaussian(uint64_t seed, uint32_t worker, uint64_t t, int64_t n, float* 
   }
 }
 
-static int cmp_i64(const void* a, const void* b) {
-  const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
-  return (x > y) - (x < y);
-}
-
 /* src/collectives.cpp:14-28 — concat in worker order, sort, unique.
- * sel_idx: n rows, row i holds counts[i] sorted indices at sel_idx + offs[i].
+ * sel_idx: n rows, row i holds counts[i] indices in ascending order (every
+ * selection here is: sparsifier.cpp:29-35), so sort + unique of the
+ * concatenation is the n-way merge of the rows with duplicates dropped —
+ * the same sorted unique union in O(K n) instead of O(K log K).
  * Returns the union size in *K. */
 int orc_all_gather_indices(int n, const int64_t* counts, const int64_t* const* sel_idx,
                            int64_t* union_idx, int64_t* K) {
-  int64_t total = 0;
-  for (int i = 0; i < n; ++i) {
-    memcpy(union_idx + total, sel_idx[i], (size_t)counts[i] * sizeof(int64_t));
-    total += counts[i];
-  }
-  qsort(union_idx, (size_t)total, sizeof(int64_t), cmp_i64);
+  int64_t pos[64] = {0};
   int64_t w = 0;
-  for (int64_t r = 0; r < total; ++r)
-    if (w == 0 || union_idx[w - 1] != union_idx[r]) union_idx[w++] = union_idx[r];
+  if (n > 64) return orc_fail(ORC_EINVAL, "all_gather_indices: at most 64 workers");
+  for (;;) {
+    int best = -1;
+    int64_t v = 0;
+    for (int i = 0; i < n; ++i)
+      if (pos[i] < counts[i] && (best < 0 || sel_idx[i][pos[i]] < v)) {
+        best = i;
+        v = sel_idx[i][pos[i]];
+      }
+    if (best < 0) break;
+    ++pos[best];
+    if (w == 0 || union_idx[w - 1] != v) union_idx[w++] = v;
+  }
   *K = w;
+  return ORC_OK;
+}
+
+static int64_t* orc_union_idx = NULL;
+static float* orc_union_sum_f32 = NULL;
+static double* orc_union_sum_f64 = NULL;
+
+/* The union kept by the last orc_step_* call made with union_idx == NULL. */
+int orc_fetch_union_f32(int64_t* idx, float* sum, int64_t K) {
+  if (K) { memcpy(idx, orc_union_idx, (size_t)K * 8); memcpy(sum, orc_union_sum_f32, (size_t)K * 4); }
+  return ORC_OK;
+}
+int orc_fetch_union_f64(int64_t* idx, double* sum, int64_t K) {
+  if (K) { memcpy(idx, orc_union_idx, (size_t)K * 8); memcpy(sum, orc_union_sum_f64, (size_t)K * 8); }
   return ORC_OK;
 }
 
@@ -194,29 +212,51 @@ int orc_all_gather_indices(int n, const int64_t* counts, const int64_t* const* s
         a[j] = a[j] + p;                                                                        \
       }                                                                                         \
     }                                                                                           \
-    /* harness.cpp:139-151: select in the cyclic partition with this worker's delta */          \
-    int64_t* sel_idx = (int64_t*)malloc((size_t)n_g * sizeof(int64_t));                         \
-    T* sel_val = (T*)malloc((size_t)n_g * sizeof(T));                                           \
-    const int64_t** rows = (const int64_t**)malloc((size_t)n * sizeof(int64_t*));               \
-    if (!sel_idx || !sel_val || !rows) {                                                        \
-      free(sel_idx); free(sel_val); free(rows);                                                 \
-      return orc_fail(ORC_ENOMEM, "oracle: out of memory");                                     \
-    }                                                                                           \
-    int64_t off = 0;                                                                            \
-    for (int i = 0; i < n; ++i) {                                                               \
-      int64_t s, en, k;                                                                         \
-      orc_partition(n_g, n, t, i, &s, &en);                                                     \
-      delta_used[i] = delta[i];                                                                 \
-      rc = orc_select_##SUF(e + (int64_t)i * n_g, n_g, s, en, delta[i], sel_idx + off,          \
-                            sel_val + off, &k);                                                 \
-      if (rc) { free(sel_idx); free(sel_val); free(rows); return rc; }                          \
-      rows[i] = sel_idx + off;                                                                  \
-      counts[i] = k;                                                                            \
-      off += k;                                                                                 \
-    }                                                                                           \
-    /* harness.cpp:185-186: all_gather_indices, all_reduce_sparse_values */                     \
-    orc_all_gather_indices(n, counts, rows, union_idx, K);                                      \
-    orc_all_reduce_sparse_values_##SUF(e, n, n_g, union_idx, *K, union_sum);                    \
+    /* harness.cpp:139-151: select in the cyclic partition with this worker's delta    \
+     * (buffers sized to the selection: one counting pass, then the scan itself) */       \
+    int64_t total = 0;                                                                      \
+    for (int i = 0; i < n; ++i) {                                                           \
+      int64_t s, en;                                                                        \
+      orc_partition(n_g, n, t, i, &s, &en);                                                 \
+      if (!(delta[i] >= 0.0) || !isfinite(delta[i]))                                        \
+        return orc_fail(ORC_EINVAL, "selection: threshold must be finite and nonnegative"); \
+      const T* a = e + (int64_t)i * n_g;                                                    \
+      for (int64_t j = s; j < en; ++j) total += (double)ABS(a[j]) > delta[i];               \
+    }                                                                                       \
+    int64_t* sel_idx = (int64_t*)malloc((size_t)(total + 1) * sizeof(int64_t));            \
+    T* sel_val = (T*)malloc((size_t)(total + 1) * sizeof(T));                               \
+    const int64_t** rows = (const int64_t**)malloc((size_t)n * sizeof(int64_t*));           \
+    if (!sel_idx || !sel_val || !rows) {                                                    \
+      free(sel_idx); free(sel_val); free(rows);                                             \
+      return orc_fail(ORC_ENOMEM, "oracle: out of memory");                                 \
+    }                                                                                       \
+    int64_t off = 0;                                                                        \
+    for (int i = 0; i < n; ++i) {                                                           \
+      int64_t s, en, k;                                                                     \
+      orc_partition(n_g, n, t, i, &s, &en);                                                 \
+      delta_used[i] = delta[i];                                                             \
+      rc = orc_select_##SUF(e + (int64_t)i * n_g, n_g, s, en, delta[i], sel_idx + off,      \
+                            sel_val + off, &k);                                             \
+      if (rc) { free(sel_idx); free(sel_val); free(rows); return rc; }                      \
+      rows[i] = sel_idx + off;                                                              \
+      counts[i] = k;                                                                        \
+      off += k;                                                                             \
+    }                                                                                       \
+    /* harness.cpp:185-186: all_gather_indices, all_reduce_sparse_values.  With            \
+     * union_idx == NULL the union is kept here (sized to it) for orc_fetch_union_*. */     \
+    if (!union_idx) {                                                                       \
+      free(orc_union_idx); free(orc_union_sum_##SUF);                                       \
+      orc_union_idx = (int64_t*)malloc((size_t)(total + 1) * sizeof(int64_t));             \
+      orc_union_sum_##SUF = (T*)malloc((size_t)(total + 1) * sizeof(T));                    \
+      if (!orc_union_idx || !orc_union_sum_##SUF) {                                         \
+        free(sel_idx); free(sel_val); free(rows);                                           \
+        return orc_fail(ORC_ENOMEM, "oracle: out of memory");                               \
+      }                                                                                     \
+      union_idx = orc_union_idx;                                                            \
+      union_sum = orc_union_sum_##SUF;                                                      \
+    }                                                                                       \
+    orc_all_gather_indices(n, counts, rows, union_idx, K);                                  \
+    orc_all_reduce_sparse_values_##SUF(e, n, n_g, union_idx, *K, union_sum);                \
     /* harness.cpp:201-208: threshold estimate for t+1 with this iteration's count */           \
     for (int i = 0; i < n; ++i)                                                                 \
       orc_update_threshold(&delta[i], k_worker, (uint64_t)counts[i], alpha, min_threshold);     \

@@ -62,7 +62,8 @@ class Oracle:
             getattr(L, f"orc_all_reduce_sparse_values_{suf}").argtypes = [fp, I32, I64, i64p, I64, fp]
             getattr(L, f"orc_step_{suf}").argtypes = [
                 I64, I32, DBL, DBL, DBL, I32, I32, I64, DBL, fp, fp, f64p, C.c_void_p,
-                i64p, i64p, fp, C.POINTER(I64), f64p]
+                i64p, C.c_void_p, C.c_void_p, C.POINTER(I64), f64p]
+            getattr(L, f"orc_fetch_union_{suf}").argtypes = [i64p, fp, I64]
 
     def _check(self, rc):
         if rc:
@@ -125,22 +126,26 @@ class OracleCluster:
         self.e = np.zeros((n, n_g), self.dtype)
         self.delta = np.full(n, delta0, np.float64)
         self.x = np.zeros(n_g, self.dtype) if model else None
-        self.fn = getattr(self.o.lib, "orc_step_" + ("f32" if self.dtype == np.float32 else "f64"))
+        suf = "f32" if self.dtype == np.float32 else "f64"
+        self.fn = getattr(self.o.lib, "orc_step_" + suf)
+        self.fetch = getattr(self.o.lib, "orc_fetch_union_" + suf)
 
     def step(self, G, eta, t):
         G = np.ascontiguousarray(G, self.dtype).reshape(self.n, self.n_g)
         counts = np.empty(self.n, np.int64)
-        uidx = np.empty(self.n_g, np.int64)
-        usum = np.empty(self.n_g, self.dtype)
         K = I64()
         dused = np.empty(self.n, np.float64)
         d, a, eps, full, ef = self.cfg
         xp = self.x.ctypes.data if self.x is not None else None
+        # the union stays inside the oracle (sized to it) and is fetched at its size
         rc = self.fn(self.n_g, self.n, d, a, eps, full, ef, t, eta, self.e, G, self.delta, xp,
-                     counts, uidx, usum, C.byref(K), dused)
+                     counts, None, None, C.byref(K), dused)
         if rc:
             raise OracleError(rc, self.o.lib.orc_last_error().decode())
-        return dict(counts=counts, union_idx=uidx[: K.value].copy(), union_sum=usum[: K.value].copy(),
+        uidx = np.empty(K.value, np.int64)
+        usum = np.empty(K.value, self.dtype)
+        self.fetch(uidx, usum, K.value)
+        return dict(counts=counts, union_idx=uidx, union_sum=usum,
                     delta_used=dused, delta_next=self.delta.copy())
 
 
@@ -173,6 +178,9 @@ class Reference:
                                        C.POINTER(I64), f64p]
         L.ref_cluster_residual.argtypes = [C.c_void_p, I32, f64p]
         L.ref_cluster_thresholds.argtypes = [C.c_void_p, f64p]
+        L.ref_cluster_set_options.argtypes = [C.c_void_p, I32, I32]
+        L.ref_cluster_set_state.argtypes = [C.c_void_p, I32, f64p, DBL]
+        L.ref_cluster_dense.argtypes = [C.c_void_p, f64p]
         L.ref_cluster_phase_times.argtypes = [C.c_void_p, f64p]
         L.ref_cluster_phase_times.restype = None
         L.ref_cluster_step_kind.argtypes = [C.c_void_p, I32, f64p, DBL, I64, C.c_void_p, i64p, i64p, f64p,
@@ -301,6 +309,20 @@ class RefCluster:
         self.r.lib.ref_cluster_thresholds(self.h, dn)
         return dict(counts=counts, union_idx=uidx[: K.value].copy(), union_sum=usum[: K.value].copy(),
                     delta_used=dused, delta_next=dn)
+
+    def set_options(self, dense=False, threads=1):
+        """dense: also form all_reduce_sparse(...) / n each step; threads: run
+        the per-worker loops on that many host threads."""
+        self.r.lib.ref_cluster_set_options(self.h, int(dense), int(threads))
+
+    def set_state(self, i, residual, delta):
+        self.r._check(self.r.lib.ref_cluster_set_state(self.h, i, np.ascontiguousarray(residual, np.float64),
+                                                       float(delta)))
+
+    def dense(self):
+        out = np.empty(self.n_g, np.float64)
+        self.r._check(self.r.lib.ref_cluster_dense(self.h, out))
+        return out
 
     def residual(self, i):
         out = np.empty(self.n_g, np.float64)

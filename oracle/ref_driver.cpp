@@ -22,6 +22,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace sparsim;
@@ -76,7 +77,40 @@ struct RefCluster {
   std::vector<GradientVector> accumulators;  // ClusterState::accumulators
   std::size_t k_global = 0, k_worker = 0;
   double phase[4] = {0, 0, 0, 0};  // accumulate, select, gather+reduce, threshold+compensate
+  // bench options (ref_cluster_set_options): the dense averaged gradient
+  // all_reduce_sparse(...) / n (collectives.cpp:51-57) each step, and host
+  // threads for the per-worker loops (harness.cpp runs its workers one after
+  // the other; with threads > 1 the same per-worker calls run concurrently)
+  bool dense_on = false;
+  GradientVector dense;
+  int threads = 1;
 };
+
+// f(i) for every worker i, on up to `threads` host threads (workers are
+// independent in the accumulate, select and compensate loops).
+template <class F>
+void for_workers(int n, int threads, F&& f) {
+  if (threads <= 1 || n <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::vector<std::exception_ptr> err(static_cast<std::size_t>(n));
+  const int T = threads < n ? threads : n;
+  for (int w = 0; w < T; ++w)
+    pool.emplace_back([&, w] {
+      for (int i = w; i < n; i += T) {
+        try {
+          f(i);
+        } catch (...) {
+          err[static_cast<std::size_t>(i)] = std::current_exception();
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
 
 }  // namespace
 
@@ -235,26 +269,33 @@ int ref_cluster_step(void* h, const double* G, double eta, std::int64_t t, doubl
         if (!std::isfinite(g[j]))
           throw std::runtime_error("iteration " + std::to_string(t) +
                                    ": non-finite gradient on worker " + std::to_string(i));
+    }
+    for_workers(n, cs.threads, [&](int i) {
       // cs.accumulators[i] = w.residual + eta * grad; — evaluated in place like Eigen's
       // lazy assignment (no temporary), the same IEEE op per element.
+      const double* g = G + static_cast<std::int64_t>(i) * n_g;
       double* acc = cs.accumulators[static_cast<std::size_t>(i)].data();
       const double* res = cs.residuals[static_cast<std::size_t>(i)].data();
       for (Index j = 0; j < n_g; ++j) acc[j] = res[j] + eta * g[j];
-    }
+    });
     auto t1 = Clock::now();
     // selection (harness.cpp:139-151)
     std::vector<SparseSelection> selections(static_cast<std::size_t>(n));
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < n; ++i) delta_used[i] = cs.thresholds[static_cast<std::size_t>(i)].delta;
+    for_workers(n, cs.threads, [&](int i) {
       const auto range = partition(n_g, n, t, i);
-      const double delta = cs.thresholds[static_cast<std::size_t>(i)].delta;
-      delta_used[i] = delta;
       selections[static_cast<std::size_t>(i)] =
-          select_by_threshold(cs.accumulators[static_cast<std::size_t>(i)], range, delta);
-    }
+          select_by_threshold(cs.accumulators[static_cast<std::size_t>(i)], range, delta_used[i]);
+    });
     auto t2 = Clock::now();
     // collectives (harness.cpp:185-186)
     const AggregatedSelection agg = all_gather_indices(selections);
     const std::vector<double> sums = all_reduce_sparse_values(cs.accumulators, agg);
+    if (cs.dense_on) {  // the dense averaged gradient: all_reduce_sparse / n
+      cs.dense = all_reduce_sparse(cs.accumulators, agg);
+      if (n > 1)
+        for (Index j = 0; j < n_g; ++j) cs.dense[j] /= n;
+    }
     auto t3 = Clock::now();
     // threshold estimate (harness.cpp:201-208)
     for (int i = 0; i < n; ++i)
@@ -266,12 +307,12 @@ int ref_cluster_step(void* h, const double* G, double eta, std::int64_t t, doubl
     if (x)
       for (std::size_t k = 0; k < agg.indices.size(); ++k) x[agg.indices[k]] -= sums[k] / n;
     // compensate + swap (harness.cpp:219-224)
-    for (int i = 0; i < n; ++i) {
+    for_workers(n, cs.threads, [&](int i) {
       auto& acc = cs.accumulators[static_cast<std::size_t>(i)];
       for (Index j : agg.indices) acc[j] = 0.0;
       if (!cs.error_feedback) acc.setZero();
       std::swap(cs.residuals[static_cast<std::size_t>(i)], acc);
-    }
+    });
     auto t4 = Clock::now();
     cs.phase[0] += secs(t0, t1);
     cs.phase[1] += secs(t1, t2);
@@ -351,6 +392,36 @@ int ref_cluster_residual(void* h, int i, double* out) {
   return guarded([&] {
     if (i < 0 || i >= cs.n) throw std::invalid_argument("worker out of range");
     to_ptr(cs.residuals[static_cast<std::size_t>(i)], out);
+  });
+}
+
+// Bench options: dense != 0 also forms the dense averaged gradient each step;
+// threads > 1 runs the per-worker loops concurrently.
+int ref_cluster_set_options(void* h, int dense, int threads) {
+  auto& cs = *static_cast<RefCluster*>(h);
+  cs.dense_on = dense != 0;
+  cs.threads = threads < 1 ? 1 : threads;
+  return 0;
+}
+
+// Overwrite worker i's state (residual, threshold): the bench transplants a
+// converged state adapted at a smaller n_g (tiled) so the timed steps start
+// in the stationary regime.
+int ref_cluster_set_state(void* h, int i, const double* residual, double delta) {
+  auto& cs = *static_cast<RefCluster*>(h);
+  return guarded([&] {
+    if (i < 0 || i >= cs.n) throw std::invalid_argument("worker out of range");
+    std::memcpy(cs.residuals[static_cast<std::size_t>(i)].data(), residual,
+                static_cast<std::size_t>(cs.n_g) * sizeof(double));
+    cs.thresholds[static_cast<std::size_t>(i)] = ThresholdState{delta};
+  });
+}
+
+int ref_cluster_dense(void* h, double* out) {
+  auto& cs = *static_cast<RefCluster*>(h);
+  return guarded([&] {
+    if (!cs.dense_on || cs.dense.size() != cs.n_g) throw std::logic_error("dense output not formed");
+    to_ptr(cs.dense, out);
   });
 }
 

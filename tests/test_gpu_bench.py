@@ -35,6 +35,14 @@ def test_bench_line_n1():
     assert set(d["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
     assert set(d["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 1
+    assert d["dtype"] == "f64" and d["config"]["dense_g_over_n"] and d["config"]["model_update"]
+    assert d["other_dtype"]["dtype"] == "f32" and d["other_dtype"]["value"] > 0
+    # the reference arm runs the identical workload
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "c1", "--steps", "2",
+                        "--warmup", "1", "--prime", "50"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    ref = _line(r.stdout)
+    assert ref["impl"] == "reference" and ref["config"] == d["config"] and ref["metric"] == d["metric"]
 
 
 @pytest.mark.parametrize("transport", ["peer", "peer_pull", "nccl"])
