@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define MICRO_ABI_VERSION 3
+#define MICRO_ABI_VERSION 4
 #define MICRO_MAX_WORKERS 64
 
 typedef enum micro_status {
@@ -185,7 +185,9 @@ int micro_set_model(micro_ctx* ctx, void* d_x);
  * array of n_local device pointers.  Asynchronous. */
 int micro_compress(micro_ctx* ctx, const void* const* d_grads, double eta, int64_t t);
 /* Single-device cluster: union + ordered all-worker reduce + foreign zeroing
- * + threshold update + dense g/n (+ model).  Asynchronous. */
+ * + threshold update + dense g/n (+ model).  A rank context with NCCL
+ * attached (micro_dist_attach_nccl): the n-GPU exchange + finalize.
+ * Asynchronous. */
 int micro_aggregate(micro_ctx* ctx);
 /* micro_compress + micro_aggregate. */
 int micro_step(micro_ctx* ctx, const void* const* d_grads, double eta, int64_t t);
@@ -256,23 +258,62 @@ int micro_copy_residual(micro_ctx* ctx, int local_worker, void* h_out);
 int micro_copy_dense(micro_ctx* ctx, void* h_out);
 
 /* ---- one rank of a multi-GPU job (n_local == 1 < n_workers) -------------- *
- * Host protocol per iteration (paper_2310_00967_b200/dist.py drives it over
- * torch.distributed / NCCL):
- *   micro_compress                      -> own k_i and pairs on device
- *   all-gather k (n counts)             -> h_counts on host
- *   all-gather own indices, padded to kmax = max k -> d_all_idx[n][kmax]
- *   micro_dist_gather_foreign           -> d_send (acc at other owners' indices,
- *                                          rank order, segment o has k_o values)
- *   all-to-all-v  send -> owners        -> d_recv (segment r has k_own values)
- *   micro_dist_owner_reduce             -> d_own_sums[k_own] (rank-ordered sum)
- *   all-gather own sums, padded to kmax -> d_all_sums[n][kmax]
- *   micro_dist_finalize                 -> union, dense g/n, model, delta, stats */
-int micro_dist_gather_foreign(micro_ctx* ctx, const int32_t* d_all_idx, const int64_t* h_counts,
-                              int64_t kmax, void* d_send);
-int micro_dist_owner_reduce(micro_ctx* ctx, const void* d_recv, const int64_t* h_counts,
-                            void* d_own_sums);
-int micro_dist_finalize(micro_ctx* ctx, const int32_t* d_all_idx, const void* d_all_sums,
-                        const int64_t* h_counts, int64_t kmax);
+ * The collective protocol (collectives.cpp:14-57 semantics,
+ * harness.cpp:185-224 order) as device halves around host-driven
+ * collectives.  Every buffer has a fixed stride kcap (the selection
+ * capacity, micro_config.selection_capacity or the partition size) per rank
+ * and every count stays on the device, so the host never reads one: the
+ * whole iteration is stream-ordered.  A selection larger than kcap raises
+ * the overflow flag (MICRO_ECAPACITY at the next synchronising call).
+ *   micro_compress                              own_count, own_idx
+ *   all-gather own_count -> all_counts[n]       (int64)
+ *   all-gather own_idx   -> all_idx[n][kcap]    (int32)
+ *   micro_dist_gather_foreign                   send[o][kcap]: own acc at owner o's
+ *                                               indices (zeroed in the residual)
+ *   all-to-all: send[o] -> rank o's recv[me]    (kcap values per pair)
+ *   micro_dist_owner_reduce                     own_sums[kcap]: rank-ordered sums
+ *   all-gather own_sums  -> all_sums[n][kcap]
+ *   micro_dist_finalize                         union, dense g/n, model, delta, stats
+ * micro_dist_attach_nccl / micro_dist_init_nccl run exactly this (or the peer
+ * exchange below) inside micro_aggregate with NCCL; dist.py runs it over
+ * torch.distributed. */
+typedef struct micro_dist_bufs {
+  int64_t kcap;
+  const int64_t* own_count; /* [1]   this rank's k_i */
+  const int32_t* own_idx;   /* [kcap] this rank's selection, ascending */
+  int64_t* all_counts;      /* [n]   <- all-gather of own_count */
+  int32_t* all_idx;         /* [n][kcap] <- all-gather of own_idx */
+  void* send;               /* [n][kcap] segment o goes to rank o */
+  void* recv;               /* [n][kcap] segment r <- rank r's send[me] */
+  void* own_sums;           /* [kcap] */
+  void* all_sums;           /* [n][kcap] <- all-gather of own_sums */
+} micro_dist_bufs;
+int micro_dist_buffers(micro_ctx* ctx, micro_dist_bufs* out);
+int micro_dist_gather_foreign(micro_ctx* ctx);
+int micro_dist_owner_reduce(micro_ctx* ctx);
+int micro_dist_finalize(micro_ctx* ctx);
+
+/* ---- the exchange behind the C ABI over NCCL (no Python, no host sync) ---- *
+ * One process per GPU, one rank context each.  Either the host brings its
+ * own communicator (micro_dist_attach_nccl; an ncclComm_t of n ranks, rank ==
+ * the context's rank), or the library makes one: rank 0 calls
+ * micro_nccl_unique_id, the host hands the 128 bytes to every rank (MPI, a
+ * file, ...), each calls micro_dist_init_nccl.  Afterwards micro_aggregate /
+ * micro_step on the rank context run the whole exchange on ctx's stream:
+ *   MICRO_XCHG_PEER  the bulk peer-memory exchange below (NVLink P2P through
+ *                    CUDA IPC mappings made at attach, handles all-gathered
+ *                    over NCCL); the three barriers are 4-byte ncclAllReduce
+ *                    calls on ctx's stream.  The default.
+ *   MICRO_XCHG_NCCL  the collective protocol above: ncclAllGather of the
+ *                    counts, indices and sums, grouped ncclSend/ncclRecv for
+ *                    the contributions (kcap per pair).
+ * NCCL is loaded at attach (libnccl.so.2, the process's copy if one is
+ * loaded); MICRO_ENCCL reports its errors. */
+#define MICRO_NCCL_UNIQUE_ID_BYTES 128
+enum { MICRO_XCHG_PEER = 0, MICRO_XCHG_NCCL = 1 };
+int micro_nccl_unique_id(void* out);
+int micro_dist_init_nccl(micro_ctx* ctx, const void* unique_id, int transport);
+int micro_dist_attach_nccl(micro_ctx* ctx, void* nccl_comm, int transport);
 
 /* ---- the same exchange as ONE kernel over peer memory (NVLink) ----------- *
  * Replaces K2..K7 above (collectives.cpp:14-57 semantics, harness.cpp:185-224

@@ -43,6 +43,15 @@ class micro_record(C.Structure):
                 ("threshold", DBL)]
 
 
+class micro_dist_bufs(C.Structure):
+    _fields_ = [("kcap", I64), ("own_count", VP), ("own_idx", VP), ("all_counts", VP), ("all_idx", VP),
+                ("send", VP), ("recv", VP), ("own_sums", VP), ("all_sums", VP)]
+
+
+MICRO_NCCL_UNIQUE_ID_BYTES = 128
+MICRO_XCHG_PEER, MICRO_XCHG_NCCL = 0, 1
+
+
 class MicroError(RuntimeError):
     """Base of the status-code exceptions (include/micro.h)."""
 
@@ -125,9 +134,13 @@ _SIGS = {
     "micro_copy_union": ([VP, VP, VP, I64, PI64], I32),
     "micro_copy_residual": ([VP, I32, VP], I32),
     "micro_copy_dense": ([VP, VP], I32),
-    "micro_dist_gather_foreign": ([VP, VP, PI64, I64, VP], I32),
-    "micro_dist_owner_reduce": ([VP, VP, PI64, VP], I32),
-    "micro_dist_finalize": ([VP, VP, VP, PI64, I64], I32),
+    "micro_dist_buffers": ([VP, C.POINTER(micro_dist_bufs)], I32),
+    "micro_dist_gather_foreign": ([VP], I32),
+    "micro_dist_owner_reduce": ([VP], I32),
+    "micro_dist_finalize": ([VP], I32),
+    "micro_nccl_unique_id": ([VP], I32),
+    "micro_dist_init_nccl": ([VP, VP, I32], I32),
+    "micro_dist_attach_nccl": ([VP, VP, I32], I32),
     "micro_peer_export": ([VP, VP], I32),
     "micro_peer_import": ([VP, VP], I32),
     "micro_peer_exchange": ([VP], I32),
@@ -158,7 +171,7 @@ def lib() -> C.CDLL:
                 f = getattr(L, name)
                 f.argtypes = args
                 f.restype = res
-            if L.micro_abi_version() != 3:
+            if L.micro_abi_version() != 4:
                 raise ImportError("libmicro_b200.so ABI version mismatch")
             _lib = L
     return _lib

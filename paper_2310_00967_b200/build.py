@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmicro_b200.so")
-SOURCES = ["api.cu", "dist_api.cu", "value_api.cu"]
+SOURCES = ["api.cu", "dist_api.cu", "value_api.cu", "nccl_api.cu"]
 HEADERS = ["internal.cuh", "baselines.cuh", "common.cuh", "norm.cuh", "scan.cuh", "select.cuh", "select_stream.cuh",
            "exchange.cuh", "peer.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                                        "-c", "-o", obj, os.path.join(CSRC, src)]))
     if any(p.wait() != 0 for p in procs):
         raise subprocess.CalledProcessError(1, "nvcc")
-    subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs], check=True)
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"], check=True)
     return LIB
 
 
@@ -58,15 +58,23 @@ if __name__ == "__main__":
     print(build(force=True, verbose="-v" in sys.argv))
 
 
-CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
-CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
+CPP_TESTS = {  # name -> source: the C++ hosts of the C ABI (no Python on their path)
+    "test_dropin": os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp"),
+    "test_dist_ipc": os.path.join(ROOT, "tests", "cpp", "test_dist_ipc.cpp"),
+}
+CPP_BIN_DIR = os.path.join(ROOT, "tests", "cpp", "build")
+CPP_TEST_BIN = os.path.join(CPP_BIN_DIR, "test_dropin")
 
 
 def build_cpp_tests() -> str:
     """The reference's hot-path unit tests restated against the C++ drop-in
-    header (include/sparsim_b200.hpp), linked against the in-tree library."""
+    header (include/sparsim_b200.hpp), and the n-process C++ host of the
+    peer exchange, linked against the in-tree library."""
     build()
-    os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
-    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), CPP_TEST_SRC,
-                    "-L", LIBDIR, "-lmicro_b200", "-Wl,-rpath,$ORIGIN/../../../paper_2310_00967_b200/lib", "-o", CPP_TEST_BIN], check=True)
+    os.makedirs(CPP_BIN_DIR, exist_ok=True)
+    for name, src in CPP_TESTS.items():
+        subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), src,
+                        "-L", LIBDIR, "-lmicro_b200", "-pthread",
+                        "-Wl,-rpath,$ORIGIN/../../../paper_2310_00967_b200/lib",
+                        "-o", os.path.join(CPP_BIN_DIR, name)], check=True)
     return CPP_TEST_BIN

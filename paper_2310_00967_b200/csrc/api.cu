@@ -745,6 +745,7 @@ int micro_ctx_destroy(micro_ctx* c) {
   DeviceGuard dg(c->dev);
   cudaStreamSynchronize(c->stream);
   if (c->aux) cudaStreamSynchronize(c->aux);
+  nccl_release(c);
   for (void* p : c->peer_opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->allocs) cudaFree(p);
   for (cudaEvent_t ev : c->t_ev) cudaEventDestroy(ev);
@@ -813,9 +814,13 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
 int micro_aggregate(micro_ctx* c) {
   TRY(check_ctx(c));
   TRY(check_poison(c));
-  if (!c->cluster)
-    return fail(MICRO_ELOGIC, "micro_aggregate: multi-rank context; use the micro_dist_* protocol");
   if (!c->compressed) return fail(MICRO_ELOGIC, "micro_aggregate without a preceding micro_compress");
+  if (!c->cluster) {
+    if (c->nccl_comm) return nccl_aggregate(c);
+    return fail(MICRO_ELOGIC,
+                "micro_aggregate: multi-rank context without NCCL attached; use micro_dist_attach_nccl, "
+                "or the micro_dist_* / micro_peer_* protocol");
+  }
   DeviceGuard dg(c->dev);
   return c->esz == 4 ? aggregate_cluster<float>(c) : aggregate_cluster<double>(c);
 }

@@ -6,74 +6,124 @@
 using namespace micro;
 using namespace micro::host;
 
+namespace micro {
+namespace host {
+
+int dist_ensure_buffers(micro_ctx* c) {
+  if (c->dist_all_counts) return MICRO_OK;
+  const size_t nk = (size_t)c->n * c->sel_cap;
+  TRY(c->alloc((void**)&c->dist_all_counts, sizeof(long long) * c->n));
+  TRY(c->alloc((void**)&c->dist_all_idx, 4 * nk));
+  TRY(c->alloc(&c->dist_send, c->esz * nk));
+  if (!c->recv) TRY(c->alloc(&c->recv, c->esz * nk));
+  TRY(c->alloc(&c->dist_own_sums, c->esz * c->sel_cap));
+  TRY(c->alloc(&c->dist_all_sums, c->esz * nk));
+  CU(cudaMemsetAsync(c->dist_all_counts, 0, sizeof(long long) * c->n, c->stream));
+  return MICRO_OK;
+}
+
+}  // namespace host
+}  // namespace micro
+
 extern "C" {
 
-static int dist_counts(micro_ctx* c, const int64_t* h_counts, Counts* out, bool own_segments) {
-  if (!h_counts) return fail(MICRO_EINVAL, "null counts");
-  long long off = 0;
-  const int me = c->cfg.rank;
-  for (int r = 0; r < c->n; ++r) {
-    if (h_counts[r] < 0) return fail(MICRO_EINVAL, "negative count");
-    out->k[r] = h_counts[r];
-    out->off[r] = off;
-    // send layout: segment o has k_o values (o != me); recv layout: segment r has k_me values
-    if (r != me) off += own_segments ? h_counts[me] : h_counts[r];
-  }
+// ---- the collective protocol's device halves (fixed stride, device counts) ----
+
+static int check_dist_ctx(micro_ctx* c, const char* what) {
+  TRY(check_ctx(c));
+  TRY(check_poison(c));
+  if (c->cluster) return fail(MICRO_ELOGIC, "%s: context is a single-device cluster", what);
+  if (!c->compressed) return fail(MICRO_ELOGIC, "%s before micro_compress", what);
   return MICRO_OK;
 }
 
-int micro_dist_gather_foreign(micro_ctx* c, const int32_t* d_all_idx, const int64_t* h_counts,
-                              int64_t kmax, void* d_send) {
+// grid rows sized for the expected selection (the kernels read the real count)
+static unsigned dist_grid_x(micro_ctx* c) {
+  return grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev) / 4 + 1;
+}
+
+int micro_dist_buffers(micro_ctx* c, micro_dist_bufs* b) {
   TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
-  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_gather_foreign before micro_compress");
-  Counts cs{};
-  TRY(dist_counts(c, h_counts, &cs, false));
+  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_buffers: context is a single-device cluster");
+  if (!b) return fail(MICRO_EINVAL, "null buffer descriptor");
   DeviceGuard dg(c->dev);
-  long long mx = 0;
-  for (int r = 0; r < c->n; ++r) mx = std::max<long long>(mx, cs.k[r]);
-  if (mx > kmax) return fail(MICRO_EINVAL, "kmax %lld smaller than a count %lld", (long long)kmax, mx);
-  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
+  TRY(dist_ensure_buffers(c));
+  b->kcap = c->sel_cap;
+  b->own_count = (const int64_t*)c->counts;
+  b->own_idx = c->sel_idx[0][0];  // single-buffered at n > 1
+  b->all_counts = (int64_t*)c->dist_all_counts;
+  b->all_idx = c->dist_all_idx;
+  b->send = c->dist_send;
+  b->recv = c->recv;
+  b->own_sums = c->dist_own_sums;
+  b->all_sums = c->dist_all_sums;
+  return MICRO_OK;
+}
+
+int micro_dist_gather_foreign(micro_ctx* c) {
+  TRY(check_dist_ctx(c, "micro_dist_gather_foreign"));
+  DeviceGuard dg(c->dev);
+  TRY(dist_ensure_buffers(c));
+  const dim3 grid(dist_grid_x(c), c->n);
   NormSlot* corr = c->norm ? c->norm_slot : nullptr;
+  const int me = c->cfg.rank;
+  const long long* cnt = c->dist_all_counts;
   if (c->esz == 4) {
     if (c->cfg.error_feedback)
-      k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                      (float*)c->resid[0], (float*)d_send, corr);
+      k_dist_gather_foreign<float, true><<<grid, 256, 0, c->stream>>>(c->dist_all_idx, cnt, c->sel_cap, me,
+                                                                      (float*)c->resid[0], (float*)c->dist_send, corr);
     else
-      k_dist_gather_foreign<float, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                       (float*)c->resid[0], (float*)d_send, corr);
+      k_dist_gather_foreign<float, false><<<grid, 256, 0, c->stream>>>(c->dist_all_idx, cnt, c->sel_cap, me,
+                                                                       (float*)c->resid[0], (float*)c->dist_send, corr);
   } else {
     if (c->cfg.error_feedback)
-      k_dist_gather_foreign<double, true><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                       (double*)c->resid[0], (double*)d_send, corr);
+      k_dist_gather_foreign<double, true><<<grid, 256, 0, c->stream>>>(c->dist_all_idx, cnt, c->sel_cap, me,
+                                                                       (double*)c->resid[0], (double*)c->dist_send, corr);
     else
-      k_dist_gather_foreign<double, false><<<grid, 256, 0, c->stream>>>(d_all_idx, kmax, cs, c->cfg.rank,
-                                                                        (double*)c->resid[0], (double*)d_send, corr);
+      k_dist_gather_foreign<double, false><<<grid, 256, 0, c->stream>>>(c->dist_all_idx, cnt, c->sel_cap, me,
+                                                                        (double*)c->resid[0], (double*)c->dist_send, corr);
   }
   CU(cudaGetLastError());
   return MICRO_OK;
 }
 
-int micro_dist_owner_reduce(micro_ctx* c, const void* d_recv, const int64_t* h_counts, void* d_own_sums) {
-  TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
-  Counts cs{};
-  TRY(dist_counts(c, h_counts, &cs, true));
+int micro_dist_owner_reduce(micro_ctx* c) {
+  TRY(check_dist_ctx(c, "micro_dist_owner_reduce"));
   DeviceGuard dg(c->dev);
+  TRY(dist_ensure_buffers(c));
+  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
   const int me = c->cfg.rank;
-  const long long k = cs.k[me];
-  const unsigned grid = grid_for(k, c->dev);
   if (c->esz == 4)
-    k_dist_owner_reduce<float><<<grid, 256, 0, c->stream>>>((const float*)c->sel_val[c->buf][0], k,
-                                                            (const float*)d_recv, cs, c->n, me, (float*)d_own_sums);
+    k_dist_owner_reduce<float><<<grid, 256, 0, c->stream>>>((const float*)c->sel_val[c->buf][0], c->dist_all_counts,
+                                                            (const float*)c->recv, c->sel_cap, c->n, me,
+                                                            (float*)c->dist_own_sums);
   else
-    k_dist_owner_reduce<double><<<grid, 256, 0, c->stream>>>((const double*)c->sel_val[c->buf][0], k,
-                                                             (const double*)d_recv, cs, c->n, me,
-                                                             (double*)d_own_sums);
+    k_dist_owner_reduce<double><<<grid, 256, 0, c->stream>>>((const double*)c->sel_val[c->buf][0], c->dist_all_counts,
+                                                             (const double*)c->recv, c->sel_cap, c->n, me,
+                                                             (double*)c->dist_own_sums);
   CU(cudaGetLastError());
   return MICRO_OK;
+}
+
+int micro_dist_finalize(micro_ctx* c) {
+  TRY(check_dist_ctx(c, "micro_dist_finalize"));
+  DeviceGuard dg(c->dev);
+  TRY(dist_ensure_buffers(c));
+  const dim3 grid(dist_grid_x(c), c->n);
+  if (c->esz == 4) {
+    k_dist_build_union<float><<<grid, 256, 0, c->stream>>>(c->dist_all_idx, (const float*)c->dist_all_sums,
+                                                           c->dist_all_counts, c->sel_cap, c->n, c->t_cur,
+                                                           c->uni_idx[c->buf], (float*)c->uni_sum[c->buf],
+                                                           c->Kbuf + c->buf);
+    CU(cudaGetLastError());
+    return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
+  }
+  k_dist_build_union<double><<<grid, 256, 0, c->stream>>>(c->dist_all_idx, (const double*)c->dist_all_sums,
+                                                          c->dist_all_counts, c->sel_cap, c->n, c->t_cur,
+                                                          c->uni_idx[c->buf], (double*)c->uni_sum[c->buf],
+                                                          c->Kbuf + c->buf);
+  CU(cudaGetLastError());
+  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
 }
 
 // ---- peer-memory exchange (peer.cuh) ------------------------------------
@@ -258,36 +308,6 @@ int micro_peer_finalize(micro_ctx* c) {
   DeviceGuard dg(c->dev);
   c->peer_phase = 0;
   if (c->esz == 4) return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-  return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-}
-
-int micro_dist_finalize(micro_ctx* c, const int32_t* d_all_idx, const void* d_all_sums,
-                        const int64_t* h_counts, int64_t kmax) {
-  TRY(check_ctx(c));
-  TRY(check_poison(c));
-  if (c->cluster) return fail(MICRO_ELOGIC, "micro_dist_*: context is a single-device cluster");
-  if (!c->compressed) return fail(MICRO_ELOGIC, "micro_dist_finalize before micro_compress");
-  Counts cs{};
-  TRY(dist_counts(c, h_counts, &cs, false));
-  long long K = 0, mx = 0;
-  for (int r = 0; r < c->n; ++r) {
-    K += cs.k[r];
-    mx = std::max<long long>(mx, cs.k[r]);
-  }
-  if (K > c->uni_cap) return fail(MICRO_ECAPACITY, "union %lld exceeds capacity %lld", K, (long long)c->uni_cap);
-  DeviceGuard dg(c->dev);
-  const dim3 grid(grid_for(mx, c->dev) / 4 + 1, c->n);
-  if (c->esz == 4) {
-    k_dist_build_union<float><<<grid, 256, 0, c->stream>>>(d_all_idx, (const float*)d_all_sums, kmax, cs, c->n,
-                                                           c->t_cur, c->uni_idx[c->buf],
-                                                           (float*)c->uni_sum[c->buf], c->Kbuf + c->buf);
-    CU(cudaGetLastError());
-    return launch_finalize<float>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
-  }
-  k_dist_build_union<double><<<grid, 256, 0, c->stream>>>(d_all_idx, (const double*)d_all_sums, kmax, cs, c->n,
-                                                          c->t_cur, c->uni_idx[c->buf],
-                                                          (double*)c->uni_sum[c->buf], c->Kbuf + c->buf);
-  CU(cudaGetLastError());
   return launch_finalize<double>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 0);
 }
 

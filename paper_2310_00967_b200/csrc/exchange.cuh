@@ -21,11 +21,6 @@ struct WorkerPtrs {
   void* resid[kMaxWorkers];
 };
 
-struct Counts {
-  long long k[kMaxWorkers];    // per worker (rank order)
-  long long off[kMaxWorkers];  // per worker: segment offset in a packed buffer
-};
-
 // Single-device cluster, n > 1: one block row per partition p; the owner's
 // own value comes from its K1 pairs (its residual entry is already zeroed),
 // every other worker's from its accumulator, summed in worker order.
@@ -104,18 +99,25 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
   }
 }
 
-// One rank: gather own accumulator at every OTHER owner's indices into the
-// send buffer (segment per destination, rank order) and zero them.
+// ---- one rank of an n-GPU job: the collective protocol's device halves ----
+// Buffers have a fixed stride kcap (the selection capacity) per rank, and
+// every count is read from device memory (the all-gathered k_r), so the host
+// never reads a count: the protocol is stream-ordered end to end (the NCCL
+// calls of nccl_api.cu, or torch.distributed in dist.py, move the buffers).
+
+// K4: gather own acc at every OTHER owner's indices into send[o][kcap] and
+// zero them there (harness.cpp:219-221).
 template <typename T, bool kZero>
-__global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_idx, int64_t kmax,
-                                                             Counts c, int me, T* resid, T* send,
+__global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_idx, const long long* all_counts,
+                                                             long long kcap, int me, T* resid, T* send,
                                                              NormSlot* sq_corr) {
   __shared__ double s_corr[8];
   const int o = blockIdx.y;
   if (o == me) return;  // block-uniform
-  const long long k = c.k[o];
-  const int32_t* __restrict__ idx = all_idx + (int64_t)o * kmax;
-  T* __restrict__ out = send + c.off[o];
+  pdl_wait();
+  const long long k = clamp_count(all_counts[o], kcap);
+  const int32_t* __restrict__ idx = all_idx + (int64_t)o * kcap;
+  T* __restrict__ out = send + (int64_t)o * kcap;
   double q = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 4 * stride) {
@@ -149,40 +151,43 @@ __global__ void __launch_bounds__(256) k_dist_gather_foreign(const int32_t* all_
   }
 }
 
-// One rank, as owner: s = 0; for r in rank order: s += contribution_r.
+// K6: as owner, s = 0; for r in rank order: s += contribution_r (recv[r][kcap];
+// its own value from the K1 pairs).
 template <typename T>
-__global__ void __launch_bounds__(256) k_dist_owner_reduce(const T* own_val, long long k_own,
-                                                           const T* recv, Counts c, int n, int me,
-                                                           T* sums) {
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k_own;
+__global__ void __launch_bounds__(256) k_dist_owner_reduce(const T* own_val, const long long* all_counts,
+                                                           const T* recv, long long kcap, int n, int me, T* sums) {
+  pdl_wait();
+  const long long k = clamp_count(all_counts[me], kcap);
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
        m += (long long)gridDim.x * blockDim.x) {
     T s = (T)0;
-    for (int r = 0; r < n; ++r) s = add_rn(s, r == me ? own_val[m] : recv[c.off[r] + m]);
+    for (int r = 0; r < n; ++r) s = add_rn(s, r == me ? own_val[m] : recv[(int64_t)r * kcap + m]);
     sums[m] = s;
   }
 }
 
-// One rank: lay the gathered (index, sum) lists out as the union in
-// partition order.
+// K8: lay the all-gathered (index, sum) lists out as the union in partition
+// order; K = sum of the (clamped) counts.
 template <typename T>
 __global__ void __launch_bounds__(256) k_dist_build_union(const int32_t* all_idx, const T* all_sums,
-                                                          int64_t kmax, Counts c, int n, int64_t t,
-                                                          int32_t* union_idx, T* union_sum,
+                                                          const long long* all_counts, long long kcap, int n,
+                                                          int64_t t, int32_t* union_idx, T* union_sum,
                                                           long long* K_out) {
+  pdl_wait();
   const int p = blockIdx.y;
   const int owner = partition_owner(p, n, t);
   long long off = 0, K = 0;
   for (int q = 0; q < n; ++q) {
-    const long long kq = c.k[partition_owner(q, n, t)];
+    const long long kq = clamp_count(all_counts[partition_owner(q, n, t)], kcap);
     if (q < p) off += kq;
     K += kq;
   }
   if (p == 0 && blockIdx.x == 0 && threadIdx.x == 0) *K_out = K;
-  const long long k = c.k[owner];
+  const long long k = clamp_count(all_counts[owner], kcap);
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k;
        m += (long long)gridDim.x * blockDim.x) {
-    union_idx[off + m] = all_idx[(int64_t)owner * kmax + m];
-    union_sum[off + m] = all_sums[(int64_t)owner * kmax + m];
+    union_idx[off + m] = all_idx[(int64_t)owner * kcap + m];
+    union_sum[off + m] = all_sums[(int64_t)owner * kcap + m];
   }
 }
 

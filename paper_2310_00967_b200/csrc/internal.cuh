@@ -207,9 +207,20 @@ struct micro_ctx {
   micro::NormSlot* peer_corr[micro::kMaxWorkers] = {};
   const int32_t* peer_sel[2][micro::kMaxWorkers] = {};
   void* peer_recv[micro::kMaxWorkers] = {};
-  void* recv = nullptr;          // bulk exchange: receive slabs [source rank][sel_cap] (lazy)
+  void* recv = nullptr;          // bulk exchange / collective protocol: receive slabs [source rank][sel_cap] (lazy)
+  // the collective protocol (micro_dist_*, nccl_api.cu): fixed stride sel_cap per rank (lazy)
+  long long* dist_all_counts = nullptr;  // [n]
+  int32_t* dist_all_idx = nullptr;       // [n][sel_cap]
+  void* dist_send = nullptr;             // [n][sel_cap]: segment o -> owner o
+  void* dist_own_sums = nullptr;         // [sel_cap]
+  void* dist_all_sums = nullptr;         // [n][sel_cap]
   int peer_phase = 0;            // 0 idle, 1 contributed (bulk), 2 exchanged (ready to finalize)
   cudaEvent_t group_ev = nullptr;  // micro_group_step barriers (one process, all ranks)
+  // NCCL attached (nccl_api.cu): micro_aggregate runs the n-GPU exchange
+  void* nccl_comm = nullptr;     // ncclComm_t
+  bool nccl_owned = false;       // made by micro_dist_init_nccl: destroyed with the context
+  int xchg = 0;                  // MICRO_XCHG_PEER / MICRO_XCHG_NCCL
+  int* nccl_bar = nullptr;       // 4-byte barrier all-reduce buffer
   std::vector<void*> peer_opened;  // cudaIpcOpenMemHandle mappings to close
 
   int alloc(void** p, size_t bytes) {
@@ -230,6 +241,9 @@ inline int norm_mode(const micro_ctx* c) { return !c->cfg.error_feedback ? 2 : c
 int check_ctx(micro_ctx* c);
 int check_poison(micro_ctx* c);
 int ensure_staging(micro_ctx* c);
+int dist_ensure_buffers(micro_ctx* c);
+int nccl_aggregate(micro_ctx* c);  // nccl_api.cu
+void nccl_release(micro_ctx* c);
 int read_flags(micro_ctx* c, int* flags);
 // word offsets of a union bitmap: off[w] = popcount of words [0, w) (scan.cuh);
 // `tiles` holds scan_tiles(nwords) ints of scratch

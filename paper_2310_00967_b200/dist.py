@@ -34,90 +34,84 @@ from ._lib import check, lib
 from .engine import Micro, device_view
 
 
-def exchange(ops, group=None, comm_device=None) -> int:
-    """Run K2..K8 for one rank after ops' compress.  Returns |union|.
+def exchange(ops, group=None, comm_device=None) -> None:
+    """Run K2..K8 for one rank after ops' compress (include/micro.h, the
+    collective protocol): every buffer has the fixed stride ``ops.kcap`` and
+    every count stays on the device, so nothing here waits for the GPU — the
+    same protocol nccl_api.cu runs behind the C ABI with NCCL calls.
 
     Collectives run on ``ops.device`` tensors (NCCL).  ``comm_device`` (e.g.
     ``"cpu"`` with gloo) stages them through another device instead — used to
     run several ranks' device halves on one GPU in tests."""
-    n = dist.get_world_size(group)
-    me = dist.get_rank(group)
     dev = ops.device
     cdev = torch.device(comm_device) if comm_device is not None else dev
+    b = ops.buffers()
 
-    def to_c(t):
-        return t if t.device == cdev else t.to(cdev)
+    def all_gather(dst, src):
+        if cdev == dev:
+            dist.all_gather_into_tensor(dst, src, group=group)
+        else:
+            out = torch.empty(dst.numel(), dtype=dst.dtype, device=cdev)
+            dist.all_gather_into_tensor(out, src.to(cdev), group=group)
+            dst.copy_(out)
 
-    def to_d(t):
-        return t if t.device == dev else t.to(dev)
+    def all_to_all(dst, src):  # equal splits: kcap values per pair
+        if cdev == dev:
+            dist.all_to_all_single(dst, src, group=group)
+        else:
+            out = torch.empty(dst.numel(), dtype=dst.dtype, device=cdev)
+            dist.all_to_all_single(out, src.to(cdev), group=group)
+            dst.copy_(out)
 
-    cnt = torch.empty(n, dtype=torch.int64, device=cdev)
-    dist.all_gather_into_tensor(cnt, to_c(ops.own_count()), group=group)      # K2
-    counts = [int(v) for v in cnt.cpu().tolist()]
-    kmax = max(counts)
-    if kmax > ops.capacity:  # every rank sees the same counts, so every rank raises
-        raise _lib.CapacityError(_lib.MICRO_ECAPACITY,
-                                 f"selection of {kmax} exceeds capacity {ops.capacity} on some rank")
-    if kmax == 0:
-        ops.finalize(None, None, counts, 0)
-        return 0
-    all_idx = torch.empty(n * kmax, dtype=torch.int32, device=cdev)
-    dist.all_gather_into_tensor(all_idx, to_c(ops.own_indices(kmax)), group=group)  # K3
-    all_idx = to_d(all_idx)
-    send = to_c(ops.gather_foreign(all_idx, counts, kmax))                     # K4
-    recv = torch.empty((n - 1) * counts[me], dtype=ops.dtype, device=cdev)
-    dist.all_to_all_single(recv, send,                                          # K5
-                           output_split_sizes=[0 if r == me else counts[me] for r in range(n)],
-                           input_split_sizes=[0 if o == me else counts[o] for o in range(n)],
-                           group=group)
-    own_sums = to_c(ops.owner_reduce(to_d(recv), counts, kmax))                # K6
-    all_sums = torch.empty(n * kmax, dtype=ops.dtype, device=cdev)
-    dist.all_gather_into_tensor(all_sums, own_sums, group=group)               # K7
-    ops.finalize(all_idx, to_d(all_sums), counts, kmax)                         # K8
-    return sum(counts)
+    all_gather(b["all_counts"], b["own_count"])   # K2
+    all_gather(b["all_idx"], b["own_idx"])        # K3
+    ops.gather_foreign()                           # K4
+    all_to_all(b["recv"], b["send"])              # K5
+    ops.owner_reduce()                             # K6
+    all_gather(b["all_sums"], b["own_sums"])      # K7
+    ops.finalize()                                 # K8
 
 
 class DeviceOps:
-    """Binds :func:`exchange` to one rank's `micro_ctx` (n_local == 1)."""
+    """Binds :func:`exchange` to one rank's `micro_ctx` (n_local == 1): the
+    library's exchange buffers as torch views, and its device halves."""
 
     def __init__(self, m: Micro):
         self.m = m
         self.device, self.dtype = m.device, m.dtype
-        self.capacity = m.selection_capacity
+        bd = _lib.micro_dist_bufs()
+        check(lib().micro_dist_buffers(m.handle, C.byref(bd)))
+        self.kcap = kc = int(bd.kcap)
+        n, dev, dt = m.n, m.device, m.dtype
+        self._b = {"own_count": device_view(bd.own_count, 1, torch.int64, dev),
+                   "own_idx": device_view(bd.own_idx, kc, torch.int32, dev),
+                   "all_counts": device_view(bd.all_counts, n, torch.int64, dev),
+                   "all_idx": device_view(bd.all_idx, n * kc, torch.int32, dev),
+                   "send": device_view(bd.send, n * kc, dt, dev),
+                   "recv": device_view(bd.recv, n * kc, dt, dev),
+                   "own_sums": device_view(bd.own_sums, kc, dt, dev),
+                   "all_sums": device_view(bd.all_sums, n * kc, dt, dev)}
 
-    def own_count(self) -> torch.Tensor:
-        _, _, cnt = self.m.selection_device(0)
-        return cnt
+    def buffers(self) -> dict:
+        return self._b
 
-    def own_indices(self, kmax: int) -> torch.Tensor:
-        pi, _, _ = self.m.selection_device(0)
-        return device_view(pi, kmax, torch.int32, self.device)  # kmax <= selection capacity
+    def gather_foreign(self):
+        check(lib().micro_dist_gather_foreign(self.m.handle))
 
-    def gather_foreign(self, all_idx, counts, kmax):
-        me = self.m.rank
-        send = torch.empty(max(sum(counts) - counts[me], 1), dtype=self.dtype, device=self.device)
-        hc = (C.c_int64 * len(counts))(*counts)
-        check(lib().micro_dist_gather_foreign(self.m.handle, C.c_void_p(all_idx.data_ptr()), hc, kmax,
-                                              C.c_void_p(send.data_ptr())))
-        return send[: sum(counts) - counts[me]]
+    def owner_reduce(self):
+        check(lib().micro_dist_owner_reduce(self.m.handle))
 
-    def owner_reduce(self, recv, counts, kmax):
-        out = torch.zeros(kmax, dtype=self.dtype, device=self.device)
-        hc = (C.c_int64 * len(counts))(*counts)
-        check(lib().micro_dist_owner_reduce(self.m.handle, C.c_void_p(recv.data_ptr() if recv.numel() else 0), hc,
-                                            C.c_void_p(out.data_ptr())))
-        return out
-
-    def finalize(self, all_idx, all_sums, counts, kmax):
-        hc = (C.c_int64 * len(counts))(*counts)
-        check(lib().micro_dist_finalize(self.m.handle, C.c_void_p(all_idx.data_ptr() if all_idx is not None else 0),
-                                        C.c_void_p(all_sums.data_ptr() if all_sums is not None else 0), hc, kmax))
+    def finalize(self):
+        check(lib().micro_dist_finalize(self.m.handle))
 
 
 class DistMicro:
     """One rank's MiCRO engine; same calls as :class:`engine.Micro`.
 
-    ``transport="nccl"``: the protocol above (NCCL moves the data).
+    ``transport="nccl"``: the protocol above (NCCL moves the data, through
+    torch.distributed).  ``"abi_peer"`` / ``"abi_nccl"``: the same exchanges
+    run entirely inside the library over its own NCCL communicator
+    (micro_dist_init_nccl + micro_aggregate — what a C++ host calls).
     ``transport="peer"``: two kernels per rank over peer memory with every
     NVLink transfer contiguous (micro_peer_contribute / _reduce,
     csrc/peer.cuh) between barriers; ``"peer_pull"``: one kernel whose owners
@@ -129,16 +123,27 @@ class DistMicro:
     def __init__(self, n_g: int, group=None, comm_device=None, transport: str = "nccl", **kw):
         if not dist.is_initialized():
             raise _lib.LogicError(_lib.MICRO_ELOGIC, "torch.distributed is not initialized")
-        if transport not in ("nccl", "peer", "peer_pull"):
+        if transport not in ("nccl", "peer", "peer_pull", "abi_peer", "abi_nccl"):
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unknown transport {transport!r}")
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.m = Micro(n_g, self.world, n_local=1, rank=self.rank, **kw)
-        self.ops = DeviceOps(self.m)
+        self.ops = DeviceOps(self.m) if transport == "nccl" else None
         self.n_g = n_g
         self.comm_device = comm_device
         self.transport = transport
+        if transport in ("abi_peer", "abi_nccl"):
+            # the library's own NCCL communicator (micro_dist_init_nccl): rank 0's
+            # unique id travels over this process group once
+            uid = C.create_string_buffer(_lib.MICRO_NCCL_UNIQUE_ID_BYTES)
+            if self.rank == 0:
+                check(lib().micro_nccl_unique_id(uid))
+            obj = [uid.raw]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            uid = C.create_string_buffer(obj[0], _lib.MICRO_NCCL_UNIQUE_ID_BYTES)
+            check(lib().micro_dist_init_nccl(self.m.handle, uid,
+                                             _lib.MICRO_XCHG_PEER if transport == "abi_peer" else _lib.MICRO_XCHG_NCCL))
         if transport in ("peer", "peer_pull"):
             self._bar = torch.zeros(1, dtype=torch.int32, device=self.m.device)
             ok, why = True, ""
@@ -159,6 +164,7 @@ class DistMicro:
                 warnings.warn(f"peer-memory exchange unavailable on some rank ({why or 'remote failure'}); "
                               "falling back to the NCCL protocol")
                 self.transport = "nccl"
+                self.ops = DeviceOps(self.m)
 
     def _barrier(self):
         if self.comm_device is not None:  # host barrier (gloo): the stream's work is done first
@@ -193,9 +199,8 @@ class DistMicro:
         parts.append((a, b))
         return r
 
-    def aggregate(self) -> int | None:
-        """NCCL transport: returns |union| (known on the host).  Peer
-        transport: asynchronous, returns None (``query().K`` has it)."""
+    def aggregate(self) -> None:
+        """Asynchronous for every transport (``query().K`` has |union|)."""
         parts = []
         if getattr(self, "_xt", None) is not None:
             self._xt.append(parts)
@@ -214,9 +219,14 @@ class DistMicro:
             self._barrier()
             check(lib().micro_peer_finalize(h))
             return None
-        return self._timed(parts, lambda: exchange(self.ops, self.group, self.comm_device))
+        if self.transport in ("abi_peer", "abi_nccl"):  # the C ABI runs it (nccl_api.cu)
+            self._timed(parts, lambda: check(lib().micro_aggregate(h)))
+            return None
+        with torch.cuda.stream(self.m.stream):  # the collectives ordered with the library's kernels
+            self._timed(parts, lambda: exchange(self.ops, self.group, self.comm_device))
+        return None
 
-    def step(self, grads, eta: float, t: int) -> int | None:
+    def step(self, grads, eta: float, t: int) -> None:
         self.compress(grads, eta, t)
         return self.aggregate()
 

@@ -15,17 +15,25 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 class OracleOps:
-    """numpy stand-in for DeviceOps (one rank): same contract, CPU tensors."""
+    """numpy stand-in for DeviceOps (one rank): the same buffer contract
+    (fixed stride kcap, counts in the buffers), CPU tensors."""
 
     device = torch.device("cpu")
     dtype = torch.float32
-    capacity = 1 << 40
 
     def __init__(self, o, n_g, n, rank, d, delta0, alpha=0.01, eps=1e-12, ef=True):
         self.o, self.n_g, self.n, self.rank = o, n_g, n, rank
         self.e = np.zeros(n_g, np.float32)
         self.delta, self.alpha, self.eps, self.ef = delta0, alpha, eps, ef
         self.k_w = o.per_worker_target_count(d, n_g, n)
+        self.kcap = kc = -(-n_g // n)  # the partition size (never overflows)
+        self.b = {"own_count": torch.zeros(1, dtype=torch.int64), "own_idx": torch.zeros(kc, dtype=torch.int32),
+                  "all_counts": torch.zeros(n, dtype=torch.int64), "all_idx": torch.zeros(n * kc, dtype=torch.int32),
+                  "send": torch.zeros(n * kc), "recv": torch.zeros(n * kc), "own_sums": torch.zeros(kc),
+                  "all_sums": torch.zeros(n * kc)}
+
+    def buffers(self):
+        return self.b
 
     def compress(self, G, eta, t):
         acc = self.e + np.float32(eta) * G
@@ -34,52 +42,39 @@ class OracleOps:
         if self.ef:
             acc[self.idx] = 0
         self.e, self.t = acc, t
+        self.b["own_count"][0] = self.idx.size
+        self.b["own_idx"][: self.idx.size] = torch.from_numpy(self.idx.astype(np.int32))
 
-    def own_count(self):
-        return torch.tensor([self.idx.size], dtype=torch.int64)
-
-    def own_indices(self, kmax):
-        out = np.zeros(kmax, np.int32)
-        out[: self.idx.size] = self.idx
-        return torch.from_numpy(out)
-
-    def gather_foreign(self, all_idx, counts, kmax):
-        a = all_idx.numpy()
-        parts = []
+    def gather_foreign(self):
+        a, cnt, kc = self.b["all_idx"].numpy(), self.b["all_counts"].numpy(), self.kcap
+        send = self.b["send"].numpy()
         for o in range(self.n):
             if o == self.rank:
                 continue
-            j = a[o * kmax:o * kmax + counts[o]]
-            parts.append(self.e[j].copy())
+            j = a[o * kc:o * kc + cnt[o]]
+            send[o * kc:o * kc + cnt[o]] = self.e[j]
             if self.ef:
                 self.e[j] = 0
-        return torch.from_numpy(np.concatenate(parts) if parts else np.zeros(0, np.float32))
 
-    def owner_reduce(self, recv, counts, kmax):
-        r_ = recv.numpy()
-        k = counts[self.rank]
+    def owner_reduce(self):
+        r_, kc = self.b["recv"].numpy(), self.kcap
+        k = int(self.b["all_counts"][self.rank])
         s = np.zeros(k, np.float32)
-        seg = 0
         for r in range(self.n):
-            if r == self.rank:
-                s = s + self.val
-            else:
-                s = s + r_[seg:seg + k]
-                seg += k
-        out = np.zeros(kmax, np.float32)
-        out[:k] = s
-        return torch.from_numpy(out)
+            s = s + (self.val if r == self.rank else r_[r * kc:r * kc + k])
+        self.b["own_sums"].numpy()[:k] = s
 
-    def finalize(self, all_idx, all_sums, counts, kmax):
+    def finalize(self):
+        cnt, kc = self.b["all_counts"].numpy(), self.kcap
+        ai, asum = self.b["all_idx"].numpy(), self.b["all_sums"].numpy()
         ui, us = [], []
         for p in range(self.n):
             o = (p - self.t % self.n) % self.n
-            if kmax:
-                ui.append(all_idx.numpy()[o * kmax:o * kmax + counts[o]])
-                us.append(all_sums.numpy()[o * kmax:o * kmax + counts[o]])
-        self.union_idx = np.concatenate(ui) if ui else np.zeros(0, np.int32)
-        self.union_sum = np.concatenate(us) if us else np.zeros(0, np.float32)
-        self.delta = self.o.update_threshold(self.delta, self.k_w, counts[self.rank], self.alpha, self.eps)
+            ui.append(ai[o * kc:o * kc + cnt[o]])
+            us.append(asum[o * kc:o * kc + cnt[o]])
+        self.union_idx = np.concatenate(ui)
+        self.union_sum = np.concatenate(us)
+        self.delta = self.o.update_threshold(self.delta, self.k_w, int(cnt[self.rank]), self.alpha, self.eps)
         if not self.ef:
             self.e[:] = 0
 
@@ -100,9 +95,9 @@ def _worker(rank, world, port, n_g, iters, ef, q):
     for t in range(iters):
         G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)])
         ops.compress(G[rank], eta, t)
-        K = exchange(ops)
+        exchange(ops)
         r = ref.step(G, eta, t)
-        if K != r["union_idx"].size or not np.array_equal(ops.union_idx, r["union_idx"]):
+        if not np.array_equal(ops.union_idx, r["union_idx"]):
             bad.append((t, "union"))
         if not np.array_equal(ops.union_sum, r["union_sum"]):
             bad.append((t, "sums"))
