@@ -240,6 +240,10 @@ int launch_sumsq(micro_ctx* c, int i) {
   return MICRO_OK;
 }
 
+// Steps whose streamed bytes (e, G read; e written) stay below this prefetch
+// the model's selected lines during k1_stream (C1: 140 MB; C3: 1.66 GB does not).
+constexpr int64_t kPrefetchStepBytes = 256ll << 20;
+
 template <typename T>
 int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe,
                      const double* thr = nullptr, const long long* tie = nullptr, bool acc_in_e = false) {
@@ -264,6 +268,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   a.super_counts = c->super_counts + c->super_par * kMaxSupers;
   a.super_runs = c->super_runs;
   a.sq_part = c->norm_part;
+  a.model = c->model;
   const int units = (int)((c->n_g + UE - 1) / UE);
   const unsigned grid = (unsigned)((units + kStreamWarps - 1) / kStreamWarps);
   const bool fd = c->dense_fused;
@@ -291,7 +296,16 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
       if (c->cfg.error_feedback) K1N(false);
       else K1S(kWriteAcc, false);
     } else if (c->cfg.error_feedback) {
-      if (fd) K1N(true);
+      // small steps: prefetch x's selected lines into L2 for k1_gather's update
+      const bool pf = c->model && (int64_t)c->n_g * (int64_t)c->esz * 3 <= kPrefetchStepBytes;
+      if (pf) {
+#define K1P(D, N) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, N, false, false, true>, dim3(g), dim3(kStreamThreads), st, a))
+        if (fd && c->norm) K1P(true, true);
+        else if (fd) K1P(true, false);
+        else if (c->norm) K1P(false, true);
+        else K1P(false, false);
+#undef K1P
+      } else if (fd) K1N(true);
       else K1N(false);
     } else {
       if (fd) K1S(kWriteNone, true);
@@ -492,14 +506,20 @@ int aggregate_cluster(micro_ctx* c) {
   const int64_t expect = std::max<int64_t>((int64_t)c->k_worker * 3 / 2, 256);
   const unsigned gx = (unsigned)std::min<int64_t>((expect + 255) / 256, 2048);
   const dim3 grid(gx, (unsigned)c->n);
-  if (c->cfg.error_feedback)
-    CU(launch_pdl(k_cluster_reduce<T, true>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
-                        (long long)c->sel_cap, c->n, (int64_t)c->t_cur, c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
-                        c->norm ? c->norm_slot : (NormSlot*)nullptr));
+  const long long* cnt = (const long long*)c->counts;
+  NormSlot* slots = c->norm ? c->norm_slot : (NormSlot*)nullptr;
+  int32_t* ui = c->uni_idx[c->buf];
+  T* us = (T*)c->uni_sum[c->buf];
+  const long long cap = c->sel_cap;
+  if (c->cfg.error_feedback && c->n <= 8)
+    CU(launch_pdl(k_cluster_reduce<T, true, true>, grid, dim3(256), c->stream, w, cnt, cap, c->n, (int64_t)c->t_cur, ui,
+                  us, slots));
+  else if (c->cfg.error_feedback)
+    CU(launch_pdl(k_cluster_reduce<T, true>, grid, dim3(256), c->stream, w, cnt, cap, c->n, (int64_t)c->t_cur, ui, us,
+                  slots));
   else
-    CU(launch_pdl(k_cluster_reduce<T, false>, grid, dim3(256), c->stream, w, (const long long*)c->counts,
-                        (long long)c->sel_cap, c->n, (int64_t)c->t_cur, c->uni_idx[c->buf], (T*)c->uni_sum[c->buf],
-                        (NormSlot*)nullptr));
+    CU(launch_pdl(k_cluster_reduce<T, false>, grid, dim3(256), c->stream, w, cnt, cap, c->n, (int64_t)c->t_cur, ui, us,
+                  (NormSlot*)nullptr));
   CU(cudaGetLastError());
   return launch_finalize<T>(c, c->uni_idx[c->buf], c->uni_sum[c->buf], 1);
 }

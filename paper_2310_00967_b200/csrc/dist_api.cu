@@ -263,7 +263,11 @@ int micro_peer_contribute(micro_ctx* c) {
   if (c->peer_phase) return fail(MICRO_ELOGIC, "micro_peer_contribute called twice");
   DeviceGuard dg(c->dev);
   const PeerBulkPtrs pb = bulk_ptrs(c);
-  const dim3 grid(grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev) / 2 + 1, c->n);
+  // per owner: CTAs of 8 warps x 32 lanes x kPeerILP entries for the expected selection
+  const int64_t expect = std::min<int64_t>((int64_t)c->k_worker * 3 / 2 + 1, c->sel_cap);
+  const int64_t per_cta = 8 * 32 * kPeerILP;
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((expect + per_cta - 1) / per_cta,
+                                                                    2 * (int64_t)num_sms(c->dev))), c->n);
   NormSlot* corr = c->norm ? c->norm_slot : nullptr;
   const int me = c->cfg.rank;
   if (c->esz == 4) {
@@ -287,7 +291,8 @@ int micro_peer_reduce(micro_ctx* c) {
   if (c->peer_phase != 1) return fail(MICRO_ELOGIC, "micro_peer_reduce before micro_peer_contribute");
   DeviceGuard dg(c->dev);
   const PeerBulkPtrs pb = bulk_ptrs(c);
-  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 2, c->sel_cap), c->dev);
+  // two entries per thread for the expected selection (the kernel reads the real count)
+  const unsigned grid = grid_for(std::min<int64_t>((int64_t)c->k_worker * 3 / 4 + 1, c->sel_cap), c->dev);
   long long* Kout = c->Kbuf + c->buf;
   if (c->esz == 4)
     k_peer_reduce_push<float><<<grid, 256, 0, c->stream>>>(pb, c->n, c->cfg.rank, c->t_cur, c->sel_cap,

@@ -28,16 +28,20 @@ struct WorkerPtrs {
 // overflow flag, reported at the next sync); consumers read at most `cap`.
 __device__ __forceinline__ long long clamp_count(long long k, long long cap) { return k < cap ? k : cap; }
 
-template <typename T, bool kZero>
+template <typename T, bool kZero, bool kFew = false>
 __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long long* counts,
                                                         long long cap, int n, int64_t t,
                                                         int32_t* union_idx, T* union_sum,
                                                         NormSlot* sq_corr) {
   // sq_corr (kZero, error norm on): per worker, the squares of the residual
   // entries zeroed here (foreign union indices), subtracted from K1's
-  // ||e||^2 by k_finalize.  Lane r of each warp accumulates worker r
-  // (r + 32 in a second register); one order-independent fixed-point add
-  // (norm.cuh fx_add) per block and worker.
+  // ||e||^2 by k_finalize.  kFew (n <= 8): each thread keeps one partial
+  // per worker in registers and the warps reduce them once at the end;
+  // otherwise lane r of each warp accumulates worker r (r + 32 in a second
+  // register) with one warp reduction per worker and iteration.  Either way
+  // the per-CTA partials are fixed by the grid shape, and one
+  // order-independent fixed-point add (norm.cuh fx_add) per block and worker
+  // makes the total independent of CTA timing.
   __shared__ double s_corr[8][kMaxWorkers];
   pdl_wait();  // the workers' K1 results are complete
   pdl_trigger();
@@ -51,6 +55,9 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
   const T* __restrict__ val = (const T*)w.sel_val[owner];
   const bool corr = kZero && sq_corr != nullptr;  // grid-uniform
   double c_lo = 0.0, c_hi = 0.0;
+  double qt[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) qt[u] = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long b = (long long)blockIdx.x * blockDim.x; b < k; b += stride) {  // warp-uniform trip count
     const long long m = b + threadIdx.x;
@@ -73,7 +80,9 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
         if (r >= n) break;
         s = add_rn(s, v[u]);
         if (kZero && act && r != owner) ((T*)w.resid[r])[j] = (T)0;
-        if (corr && r != owner) {
+        if (kFew) {
+          if (corr && r != owner) qt[u] += (double)v[u] * (double)v[u];  // v = 0 when !act
+        } else if (corr && r != owner) {
           const double q = warp_sum_f64(act ? (double)v[u] * (double)v[u] : 0.0);
           if (lane == (r & 31)) {
             if (r < 32) c_lo += q;
@@ -81,6 +90,7 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
           }
         }
       }
+      if (kFew) break;
     }
     if (act) {
       union_idx[off + m] = j;
@@ -88,8 +98,16 @@ __global__ void __launch_bounds__(256) k_cluster_reduce(WorkerPtrs w, const long
     }
   }
   if (corr) {
-    if (lane < n) s_corr[wid][lane] = c_lo;
-    if (lane + 32 < n) s_corr[wid][lane + 32] = c_hi;
+    if (kFew) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double q = warp_sum_f64(qt[u]);
+        if (lane == 0 && u < n) s_corr[wid][u] = q;
+      }
+    } else {
+      if (lane < n) s_corr[wid][lane] = c_lo;
+      if (lane + 32 < n) s_corr[wid][lane + 32] = c_hi;
+    }
     __syncthreads();
     if ((int)threadIdx.x < n) {
       double tot = 0.0;

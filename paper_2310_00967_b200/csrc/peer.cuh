@@ -37,28 +37,53 @@ __device__ __forceinline__ long long ld_volatile_i64(const long long* p) {
   return *reinterpret_cast<const volatile long long*>(p);
 }
 
+// The CTA's peer stores, released at system scope once: the barrier orders
+// every thread's stores before thread 0's fence (cumulative).  The kernel
+// boundary and the caller's barrier order them as well; the single fence
+// keeps the protocol safe for a caller whose barrier is only a flag, at the
+// cost of one membar.sys per CTA instead of one per thread (ncu: the
+// per-thread fence was 70 % of the exchange kernels' stalls).
+// Every rank's count (peer loads, one per lane, all in flight) -> this
+// rank's segment offset in partition order, its own (clamped) count and K.
+// Warp 0 only; results in *off, *km, *K (lane 0).
+__device__ __forceinline__ void peer_offsets(const long long* const* counts, int n, int me, int64_t t, long long cap,
+                                             long long* off, long long* km, long long* K) {
+  const int lane = threadIdx.x & 31;
+  const int pme = (int)((t % n + me) % n);  // my partition (tensor.hpp:57)
+  long long o = 0, tot = 0;
+  for (int q0 = 0; q0 < n; q0 += 32) {
+    const int q = q0 + lane;  // partition q, owned by partition_owner(q)
+    long long kc = 0;
+    if (q < n) {
+      const long long kq = ld_volatile_i64(counts[partition_owner(q, n, t)]);
+      kc = kq < cap ? kq : cap;
+    }
+    o += (long long)warp_sum_u64((unsigned long long)(q < pme ? kc : 0));
+    tot += (long long)warp_sum_u64((unsigned long long)kc);
+  }
+  if (lane == 0) {
+    const long long k = ld_volatile_i64(counts[me]);
+    *off = o;
+    *km = k < cap ? k : cap;
+    *K = tot;
+  }
+}
+
+__device__ __forceinline__ void cta_release_system() {
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_peer_exchange(PeerPtrs p, int n, int me, int64_t t, long long cap,
                                                        const int32_t* __restrict__ own_idx,
                                                        const T* __restrict__ own_val, long long* K_out) {
-  __shared__ long long s_off, s_k;
+  __shared__ long long s_off, s_k, s_K;
   __shared__ double s_corr[8][kMaxWorkers];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    const int pme = (int)((t % n + me) % n);  // my partition (tensor.hpp:57)
-    long long off = 0, K = 0;
-    for (int q = 0; q < n; ++q) {
-      const long long kq = ld_volatile_i64(p.counts[partition_owner(q, n, t)]);
-      const long long kc = kq < cap ? kq : cap;
-      if (q < pme) off += kc;
-      K += kc;
-    }
-    const long long km = ld_volatile_i64(p.counts[me]);
-    s_off = off;
-    s_k = km < cap ? km : cap;
-    if (blockIdx.x == 0) *K_out = K;
-  }
+  if (wid == 0) peer_offsets(p.counts, n, me, t, cap, &s_off, &s_k, &s_K);
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *K_out = s_K;
   const long long off = s_off, k = s_k;
   const bool corr = kZero && p.corr[0] != nullptr;  // grid-uniform
   double c_lo = 0.0, c_hi = 0.0;
@@ -108,7 +133,7 @@ __global__ void __launch_bounds__(256) k_peer_exchange(PeerPtrs p, int n, int me
       if (tot != 0.0) fx_add(p.corr[threadIdx.x], tot);
     }
   }
-  __threadfence_system();  // peer stores visible before the caller's barrier
+  cta_release_system();  // peer stores visible before the caller's barrier
 }
 
 }  // namespace micro
@@ -134,6 +159,10 @@ struct PeerBulkPtrs {
   void* usum[kMaxWorkers];
 };
 
+constexpr int kPeerILP = 8;  // entries per lane in flight in the bulk exchange kernels
+
+// Grid: x = CTAs per owner (each warp takes 32 * kPeerILP consecutive
+// entries of the owner's list per round), y = owner.
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me, long long cap, T* __restrict__ resid,
                                                          NormSlot* corr) {
@@ -144,21 +173,24 @@ __global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me,
   k = k < cap ? k : cap;
   const int32_t* __restrict__ idx = p.sel_idx[o];
   T* __restrict__ out = (T*)p.recv[o] + (long long)me * cap;
+  const int lane = threadIdx.x & 31;
+  constexpr long long kChunk = 32 * kPeerILP;
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   double q = 0.0;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 4 * stride) {
-    int32_t j[4];
-    T v[4];
+  for (long long base = warp * kChunk; base < k; base += nwarps * kChunk) {
+    int32_t j[kPeerILP];
+    T v[kPeerILP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)  // four index reads (remote, coalesced) in flight
-      if (m0 + u * stride < k) j[u] = idx[m0 + u * stride];
+    for (int u = 0; u < kPeerILP; ++u)  // the owner's index list: remote, coalesced
+      if (base + u * 32 + lane < k) j[u] = idx[base + u * 32 + lane];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)  // four local gathers in flight
-      if (m0 + u * stride < k) v[u] = ld_rand(resid + j[u]);
+    for (int u = 0; u < kPeerILP; ++u)  // own accumulator: local random reads, all in flight
+      if (base + u * 32 + lane < k) v[u] = ld_rand(resid + j[u]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (m0 + u * stride < k) {
-        out[m0 + u * stride] = v[u];
+    for (int u = 0; u < kPeerILP; ++u)
+      if (base + u * 32 + lane < k) {
+        out[base + u * 32 + lane] = v[u];  // the owner's receive slab: remote, coalesced
         if (kZero) {
           resid[j[u]] = (T)0;
           q += (double)v[u] * (double)v[u];
@@ -175,41 +207,58 @@ __global__ void __launch_bounds__(256) k_peer_contribute(PeerBulkPtrs p, int me,
       if (tot != 0.0) fx_add(corr, tot);
     }
   }
-  __threadfence_system();
+  cta_release_system();
 }
 
+// Owner: s = 0; s += contribution_r in rank order (all n values in flight,
+// eight at a time), then the (index, sum) pair pushed to every rank.
 template <typename T>
 __global__ void __launch_bounds__(256) k_peer_reduce_push(PeerBulkPtrs p, int n, int me, int64_t t, long long cap,
                                                           const int32_t* __restrict__ own_idx,
                                                           const T* __restrict__ own_val, long long* K_out) {
-  __shared__ long long s_off, s_k;
-  if (threadIdx.x == 0) {
-    const int pme = (int)((t % n + me) % n);
-    long long off = 0, K = 0;
-    for (int q = 0; q < n; ++q) {
-      const long long kq = ld_volatile_i64(p.counts[partition_owner(q, n, t)]);
-      const long long kc = kq < cap ? kq : cap;
-      if (q < pme) off += kc;
-      K += kc;
-    }
-    const long long km = ld_volatile_i64(p.counts[me]);
-    s_off = off;
-    s_k = km < cap ? km : cap;
-    if (blockIdx.x == 0) *K_out = K;
-  }
+  __shared__ long long s_off, s_k, s_K;
+  if (threadIdx.x < 32) peer_offsets(p.counts, n, me, t, cap, &s_off, &s_k, &s_K);
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *K_out = s_K;
   const long long off = s_off, k = s_k;
   const T* __restrict__ recv = (const T*)p.recv[me];
-  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
-    T s = (T)0;
-    for (int r = 0; r < n; ++r) s = add_rn(s, r == me ? own_val[m] : recv[(long long)r * cap + m]);
-    const int32_t j = own_idx[m];
-    for (int q = 0; q < n; ++q) {
-      p.uidx[q][off + m] = j;
-      ((T*)p.usum[q])[off + m] = s;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 2 * stride) {
+    // two entries per thread, each with n contributions (eight at a time) in flight
+    T s[2] = {(T)0, (T)0};
+    int32_t j[2] = {0, 0};
+    for (int r0 = 0; r0 < n; r0 += 8) {
+      T v[2][8];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const long long m = m0 + e * stride;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int r = r0 + u;
+          v[e][u] = (T)0;
+          if (m < k && r < n) v[e][u] = r == me ? own_val[m] : recv[(long long)r * cap + m];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (r0 + u < n) s[e] = add_rn(s[e], v[e][u]);
     }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (m0 + e * stride < k) j[e] = own_idx[m0 + e * stride];
+    for (int q = 0; q < n; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const long long m = m0 + e * stride;
+        if (m < k) {
+          p.uidx[q][off + m] = j[e];
+          ((T*)p.usum[q])[off + m] = s[e];
+        }
+      }
   }
-  __threadfence_system();
+  cta_release_system();
 }
 
 }  // namespace micro

@@ -72,7 +72,14 @@ struct StreamArgs {
   double* sq_part;         // kNorm: per CTA, sum of e_{t+1}^2 (own selections zeroed); reduced by k1_gather
   const long long* tie_j;  // kTie (top-k baseline): also select |acc| == thr at j <= *tie_j
   int cta_offset;          // this launch covers CTAs [cta_offset, cta_offset + gridDim.x) (chunked H2D)
+  const void* model;       // kPf: the model x whose selected lines k1_gather will read-modify-write
 };
+
+// L2 prefetch with the evict-last priority: the line survives the rest of
+// the (evict-first) stream and k1_gather's read of it hits L2.
+__device__ __forceinline__ void prefetch_l2_keep(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
 
 __device__ __forceinline__ float nan_probe_s(float g, float acc) { return __fmaf_rn(g, 0.0f, acc); }
 __device__ __forceinline__ double nan_probe_s(double g, double acc) { return __fma_rn(g, 0.0, acc); }
@@ -93,7 +100,10 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 
 // kNoG (top-k baseline): e already holds acc (written by the first histogram
 // pass), G is not read.
-template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false>
+// kPf (small steps, n = 1 with the model update): the lines of x at this
+// unit's selections are prefetched into L2 while the stream runs, taking the
+// model's DRAM latency off k1_gather's critical path.
+template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false, bool kPf = false>
 __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(StreamArgs a) {  // acc-only: 51 regs, 5 CTAs/SM
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -179,6 +189,12 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
                          (all_in || (j >= a.p_start && j < a.p_end));
         mask[i] |= (unsigned)tie << c;
       }
+  }
+
+  if (kPf) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+      if (mask[i]) prefetch_l2_keep((const T*)a.model + base + (i * 32 + lane) * VN);
   }
 
   if (kMode != kWriteNone) {
@@ -424,9 +440,24 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   const int gb = (int)blockIdx.x - (a.sq_part ? 1 : 0);
   const int r0 = gb * kGatherWarps;
   const int sb = r0 / a.super_runs;
-  // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0)
-  long long base = block_sum_range(a.super_counts, 0, sb, s_part) +
-                   block_sum_range(a.run_counts, sb * a.super_runs, r0, s_part);
+  const int r = r0 + w;
+  // this CTA's run counts first (independent of the prefix below): one round
+  // of L2 reads for everything the CTA needs
+  const int mine = (r0 + lane < a.num_runs && lane < w) ? a.run_counts[r0 + lane] : 0;
+  const int n = r < a.num_runs ? a.run_counts[r] : 0;
+  // pairs before this CTA: super blocks [0, sb) + runs [sb * S, r0), summed in one pass
+  long long base = 0;
+  {
+    const int nsup = sb, nrun = r0 - sb * a.super_runs;
+    long long v = 0;
+    for (int q = threadIdx.x; q < nsup + nrun; q += kGatherWarps * 32)
+      v += q < nsup ? a.super_counts[q] : a.run_counts[sb * a.super_runs + (q - nsup)];
+    v = (long long)warp_sum_u64((unsigned long long)v);
+    if (lane == 0) s_part[w] = v;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kGatherWarps; ++q) base += s_part[q];
+  }
   if (gb == 0) {
     const int nsup = (a.num_runs + a.super_runs - 1) / a.super_runs;
     const long long total = block_sum_range(a.super_counts, 0, nsup, s_part);
@@ -437,12 +468,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     }
     for (int q = threadIdx.x; q < a.super_len; q += kGatherWarps * 32) a.super_clear[q] = 0;
   }
-  const int r = r0 + w;
-  // runs of this CTA before r (<= 7 L2 hits)
-  const int mine = (r0 + lane < a.num_runs && lane < w) ? a.run_counts[r0 + lane] : 0;
+  // runs of this CTA before r (<= 7 L2 hits, loaded above)
   base += (long long)__reduce_add_sync(0xffffffffu, (unsigned)mine);
   if (r >= a.num_runs) return;
-  const int n = a.run_counts[r];
   if (!n) return;
   const long long off = base < a.cap ? base : a.cap;
   const long long src = (long long)r * a.run_stride;

@@ -170,7 +170,11 @@ int run_world(int n) {
   std::vector<pid_t> kids;
   for (int r = 0; r < n; ++r) {
     const pid_t p = fork();
-    if (p == 0) _exit(rank_main(sh, r));
+    if (p == 0) {
+      const int rc = rank_main(sh, r);
+      std::fflush(stdout);
+      _exit(rc);
+    }
     kids.push_back(p);
   }
   for (pid_t p : kids) {
@@ -213,6 +217,7 @@ int in_child(int (*f)(int), int arg) {
   const pid_t p = fork();
   if (p == 0) {
     f(arg);
+    std::fflush(stdout);  // _exit skips stdio's buffers
     _exit(g_fail ? 1 : 0);
   }
   int st = 0;

@@ -219,3 +219,22 @@ def test_spec_examples_error_metric_accumulate():
         e = S.accumulate(e, 0.5, g)
         norms.append(S.error_metric([e]))
     assert all(b > a for a, b in zip(norms, norms[1:]))
+
+
+@pytest.mark.parametrize("extent,sizes", [(1_000, [7, 300, 0]), (5_000_000, [200_000, 150_000]),
+                                          (200_000_000, [400_000, 1, 250_000])])
+def test_all_gather_indices_unsorted_overlapping(extent, sizes):
+    """collectives.cpp:14-28 is sort + unique of the concatenation for ANY
+    input: unsorted, overlapping, duplicated lists — here the bitmap + the
+    hand-written popcount scan (scan.cuh) over up to 6M words (several
+    passes of the one-CTA tile-total scan)."""
+    def sel(ix):
+        t = torch.tensor(ix, dtype=torch.int32, device="cuda")
+        return S.SparseSelection(t, torch.ones(len(ix), dtype=torch.float64, device="cuda"))
+    rng = np.random.default_rng(extent)
+    lists = [rng.integers(0, extent, k) for k in sizes]  # unsorted, with duplicates
+    lists.append(np.array([extent - 1, 0, extent - 1]))
+    agg = S.all_gather_indices([sel(x.tolist()) for x in lists])
+    want = np.unique(np.concatenate(lists))
+    assert np.array_equal(agg.indices.cpu().numpy().astype(np.int64), want)
+    assert agg.per_worker_counts == [len(x) for x in lists]
