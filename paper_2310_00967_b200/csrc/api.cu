@@ -376,7 +376,10 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     b.fin_slot = c->steps % kHistCap;
     gblocks += 1;
   }
-  CU(launch_pdl(k1_gather<T>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
+  if (c->cfg.density >= 0.05)
+    CU(launch_pdl(k1_gather<T, false>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
+  else
+    CU(launch_pdl(k1_gather<T, true>, dim3(gblocks), dim3(kGatherWarps * 32), c->stream, b));
   return MICRO_OK;
 }
 

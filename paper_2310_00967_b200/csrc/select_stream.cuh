@@ -412,7 +412,10 @@ __device__ __forceinline__ long long block_sum_range(const int* p, int lo, int h
 // One warp per CTA run: coalesced copy into the ordered output at the run's
 // exclusive prefix, then the run's staging lines are dropped from L2 without
 // write-back.  n = 1: the model update rides along.
-template <typename T>
+// kWide: fetch the model's lines 64 B at a time (L2::64B: fewer DRAM
+// transactions when the selections are sparse); dense selections (d >= 5 %)
+// already touch most sectors, and plain sector loads move fewer bytes.
+template <typename T, bool kWide = true>
 __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   __shared__ long long s_part[kGatherWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
     if (x) {  // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
 #pragma unroll
       for (int q = 0; q < kG; ++q)
-        if (m0 + 32 * q < lim) xv[q] = ld_rand(x + j[q]);
+        if (m0 + 32 * q < lim) xv[q] = kWide ? ld_rand(x + j[q]) : x[j[q]];
 #pragma unroll
       for (int q = 0; q < kG; ++q)
         if (m0 + 32 * q < lim) x[j[q]] = xv[q] - v[q];
