@@ -315,10 +315,19 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     for r in range(R):
         engine.synth_gaussian(G[r], args.seed, rank + r % W, t + r)
     t0_bufs = t
+    # not enough HBM for one resident gradient per step (C5 in f64: 12 GB
+    # each): each step's gradients are generated fresh into the R buffers
+    # just before the step, outside its events (re-fed gradients would make
+    # the residual grow coherently and inflate the selection)
+    fresh = R < need
 
     def grads(t):
         q = (t - t0_bufs) * W
-        return [G[(q + i) % R] for i in range(W)]
+        out = [G[(q + i) % R] for i in range(W)]
+        if fresh:
+            for i, g in enumerate(out):
+                engine.synth_gaussian(g, args.seed, rank + i, t)
+        return out
 
     for s in range(args.warmup):
         m.step(grads(t), ETA, t)
@@ -343,17 +352,20 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and 3 * esz * n_g < 2 * 126e6)
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
     scratch2 = torch.empty(64 << 20, dtype=torch.float32, device=dev) if flush else None
+    per_step = flush or fresh  # each step timed alone (events around the step only)
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)] if flush else []
+               for _ in range(args.steps)] if per_step else []
     with ClockSampler(local) as clk:
         start.record(stream)
         for s in range(args.steps):
+            gs = grads(t)  # fresh mode: generated here, before the step's events
             if flush:
                 scratch.fill_(s & 0xFF)
                 scratch2.sum()
+            if per_step:
                 step_ev[s][0].record(stream)
-            m.step(grads(t), ETA, t)  # the whole iteration, one library call
-            if flush:
+            m.step(gs, ETA, t)  # the whole iteration, one library call
+            if per_step:
                 step_ev[s][1].record(stream)
             t += 1
         end.record(stream)
@@ -366,7 +378,7 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     # With per-step events (flush mode) the step time is taken over the other
     # steps; without them (C3 and up) the sampled steps stay in (< 1 %).
     plain = [v for s_, v in enumerate(step_ms) if s_ % 4] or step_ms
-    total_ms = statistics.mean(plain) * args.steps if flush else start.elapsed_time(end)
+    total_ms = statistics.mean(plain) * args.steps if per_step else start.elapsed_time(end)
     k1a_ms = [float(v) for v in m.kernel_times(args.steps)]  # k1_stream alone (sampled launches)
     m.kernel_timing(False)
     xchg_ms = None
@@ -385,7 +397,7 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     K = hist["K"].astype(np.float64)
     k_own = hist["counts"][:, 0].astype(np.float64)
     out = dict(ms_step=ms_step, step_ms=step_ms, k1a_ms=k1a_ms, xchg_ms=xchg_ms, K=K, k_own=k_own, R=R,
-               flush=flush, t_first=t_first, t_next=t, W=W, esz=esz, clocks=clk.summary(),
+               flush=flush, fresh=fresh, t_first=t_first, t_next=t, W=W, esz=esz, clocks=clk.summary(),
                transport=getattr(m, "transport", None))
     if keep:
         out.update(m=m, G=G)
@@ -463,7 +475,8 @@ def our_arm(args, wl):
     # k_cluster_reduce + k_finalize (+ k_dense_clear); n > 1 ranks: K1 x2 +
     # the exchange + finalize (NCCL kernels not counted)
     launches_per_step = ((2 if W == 1 else 2 * W + 2 + (1 if args.dense else 0)) if world == 1
-                         else {"peer": 5, "peer_pull": 4, "nccl": 6}[r["transport"]])
+                         else {"peer": 5, "peer_pull": 4, "nccl": 6, "abi_peer": 5, "abi_nccl": 6}[r["transport"]]
+                         + (1 if args.dense else 0))  # + k_dense_clear (aux stream) at n > 1
     if args.sparsifier != "micro":  # baselines.cuh: per selecting worker, top-k = init + 2 per digit +
         # tie count/find + stream + gather (fp32: 11), hard = 2, else accumulate + count = 2; then
         # union marks (W) + 3 scan passes + emit + reduce + finalize (dense: dense_all + finalize)
@@ -590,8 +603,10 @@ def our_arm(args, wl):
             "data": f"synthetic N(0,1) {args.dtype} gradients (include/micro_synth.h)",
             "config": bench_config(args, wl, world),
             "protocol": {"adaptation_iterations": args.prime, "first_timed_t": r["t_first"], "seed": args.seed,
-                         "inputs": (f"{R} resident N(0,1) gradients ("
-                                    + ("one fresh per step" if R >= args.warmup + args.steps else "rotated")
+                         "inputs": (f"{R} resident N(0,1) gradient buffers ("
+                                    + ("one fresh gradient per step" if not r["fresh"] else
+                                       "each step's gradient generated fresh into them just before the step, "
+                                       "outside its events; steps timed one by one")
                                     + (f"); L2 flushed between timed steps (256 MB write + 256 MB read outside "
                                        f"the per-step events: the working set {3 * esz * n_g / 1e6:.0f} MB would "
                                        f"fit L2)" if r["flush"] else f"); each {esz}*n_g bytes > L2 (no flush "
@@ -637,8 +652,10 @@ def main():
                     help="N = 1: a comparison sparsifier of the reference's harness instead of MiCRO")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: exercise the N > 1 path with all ranks on one GPU (code check only)")
-    ap.add_argument("--transport", choices=["peer", "peer_pull", "nccl"], default="peer",
-                    help="N > 1: exchange over peer memory (one kernel per rank) or the NCCL protocol")
+    ap.add_argument("--transport", choices=["peer", "peer_pull", "nccl", "abi_peer", "abi_nccl"], default="peer",
+                    help="N > 1: exchange over peer memory (bulk or pull) or the collective protocol, driven from "
+                         "Python over torch.distributed, or entirely inside the library (abi_*: "
+                         "micro_dist_init_nccl + micro_step, what a C++ host calls)")
     ap.add_argument("--seed", type=int, default=SEED, help="synthetic gradient stream (SURVEY.md 8d: 1, 2, 3)")
     ap.add_argument("--flush-l2", choices=["auto", "on", "off"], default="auto",
                     help="flush L2 between timed steps (auto: when e, G and x would fit in L2)")
