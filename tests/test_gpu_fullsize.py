@@ -71,3 +71,53 @@ def test_c3_properties_long_run():
         want_x[idx] = x_t[idx] - sums                             # x -= g/n with n = 1
         assert torch.equal(x, want_x)
     m.close()
+
+
+def test_maximum_size_int32_indices():
+    """The largest gradient the int32 index format admits (n_g = 2^31 - 2,
+    8.6 GB per fp32 vector), two workers: the last partition ends one short
+    of 2^31, so every index, unit base and partition bound sits at the edge
+    of int32.  Size-independent properties against torch on the same
+    inputs: the exact strict predicate count, the union = the ascending
+    selected indices, the sums, and bitwise error-feedback conservation."""
+    n_g, eta = 2**31 - 2, 0.01
+    torch.cuda.empty_cache()
+    m = engine.Micro(n_g, 2, density=0.0005, initial_threshold=3.48 * eta, dense_output=False,
+                     record_error_norm=False)
+    G = [torch.empty(n_g, device="cuda") for _ in range(2)]
+    for t in range(2):
+        for i in range(2):
+            engine.synth_gaussian(G[i], 17, i, t)
+        e0 = [m.residual_device(i).clone() for i in range(2)]
+        delta = m.query().deltas.copy()
+        m.step(G, eta, t)
+        idx, sums = m.union()
+        it = torch.from_numpy(idx.astype(np.int64)).cuda()
+        want_i, want_s = [], []
+        for i in range(2):  # partition(n_g, 2, t, i): contiguous halves, cyclic in t
+            acc = e0[i] + torch.tensor(eta, dtype=torch.float32) * G[i]
+            s, e = (0, n_g // 2) if (t + i) % 2 == 0 else (n_g // 2, n_g)
+            sel = torch.nonzero(acc[s:e].abs().double() > delta[i]).flatten() + s
+            want_i.append(sel)
+            del acc
+        order = sorted(range(2), key=lambda i: int(want_i[i][0]) if want_i[i].numel() else 0)
+        wi = torch.cat([want_i[i] for i in order])
+        assert torch.equal(it, wi), t
+        assert int(idx[-1]) > 2**31 - 2**24  # the top of int32 is reached
+        # sums: both workers' accumulators at the union, in worker order from +0
+        acc0 = e0[0] + torch.tensor(eta, dtype=torch.float32) * G[0]
+        s01 = torch.zeros(it.numel(), device="cuda") + acc0[it]
+        del acc0
+        acc1 = e0[1] + torch.tensor(eta, dtype=torch.float32) * G[1]
+        s01 = s01 + acc1[it]
+        assert torch.equal(torch.from_numpy(sums).cuda(), s01), t
+        # conservation: e_{t+1} + (acc at the union) == acc, elementwise, worker 1
+        e1 = m.residual_device(1)
+        sent = torch.zeros_like(acc1)
+        sent[it] = acc1[it]
+        assert torch.equal(e1 + sent, acc1), t
+        del acc1, sent, e0, s01
+        torch.cuda.empty_cache()
+    m.close()
+    del G
+    torch.cuda.empty_cache()
