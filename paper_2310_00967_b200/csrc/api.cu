@@ -243,11 +243,6 @@ int launch_sumsq(micro_ctx* c, int i) {
 // Steps whose streamed bytes (e, G read; e written) stay below this prefetch
 // the model's selected lines during k1_stream (C1: 140 MB; C3: 1.66 GB does not).
 constexpr int64_t kPrefetchStepBytes = 256ll << 20;
-// One worker, EF on, model set, dense selections: k1_stream applies the model update.
-constexpr double kModelInK1Density = 0.05;
-inline bool model_in_k1(const micro_ctx* c) {
-  return c->sel_is_union && c->kind == 0 && c->model && c->cfg.error_feedback && c->cfg.density >= kModelInK1Density;
-}
 
 template <typename T>
 int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe,
@@ -303,14 +298,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     } else if (c->cfg.error_feedback) {
       // small steps: prefetch x's selected lines into L2 for k1_gather's update
       const bool pf = c->model && (int64_t)c->n_g * (int64_t)c->esz * 3 <= kPrefetchStepBytes;
-      if (model_in_k1(c)) {
-#define K1M(D, N) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, N, false, false, false, true>, dim3(g), dim3(kStreamThreads), st, a))
-        if (fd && c->norm) K1M(true, true);
-        else if (fd) K1M(true, false);
-        else if (c->norm) K1M(false, true);
-        else K1M(false, false);
-#undef K1M
-      } else if (pf) {
+      if (pf) {
 #define K1P(D, N) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, N, false, false, true>, dim3(g), dim3(kStreamThreads), st, a))
         if (fd && c->norm) K1P(true, true);
         else if (fd) K1P(true, false);
@@ -360,8 +348,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.cap = c->sel_cap;
   b.count = c->counts + i;
   b.flags = c->flags;
-  // n = 1: the union is this selection, g/n = acc (dense selections: k1_stream updated x already)
-  b.model = (c->sel_is_union && !model_in_k1(c)) ? c->model : nullptr;
+  b.model = c->sel_is_union ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
   if ((b.num_runs + b.super_runs - 1) / b.super_runs > kMaxSupers)
     return fail(MICRO_ECAPACITY, "super-block workspace too small");
   if (c->fuse_step) {

@@ -103,15 +103,8 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 // kPf (small steps, n = 1 with the model update): the lines of x at this
 // unit's selections are prefetched into L2 while the stream runs, taking the
 // model's DRAM latency off k1_gather's critical path.
-// kModel (n = 1, dense selections, d >= 5 %): the model update x -= g/n =
-// acc at this unit's selections happens here, with the lines of x loaded
-// right after the compare so their latency overlaps the stores and the
-// compaction; k1_gather then copies the union only.  At d = 0.1 half of x's
-// sectors hold a selection, and reading them in unit order beats the
-// gather's scattered read-modify-write of the same sectors.
-template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false, bool kPf = false,
-          bool kModel = false>
-__global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : (kModel ? 3 : 4)) k1_stream(StreamArgs a) {  // acc-only: 51 regs, 5 CTAs/SM
+template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false, bool kPf = false>
+__global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(StreamArgs a) {  // acc-only: 51 regs, 5 CTAs/SM
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
   constexpr int UE = stream_unit_elems<T>();
@@ -203,14 +196,6 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : (kModel ? 3 : 4)) k
     for (int i = 0; i < VPL; ++i)
       if (mask[i]) prefetch_l2_keep((const T*)a.model + base + (i * 32 + lane) * VN);
   }
-  V xm[kModel ? VPL : 1];
-  T* __restrict__ X = kModel ? (T*)a.model + base : nullptr;
-  if (kModel && elems == UE) {
-#pragma unroll
-    for (int i = 0; i < VPL; ++i)
-      if (mask[i]) xm[i] = ld_hint(reinterpret_cast<const V*>(X) + i * 32 + lane, pol_stream);
-  }
-
   if (kMode != kWriteNone) {
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
@@ -325,27 +310,6 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : (kModel ? 3 : 4)) k
         }
         cb += (tot >> (8 * i)) & 0xFFu;
       }
-    }
-  }
-  if (kModel) {  // x -= acc at the selections (n = 1: g/n = (0 + acc) / 1 exactly)
-    if (elems == UE) {
-#pragma unroll
-      for (int i = 0; i < VPL; ++i)
-        if (mask[i]) {
-#pragma unroll
-          for (int c = 0; c < VN; ++c)
-            if (mask[i] & (1u << c)) set_comp(xm[i], c, sub_rn(comp(xm[i], c), comp(e[i], c)));
-          st_hint(reinterpret_cast<V*>(X) + i * 32 + lane, xm[i], pol_stream);
-        }
-    } else {
-#pragma unroll
-      for (int i = 0; i < VPL; ++i)
-#pragma unroll
-        for (int c = 0; c < VN; ++c)
-          if (mask[i] & (1u << c)) {
-            const int off = (i * 32 + lane) * VN + c;
-            X[off] = sub_rn(X[off], comp(e[i], c));
-          }
     }
   }
   if (probe != probe) atomicOr(a.flags, 1);
