@@ -117,6 +117,9 @@ int micro_host_malloc(void** h_ptr, int64_t bytes);
 int micro_host_free(void* h_ptr);
 int micro_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 int micro_device_count(int* count);
+/* The calling thread's current CUDA device (what micro_synth_gaussian and
+ * the value-level calls launch on). */
+int micro_set_device(int device);
 
 /* Synthetic N(0,1) gradients of include/micro_synth.h (bench/test inputs). */
 int micro_synth_gaussian(int dtype, uint64_t seed, uint32_t worker, uint64_t t, int64_t n,

@@ -139,6 +139,7 @@ _SIGS = {
     "micro_dist_owner_reduce": ([VP], I32),
     "micro_dist_finalize": ([VP], I32),
     "micro_nccl_unique_id": ([VP], I32),
+    "micro_set_device": ([I32], I32),
     "micro_dist_init_nccl": ([VP, VP, I32], I32),
     "micro_dist_attach_nccl": ([VP, VP, I32], I32),
     "micro_peer_export": ([VP, VP], I32),

@@ -86,6 +86,11 @@ int micro_device_count(int* count) {
   return MICRO_OK;
 }
 
+int micro_set_device(int device) {
+  CU(cudaSetDevice(device));
+  return MICRO_OK;
+}
+
 int micro_device_malloc(void** d, int64_t bytes, int device) {
   if (!d || bytes < 0) return fail(MICRO_EINVAL, "bad allocation request");
   *d = nullptr;

@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -33,6 +34,9 @@ constexpr uint64_t kSeed = 11;
 struct Shared {
   pthread_barrier_t bar;
   int n;
+  int mode;  // 0: peer protocol, host barriers, all ranks on device 0;
+             // 1 / 2: micro_dist_init_nccl (MICRO_XCHG_PEER / _NCCL), rank r on device r
+  unsigned char uid[MICRO_NCCL_UNIQUE_ID_BYTES];
   int failed;
   unsigned char handles[8][MICRO_PEER_HANDLE_BYTES];
   int64_t K[kSteps][8];
@@ -78,28 +82,41 @@ micro_config config(int n, int n_local, int rank) {
 
 int rank_main(Shared* sh, int r) {
   const int n = sh->n;
+  const int dev = sh->mode ? r : 0;
   micro_ctx* ctx = nullptr;
-  const micro_config cfg = config(n, 1, r);
+  micro_config cfg = config(n, 1, r);
+  cfg.device = dev;
+  OK(micro_set_device(dev));
   OK(micro_ctx_create(&ctx, &cfg, nullptr));
-  OK(micro_peer_export(ctx, sh->handles[r]));
-  pthread_barrier_wait(&sh->bar);
-  OK(micro_peer_import(ctx, sh->handles));
+  if (sh->mode == 0) {
+    OK(micro_peer_export(ctx, sh->handles[r]));
+    pthread_barrier_wait(&sh->bar);
+    OK(micro_peer_import(ctx, sh->handles));
+  } else {  // the exchange behind the C ABI: one call per step, no host barriers
+    if (r == 0) OK(micro_nccl_unique_id(sh->uid));
+    pthread_barrier_wait(&sh->bar);
+    OK(micro_dist_init_nccl(ctx, sh->uid, sh->mode == 1 ? MICRO_XCHG_PEER : MICRO_XCHG_NCCL));
+  }
   pthread_barrier_wait(&sh->bar);
   void* g = nullptr;
-  OK(micro_device_malloc(&g, kNg * 4, 0));
+  OK(micro_device_malloc(&g, kNg * 4, dev));
   for (int t = 0; t < kSteps; ++t) {
     OK(micro_synth_gaussian(MICRO_F32, kSeed, (uint32_t)r, (uint64_t)t, kNg, g, nullptr));
     const void* gs[1] = {g};
-    OK(micro_compress(ctx, gs, kEta, t));
-    OK(micro_sync(ctx));
-    pthread_barrier_wait(&sh->bar);  // every rank's K1 done
-    OK(micro_peer_contribute(ctx));
-    OK(micro_sync(ctx));
-    pthread_barrier_wait(&sh->bar);  // every contribution landed
-    OK(micro_peer_reduce(ctx));
-    OK(micro_sync(ctx));
-    pthread_barrier_wait(&sh->bar);  // every owner pushed its segment
-    OK(micro_peer_finalize(ctx));
+    if (sh->mode) {
+      OK(micro_step(ctx, gs, kEta, t));
+    } else {
+      OK(micro_compress(ctx, gs, kEta, t));
+      OK(micro_sync(ctx));
+      pthread_barrier_wait(&sh->bar);  // every rank's K1 done
+      OK(micro_peer_contribute(ctx));
+      OK(micro_sync(ctx));
+      pthread_barrier_wait(&sh->bar);  // every contribution landed
+      OK(micro_peer_reduce(ctx));
+      OK(micro_sync(ctx));
+      pthread_barrier_wait(&sh->bar);  // every owner pushed its segment
+      OK(micro_peer_finalize(ctx));
+    }
     micro_stats st;
     int64_t k = 0;
     double d = 0;
@@ -151,18 +168,20 @@ void run_check(Shared* sh, int n) {
     CHECK(micro_copy_residual(ctx, r, res.data()) == MICRO_OK);
     CHECK(std::memcmp(sh->residual[r], res.data(), (size_t)kNg * 4) == 0);
   }
-  std::printf("world %d: %d steps, K = %lld at the last, %s vs the single-device cluster\n", n, kSteps,
-              (long long)K, g_fail ? "MISMATCH" : "bit-exact");
+  std::printf("world %d%s: %d steps, K = %lld at the last, %s vs the single-device cluster\n", n,
+              sh->mode == 0 ? "" : sh->mode == 1 ? " (NCCL attach, peer exchange)" : " (NCCL attach, collectives)",
+              kSteps, (long long)K, g_fail ? "MISMATCH" : "bit-exact");
   for (int i = 0; i < n; ++i) micro_device_free(g[i]);
   micro_ctx_destroy(ctx);
 }
 
-int run_world(int n) {
+int run_world_mode(int n, int mode) {
   auto* sh = static_cast<Shared*>(
       mmap(nullptr, sizeof(Shared), PROT_READ | PROT_WRITE, MAP_SHARED | MAP_ANONYMOUS, -1, 0));
   if (sh == MAP_FAILED) return 1;
   std::memset(sh, 0, sizeof(Shared));
   sh->n = n;
+  sh->mode = mode;
   pthread_barrierattr_t at;
   pthread_barrierattr_init(&at);
   pthread_barrierattr_setpshared(&at, PTHREAD_PROCESS_SHARED);
@@ -213,6 +232,15 @@ int nccl_checks() {
 
 // Each case in its own child: a process must not fork ranks after it has
 // initialised CUDA, and this one never does.
+int run_world(int n) { return run_world_mode(n, 0); }
+int run_nccl_peer(int n) { return run_world_mode(n, 1); }
+int run_nccl_coll(int n) { return run_world_mode(n, 2); }
+int device_count(int) {
+  int c = 0;
+  micro_device_count(&c);
+  return c;
+}
+
 int in_child(int (*f)(int), int arg) {
   const pid_t p = fork();
   if (p == 0) {
@@ -232,6 +260,19 @@ int main() {
   bad += in_child(run_world, 2);
   bad += in_child(run_world, 3);
   bad += in_child([](int) { return nccl_checks(); }, 0);
+  // one rank per GPU through micro_dist_init_nccl + micro_step (needs 2 GPUs;
+  // NCCL does not put two ranks on one device)
+  const pid_t p = fork();
+  if (p == 0) _exit(std::min(device_count(0), 100));
+  int st = 0;
+  waitpid(p, &st, 0);
+  const int ndev = WIFEXITED(st) ? WEXITSTATUS(st) : 0;
+  if (ndev >= 2) {
+    bad += in_child(run_nccl_peer, 2);
+    bad += in_child(run_nccl_coll, 2);
+  } else {
+    std::printf("NCCL worlds skipped: %d GPU(s) visible\n", ndev);
+  }
   std::printf("%s: %d failing cases\n", bad ? "FAIL" : "OK", bad);
   return bad;
 }
