@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmicro_b200.so")
 SOURCES = ["api.cu", "dist_api.cu", "value_api.cu", "nccl_api.cu"]
-HEADERS = ["internal.cuh", "baselines.cuh", "common.cuh", "norm.cuh", "scan.cuh", "select.cuh", "select_stream.cuh",
+HEADERS = ["internal.cuh", "baselines.cuh", "common.cuh", "norm.cuh", "scan.cuh", "select_stream.cuh",
            "exchange.cuh", "peer.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -20,7 +20,6 @@
 #include "exchange.cuh"
 #include "peer.cuh"
 #include "scan.cuh"
-#include "select.cuh"
 #include "select_stream.cuh"
 
 namespace micro {

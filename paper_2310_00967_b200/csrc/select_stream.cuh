@@ -1,8 +1,15 @@
 // select_stream.cuh — K1 as two kernels: an unordered streaming pass and a
-// small ordered compaction (the production path).
+// small ordered compaction.
 //
-// Same semantics as k1_fused_select (select.cuh; reference harness.cpp:131,
-// sparsifier.cpp:22-37, harness.cpp:219-221).
+// Reference semantics (paths relative to /root/reference/proj):
+//   acc_i = e_i + eta * G_i over ALL n_g            harness.cpp:131 (P4)
+//   non-finite G  -> runtime_error                  harness.cpp:128-130
+//   S_i = { j in partition : |acc_i[j]| > delta_i } sparsifier.cpp:22-37,
+//         ascending, strict, (index, acc value)     tensor.hpp:48-63
+//   e_{i,t+1}[j] = 0 for j in S_i (own part of the union zeroing)
+//                                                   harness.cpp:219-221
+// The same two kernels serve the value-level select_by_threshold /
+// select_topk (acc only: kNoG, kWriteNone) over a range.
 //
 // K1a  k1_stream: one warp per 512-element unit (2 KB per operand), eight
 //      units per CTA, ~32 warps resident per SM.  Each lane issues its eight
@@ -21,19 +28,25 @@
 //      before it inside its super block (<= 1024 + S L2 reads per CTA, no
 //      scan kernel, no look-back); block 0 also forms k_i.
 //
-// Why not one pass: every single-pass variant we measured (per-tile
-// look-back; persistent CTAs with TMA bulk-copy rings; per-warp rings;
-// LDG streaming with per-warp ordered runs) stayed at 2.5-3.6 TB/s — the
-// ordering machinery sat on the critical path of every tile.  The staging
+// Why not one pass: every single-pass variant we measured in round 1
+// (per-tile decoupled look-back; persistent CTAs with TMA bulk-copy rings;
+// per-warp rings; LDG streaming with per-warp ordered runs) stayed at
+// 2.5-3.6 TB/s — the ordering machinery sat on the critical path of every
+// tile (profiles/README.md, round 1).  The staging
 // round trip costs 16 bytes per selected pair plus 4 bytes per 512
 // elements (0.2 B/elem at d = 1%, vs 12 B/elem streamed).
 #pragma once
 
 #include "common.cuh"
 #include "norm.cuh"
-#include "select.cuh"
 
 namespace micro {
+
+enum WriteMode : int {
+  kWriteZeroSel = 0,  // e <- acc with own selections zeroed (error feedback on)
+  kWriteAcc = 1,      // e <- acc (error feedback off, n > 1: peers still read acc)
+  kWriteNone = 2,     // no residual write (EF off at n = 1, or select-only)
+};
 
 constexpr int kStreamWarps = 8;                  // units per CTA
 constexpr int kStreamThreads = kStreamWarps * 32;

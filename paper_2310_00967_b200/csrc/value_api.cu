@@ -159,8 +159,88 @@ int micro_accumulate(int dtype, const void* d_e, double eta, const void* d_g, vo
   return MICRO_OK;
 }
 
+}  // extern "C"
+
 // Ordered compaction of {j in [start, end) : |acc_j| > thr} (thr = *d_thr or
-// delta), plus, with d_tie, {|acc_j| == thr, j <= *d_tie} (top-k's ties).
+// delta), plus, with d_tie, {|acc_j| == thr, j <= *d_tie} (top-k's ties):
+// the engine's two kernels over the range only — k1_stream in its acc-only
+// form (one 4-byte read per element, per-CTA staging runs) and k1_gather
+// (ordered copy at each run's prefix) — with scratch from the stream-ordered
+// allocator.
+template <typename T>
+static int select_stream_range(const void* d_acc, int64_t n_g, int64_t start, int64_t end, const double* d_thr,
+                               double delta, const long long* d_tie, int32_t* d_idx, void* d_val, int64_t cap,
+                               int64_t* d_count, cudaStream_t s) {
+  constexpr int UE = stream_unit_elems<T>();
+  const int64_t cta_lo = start / UE / kStreamWarps, cta_hi = (end - 1) / UE / kStreamWarps;
+  const int64_t runs = cta_hi - cta_lo + 1;
+  const int64_t per_run = (int64_t)kStreamWarps * UE;
+  const int64_t sup = (runs + kMaxSupers - 1) / kMaxSupers;
+  const int super_runs = (int)std::max<int64_t>(kGatherWarps, (sup + kGatherWarps - 1) / kGatherWarps * kGatherWarps);
+  const size_t b_idx = sizeof(int32_t) * runs * per_run, b_val = sizeof(T) * runs * per_run;
+  const size_t b_cnt = sizeof(int) * runs, b_sup = sizeof(int) * kMaxSupers;
+  char* ws = nullptr;
+  const size_t tail = (b_idx + b_val + b_cnt + b_sup + 15) / 16 * 16;
+  CU(cudaMallocAsync((void**)&ws, tail + 32, s));
+  int32_t* stage_idx = (int32_t*)ws;
+  T* stage_val = (T*)(ws + b_idx);
+  int* counts = (int*)(ws + b_idx + b_val);
+  int* supers = (int*)(ws + b_idx + b_val + b_cnt);
+  int* flags = (int*)(ws + tail);
+  double* thr = (double*)(ws + tail + 16);
+  CU(cudaMemsetAsync(supers, 0, b_sup, s));
+  CU(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  if (!d_thr) {
+    long long bits;
+    std::memcpy(&bits, &delta, sizeof bits);
+    k_fill_i64<<<1, 32, 0, s>>>((long long*)thr, 1, bits);
+    CU(cudaGetLastError());
+    d_thr = thr;
+  }
+  StreamArgs a{};
+  a.resid = const_cast<void*>(d_acc);  // acc, read only (kNoG, kWriteNone)
+  a.n_g = (int)n_g;
+  a.p_start = (int)start;
+  a.p_end = (int)end;
+  a.eta = 1.0;
+  a.delta = d_thr;
+  a.tie_j = d_tie;
+  a.unit_lo = (int)(start / UE);
+  a.unit_hi = (int)((end - 1) / UE);
+  a.stage_idx = stage_idx;
+  a.stage_val = stage_val;
+  a.unit_counts = counts;
+  a.flags = flags;
+  a.super_counts = supers;
+  a.super_runs = super_runs;
+  a.cta_offset = (int)cta_lo;
+  if (d_tie)
+    k1_stream<T, kWriteNone, false, false, true, true><<<(unsigned)runs, kStreamThreads, 0, s>>>(a);
+  else
+    k1_stream<T, kWriteNone, false, false, false, true><<<(unsigned)runs, kStreamThreads, 0, s>>>(a);
+  CU(cudaGetLastError());
+  CompactArgs b{};
+  b.stage_idx = stage_idx;
+  b.stage_val = stage_val;
+  b.run_counts = counts;
+  b.super_counts = supers;
+  b.super_clear = supers;
+  b.super_len = 0;  // single use
+  b.num_runs = (int)runs;
+  b.super_runs = super_runs;
+  b.run_stride = (int)per_run;
+  b.sel_idx = d_idx;
+  b.sel_val = d_val;
+  b.cap = cap;
+  b.count = (long long*)d_count;
+  b.flags = flags;
+  CU(launch_pdl(k1_gather<T>, dim3((unsigned)((runs + kGatherWarps - 1) / kGatherWarps)), dim3(kGatherWarps * 32), s, b));
+  CU(cudaFreeAsync(ws, s));
+  return MICRO_OK;
+}
+
+extern "C" {
+
 static int select_range(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end, double delta,
                         const double* d_thr, const long long* d_tie, int32_t* d_idx, void* d_val, int64_t cap,
                         int64_t* d_count, void* stream) {
@@ -176,43 +256,9 @@ static int select_range(int dtype, const void* d_acc, int64_t n_g, int64_t start
     return MICRO_OK;
   }
   if ((uintptr_t)d_acc % 16) return fail(MICRO_EINVAL, "acc not 16-byte aligned");
-  const int TILE = dtype == MICRO_F32 ? tile_elems<float>() : tile_elems<double>();
-  const int64_t tlo = start / TILE, thi = (end - 1) / TILE;
-  const int64_t ntiles = thi - tlo + 1;
-  const int64_t pmax = ntiles + 2;
-  // scratch: status words, ticket, flags (stream-ordered allocator)
-  char* ws = nullptr;
-  const size_t wbytes = sizeof(unsigned long long) * pmax + 16;
-  CU(cudaMallocAsync((void**)&ws, wbytes, s));
-  CU(cudaMemsetAsync(ws, 0, wbytes, s));
-  SelectArgs a{};
-  a.grad = nullptr;
-  a.resid = const_cast<void*>(d_acc);
-  a.n_g = n_g;
-  a.p_start = start;
-  a.p_end = end;
-  a.eta = 1.0;
-  a.delta = d_thr;
-  a.delta_value = delta;
-  a.tie_j = d_tie;
-  a.sel_idx = d_idx;
-  a.sel_val = d_val;
-  a.cap = cap;
-  a.count = (long long*)d_count;
-  a.status = (unsigned long long*)ws;
-  a.p_max = pmax;
-  a.ticket = (unsigned int*)(ws + sizeof(unsigned long long) * pmax);
-  a.flags = (int*)(ws + sizeof(unsigned long long) * pmax + 8);
-  a.epoch = 1;
-  a.tile_lo = tlo;
-  a.num_tiles = ntiles;
   if (dtype == MICRO_F32)
-    k1_fused_select<float, false, kWriteNone><<<(unsigned)ntiles, kThreads, 0, s>>>(a);
-  else
-    k1_fused_select<double, false, kWriteNone><<<(unsigned)ntiles, kThreads, 0, s>>>(a);
-  CU(cudaGetLastError());
-  CU(cudaFreeAsync(ws, s));
-  return MICRO_OK;
+    return select_stream_range<float>(d_acc, n_g, start, end, d_thr, delta, d_tie, d_idx, d_val, cap, d_count, s);
+  return select_stream_range<double>(d_acc, n_g, start, end, d_thr, delta, d_tie, d_idx, d_val, cap, d_count, s);
 }
 
 int micro_select_by_threshold(int dtype, const void* d_acc, int64_t n_g, int64_t start, int64_t end,
