@@ -165,30 +165,60 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   const long long tie_limit = kTie ? *a.tie_j : 0;
   const T eta = (T)a.eta;
   T probe = (T)0;  // becomes NaN iff some G is Inf/NaN
-  unsigned mask[VPL];
+  // bit i * VN + c: element (vector i, lane, component c) is selected
+  unsigned bits = 0;
   bool tie_seen = false;
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    mask[i] = 0;
-#pragma unroll
-    for (int c = 0; c < VN; ++c) {
-      T acc;
-      if (kNoG) {
-        acc = comp(e[i], c);
-      } else {
-        const T gv = comp(g[i], c);
-        probe = nan_probe_s(gv, probe);
-        acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
-      }
-      set_comp(e[i], c, acc);
-      bool sel = sel_unit && absx(acc) > thr;
-      if (kTie) tie_seen |= sel_unit && absx(acc) == thr;
-      if (!all_in) {
-        const int j = base + (i * 32 + lane) * VN + c;
-        sel = sel && j >= a.p_start && j < a.p_end;
-      }
-      mask[i] |= (unsigned)sel << c;
+  V out[VPL];  // e_{t+1} as stored (own selections zeroed when EF is on)
+  static_assert(!(kTie && kMode == kWriteZeroSel), "tie selections are never zeroed here");
+  // one element: acc, the compare, the stored value.  `ranged`: the unit
+  // straddles the partition's ends (or is the vector's partial last unit).
+  auto element = [&](int i, int c, bool ranged) {
+    T acc;
+    if (kNoG) {
+      acc = comp(e[i], c);
+    } else {
+      const T gv = comp(g[i], c);
+      probe = nan_probe_s(gv, probe);
+      acc = add_rn(comp(e[i], c), mul_rn(eta, gv));  // two roundings, no FMA
     }
+    set_comp(e[i], c, acc);
+    bool sel = absx(acc) > thr;
+    if (kTie) tie_seen |= absx(acc) == thr;
+    if (ranged) {
+      const int j = base + (i * 32 + lane) * VN + c;
+      sel = sel && j >= a.p_start && j < a.p_end;
+    }
+    if (sel) bits |= 1u << (i * VN + c);
+    set_comp(out[i], c, (kMode == kWriteZeroSel && sel) ? (T)0 : acc);
+  };
+  // warp-uniform branches: the common case (every element of the unit in the
+  // partition) carries no index arithmetic
+  if (sel_unit && all_in) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) element(i, c, false);
+  } else if (sel_unit) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) element(i, c, true);
+  } else {  // outside the partition: accumulate only
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        T acc;
+        if (kNoG) {
+          acc = comp(e[i], c);
+        } else {
+          const T gv = comp(g[i], c);
+          probe = nan_probe_s(gv, probe);
+          acc = add_rn(comp(e[i], c), mul_rn(eta, gv));
+        }
+        set_comp(e[i], c, acc);
+        set_comp(out[i], c, acc);
+      }
   }
   // top-k: ties at the pivot are selected up to index J.  They are rare, so
   // the index comparisons run only in the warps that hold one.
@@ -200,34 +230,41 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
         const int j = base + (i * 32 + lane) * VN + c;
         const bool tie = sel_unit && absx(comp(e[i], c)) == thr && (long long)j <= tie_limit &&
                          (all_in || (j >= a.p_start && j < a.p_end));
-        mask[i] |= (unsigned)tie << c;
+        if (tie) bits |= 1u << (i * VN + c);
       }
   }
+  constexpr unsigned VMASK = (1u << VN) - 1u;
 
   if (kPf) {
 #pragma unroll
     for (int i = 0; i < VPL; ++i)
-      if (mask[i]) prefetch_l2_keep((const T*)a.model + base + (i * 32 + lane) * VN);
+      if ((bits >> (i * VN)) & VMASK) prefetch_l2_keep((const T*)a.model + base + (i * 32 + lane) * VN);
   }
   if (kMode != kWriteNone) {
+    if (elems == UE) {
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      V out = e[i];
-      if (kMode == kWriteZeroSel) {
+      for (int i = 0; i < VPL; ++i) st_hint(reinterpret_cast<V*>(E) + i * 32 + lane, out[i], pol_stream);
+    } else {
 #pragma unroll
-        for (int c = 0; c < VN; ++c)
-          if (mask[i] & (1u << c)) set_comp(out, c, (T)0);
-      }
-      if (elems == UE) {
-        st_hint(reinterpret_cast<V*>(E) + i * 32 + lane, out, pol_stream);
-      } else {
+      for (int i = 0; i < VPL; ++i)
 #pragma unroll
         for (int c = 0; c < VN; ++c) {
           const int off = (i * 32 + lane) * VN + c;
-          if (off < elems) E[off] = comp(out, c);
+          if (off < elems) E[off] = comp(out[i], c);
         }
-      }
     }
+  }
+
+  // kNorm: this lane's part of ||e_{t+1}||^2 (the stored values; zeros add nothing)
+  double sq = 0.0;
+  if (kNorm) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i)
+#pragma unroll
+      for (int c = 0; c < VN; ++c) {
+        const double y = (double)comp(out[i], c);
+        sq += y * y;
+      }
   }
 
   if (kDense && live) {  // live is warp-uniform: the shuffles below see every lane
@@ -241,8 +278,8 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
     T* D = (T*)a.dense + base;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
-      const bool half = mask[i] != 0;
-      bool sec = half;  // the lanes of one kDenseLanes * 16-byte chunk agree (every lane shuffles)
+      const unsigned m = (bits >> (i * VN)) & VMASK;
+      bool sec = m != 0;  // the lanes of one kDenseLanes * 16-byte chunk agree (every lane shuffles)
 #pragma unroll
       for (int o = 1; o < kDenseLanes; o <<= 1) {
         const bool peer = __shfl_xor_sync(0xffffffffu, sec, o);  // unconditional: no short-circuit
@@ -251,16 +288,16 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       const unsigned secbits = even_bits(__ballot_sync(0xffffffffu, sec));
       now |= (unsigned long long)secbits << (16 * i);
       if (sec || ((prev >> (16 * i + (lane >> 1))) & 1ull)) {
-        V out;
+        V dv;
 #pragma unroll
-        for (int c = 0; c < VN; ++c) set_comp(out, c, (mask[i] & (1u << c)) ? comp(e[i], c) : (T)0);
+        for (int c = 0; c < VN; ++c) set_comp(dv, c, (m & (1u << c)) ? comp(e[i], c) : (T)0);
         if (elems == UE) {
-          st_hint(reinterpret_cast<V*>(D) + i * 32 + lane, out, pol_stream);
+          st_hint(reinterpret_cast<V*>(D) + i * 32 + lane, dv, pol_stream);
         } else {
 #pragma unroll
           for (int c = 0; c < VN; ++c) {
             const int off = (i * 32 + lane) * VN + c;
-            if (off < elems) D[off] = comp(out, c);
+            if (off < elems) D[off] = comp(dv, c);
           }
         }
       }
@@ -277,7 +314,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   if (sel_cta) {
     unsigned packed = 0;
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) packed |= (unsigned)__popc(mask[i]) << (8 * i);  // mask = 0 unless sel_unit
+    for (int i = 0; i < VPL; ++i) packed |= (unsigned)__popc((bits >> (i * VN)) & VMASK) << (8 * i);  // 0 unless sel_unit
     unsigned incl = packed;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -285,10 +322,18 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       if (lane >= o) incl += y;
     }
     const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned unit_count = 0;
+    const unsigned excl = incl - packed;
+    // first position of this lane's pairs of vector i: the warp's pairs of
+    // vectors < i + this vector's pairs in lanes < this one (sums reach 512:
+    // not packable in bytes)
+    int first[VPL];
+    int unit_count = 0;
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) unit_count += (tot >> (8 * i)) & 0xFFu;
-    if (lane == 0) s_cnt[w] = (int)unit_count;
+    for (int i = 0; i < VPL; ++i) {
+      first[i] = unit_count + (int)((excl >> (8 * i)) & 0xFFu);
+      unit_count += (int)((tot >> (8 * i)) & 0xFFu);
+    }
+    if (lane == 0) s_cnt[w] = unit_count;
     __syncthreads();
     int woff = 0, cta_count = 0;
 #pragma unroll
@@ -303,40 +348,28 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       if (cta_count) atomicAdd(a.super_counts + slot / a.super_runs, cta_count);
     }
     if (unit_count) {
-      const unsigned excl = incl - packed;
       const unsigned long long pol_keep = policy_evict_last();  // read back by k1_gather, then discarded
       int32_t* __restrict__ si = a.stage_idx + (long long)slot * (kStreamWarps * UE) + woff;
       T* __restrict__ sv = (T*)a.stage_val + (long long)slot * (kStreamWarps * UE) + woff;
-      unsigned cb = 0;
+      // one iteration per selected component (a warp runs its lanes' maximum)
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
-        if (mask[i]) {
-          int pos = (int)(cb + ((excl >> (8 * i)) & 0xFFu));
-          const int j0 = base + (i * 32 + lane) * VN;
-#pragma unroll
-          for (int c = 0; c < VN; ++c)
-            if (mask[i] & (1u << c)) {
-              st_hint(si + pos, j0 + c, pol_keep);
-              st_hint(sv + pos, comp(e[i], c), pol_keep);
-              ++pos;
-            }
+        unsigned m = (bits >> (i * VN)) & VMASK;
+        int pos = first[i];
+        const int j0 = base + (i * 32 + lane) * VN;
+        while (m) {
+          const int c = __ffs(m) - 1;
+          m &= m - 1;
+          st_hint(si + pos, j0 + c, pol_keep);
+          st_hint(sv + pos, comp(e[i], c), pol_keep);
+          ++pos;
         }
-        cb += (tot >> (8 * i)) & 0xFFu;
       }
     }
   }
   if (probe != probe) atomicOr(a.flags, 1);
   pdl_trigger();  // this CTA's results are written: k1_gather may start launching
   if (kNorm) {  // the stored e_{t+1}: acc with the own selections zeroed (EF on)
-    double sq = 0.0;
-#pragma unroll
-    for (int i = 0; i < VPL; ++i)
-#pragma unroll
-      for (int c = 0; c < VN; ++c)
-        if (!(mask[i] & (1u << c))) {
-          const double y = (double)comp(e[i], c);
-          sq += y * y;
-        }
     // CTA partial only: no fence, no ticket on the streaming pass (a
     // per-CTA release costs ~20 % of K1); k1_gather's extra CTA sums them
     __shared__ double s_sq[kStreamWarps];
