@@ -101,15 +101,6 @@ class ClockSampler:
                 "reasons": [v for k, v in self.NAMES.items() if self.reasons & k]}
 
 
-def traffic_from_profiles(workload: str):
-    p = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            j = json.load(f)
-        return j.get(workload)
-    return None
-
-
 # ---------------------------------------------------------------- reference
 
 
