@@ -131,7 +131,7 @@ def _fresh_normal(rng_pool, out: np.ndarray):
 
 def run_reference_converged(n_g: int, n: int, d: float, steps: int, warmup: int, adapt_iters: int = 1000,
                             adapt_n: int = 1 << 20, dense: bool = True, model: bool = True, threads: int = 1,
-                            seed: int = SEED):
+                            seed: int = SEED, grad32: bool = False):
     """The reference's own hot-path code (oracle/_ref: its sparsifier and
     collectives TUs compiled verbatim, re-driven in run_iteration's order),
     fp64, timed in the STATIONARY regime:
@@ -146,6 +146,10 @@ def run_reference_converged(n_g: int, n: int, d: float, steps: int, warmup: int,
       3. `warmup` + `steps` iterations at the full n_g, a fresh gradient per
          step generated outside the timed region; each step is timed alone.
 
+    grad32: every gradient is rounded to fp32 values first (BASELINE's "fp32
+    gradient"), outside the timed region; the reference computes on them in
+    fp64, as our f64 engine does on the same fp32 gradients.
+
     Returns per-step seconds, the realised density of each timed step, the
     first timed iteration and a description."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -157,8 +161,13 @@ def run_reference_converged(n_g: int, n: int, d: float, steps: int, warmup: int,
     small = RefCluster(n_s, n, density=d, delta0=delta0, alpha=ALPHA)
     small.set_options(dense=False, threads=threads)
     Gs = np.empty((n, n_s))
+    def fresh(buf):
+        _fresh_normal(pool, buf)
+        if grad32:
+            np.copyto(buf, buf.astype(np.float32))
+
     for t in range(adapt_iters):
-        _fresh_normal(pool, Gs)
+        fresh(Gs)
         small.step(Gs, ETA, t)
     res = [small.residual(i) for i in range(n)]
     thr = np.empty(n)
@@ -177,7 +186,7 @@ def run_reference_converged(n_g: int, n: int, d: float, steps: int, warmup: int,
     times, dens = [], []
     t = adapt_iters
     for s in range(warmup + steps):
-        _fresh_normal(pool, G)
+        fresh(G)
         t0 = time.perf_counter()
         r = ref.step(G, ETA, t)
         dt = time.perf_counter() - t0
@@ -186,7 +195,8 @@ def run_reference_converged(n_g: int, n: int, d: float, steps: int, warmup: int,
             times.append(dt)
             dens.append(r["union_idx"].size / n_g)
     sample = (f"{steps} timed iterations (after {warmup} warm-up) at the full n_g={n_g}, n={n} workers "
-              f"({'serially on 1 thread' if threads == 1 else f'per-worker loops on {threads} threads'}), fp64, "
+              f"({'serially on 1 thread' if threads == 1 else f'per-worker loops on {threads} threads'}), fp64"
+              f"{' on fp32-valued gradients' if grad32 else ''}, "
               f"the reference's sparsifier/collectives TUs compiled verbatim (oracle/_ref) driven in "
               f"run_iteration order with the model update{' and the dense all_reduce_sparse / n' if dense else ''}; "
               f"stationary start: {adapt_iters} adaptation iterations at n_s={n_s} (fresh N(0,1) gradients), "
@@ -201,14 +211,16 @@ def reference_arm(args, wl):
     n = args.gpus
     threads = max(1, min(n, len(os.sched_getaffinity(0))))
     r = run_reference_converged(wl["n_g"], n, wl["d"], args.steps, args.warmup, adapt_iters=args.prime,
-                                dense=args.dense, model=args.model, threads=threads, seed=args.seed)
+                                dense=args.dense, model=args.model, threads=threads, seed=args.seed,
+                                grad32=args.grad == "f32")
     per = statistics.mean(r["times"])
     us = per * 1e6
     dens = float(np.mean(r["density"]))
     line = {"metric": METRIC, "value": us, "unit": "us/iter", "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic N(0,1) gradients (numpy, fresh per step)",
+            "data": ("synthetic N(0,1) gradients rounded to fp32 values (numpy, fresh per step)" if args.grad == "f32"
+                     else "synthetic N(0,1) gradients (numpy, fresh per step)"),
             "impl": "reference",
             "config": bench_config(args, wl, n),
             "protocol": {"adaptation_iterations": args.prime, "first_timed_t": r["first_timed_t"],
@@ -238,6 +250,9 @@ def bench_config(args, wl, world: int) -> dict:
             "error_norm_recorded": bool(args.error_norm), "sparsifier": args.sparsifier,
             "arithmetic": "f64 (the reference's own, bit-exact with its code)" if args.dtype == "f64"
             else "f32 (the north star's gradient type)",
+            "gradient": ("f32 (BASELINE configs' 'fp32 gradient'; widened exactly into the f64 state, so the "
+                         "reference computes on the same values)" if args.dtype == "f64" and args.grad == "f32"
+                         else args.dtype),
             "parallelism": (f"dp{world} (exclusive cyclic partitions"
                             + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
                             f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)"),
@@ -259,8 +274,16 @@ def traffic_from_profiles(key: str):
     return None, None
 
 
-def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
-    """Adapt, warm up and time K steps of the device path at dtype tdt.
+def grad_dtype(args, tdt):
+    """The gradients' element type: fp32 (BASELINE's "fp32 gradient"; widened
+    exactly into the f64 state when the arithmetic is f64) or the arithmetic's."""
+    import torch
+    return torch.float32 if args.grad == "f32" else tdt
+
+
+def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False, gdt=None):
+    """Adapt, warm up and time K steps of the device path at dtype tdt
+    (gradients of dtype gdt, default grad_dtype(args, tdt)).
     Returns the measurement dict (and the engine + buffers when keep)."""
     import torch
 
@@ -269,15 +292,18 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     n_g, d = wl["n_g"], wl["d"]
     delta0 = warm_delta0(d)
     esz = 8 if tdt == torch.float64 else 4
+    gdt = gdt or grad_dtype(args, tdt)
+    gsz = 8 if gdt == torch.float64 else 4
     W = args.cluster_workers if (world == 1 and args.cluster_workers > 1) else 1
     if dist is not None:
         from paper_2310_00967_b200.dist import DistMicro
         m = DistMicro(n_g, transport=args.transport, density=d, initial_threshold=delta0, scaling_factor=ALPHA,
-                      dense_output=args.dense, record_error_norm=args.error_norm, dtype=tdt,
+                      dense_output=args.dense, record_error_norm=args.error_norm, dtype=tdt, grad_dtype=gdt,
                       comm_device="cpu" if args.dist_backend == "gloo" else None)
     else:
         m = engine.Micro(n_g, W, density=d, initial_threshold=delta0, scaling_factor=ALPHA, dense_output=args.dense,
-                         record_error_norm=args.error_norm, sparsifier=args.sparsifier, dtype=tdt)
+                         record_error_norm=args.error_norm, sparsifier=args.sparsifier, dtype=tdt,
+                         grad_dtype=gdt)
     stream = torch.cuda.current_stream(dev)
     # the model update x -= g/n at the union is part of the reference's
     # iteration (harness.cpp:212-215)
@@ -292,7 +318,7 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     # when memory allows (same statistics as the prime phase), otherwise R
     # buffers rotated.
     t = 0
-    gen = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(W)]
+    gen = [torch.empty(n_g, device=dev, dtype=gdt) for _ in range(W)]
     for _ in range(args.prime):
         for i in range(W):
             engine.synth_gaussian(gen[i], args.seed, rank + i, t)
@@ -301,8 +327,8 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     del gen
     torch.cuda.synchronize()
     need = (args.warmup + args.steps) * W
-    R = max(W + 1, min(need, args.buffers, int(0.5 * torch.cuda.mem_get_info(dev)[0] // (esz * n_g))))
-    G = [torch.empty(n_g, device=dev, dtype=tdt) for _ in range(R)]
+    R = max(W + 1, min(need, args.buffers, int(0.5 * torch.cuda.mem_get_info(dev)[0] // (gsz * n_g))))
+    G = [torch.empty(n_g, device=dev, dtype=gdt) for _ in range(R)]
     for r in range(R):
         engine.synth_gaussian(G[r], args.seed, rank + r % W, t + r)
     t0_bufs = t
@@ -340,7 +366,7 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     # a 256 MB write (evicts the step's lines) then a 256 MB read (so the
     # flush's own dirty lines are written back inside the flush, not charged
     # to the next step).  At C3 and up the inputs are larger than L2.
-    flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and 3 * esz * n_g < 2 * 126e6)
+    flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and (2 * esz + gsz) * n_g < 2 * 126e6)
     scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
     scratch2 = torch.empty(64 << 20, dtype=torch.float32, device=dev) if flush else None
     per_step = flush or fresh  # each step timed alone (events around the step only)
@@ -388,7 +414,7 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
     K = hist["K"].astype(np.float64)
     k_own = hist["counts"][:, 0].astype(np.float64)
     out = dict(ms_step=ms_step, step_ms=step_ms, k1a_ms=k1a_ms, xchg_ms=xchg_ms, K=K, k_own=k_own, R=R,
-               flush=flush, fresh=fresh, t_first=t_first, t_next=t, W=W, esz=esz, clocks=clk.summary(),
+               flush=flush, fresh=fresh, t_first=t_first, t_next=t, W=W, esz=esz, gsz=gsz, clocks=clk.summary(),
                transport=getattr(m, "transport", None))
     if keep:
         out.update(m=m, G=G)
@@ -401,7 +427,7 @@ def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False):
 
 def roofline_of(args, r, wl, world, peak, peak_kind):
     """Algorithmic bytes of the dominant kernel (k1_stream) and of the step."""
-    n_g, W, esz = wl["n_g"], r["W"], r["esz"]
+    n_g, W, esz, gsz = wl["n_g"], r["W"], r["esz"], r["gsz"]
     K, k_own = r["K"], r["k_own"]
     # k1_stream: read e and G, write e (all n_g, SURVEY.md P4) + one (int32,
     # value) pair per selection; with the dense g/n (fused at n = 1) the
@@ -410,7 +436,7 @@ def roofline_of(args, r, wl, world, peak, peak_kind):
     # it); CLT-k's leader is top-k, its other workers select by threshold.
     acc_only = {"topk": W, "cltk": 1}.get(args.sparsifier, 0)
     dense_fused = args.dense and world == 1 and W == 1 and args.sparsifier == "micro"
-    k1_bytes = ((esz * n_g * (acc_only + 3.0 * (W - acc_only)) / W) + (4.0 + esz) * float(k_own.mean())
+    k1_bytes = ((n_g * (esz * acc_only + (2.0 * esz + gsz) * (W - acc_only)) / W) + (4.0 + esz) * float(k_own.mean())
                 + (2.0 * esz * float(K.mean()) if dense_fused else 0.0))
     k1a_avg_ms = statistics.mean(r["k1a_ms"]) if r["k1a_ms"] else r["ms_step"]
     achieved = k1_bytes / (k1a_avg_ms * 1e-3) / 1e9
@@ -453,13 +479,14 @@ def our_arm(args, wl):
             tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
     r = device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=True)
-    m, G, W, esz = r["m"], r["G"], r["W"], r["esz"]
+    m, G, W, esz, gsz = r["m"], r["G"], r["W"], r["esz"], r["gsz"]
+    gdt = grad_dtype(args, tdt)
     t = r["t_next"]
     ms_step, K, k_own = r["ms_step"], r["K"], r["k_own"]
     density = float(K.mean() / n_g)
     peak, peak_kind = peaks()
     roof = roofline_of(args, r, wl, world, peak, peak_kind)
-    tkey = f"{args.workload}_{args.dtype}{'_dense' if args.dense else ''}"
+    tkey = f"{args.workload}_{args.dtype}{'_g32' if gsz != esz else ''}{'_dense' if args.dense else ''}"
     roof["traffic"], roof["traffic_source"] = traffic_from_profiles(tkey)
     # our kernels per step: k1_stream, k1_gather (+ threshold update + model
     # update + dense g/n) at n = 1; a W-worker cluster: 2 per worker +
@@ -481,10 +508,10 @@ def our_arm(args, wl):
         # as the timed steps; re-feeding one gradient would make the residual
         # grow coherently and inflate the selection)
         ke = max(3, min(args.steps, 10))
-        nb = int(max(2, min(ke + 1, 16e9 // (esz * n_g * W))))  # <= 16 GB of pinned host gradients
+        nb = int(max(2, min(ke + 1, 16e9 // (gsz * n_g * W))))  # <= 16 GB of pinned host gradients
         hGs = []
         for b in range(nb):
-            hG = torch.empty(W * n_g, dtype=tdt).pin_memory()
+            hG = torch.empty(W * n_g, dtype=gdt).pin_memory()
             for i in range(W):
                 engine.synth_gaussian(G[i], args.seed, rank + i, t + 1 + b)  # fresh: steps t+1 .. t+nb
                 hG[i * n_g:(i + 1) * n_g].copy_(G[i].cpu())
@@ -495,29 +522,33 @@ def our_arm(args, wl):
         t += 1
         kk = []
         t0 = time.perf_counter()
+        per = []
         for s in range(ke):
-            i_, _s = m.step_host(hGs[s % (nb - 1)], ETA, t, idx, sums)
+            ts = time.perf_counter()
+            i_, _s = m.step_host(hGs[s % (nb - 1)], ETA, t, idx, sums)  # returns after the D2H landed
+            per.append(time.perf_counter() - ts)
             kk.append(i_.size)
             t += 1
         e2e_s = (time.perf_counter() - t0) / ke
-        e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g * W,
+        e2e = {"value": e2e_s * 1e6, "unit": "us/iter", "h2d_bytes_per_step": gsz * n_g * W,
+               "median_us_per_step": statistics.median(per) * 1e6, "min_us_per_step": min(per) * 1e6,
                "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
                "api": "micro_step_host (include/micro.h)",
                "host_gradients": f"{nb - 1} distinct pinned buffers over {ke} steps",
                "density": float(statistics.mean(kk)) / n_g,
                # what bounds it: the H2D of the gradient over PCIe (Gen5 x16: ~64 GB/s nominal)
-               "h2d_gbs_effective": esz * n_g * W / e2e_s / 1e9}
+               "h2d_gbs_effective": gsz * n_g * W / e2e_s / 1e9}
         del hGs
     else:
         # N ranks: each copies its own pinned host gradient in, steps through
         # DistMicro, and reads the union back; the max over ranks is reported
         ke = max(3, min(args.steps, 10))
-        nb = int(max(2, min(ke + 1, 4e9 // (esz * n_g))))
+        nb = int(max(2, min(ke + 1, 4e9 // (gsz * n_g))))
         hGs = []
         for b in range(nb):
             engine.synth_gaussian(G[0], args.seed, rank, t + 1 + b)
             hGs.append(G[0].cpu().pin_memory())
-        dG = torch.empty(n_g, device=dev, dtype=tdt)
+        dG = torch.empty(n_g, device=dev, dtype=gdt)
         idx = torch.empty(n_g, dtype=torch.int32).pin_memory().numpy()
         sums = torch.empty(n_g, dtype=tdt).pin_memory().numpy()
         dG.copy_(hGs[-1], non_blocking=True)
@@ -537,7 +568,7 @@ def our_arm(args, wl):
         torch.cuda.synchronize()
         v = torch.tensor([(time.perf_counter() - t0) / ke], device=cdev, dtype=torch.float64)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(v[0]) * 1e6, "unit": "us/iter", "h2d_bytes_per_step": esz * n_g,
+        e2e = {"value": float(v[0]) * 1e6, "unit": "us/iter", "h2d_bytes_per_step": gsz * n_g,
                "d2h_bytes_per_step": int((4 + esz) * statistics.mean(kk) + 8 + 4),
                "api": "DistMicro.step + union (paper_2310_00967_b200/dist.py)",
                "host_gradients": f"{nb - 1} distinct pinned buffers per rank over {ke} steps",
@@ -557,13 +588,24 @@ def our_arm(args, wl):
                  "unit": "us/iter", "density": float(ro["K"].mean() / n_g),
                  "roofline": {k: rf[k] for k in ("achieved", "peak", "frac", "algorithmic_bytes_per_launch",
                                                  "avg_launch_ms", "step_frac")}}
+    # ---- f64 arithmetic on f64 gradients (the reference's own input type) ----
+    other_grad = None
+    if (world == 1 and args.sparsifier == "micro" and not args.no_other_dtype and tdt == torch.float64
+            and gsz != esz):
+        ro = device_measure(args, wl, tdt, None, world, rank, local, dev, gdt=torch.float64)
+        rf = roofline_of(args, ro, wl, world, peak, peak_kind)
+        other_grad = {"dtype": "f64", "gradient": "f64", "value": ro["ms_step"] * 1e3, "unit": "us/iter",
+                      "density": float(ro["K"].mean() / n_g),
+                      "roofline": {k: rf[k] for k in ("achieved", "peak", "frac", "algorithmic_bytes_per_launch",
+                                                      "avg_launch_ms", "step_frac")}}
 
     # ---- CPU baseline: the reference's own code on this host (rank 0, N = 1) ----
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
             cr = run_reference_converged(n_g, W, d, steps=args.cpu_steps, warmup=1, adapt_iters=args.prime,
-                                         dense=args.dense, model=args.model, threads=1, seed=args.seed)
+                                         dense=args.dense, model=args.model, threads=1, seed=args.seed,
+                                         grad32=gsz == 4)
             cd = float(np.mean(cr["density"]))
             cpu = {"value": statistics.mean(cr["times"]) * 1e6, "unit": "us/iter", "cores": 1, "kind": "reference",
                    "sample": cr["sample"], "density": cd, "first_timed_t": cr["first_timed_t"],
@@ -591,7 +633,7 @@ def our_arm(args, wl):
             "metric": METRIC, "value": ms_step * 1e3, "unit": "us/iter", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype,
-            "data": f"synthetic N(0,1) {args.dtype} gradients (include/micro_synth.h)",
+            "data": f"synthetic N(0,1) {'f32' if gsz == 4 else 'f64'} gradients (include/micro_synth.h)",
             "config": bench_config(args, wl, world),
             "protocol": {"adaptation_iterations": args.prime, "first_timed_t": r["t_first"], "seed": args.seed,
                          "inputs": (f"{R} resident N(0,1) gradient buffers ("
@@ -599,9 +641,9 @@ def our_arm(args, wl):
                                        "each step's gradient generated fresh into them just before the step, "
                                        "outside its events; steps timed one by one")
                                     + (f"); L2 flushed between timed steps (256 MB write + 256 MB read outside "
-                                       f"the per-step events: the working set {3 * esz * n_g / 1e6:.0f} MB would "
-                                       f"fit L2)" if r["flush"] else f"); each {esz}*n_g bytes > L2 (no flush "
-                                       f"needed)" if esz * n_g > 126e6 else "); L2 NOT flushed (--flush-l2 off)")),
+                                       f"the per-step events: the working set {(2 * esz + gsz) * n_g / 1e6:.0f} MB "
+                                       f"would fit L2)" if r["flush"] else f"); each {gsz}*n_g bytes > L2 (no flush "
+                                       f"needed)" if gsz * n_g > 126e6 else "); L2 NOT flushed (--flush-l2 off)")),
                          "median_us_per_step": (float(np.median(r["step_ms"])) * 1e3 if r["step_ms"] else None)},
             "density": density, "density_rel_err": density / d - 1.0,
             "density_reference": (cpu or {}).get("density"),
@@ -612,6 +654,7 @@ def our_arm(args, wl):
             "roofline": roof,
             "exchange": exchange_line,
             "other_dtype": other,
+            "other_gradient": other_grad,
             "clocks": r["clocks"],
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
@@ -634,6 +677,9 @@ def main():
     ap.add_argument("--buffers", type=int, default=256, help="max resident gradient buffers")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grad", choices=["f32", "same"], default="f32",
+                    help="gradient element type: f32 (BASELINE's fp32 gradient; widened exactly into f64 state "
+                         "with --dtype f64) or the arithmetic's own")
     ap.add_argument("--no-dense", dest="dense", action="store_false",
                     help="skip the dense averaged gradient g/n (all_reduce_sparse / n, collectives.cpp:51-57)")
     ap.add_argument("--cluster-workers", type=int, default=1,

@@ -159,7 +159,16 @@ typedef struct micro_config {
   int32_t sparsifier;         /* SparsifierKind (sparsifier.hpp:21): MICRO_MICRO (default) or a
                                  comparison sparsifier of harness.cpp:152-181 (single-device
                                  cluster only) */
+  int32_t grad_dtype;         /* element type of the gradients passed to micro_compress /
+                                 micro_step / micro_step_host: MICRO_GRAD_SAME (0, default) = dtype;
+                                 MICRO_GRAD_F32 = fp32 gradients (BASELINE's "fp32 gradient") into
+                                 fp64 state and arithmetic (dtype MICRO_F64, MiCRO only).  (double)g
+                                 is exact, so results equal the reference's run on the same gradient
+                                 values; G moves 4 B per element instead of 8. */
 } micro_config;
+
+/* gradient element types (micro_config.grad_dtype) */
+enum { MICRO_GRAD_SAME = 0, MICRO_GRAD_F32 = 1 };
 
 /* sparsifier kinds (sparsifier.hpp:21) */
 enum {

@@ -456,7 +456,10 @@ struct IterationRecord {
 // e_{i,t+1} and delta_{i,t+1} on the device.
 class MicroEngine {
  public:
-  MicroEngine(Index n_g, int workers, const SparsifierConfig& sc, bool error_feedback = true, int dtype = MICRO_F64)
+  // grad_dtype MICRO_GRAD_F32 (with dtype MICRO_F64): step() takes fp32
+  // gradients; state and arithmetic stay fp64 (include/micro.h).
+  MicroEngine(Index n_g, int workers, const SparsifierConfig& sc, bool error_feedback = true, int dtype = MICRO_F64,
+              int grad_dtype = MICRO_GRAD_SAME)
       : n_g_(n_g), n_(workers), esz_(dtype == MICRO_F64 ? 8 : 4) {
     micro_config cfg;
     micro_config_default(&cfg);
@@ -464,6 +467,7 @@ class MicroEngine {
     cfg.n_workers = workers;
     cfg.n_local = workers;
     cfg.dtype = dtype;
+    cfg.grad_dtype = grad_dtype;
     cfg.density = sc.density;
     cfg.initial_threshold = sc.initial_threshold;
     cfg.scaling_factor = sc.scaling_factor;
@@ -482,7 +486,8 @@ class MicroEngine {
     micro_host_free(h_sums_);
   }
 
-  // h_grads: workers * n_g elements of the engine's dtype (double for MICRO_F64).
+  // h_grads: workers * n_g elements of the engine's dtype (double for MICRO_F64),
+  // or float with grad_dtype MICRO_GRAD_F32.
   AggregatedSelection step(const void* h_grads, double eta, std::int64_t t, std::vector<double>* summed = nullptr) {
     if (!h_idx_) {  // pinned result buffers, allocated once (full-bandwidth D2H, no per-step zeroing)
       b200::check(micro_host_malloc(reinterpret_cast<void**>(&h_idx_), (int64_t)n_g_ * 4));

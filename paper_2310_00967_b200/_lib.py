@@ -28,7 +28,7 @@ class micro_config(C.Structure):
         ("n_g", I64), ("n_workers", I32), ("n_local", I32), ("rank", I32), ("dtype", I32),
         ("density", DBL), ("initial_threshold", DBL), ("scaling_factor", DBL), ("min_threshold", DBL),
         ("target", I32), ("error_feedback", I32), ("dense_output", I32), ("device", I32),
-        ("selection_capacity", I64), ("record_error_norm", I32), ("sparsifier", I32),
+        ("selection_capacity", I64), ("record_error_norm", I32), ("sparsifier", I32), ("grad_dtype", I32),
     ]
 
 
@@ -50,6 +50,7 @@ class micro_dist_bufs(C.Structure):
 
 MICRO_NCCL_UNIQUE_ID_BYTES = 128
 MICRO_XCHG_PEER, MICRO_XCHG_NCCL = 0, 1
+MICRO_GRAD_SAME, MICRO_GRAD_F32 = 0, 1  # micro_config.grad_dtype
 
 
 class MicroError(RuntimeError):

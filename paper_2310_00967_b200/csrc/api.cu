@@ -4,6 +4,7 @@
 // path exists: every array operation is a device kernel; the host only
 // validates, sizes launches and moves small scalars.
 // (dist_api.cu: one rank of an n-GPU job; value_api.cu: stateless calls.)
+#include <type_traits>
 #include "internal.cuh"
 
 using namespace micro;
@@ -199,7 +200,7 @@ int check_ctx(micro_ctx* c) {
 
 int ensure_staging(micro_ctx* c) {
   if (c->staging) return MICRO_OK;
-  c->staging_stride = ((size_t)c->n_g * c->esz + 255) / 256 * 256;
+  c->staging_stride = ((size_t)c->n_g * c->gsz + 255) / 256 * 256;
   cudaError_t e = cudaMalloc(&c->staging, c->staging_stride * c->n_local);
   if (e != cudaSuccess) {
     c->staging = nullptr;
@@ -244,7 +245,7 @@ int launch_sumsq(micro_ctx* c, int i) {
 // the model's selected lines during k1_stream (C1: 140 MB; C3: 1.66 GB does not).
 constexpr int64_t kPrefetchStepBytes = 256ll << 20;
 
-template <typename T>
+template <typename T, typename TG = T>
 int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t ps, int64_t pe,
                      const double* thr = nullptr, const long long* tie = nullptr, bool acc_in_e = false) {
   constexpr int UE = stream_unit_elems<T>();
@@ -278,20 +279,24 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   const bool timed = c->timing && c->t_next < kTimingCap && (c->t_seen++ % c->timing_period) == 0;
   if (timed) CU(cudaEventRecord(c->t_ev[2 * c->t_next], st));
   auto dispatch = [&](unsigned g) -> int {
-#define K1S(MODE, D) CU(launch_pdl(k1_stream<T, MODE, D, false>, dim3(g), dim3(kStreamThreads), st, a))
+#define K1S(MODE, D) \
+    CU(launch_pdl(k1_stream<T, MODE, D, false, false, false, false, TG>, dim3(g), dim3(kStreamThreads), st, a))
 #define K1N(D)                                                                                              \
     do {                                                                                                      \
-      if (c->norm) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, true>, dim3(g), dim3(kStreamThreads), st, a)); \
+      if (c->norm) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, true, false, false, false, TG>, dim3(g),      \
+                                 dim3(kStreamThreads), st, a));                                            \
       else K1S(kWriteZeroSel, D);                                                                             \
     } while (0)
     if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
     if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
-      if (acc_in_e)  // top-k: e holds acc already; compact only
-        CU(launch_pdl(k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
-                            dim3(kStreamThreads), st, a));
-      else if (tie)
-        CU(launch_pdl(k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
-      else K1S(kWriteAcc, false);
+      if constexpr (std::is_same<T, TG>::value) {  // (fp32 gradients are MiCRO only)
+        if (acc_in_e)  // top-k: e holds acc already; compact only
+          CU(launch_pdl(k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
+                              dim3(kStreamThreads), st, a));
+        else if (tie)
+          CU(launch_pdl(k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
+        else K1S(kWriteAcc, false);
+      }
     } else if (c->n > 1) {
       if (c->cfg.error_feedback) K1N(false);
       else K1S(kWriteAcc, false);
@@ -299,7 +304,8 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
       // small steps: prefetch x's selected lines into L2 for k1_gather's update
       const bool pf = c->model && (int64_t)c->n_g * (int64_t)c->esz * 3 <= kPrefetchStepBytes;
       if (pf) {
-#define K1P(D, N) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, N, false, false, true>, dim3(g), dim3(kStreamThreads), st, a))
+#define K1P(D, N) \
+  CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, N, false, false, true, TG>, dim3(g), dim3(kStreamThreads), st, a))
         if (fd && c->norm) K1P(true, true);
         else if (fd) K1P(true, false);
         else if (c->norm) K1P(false, true);
@@ -437,6 +443,8 @@ int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   if (c->kind) return launch_baseline<T>(c, i, grad, eta, t);  // grad realigned by micro_compress
   int64_t ps, pe;
   partition_range(c->n_g, c->n, t, c->cfg.rank + i, &ps, &pe);
+  if constexpr (std::is_same<T, double>::value)
+    if (c->gsz == 4) return launch_k1_stream<double, float>(c, i, grad, eta, ps, pe);  // fp32 gradients
   return launch_k1_stream<T>(c, i, grad, eta, ps, pe);
 }
 
@@ -554,6 +562,10 @@ int validate_config(const micro_config* g) {
   if (g->target != MICRO_TARGET_SPLIT && g->target != MICRO_TARGET_FULL)
     return fail(MICRO_EINVAL, "unknown per-worker target %d", g->target);
   if (g->selection_capacity < 0) return fail(MICRO_EINVAL, "negative selection capacity");
+  if (g->grad_dtype != MICRO_GRAD_SAME && g->grad_dtype != MICRO_GRAD_F32)
+    return fail(MICRO_EINVAL, "unknown gradient element type %d", g->grad_dtype);
+  if (g->grad_dtype == MICRO_GRAD_F32 && (g->dtype != MICRO_F64 || g->sparsifier != MICRO_MICRO))
+    return fail(MICRO_EINVAL, "fp32 gradients need fp64 state (dtype MICRO_F64) and the MiCRO sparsifier");
   return MICRO_OK;
 }
 
@@ -664,6 +676,7 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->n_local = cfg->n_local;
   c->n_g = cfg->n_g;
   c->esz = dtype_size(cfg->dtype);
+  c->gsz = cfg->grad_dtype == MICRO_GRAD_F32 ? 4 : c->esz;
   c->cluster = c->n_local == c->n;
   c->kind = cfg->sparsifier;
   c->sel_is_union = c->n == 1 && c->kind == 0;
@@ -812,7 +825,7 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
   if (c->compressed) return fail(MICRO_ELOGIC, "micro_compress called twice without aggregation");
   for (int i = 0; i < c->n_local; ++i) {
     if (!d_grads[i]) return fail(MICRO_EINVAL, "null gradient for local worker %d", i);
-    if ((uintptr_t)d_grads[i] % c->esz) return fail(MICRO_EINVAL, "gradient %d misaligned for its dtype", i);
+    if ((uintptr_t)d_grads[i] % c->gsz) return fail(MICRO_EINVAL, "gradient %d misaligned for its dtype", i);
   }
   DeviceGuard dg(c->dev);
   c->t_cur = t;
@@ -824,7 +837,7 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
       // the streaming K1 reads 16-byte vectors: realign once (8 B/elem copy)
       TRY(ensure_staging(c));
       void* dst = (char*)c->staging + (size_t)i * c->staging_stride;
-      if (dst != g) CU(cudaMemcpyAsync(dst, g, (size_t)c->n_g * c->esz, cudaMemcpyDeviceToDevice, c->stream));
+      if (dst != g) CU(cudaMemcpyAsync(dst, g, (size_t)c->n_g * c->gsz, cudaMemcpyDeviceToDevice, c->stream));
       g = dst;
     }
     if (c->esz == 4) TRY(launch_k1<float>(c, i, g, eta, t));
@@ -877,7 +890,7 @@ int micro_step_host(micro_ctx* c, const void* h_grads, double eta, int64_t t, in
   if (!c->cluster) return fail(MICRO_ELOGIC, "micro_step_host: single-device clusters only");
   DeviceGuard dg(c->dev);
   TRY(ensure_staging(c));
-  const size_t row = (size_t)c->n_g * c->esz;
+  const size_t row = (size_t)c->n_g * c->gsz;
   std::vector<const void*> g(c->n_local);
   for (int i = 0; i < c->n_local; ++i) g[i] = (const char*)c->staging + (size_t)i * c->staging_stride;
   if (c->sel_is_union && c->kind == 0) {
@@ -897,8 +910,8 @@ int micro_step_host(micro_ctx* c, const void* h_grads, double eta, int64_t t, in
       const int64_t lo = std::min<int64_t>(c->n_g, per * k * cta_elems);
       const int64_t hi = std::min<int64_t>(c->n_g, per * (k + 1) * cta_elems);
       if (hi > lo)
-        CU(cudaMemcpyAsync((char*)c->staging + lo * c->esz, (const char*)h_grads + lo * c->esz,
-                           (size_t)(hi - lo) * c->esz, cudaMemcpyHostToDevice, c->h2d_stream));
+        CU(cudaMemcpyAsync((char*)c->staging + lo * c->gsz, (const char*)h_grads + lo * c->gsz,
+                           (size_t)(hi - lo) * c->gsz, cudaMemcpyHostToDevice, c->h2d_stream));
       CU(cudaEventRecord(c->h2d_ev[k], c->h2d_stream));
     }
     c->h2d_chunks = micro_ctx::kH2DChunks;

@@ -109,6 +109,26 @@ __device__ __forceinline__ double2 ld_nc_hint(const double2* p, unsigned long lo
                : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
   return r;
 }
+// The gradient's vector of VN elements (K1's G loads): the state's own
+// vector, or VN fp32 values widened exactly to the fp64 state (float2 ->
+// double2: 8 B per lane).
+template <typename TG, int VN>
+struct GradVec;
+template <>
+struct GradVec<float, 4> { using V = float4; };
+template <>
+struct GradVec<double, 2> { using V = double2; };
+template <>
+struct GradVec<float, 2> { using V = float2; };
+template <typename V>
+__device__ __forceinline__ V ld_grad(const V* p, unsigned long long pol) { return ld_nc_hint(p, pol); }
+template <typename V>
+__device__ __forceinline__ V ld_grad(const float2* p, unsigned long long pol) {
+  float2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+               : "=f"(r.x), "=f"(r.y) : "l"(p), "l"(pol));
+  return V{(double)r.x, (double)r.y};
+}
 __device__ __forceinline__ void st_hint(float4* p, const float4& v, unsigned long long pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x),
                "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)

@@ -112,6 +112,7 @@ struct micro_ctx {
   int n = 1, n_local = 1;
   int64_t n_g = 0;
   size_t esz = 4;
+  size_t gsz = 4;  // gradient element size (esz, or 4 for fp32 gradients into fp64 state)
   uint64_t k_worker = 0;
   int64_t sel_cap = 0, uni_cap = 0;
   bool cluster = true;  // n_local == n

@@ -116,7 +116,13 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 // kPf (small steps, n = 1 with the model update): the lines of x at this
 // unit's selections are prefetched into L2 while the stream runs, taking the
 // model's DRAM latency off k1_gather's critical path.
-template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false, bool kPf = false>
+// TG: the gradient's element type.  TG = float with T = double: fp32
+// gradients (BASELINE's "fp32 gradient") into the reference's fp64 state and
+// arithmetic — (double)g is exact, so acc = e + eta*(double)g rounds exactly
+// as the reference's e + eta*G on the same gradient values; G moves 4 B per
+// element instead of 8.
+template <typename T, int kMode, bool kDense, bool kNorm, bool kTie = false, bool kNoG = false, bool kPf = false,
+          typename TG = T>
 __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(StreamArgs a) {  // acc-only: 51 regs, 5 CTAs/SM
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   // warps past the vector's end idle but still meet the CTA barrier below
   const int elems = base >= a.n_g ? 0 : (a.n_g - base < UE ? a.n_g - base : UE);
   const bool live = elems > 0;
-  const T* __restrict__ Gp = (const T*)a.grad + base;
+  const TG* __restrict__ Gp = (const TG*)a.grad + base;
   T* __restrict__ E = (T*)a.resid + base;
 
   const unsigned long long pol_stream = policy_evict_first();
@@ -144,7 +150,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       e[i] = ld_hint(reinterpret_cast<const V*>(E) + i * 32 + lane, pol_stream);
-      if (!kNoG) g[i] = ld_nc_hint(reinterpret_cast<const V*>(Gp) + i * 32 + lane, pol_stream);
+      if (!kNoG) g[i] = ld_grad<V>(reinterpret_cast<const typename GradVec<TG, VN>::V*>(Gp) + i * 32 + lane, pol_stream);
     }
   } else {  // the vector's last, partial unit
 #pragma unroll
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       for (int c = 0; c < VN; ++c) {
         const int off = (i * 32 + lane) * VN + c;
         set_comp(e[i], c, off < elems ? E[off] : (T)0);
-        set_comp(g[i], c, (!kNoG && off < elems) ? Gp[off] : (T)0);
+        set_comp(g[i], c, (!kNoG && off < elems) ? (T)Gp[off] : (T)0);
       }
   }
 

@@ -68,7 +68,8 @@ class Micro:
                  min_threshold: float = 1e-12, target: str = "split", error_feedback: bool = True,
                  dense_output: bool = True, device: int | torch.device | None = None,
                  stream: torch.cuda.Stream | None = None, selection_capacity: int = 0,
-                 record_error_norm: bool = True, sparsifier: str = "micro"):
+                 record_error_norm: bool = True, sparsifier: str = "micro",
+                 grad_dtype: torch.dtype | None = None):
         L = lib()
         if dtype not in _DT:
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unsupported dtype {dtype}")
@@ -91,6 +92,13 @@ class Micro:
         if sparsifier not in _lib.SPARSIFIERS:
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unknown sparsifier '{sparsifier}'")
         cfg.sparsifier = _lib.SPARSIFIERS[sparsifier]
+        # grad_dtype=torch.float32 with dtype=torch.float64: fp32 gradients into
+        # fp64 state and arithmetic (include/micro.h micro_config.grad_dtype)
+        grad_dtype = dtype if grad_dtype is None else grad_dtype
+        if grad_dtype not in _DT:
+            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unsupported gradient dtype {grad_dtype}")
+        cfg.grad_dtype = 0 if grad_dtype == dtype else _lib.MICRO_GRAD_F32
+        self.grad_dtype = grad_dtype
         self.sparsifier = sparsifier
         self.cfg = cfg
         self.device, self.dtype = dev, dtype
@@ -136,9 +144,9 @@ class Micro:
         if len(grads) != self.n_local:
             raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"expected {self.n_local} gradients, got {len(grads)}")
         for g in grads:
-            if not (g.is_cuda and g.dtype == self.dtype and g.numel() == self.n_g and g.is_contiguous()):
+            if not (g.is_cuda and g.dtype == self.grad_dtype and g.numel() == self.n_g and g.is_contiguous()):
                 raise _lib.InvalidArgument(_lib.MICRO_EINVAL,
-                                           f"gradient must be a contiguous {self.dtype} CUDA tensor of {self.n_g}")
+                                           f"gradient must be a contiguous {self.grad_dtype} CUDA tensor of {self.n_g}")
         return grads
 
     def compress(self, grads, eta: float, t: int):
@@ -157,7 +165,7 @@ class Micro:
     def step_host(self, h_grads: torch.Tensor, eta: float, t: int, out_idx: np.ndarray | None = None,
                   out_sums: np.ndarray | None = None):
         """End-to-end call with host buffers (pinned CPU tensor of n_local*n_g)."""
-        assert not h_grads.is_cuda and h_grads.dtype == self.dtype and h_grads.is_contiguous()
+        assert not h_grads.is_cuda and h_grads.dtype == self.grad_dtype and h_grads.is_contiguous()
         own = out_idx is None or out_sums is None
         if own:
             out_idx, out_sums = self._host_out()

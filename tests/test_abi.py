@@ -84,6 +84,20 @@ def test_device_calls_fail_loudly_without_gpu(L):
     assert L.micro_last_error()
 
 
+def test_config_rejects_bad_gradient_types(L):
+    """micro_config.grad_dtype: fp32 gradients need fp64 state and the MiCRO
+    sparsifier; anything else is EINVAL before any device call (no GPU here)."""
+    from paper_2310_00967_b200 import _lib
+    cases = [(_lib.MICRO_F32, _lib.MICRO_GRAD_F32, 0), (_lib.MICRO_F64, 7, 0), (_lib.MICRO_F64, _lib.MICRO_GRAD_F32, 1)]
+    for dtype, gd, kind in cases:
+        cfg = _lib.micro_config()
+        L.micro_config_default(C.byref(cfg))
+        cfg.n_g, cfg.dtype, cfg.grad_dtype, cfg.sparsifier = 1000, dtype, gd, kind
+        h = C.c_void_p()
+        assert L.micro_ctx_create(C.byref(h), C.byref(cfg), None) == _lib.MICRO_EINVAL and not h.value
+        assert b"gradient" in L.micro_last_error()
+
+
 @pytest.mark.ref
 def test_host_error_messages_match_the_reference(L):
     """The C ABI's status codes and messages are the reference's exceptions

@@ -72,12 +72,14 @@ class Run:
     """The CUDA path (a single-device cluster, optionally also GroupMicro) and
     the checker (restatement or the reference's code) stepped together."""
 
-    def __init__(self, n_g, n, d, delta0, dtype=np.float32, checker="restatement", group=False, dense=True):
+    def __init__(self, n_g, n, d, delta0, dtype=np.float32, checker="restatement", group=False, dense=True,
+                 grad32=False):
         self.n_g, self.n, self.d = n_g, n, d
         self.dtype = dtype
+        self.grad32 = grad32  # fp32 gradients into the fp64 engine (micro_config.grad_dtype)
         tdt = torch.float32 if dtype == np.float32 else torch.float64
         self.m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, scaling_factor=ALPHA,
-                              dense_output=dense)
+                              dense_output=dense, grad_dtype=torch.float32 if grad32 else tdt)
         self.x = torch.zeros(n_g, dtype=tdt, device="cuda")
         self.m.set_model(self.x)
         self.g = None
@@ -98,7 +100,11 @@ class Run:
         return self.ref.residuals() if self.checker == "reference" else self.ref.e
 
     def step(self, t, full_check=False):
-        dev, host = grads(self.n, self.n_g, t, self.dtype, self.buf)
+        if self.grad32:  # the device keeps fp32; the checker gets the same values widened (exact)
+            dev, host = grads(self.n, self.n_g, t, np.float32, self.buf)
+            host = host.astype(np.float64)
+        else:
+            dev, host = grads(self.n, self.n_g, t, self.dtype, self.buf)
         torch.cuda.synchronize()
         self.m.step(dev, ETA, t)
         if self.g is not None:
@@ -169,6 +175,26 @@ def test_c1_adaptation_f64_reference_code():
     run = Run(11_700_000, 1, 0.01, 0.01, dtype=np.float64, checker="reference")
     for t in range(100):
         run.step(t, full_check=t in (0, 1, 50, 99))
+    run.close()
+
+
+def test_c1_fp32_gradients_f64_reference_code():
+    """C1 as BASELINE states it ("fp32 gradient") in the reference's fp64
+    arithmetic: fp32 gradients into the f64 engine, 100 iterations against
+    the reference's compiled code fed the same values, bit for bit."""
+    run = Run(11_700_000, 1, 0.01, 0.01, dtype=np.float64, checker="reference", grad32=True)
+    for t in range(100):
+        run.step(t, full_check=t in (0, 1, 50, 99))
+    run.close()
+
+
+def test_c3_fp32_gradients_f64_n1():
+    """The bench's default step (C3's per-GPU slice: 138M, d = 0.01, n = 1,
+    fp32 gradients, fp64 state and arithmetic, model + dense g/n) against
+    the reference's own code, 3 iterations from the warm delta_0."""
+    run = Run(138_000_000, 1, 0.01, warm_delta0(0.01), dtype=np.float64, checker="reference", grad32=True)
+    for t in range(3):
+        run.step(t, full_check=t == 2)
     run.close()
 
 

@@ -36,11 +36,15 @@ def gen(o, n, n_g, t, dtype):
 
 
 def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, oracle="restatement",
-             check_every=1, split=False, unaligned=False):
+             check_every=1, split=False, unaligned=False, grad32=False):
+    """grad32: fp32 gradients into the fp64 engine (micro_config.grad_dtype);
+    the checker runs fp64 on the same values widened."""
     o = Oracle()
     tdt = torch.float32 if dtype == np.float32 else torch.float64
+    assert not grad32 or dtype == np.float64
+    gdt = torch.float32 if grad32 else tdt
     m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, target="full" if full else "split",
-                     error_feedback=ef)
+                     error_feedback=ef, grad_dtype=gdt)
     x = torch.zeros(n_g, dtype=tdt, device="cuda")
     m.set_model(x)
     if oracle == "reference":
@@ -51,15 +55,19 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     for t in range(iters):
         thr_used = seq_sum(m.query().deltas) / n
         G = gen(o, n, n_g, t, dtype)
+        G32 = None
+        if grad32:
+            G32 = gen(o, n, n_g, t, np.float32)
+            G = G32.astype(np.float64)  # exact
         # energy before the exchange zeroes foreign entries: at n > 1 the
         # norm is ||e||^2 - (squares zeroed by the exchange), accurate to
         # ~1e-15 of this, not of the result
         e_now = ref.residuals() if oracle == "reference" else ref.e
         acc = e_now.astype(dtype) + dtype(ETA) * G
         energy = float(np.sqrt((acc.astype(np.float64) ** 2).sum(axis=1)).max())
-        Gd = list(torch.from_numpy(G).cuda())
+        Gd = list(torch.from_numpy(G32 if grad32 else G).cuda())
         if unaligned:  # gradients off the 16-byte grid: the library realigns them (staging copy)
-            buf = torch.empty((n, n_g + 1), dtype=tdt, device="cuda")
+            buf = torch.empty((n, n_g + 1), dtype=gdt, device="cuda")
             buf[:, 1:] = torch.stack(Gd)
             Gd = [buf[i, 1:] for i in range(n)]
             assert Gd[0].data_ptr() % 16
@@ -105,6 +113,20 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
         else:  # (nearly) everything zeroed: the subtraction's noise floor
             assert rec["error_norm"] <= 1e-6 * energy, (t, rec["error_norm"], en, energy)
     m.close()
+
+
+@pytest.mark.parametrize("n_g,n,d,delta0,oracle", [
+    (100_003, 1, 0.01, 0.02, "reference"),
+    (65_537, 4, 0.02, 0.01, "reference"),
+    (20_000, 3, 0.05, 0.01, "restatement"),
+    (4_095, 1, 0.3, 0.5, "reference"),     # one partial unit
+])
+def test_gpu_fp32_gradients_fp64_state(n_g, n, d, delta0, oracle, k1_kernel):
+    """BASELINE's "fp32 gradient" in the reference's fp64 arithmetic
+    (micro_config.grad_dtype = MICRO_GRAD_F32): bit-exact with the reference's
+    own code (and the fp64 restatement) fed the same gradient values widened
+    to double — counts, union, sums, thresholds, residuals, dense g/n, model."""
+    run_pair(n_g, n, d, delta0, iters=12, dtype=np.float64, oracle=oracle, grad32=True, unaligned=k1_kernel)
 
 
 @pytest.fixture(params=["aligned", "unaligned"])

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--dense", action="store_true")
+    ap.add_argument("--grad", default="same", choices=["same", "f32"], help="f32: fp32 gradients (f64 state)")
     ap.add_argument("--no-model", dest="model", action="store_false")
     ap.add_argument("--mode", default="single", choices=["single", "cluster", "group"])
     ap.add_argument("--n", type=int, default=1)
@@ -35,7 +36,9 @@ def main():
     wl = WORKLOADS[a.workload]
     n_g, d = wl["n_g"], wl["d"]
     tdt = torch.float64 if a.dtype == "f64" else torch.float32
-    kw = dict(density=d, initial_threshold=warm_delta0(d), scaling_factor=ALPHA, dense_output=a.dense, dtype=tdt)
+    gdt = torch.float32 if a.grad == "f32" else tdt
+    kw = dict(density=d, initial_threshold=warm_delta0(d), scaling_factor=ALPHA, dense_output=a.dense, dtype=tdt,
+              grad_dtype=gdt)
     n = a.n if a.mode != "single" else 1
     if a.mode == "group":
         from paper_2310_00967_b200.dist import GroupMicro
@@ -51,7 +54,7 @@ def main():
         x = torch.zeros(n_g, dtype=tdt, device="cuda")
         if a.model:
             m.set_model(x)
-    G = [torch.empty(n_g, dtype=tdt, device="cuda") for _ in range(n)]
+    G = [torch.empty(n_g, dtype=gdt, device="cuda") for _ in range(n)]
     t = 0
     for _ in range(a.prime):
         for i in range(n):
