@@ -66,6 +66,20 @@ CPP_BIN_DIR = os.path.join(ROOT, "tests", "cpp", "build")
 CPP_TEST_BIN = os.path.join(CPP_BIN_DIR, "test_dropin")
 
 
+def cpp_tests_stale() -> bool:
+    """A C++ test binary older than its source, the headers or the library
+    (a micro_config layout change must never meet an old binary)."""
+    deps = [os.path.join(ROOT, "include", f) for f in ("micro.h", "sparsim_b200.hpp", "micro_synth.h")] + [LIB]
+    for name, src in CPP_TESTS.items():
+        exe = os.path.join(CPP_BIN_DIR, name)
+        if not os.path.exists(exe):
+            return True
+        t = os.path.getmtime(exe)
+        if any(os.path.getmtime(d) > t for d in deps + [src] if os.path.exists(d)):
+            return True
+    return False
+
+
 def build_cpp_tests() -> str:
     """The reference's hot-path unit tests restated against the C++ drop-in
     header (include/sparsim_b200.hpp), and the n-process C++ host of the

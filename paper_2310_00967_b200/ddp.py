@@ -18,7 +18,10 @@ gradient g/n (the dense output), which the optimizer then applies.
 reference's simulator applies the learning rate there (x -= g/n); with a
 torch optimizer applying the learning rate itself, keep ``eta = 1`` so error
 feedback runs in gradient units.  Gradients in bf16/fp16 are accumulated in
-fp32 (the library's compute type) and cast back.
+fp32 (the library's compute type) and cast back.  ``state_dtype=torch.float64``
+keeps the residuals, thresholds' arithmetic and sums in fp64 (the reference's
+own arithmetic) while the fp32 bucket gradients are read as they are
+(micro_config.grad_dtype = MICRO_GRAD_F32: widened exactly on load).
 """
 from __future__ import annotations
 
@@ -31,7 +34,7 @@ from .engine import Micro
 class MicroHookState:
     def __init__(self, process_group=None, *, density: float = 0.01, initial_threshold: float | None = None,
                  scaling_factor: float = 0.01, eta: float = 1.0, transport: str = "peer",
-                 comm_device=None, **micro_kw):
+                 comm_device=None, state_dtype: torch.dtype = torch.float32, **micro_kw):
         self.pg = process_group
         self.density = density
         self.initial_threshold = initial_threshold
@@ -39,7 +42,9 @@ class MicroHookState:
         self.eta = eta
         self.transport = transport
         self.comm_device = comm_device
-        self.kw = micro_kw
+        if state_dtype not in (torch.float32, torch.float64):
+            raise ValueError(f"state_dtype must be float32 or float64, not {state_dtype}")
+        self.kw = dict(micro_kw, dtype=state_dtype, grad_dtype=torch.float32)
         self.t = 0
         self.contexts: dict[tuple[int, int], object] = {}
 
@@ -86,7 +91,7 @@ def micro_hook(state: MicroHookState, bucket) -> torch.futures.Future:
     m = state.context(bucket.index(), g)
     g32 = g if g.dtype == torch.float32 else g.float()
     m.step([g32.contiguous()], state.eta, state.t)
-    g.copy_(m.dense_device())  # g/n: sums at the union / n, zero elsewhere (valid until the next step)
+    g.copy_(m.dense_device())  # g/n: sums at the union / n, zero elsewhere (cast to g's dtype)
     if bucket.is_last():
         state.t += 1
     fut = torch.futures.Future()

@@ -252,6 +252,31 @@ int main() {
     }
     CHECK(!is_logic);
   }
+  // fp32 gradients into the fp64 engine (MICRO_GRAD_F32) == the fp64 engine
+  // on the same values widened: selection, sums, residuals, bit for bit
+  {
+    const Index n_g = 70001;
+    const int n = 3;
+    SparsifierConfig sc;
+    sc.density = 0.02;
+    sc.initial_threshold = 0.02;
+    MicroEngine e32(n_g, n, sc, true, MICRO_F64, MICRO_GRAD_F32);
+    MicroEngine e64(n_g, n, sc, true, MICRO_F64);
+    std::mt19937_64 rng(5);
+    std::normal_distribution<float> unit(0.0f, 1.0f);
+    std::vector<float> Gf((std::size_t)(n * n_g));
+    std::vector<double> Gd(Gf.size());
+    for (int t = 0; t < 6; ++t) {
+      for (std::size_t j = 0; j < Gf.size(); ++j) Gd[j] = (double)(Gf[j] = unit(rng));
+      std::vector<double> s32, s64;
+      const auto a = e32.step(Gf.data(), 0.01, t, &s32);
+      const auto b = e64.step(Gd.data(), 0.01, t, &s64);
+      CHECK(a.indices == b.indices);
+      CHECK(a.per_worker_counts == b.per_worker_counts);
+      CHECK(s32 == s64);
+    }
+    for (int i = 0; i < n; ++i) CHECK(e32.residual(i) == e64.residual(i));
+  }
   // MicroGroup (one process, one context per rank; here all on device 0)
   // == MicroEngine (single-device cluster), bit for bit
   {

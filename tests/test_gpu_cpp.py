@@ -11,8 +11,8 @@ pytestmark = pytest.mark.gpu
 
 
 def test_cpp_dropin_suite():
-    from paper_2310_00967_b200.build import CPP_TEST_BIN, build_cpp_tests
-    if not os.path.exists(CPP_TEST_BIN):
+    from paper_2310_00967_b200.build import CPP_TEST_BIN, build_cpp_tests, cpp_tests_stale
+    if cpp_tests_stale():
         build_cpp_tests()
     r = subprocess.run([CPP_TEST_BIN], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
@@ -20,9 +20,9 @@ def test_cpp_dropin_suite():
 
 
 def test_cpp_n_process_peer_exchange():
-    from paper_2310_00967_b200.build import CPP_BIN_DIR, build_cpp_tests
+    from paper_2310_00967_b200.build import CPP_BIN_DIR, build_cpp_tests, cpp_tests_stale
     exe = os.path.join(CPP_BIN_DIR, "test_dist_ipc")
-    if not os.path.exists(exe):
+    if cpp_tests_stale():
         build_cpp_tests()
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]

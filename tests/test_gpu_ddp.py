@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _run(rank, world, port, iters, transport, q):
+def _run(rank, world, port, iters, transport, q, f64=False):
     import sys
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import OracleCluster
@@ -35,7 +35,8 @@ def _run(rank, world, port, iters, transport, q):
     torch.manual_seed(0)
     model = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Linear(256, 10)).cuda()
     ddp = torch.nn.parallel.DistributedDataParallel(model, device_ids=[0], bucket_cap_mb=0.05)
-    state = MicroHookState(density=0.05, initial_threshold=0.002, transport=transport, comm_device="cpu")
+    state = MicroHookState(density=0.05, initial_threshold=0.002, transport=transport, comm_device="cpu",
+                           state_dtype=torch.float64 if f64 else torch.float32)
     seen = []  # (bucket index, iteration, gradient in, gradient out)
 
     def hook(st, bucket):
@@ -68,15 +69,19 @@ def _run(rank, world, port, iters, transport, q):
     clusters = {}
     for k in range(len(seen)):
         idx, t, _, out = allseen[rank][k]
-        G = np.stack([allseen[r][k][2] for r in range(world)]).astype(np.float32)
+        G = np.stack([allseen[r][k][2] for r in range(world)]).astype(np.float64 if f64 else np.float32)
         key = (idx, G.shape[1])
         if key not in clusters:  # DDP rebuilt the bucket: a fresh context, like the hook
             for old in [o for o in clusters if o[0] == idx]:
                 clusters.pop(old)
-            clusters[key] = OracleCluster(G.shape[1], world, density=0.05, delta0=0.002)
+            clusters[key] = OracleCluster(G.shape[1], world, density=0.05, delta0=0.002,
+                                          dtype=np.float64 if f64 else np.float32)
         r = clusters[key].step(G, 1.0, t)
         want = np.zeros(G.shape[1], np.float32)
-        want[r["union_idx"]] = r["union_sum"].astype(np.float32) / np.float32(world)
+        if f64:  # fp64 g/n, then DDP's fp32 bucket
+            want[r["union_idx"]] = (r["union_sum"].astype(np.float64) / np.float64(world)).astype(np.float32)
+        else:
+            want[r["union_idx"]] = r["union_sum"].astype(np.float32) / np.float32(world)
         if not np.array_equal(out, want):
             bad.append((k, idx, "g/n"))
     state.close()
@@ -84,12 +89,14 @@ def _run(rank, world, port, iters, transport, q):
     q.put((rank, bad))
 
 
-@pytest.mark.parametrize("world,transport", [(1, "peer"), (2, "peer"), (2, "peer_pull"), (2, "nccl")])
-def test_ddp_hook(world, transport):
+@pytest.mark.parametrize("world,transport,f64", [(1, "peer", False), (2, "peer", False), (2, "peer_pull", False),
+                                                (2, "nccl", False), (1, "peer", True), (2, "peer", True)])
+def test_ddp_hook(world, transport, f64):
+    """f64: fp32 bucket gradients, fp64 residuals and sums (state_dtype)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, 6, transport, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, 6, transport, q, f64)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

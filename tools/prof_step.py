@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--grad", default="same", choices=["same", "f32"], help="f32: fp32 gradients (f64 state)")
+    ap.add_argument("--error-norm", action="store_true", help="record the error norm (bench.py: off by default)")
     ap.add_argument("--no-model", dest="model", action="store_false")
     ap.add_argument("--mode", default="single", choices=["single", "cluster", "group"])
     ap.add_argument("--n", type=int, default=1)
@@ -38,7 +39,7 @@ def main():
     tdt = torch.float64 if a.dtype == "f64" else torch.float32
     gdt = torch.float32 if a.grad == "f32" else tdt
     kw = dict(density=d, initial_threshold=warm_delta0(d), scaling_factor=ALPHA, dense_output=a.dense, dtype=tdt,
-              grad_dtype=gdt)
+              grad_dtype=gdt, record_error_norm=a.error_norm)
     n = a.n if a.mode != "single" else 1
     if a.mode == "group":
         from paper_2310_00967_b200.dist import GroupMicro
