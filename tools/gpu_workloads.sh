@@ -1,7 +1,8 @@
 # Bench lines for the other BASELINE configs, the in-process cluster mode and
 # the comparison sparsifiers (tables: python tools/make_tables.py).
-# Default arithmetic is f64 (the reference's own) with the f32 line beside it
-# (other_dtype); the dense g/n and the model update are in every step.
+# Default: f64 arithmetic (the reference's own) on fp32 gradients (BASELINE's
+# "fp32 gradient", widened exactly), with the f32-arithmetic line and the
+# f64-gradient line beside it; the dense g/n and the model update in every step.
 cd $GRAFT_REPO_ROOT
 run() { timeout 1200 python bench.py --no-cpu-baseline "$@" > gpurun_out/wl.log 2>&1; echo "== $* rc=$?"; tail -1 gpurun_out/wl.log >> gpurun_out/workloads.jsonl; }
 rm -f gpurun_out/workloads.jsonl
