@@ -16,7 +16,9 @@
  *
  * Element types: MICRO_F32 is the north-star contract (fp32 gradients,
  * fp32 residuals, fp64 thresholds); MICRO_F64 runs the identical kernels in the
- * reference's own precision and is bit-exact against its compiled code.
+ * reference's own precision and is bit-exact against its compiled code; with
+ * micro_config.grad_dtype = MICRO_GRAD_F32 the fp64 engine takes fp32
+ * gradients (widened exactly: the reference's result on the same values).
  */
 #ifndef MICRO_H
 #define MICRO_H
@@ -27,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MICRO_ABI_VERSION 4
+#define MICRO_ABI_VERSION 5  /* 5: micro_config.grad_dtype */
 #define MICRO_MAX_WORKERS 64
 
 typedef enum micro_status {

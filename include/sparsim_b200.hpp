@@ -574,7 +574,7 @@ class MicroEngine {
 class MicroGroup {
  public:
   MicroGroup(Index n_g, const std::vector<int>& devices, const SparsifierConfig& sc, bool error_feedback = true,
-             int dtype = MICRO_F32)
+             int dtype = MICRO_F32, int grad_dtype = MICRO_GRAD_SAME)
       : n_((int)devices.size()) {
     if (n_ < 2) throw std::invalid_argument("MicroGroup: need at least two ranks");
     ctxs_.assign((std::size_t)n_, nullptr);
@@ -586,6 +586,7 @@ class MicroGroup {
       cfg.n_local = 1;
       cfg.rank = r;
       cfg.dtype = dtype;
+      cfg.grad_dtype = grad_dtype;
       cfg.density = sc.density;
       cfg.initial_threshold = sc.initial_threshold;
       cfg.scaling_factor = sc.scaling_factor;

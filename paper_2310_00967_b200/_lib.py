@@ -173,7 +173,7 @@ def lib() -> C.CDLL:
                 f = getattr(L, name)
                 f.argtypes = args
                 f.restype = res
-            if L.micro_abi_version() != 4:
+            if L.micro_abi_version() != 5:
                 raise ImportError("libmicro_b200.so ABI version mismatch")
             _lib = L
     return _lib

@@ -95,8 +95,9 @@ class Micro:
         # grad_dtype=torch.float32 with dtype=torch.float64: fp32 gradients into
         # fp64 state and arithmetic (include/micro.h micro_config.grad_dtype)
         grad_dtype = dtype if grad_dtype is None else grad_dtype
-        if grad_dtype not in _DT:
-            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"unsupported gradient dtype {grad_dtype}")
+        if grad_dtype != dtype and not (grad_dtype == torch.float32 and dtype == torch.float64):
+            raise _lib.InvalidArgument(_lib.MICRO_EINVAL, f"gradients of {grad_dtype} need state of the same dtype "
+                                                          f"(or float32 gradients into float64 state), not {dtype}")
         cfg.grad_dtype = 0 if grad_dtype == dtype else _lib.MICRO_GRAD_F32
         self.grad_dtype = grad_dtype
         self.sparsifier = sparsifier
