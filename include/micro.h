@@ -118,6 +118,11 @@ int micro_device_free(void* d_ptr);
 int micro_host_malloc(void** h_ptr, int64_t bytes);
 int micro_host_free(void* h_ptr);
 int micro_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream);
+/* The value-level calls above take their scratch (up to (4 + esz) bytes per
+ * element of the range) from a library-owned stream-ordered pool per device
+ * that keeps freed blocks reserved, so repeated calls do not re-map it;
+ * this returns the reserve of `device` to the driver. */
+int micro_value_workspace_trim(int device);
 int micro_device_count(int* count);
 /* The calling thread's current CUDA device (what micro_synth_gaussian and
  * the value-level calls launch on). */

@@ -106,6 +106,7 @@ _SIGS = {
     "micro_error_metric": ([I32, C.POINTER(VP), I32, I64, PDBL, VP], I32),
     "micro_synth_gaussian": ([I32, U64, U32, U64, I64, VP, VP], I32),
     "micro_device_malloc": ([C.POINTER(VP), I64, I32], I32),
+    "micro_value_workspace_trim": ([I32], I32),
     "micro_device_free": ([VP], I32),
     "micro_host_malloc": ([C.POINTER(VP), I64], I32),
     "micro_host_free": ([VP], I32),

@@ -1,12 +1,57 @@
 // value_api.cu — the stateless value-level calls of include/micro.h (the
 // reference's sparsim:: free functions on device arrays), device memory
 // plumbing for hosts without the CUDA runtime, and the synthetic inputs.
+#include <mutex>
+
 #include "internal.cuh"
 
 using namespace micro;
 using namespace micro::host;
 
 namespace {
+
+// Workspace of the value-level calls: a library-owned stream-ordered pool per
+// device whose freed blocks stay reserved (release threshold = max).  On the
+// default pool a call's multi-GB staging (worst case: every element selected)
+// went back to the driver at each synchronisation and was mapped again by the
+// next call — 50-130 ms per select at C3 size.  micro_value_workspace_trim()
+// hands the reserve back.
+constexpr int kMaxPoolDevices = 64;
+cudaMemPool_t g_pools[kMaxPoolDevices] = {};
+std::mutex g_pool_mu;
+
+cudaError_t value_pool(int dev, cudaMemPool_t* out) {
+  if (dev < 0 || dev >= kMaxPoolDevices) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    cudaError_t e = cudaMemPoolCreate(&p, &props);
+    if (e != cudaSuccess) return e;
+    unsigned long long keep = ~0ull;
+    e = cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) {
+      cudaMemPoolDestroy(p);
+      return e;
+    }
+    g_pools[dev] = p;
+  }
+  *out = g_pools[dev];
+  return cudaSuccess;
+}
+
+// cudaMallocAsync from the library's pool on the current device
+cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool = nullptr;
+  if ((e = value_pool(dev, &pool)) != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
 
 template <typename T>
 __global__ void k_synth(uint64_t seed, uint32_t worker, uint64_t t, int64_t n, T* out) {
@@ -88,6 +133,17 @@ int micro_device_count(int* count) {
 
 int micro_set_device(int device) {
   CU(cudaSetDevice(device));
+  return MICRO_OK;
+}
+
+int micro_value_workspace_trim(int device) {
+  if (device < 0 || device >= kMaxPoolDevices) return fail(MICRO_EINVAL, "device %d out of range", device);
+  cudaMemPool_t p = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    p = g_pools[device];
+  }
+  if (p) CU(cudaMemPoolTrimTo(p, 0));
   return MICRO_OK;
 }
 
@@ -181,7 +237,7 @@ static int select_stream_range(const void* d_acc, int64_t n_g, int64_t start, in
   const size_t b_cnt = sizeof(int) * runs, b_sup = sizeof(int) * kMaxSupers;
   char* ws = nullptr;
   const size_t tail = (b_idx + b_val + b_cnt + b_sup + 15) / 16 * 16;
-  CU(cudaMallocAsync((void**)&ws, tail + 32, s));
+  CU(ws_alloc((void**)&ws, tail + 32, s));
   int32_t* stage_idx = (int32_t*)ws;
   T* stage_val = (T*)(ws + b_idx);
   int* counts = (int*)(ws + b_idx + b_val);
@@ -316,7 +372,7 @@ int micro_select_topk(int dtype, const void* d_acc, int64_t n_g, int64_t start, 
   // scratch: state, histogram, tie counts, the "everything" threshold
   const size_t bytes = 256 + sizeof(unsigned) * (kBins + kTieChunks);
   char* ws = nullptr;
-  CU(cudaMallocAsync((void**)&ws, bytes, s));
+  CU(ws_alloc((void**)&ws, bytes, s));
   CU(cudaMemsetAsync(ws, 0, bytes, s));
   auto* st = (TopkState*)ws;
   auto* m1 = (double*)(ws + 128);
@@ -346,7 +402,7 @@ int micro_compensate(int dtype, void* d_acc, int64_t n_g, const int32_t* d_idx, 
   if (!k) return MICRO_OK;
   cudaStream_t s = (cudaStream_t)stream;
   int* bad = nullptr;
-  CU(cudaMallocAsync((void**)&bad, sizeof(int), s));
+  CU(ws_alloc((void**)&bad, sizeof(int), s));
   CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
   const unsigned grid = grid_for(k, current_device());
   if (dtype == MICRO_F32) k_compensate<float><<<grid, 256, 0, s>>>((float*)d_acc, n_g, d_idx, k, bad);
@@ -373,7 +429,7 @@ static int reduce_values(int dtype, const void* const* h_accs, int n, int64_t n_
   WorkerPtrs w{};
   for (int r = 0; r < n; ++r) w.sel_val[r] = h_accs[r];
   int* bad = nullptr;
-  CU(cudaMallocAsync((void**)&bad, sizeof(int), s));
+  CU(ws_alloc((void**)&bad, sizeof(int), s));
   CU(cudaMemsetAsync(bad, 0, sizeof(int), s));
   const unsigned grid = grid_for(K, current_device());
   if (dtype == MICRO_F32)
@@ -418,7 +474,7 @@ int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_co
   cudaStream_t s = (cudaStream_t)stream;
   const int dev = current_device();
   int* mm = nullptr;
-  CU(cudaMallocAsync((void**)&mm, 2 * sizeof(int), s));
+  CU(ws_alloc((void**)&mm, 2 * sizeof(int), s));
   const int init[2] = {INT32_MAX, -1};
   CU(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, s));
   k_index_extent<<<grid_for(total, dev), 256, 0, s>>>(d_concat, total, mm);
@@ -432,7 +488,7 @@ int micro_all_gather_indices(int n, const int64_t* h_counts, const int32_t* d_co
   const int64_t nt = scan_tiles(nwords);
   char* ws = nullptr;
   const size_t bm = sizeof(unsigned) * nwords, ob = sizeof(int) * nwords, tb = sizeof(int) * nt;
-  CU(cudaMallocAsync((void**)&ws, bm + ob + tb + 16, s));
+  CU(ws_alloc((void**)&ws, bm + ob + tb + 16, s));
   unsigned* bitmap = (unsigned*)ws;
   int* off = (int*)(ws + bm);
   int* tiles = (int*)(ws + bm + ob);
@@ -463,7 +519,7 @@ int micro_error_metric(int dtype, const void* const* h_res, int n, int64_t n_g, 
   // one scratch block: per-worker slots (part, group, ticket) + n totals
   const size_t bytes = sizeof(double) * (size_t)n * (grid + groups + 1) + sizeof(unsigned) * (size_t)n * (groups + 1);
   char* scratch = nullptr;
-  CU(cudaMallocAsync((void**)&scratch, bytes, s));
+  CU(ws_alloc((void**)&scratch, bytes, s));
   CU(cudaMemsetAsync(scratch, 0, bytes, s));
   double* part = (double*)scratch;
   double* grp = part + (size_t)n * grid;

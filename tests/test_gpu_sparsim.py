@@ -238,3 +238,17 @@ def test_all_gather_indices_unsorted_overlapping(extent, sizes):
     want = np.unique(np.concatenate(lists))
     assert np.array_equal(agg.indices.cpu().numpy().astype(np.int64), want)
     assert agg.per_worker_counts == [len(x) for x in lists]
+
+
+def test_value_workspace_pool_trim():
+    """The value-level calls' scratch comes from a library-owned pool that
+    keeps its reserve between calls (micro_value_workspace_trim returns it);
+    results are the same before and after a trim."""
+    from paper_2310_00967_b200._lib import lib
+    acc = torch.randn(300_001, device="cuda") * 0.01
+    rng = S.PartitionRange(0, acc.numel(), 0)
+    a = S.select_by_threshold(acc, rng, 0.02)
+    assert lib().micro_value_workspace_trim(torch.cuda.current_device()) == 0
+    b = S.select_by_threshold(acc, rng, 0.02)
+    assert torch.equal(a.indices, b.indices) and torch.equal(a.values, b.values)
+    assert lib().micro_value_workspace_trim(-1) != 0
