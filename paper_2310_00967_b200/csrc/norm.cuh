@@ -122,11 +122,39 @@ __device__ __forceinline__ void cta_sumsq_publish(double v, const SumSqSlots& s)
 }
 
 // Standalone sum of squares of one vector (the value-level error_metric):
-// fixed grid, each thread sums its grid-stride elements in order.
+// fixed grid, each thread sums its grid-stride elements in order —
+// deterministic for a given n and grid.  fp32 reads 16-byte vectors (four in
+// flight) then the scalar tail (scalar 4-byte loads reached 3.5 TB/s); fp64
+// and unaligned vectors take the scalar loop (the vector form of the fp64
+// sum measured 1.4x slower: its dependent adds sit behind each vector).
 template <typename T>
 __global__ void __launch_bounds__(256) k_sumsq(const T* __restrict__ x, int64_t n, SumSqSlots s) {
+  using V = typename Vec<T>::V;
+  constexpr int VN = Vec<T>::N, U = 4;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   double v = 0.0;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+  int64_t done = 0;
+  if (sizeof(T) == 4 && ((uintptr_t)x & 15) == 0) {
+    const int64_t nv = n / VN;
+    const V* xv = reinterpret_cast<const V*>(x);
+    for (int64_t q0 = tid; q0 < nv; q0 += U * stride) {
+      V a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q0 + u * stride < nv) a[u] = ld_nc_stream(xv + q0 + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q0 + u * stride < nv) {
+#pragma unroll
+          for (int c = 0; c < VN; ++c) {
+            const double y = (double)comp(a[u], c);
+            v += y * y;
+          }
+        }
+    }
+    done = nv * VN;
+  }
+  for (int64_t j = done + tid; j < n; j += stride) {
     const double y = (double)x[j];
     v += y * y;
   }
