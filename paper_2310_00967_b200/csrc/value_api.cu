@@ -43,10 +43,11 @@ cudaError_t value_pool(int dev, cudaMemPool_t* out) {
   return cudaSuccess;
 }
 
-// cudaMallocAsync from the library's pool on the current device
+// cudaMallocAsync from the library's pool on the stream's device (the
+// legacy default stream: the current device)
 cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t s) {
   int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
+  cudaError_t e = s ? cudaStreamGetDevice(s, &dev) : cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   cudaMemPool_t pool = nullptr;
   if ((e = value_pool(dev, &pool)) != cudaSuccess) return e;
