@@ -17,7 +17,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl", f64=False, eta=0.01, d=0.02, delta0=0.015):
+def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl", f64=False, eta=0.01, d=0.02, delta0=0.015,
+            grad32=False):
     import sys
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     from oracle import Oracle, OracleCluster
@@ -28,8 +29,10 @@ def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl", f64=False, e
     torch.cuda.set_device(0)
     o = Oracle()
     tdt, ndt = (torch.float64, np.float64) if f64 else (torch.float32, np.float32)
+    # grad32: fp32 gradients into the fp64 ranks (micro_config.grad_dtype)
+    gdt = torch.float32 if grad32 else tdt
     m = DistMicro(n_g, comm_device="cpu", transport=transport, density=d, initial_threshold=delta0,
-                  error_feedback=ef, dtype=tdt)
+                  error_feedback=ef, dtype=tdt, grad_dtype=gdt)
     x = torch.zeros(n_g, device="cuda", dtype=tdt)
     m.set_model(x)
     ref = OracleCluster(n_g, world, density=d, delta0=delta0, error_feedback=ef, model=True, dtype=ndt)
@@ -39,8 +42,9 @@ def _worker(rank, world, port, n_g, iters, ef, q, transport="nccl", f64=False, e
         thr = 0.0
         for dl in ref.delta:
             thr += float(dl)
-        G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)]).astype(ndt)
+        G = np.stack([o.gaussian(3, i, t, n_g) for i in range(world)]).astype(np.float32 if grad32 else ndt)
         K = m.step([torch.from_numpy(G[rank]).cuda()], eta, t)
+        G = G.astype(ndt)  # the checker: the same values widened (exact)
         r = ref.step(G, eta, t)
         idx, sums = m.union()
         st = m.query()
@@ -151,3 +155,10 @@ def test_dist_f64_one_gpu(transport):
         p.join(timeout=60)
     for rank, bad, _ in res:
         assert not bad, (rank, bad[:5])
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer", "peer_pull"])
+def test_dist_fp32_gradients_f64_ranks(transport):
+    """fp32 gradients into fp64 rank contexts through every exchange:
+    bit-exact with the fp64 oracle cluster fed the same values widened."""
+    _run_world(2, 40_003, 6, transport, f64=True, grad32=True)
