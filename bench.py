@@ -212,7 +212,7 @@ def reference_arm(args, wl):
     threads = max(1, min(n, len(os.sched_getaffinity(0))))
     r = run_reference_converged(wl["n_g"], n, wl["d"], args.steps, args.warmup, adapt_iters=args.prime,
                                 dense=args.dense, model=args.model, threads=threads, seed=args.seed,
-                                grad32=args.grad == "f32")
+                                grad32=args.grad == "f32" and args.sparsifier == "micro")
     per = statistics.mean(r["times"])
     us = per * 1e6
     dens = float(np.mean(r["density"]))
@@ -251,8 +251,8 @@ def bench_config(args, wl, world: int) -> dict:
             "arithmetic": "f64 (the reference's own, bit-exact with its code)" if args.dtype == "f64"
             else "f32 (the north star's gradient type)",
             "gradient": ("f32 (BASELINE configs' 'fp32 gradient'; widened exactly into the f64 state, so the "
-                         "reference computes on the same values)" if args.dtype == "f64" and args.grad == "f32"
-                         else args.dtype),
+                         "reference computes on the same values)"
+                         if args.dtype == "f64" and args.grad == "f32" and args.sparsifier == "micro" else args.dtype),
             "parallelism": (f"dp{world} (exclusive cyclic partitions"
                             + (f", {args.transport} exchange)" if world > 1 else ")") if W == 1 else
                             f"{W} in-process workers on 1 GPU (exclusive cyclic partitions)"),
@@ -278,7 +278,8 @@ def grad_dtype(args, tdt):
     """The gradients' element type: fp32 (BASELINE's "fp32 gradient"; widened
     exactly into the f64 state when the arithmetic is f64) or the arithmetic's."""
     import torch
-    return torch.float32 if args.grad == "f32" else tdt
+    # (the comparison sparsifiers take gradients of their own dtype)
+    return torch.float32 if args.grad == "f32" and args.sparsifier == "micro" else tdt
 
 
 def device_measure(args, wl, tdt, dist, world, rank, local, dev, keep=False, gdt=None):

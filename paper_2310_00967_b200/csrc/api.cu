@@ -288,7 +288,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
       else K1S(kWriteZeroSel, D);                                                                             \
     } while (0)
     if (c->norm && (int64_t)grid > c->norm_ctas) return fail(MICRO_ECAPACITY, "norm workspace too small");
-    if (c->kind) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
+    if (c->kind && !c->sel_is_union) {  // comparison sparsifiers: keep acc (the union is zeroed after the reduce)
       if constexpr (std::is_same<T, TG>::value) {  // (fp32 gradients are MiCRO only)
         if (acc_in_e)  // top-k: e holds acc already; compact only
           CU(launch_pdl(k1_stream<T, kWriteNone, false, false, true, true>, dim3(g),
@@ -359,6 +359,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     return fail(MICRO_ECAPACITY, "super-block workspace too small");
   if (c->fuse_step) {
     b.fin_delta = c->delta + i;
+    b.fin_fixed = c->kind == 3;
     b.k_target = c->k_worker;
     b.alpha = c->cfg.scaling_factor;
     b.min_threshold = c->cfg.min_threshold;
@@ -374,7 +375,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     c->fin_done = true;
   }
   unsigned gblocks = (unsigned)((b.num_runs + kGatherWarps - 1) / kGatherWarps);
-  if (c->norm && c->kind == 0) {  // one more CTA reduces k1_stream's per-CTA partials
+  if (c->norm && (c->kind == 0 || c->sel_is_union)) {  // one more CTA reduces k1_stream's per-CTA partials
     b.sq_part = c->norm_part;
     b.sq_parts = (int)grid;
     b.sq_out = &c->norm_slot[i].sq;
@@ -506,7 +507,7 @@ int aggregate_baseline(micro_ctx* c) {
 
 template <typename T>
 int aggregate_cluster(micro_ctx* c) {
-  if (c->kind) return aggregate_baseline<T>(c);
+  if (c->kind && !c->sel_is_union) return aggregate_baseline<T>(c);
   if (c->n == 1) return launch_finalize<T>(c, c->sel_idx[c->buf][0], c->sel_val[c->buf][0], 1);
   WorkerPtrs w{};
   for (int i = 0; i < c->n; ++i) {
@@ -679,7 +680,10 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->gsz = cfg->grad_dtype == MICRO_GRAD_F32 ? 4 : c->esz;
   c->cluster = c->n_local == c->n;
   c->kind = cfg->sparsifier;
-  c->sel_is_union = c->n == 1 && c->kind == 0;
+  // one worker selecting without overlap: the union is its selection.  MiCRO,
+  // and the hard threshold (the same step with delta_0 fixed, no update:
+  // |acc| > delta_0 >= 0 never selects a zero, so 0 + acc = acc exactly)
+  c->sel_is_union = c->n == 1 && (c->kind == 0 || c->kind == 3);
   int rc = h_worker_target(cfg->density, cfg->n_g, cfg->n_workers, cfg->target, &c->k_worker);
   if (rc) { delete c; return rc; }
   DeviceGuard dg(c->dev);

@@ -411,6 +411,7 @@ struct CompactArgs {
   // would — K, history, threshold update (sparsifier.cpp:77-81) — so the
   // iteration is two launches.  fin_delta == NULL: not fused.
   double* fin_delta;
+  int fin_fixed;           // the hard threshold (n = 1): record delta_0, never update it
   unsigned long long k_target;
   double alpha, min_threshold;
   long long* fin_K;
@@ -436,6 +437,7 @@ __device__ __forceinline__ void gather_finalize(const CompactArgs& a, long long 
   a.hist_delta[a.fin_slot] = d;
   if (a.norm_mode != 1)  // mode 1: written by the reducing CTA
     a.hist_err[a.fin_slot] = a.norm_mode == 2 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+  if (a.fin_fixed) return;
   const unsigned long long k = (unsigned long long)total;
   if (k > a.k_target) d = d == 0.0 ? a.min_threshold : d * (1.0 + a.alpha);
   else if (k < a.k_target) d *= 1.0 - a.alpha;
