@@ -436,7 +436,9 @@ def roofline_of(args, r, wl, world, peak, peak_kind):
     # entry).  top-k's compaction reads acc only (the histogram passes formed
     # it); CLT-k's leader is top-k, its other workers select by threshold.
     acc_only = {"topk": W, "cltk": 1}.get(args.sparsifier, 0)
-    dense_fused = args.dense and world == 1 and W == 1 and args.sparsifier == "micro"
+    # one worker selecting: the union is its selection and K1 maintains the
+    # dense g/n (every sparsifier but the dense baseline's one-pass kernel)
+    dense_fused = args.dense and world == 1 and W == 1 and args.sparsifier != "dense"
     k1_bytes = ((n_g * (esz * acc_only + (2.0 * esz + gsz) * (W - acc_only)) / W) + (4.0 + esz) * float(k_own.mean())
                 + (2.0 * esz * float(K.mean()) if dense_fused else 0.0))
     k1a_avg_ms = statistics.mean(r["k1a_ms"]) if r["k1a_ms"] else r["ms_step"]
@@ -444,10 +446,20 @@ def roofline_of(args, r, wl, world, peak, peak_kind):
     # whole step vs the same roofline: K1 + the union (8 B at n = 1: written by
     # the gather) + the model's read-modify-write (2 values per union entry) +
     # the dense g/n when not fused + the cluster reduce (W reads + zeroing)
-    step_bytes = (W * k1_bytes + (4.0 + esz) * float(K.mean())
-                  + (2.0 * esz * float(K.mean()) if args.model else 0.0)
-                  + (2.0 * esz * float(K.mean()) if (args.dense and not dense_fused) else 0.0)
-                  + (2.0 * esz * float(K.mean()) * W if W > 1 else 0.0))
+    extras = ((4.0 + esz) * float(K.mean())
+              + (2.0 * esz * float(K.mean()) if args.model else 0.0)
+              + (2.0 * esz * float(K.mean()) if (args.dense and not dense_fused) else 0.0)
+              + (2.0 * esz * float(K.mean()) * W if W > 1 else 0.0))
+    if acc_only:
+        # top-k is an exact radix select: pass 1 forms acc (e, G read, acc
+        # written), one acc-only pass per further 11-bit digit, the tie count
+        # and the compaction; CLT-k's other workers accumulate only
+        digits = -(-8 * esz // 11)
+        per_topk = (n_g * (3.0 * esz + esz * (digits - 1) + 2.0 * esz) + (4.0 + esz) * float(k_own.mean())
+                    + (2.0 * esz * float(K.mean()) if dense_fused else 0.0))
+        step_bytes = acc_only * per_topk + (W - acc_only) * 3.0 * esz * n_g + extras
+    else:
+        step_bytes = W * k1_bytes + extras
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "kernel": "k1_stream", "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1a_avg_ms,
             "peak_source": peak_kind,
@@ -500,7 +512,8 @@ def our_arm(args, wl):
         # tie count/find + stream + gather (fp32: 11), hard = 2, else accumulate + count = 2; then
         # union marks (W) + 3 scan passes + emit + reduce + finalize (dense: dense_all + finalize)
         per = {"topk": 11 * W, "cltk": 11 + 2 * (W - 1), "hard": 2 * W, "dense": 2 * W}[args.sparsifier]
-        launches_per_step = per + (2 if args.sparsifier == "dense" else W + 6)
+        # one worker (not dense): the selection is the union, the gather finalizes
+        launches_per_step = per + (2 if args.sparsifier == "dense" else 0 if W == 1 else W + 6)
 
     # ---- end to end through the public API with host buffers ----
     cdev = dev if args.dist_backend == "nccl" else "cpu"

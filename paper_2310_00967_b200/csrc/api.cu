@@ -297,6 +297,15 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
           CU(launch_pdl(k1_stream<T, kWriteAcc, false, false, true>, dim3(g), dim3(kStreamThreads), st, a));
         else K1S(kWriteAcc, false);
       }
+    } else if (c->kind && acc_in_e) {  // top-k / CLT-k, one worker: compact acc (in e), zero it, dense g/n
+      if constexpr (std::is_same<T, TG>::value) {
+#define K1T(D, N) CU(launch_pdl(k1_stream<T, kWriteZeroSel, D, N, true, true>, dim3(g), dim3(kStreamThreads), st, a))
+        if (fd && c->norm) K1T(true, true);
+        else if (fd) K1T(true, false);
+        else if (c->norm) K1T(false, true);
+        else K1T(false, false);
+#undef K1T
+      }
     } else if (c->n > 1) {
       if (c->cfg.error_feedback) K1N(false);
       else K1S(kWriteAcc, false);
@@ -359,7 +368,7 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
     return fail(MICRO_ECAPACITY, "super-block workspace too small");
   if (c->fuse_step) {
     b.fin_delta = c->delta + i;
-    b.fin_fixed = c->kind == 3;
+    b.fin_fixed = c->kind != 0;
     b.k_target = c->k_worker;
     b.alpha = c->cfg.scaling_factor;
     b.min_threshold = c->cfg.min_threshold;
@@ -680,10 +689,15 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
   c->gsz = cfg->grad_dtype == MICRO_GRAD_F32 ? 4 : c->esz;
   c->cluster = c->n_local == c->n;
   c->kind = cfg->sparsifier;
-  // one worker selecting without overlap: the union is its selection.  MiCRO,
-  // and the hard threshold (the same step with delta_0 fixed, no update:
-  // |acc| > delta_0 >= 0 never selects a zero, so 0 + acc = acc exactly)
-  c->sel_is_union = c->n == 1 && (c->kind == 0 || c->kind == 3);
+  // one worker: the union is its selection, for MiCRO and the comparison
+  // selections alike (hard threshold: the same step with delta_0 fixed;
+  // top-k / CLT-k: the radix select, then the same compaction with the ties
+  // and zeroing).  The sums are 0 + acc (a selected -0 becomes +0).  The
+  // dense baseline keeps its one-pass kernel; top-k / CLT-k without error
+  // feedback keep the general path (their first pass leaves acc in e, which
+  // that path zeroes).
+  c->sel_is_union = c->n == 1 && (c->kind == 0 || c->kind == 3 ||
+                                   ((c->kind == 1 || c->kind == 2) && cfg->error_feedback));
   int rc = h_worker_target(cfg->density, cfg->n_g, cfg->n_workers, cfg->target, &c->k_worker);
   if (rc) { delete c; return rc; }
   DeviceGuard dg(c->dev);

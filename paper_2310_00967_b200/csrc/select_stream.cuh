@@ -175,7 +175,6 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
   unsigned bits = 0;
   bool tie_seen = false;
   V out[VPL];  // e_{t+1} as stored (own selections zeroed when EF is on)
-  static_assert(!(kTie && kMode == kWriteZeroSel), "tie selections are never zeroed here");
   // one element: acc, the compare, the stored value.  `ranged`: the unit
   // straddles the partition's ends (or is the vector's partial last unit).
   auto element = [&](int i, int c, bool ranged) {
@@ -236,7 +235,10 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
         const int j = base + (i * 32 + lane) * VN + c;
         const bool tie = sel_unit && absx(comp(e[i], c)) == thr && (long long)j <= tie_limit &&
                          (all_in || (j >= a.p_start && j < a.p_end));
-        if (tie) bits |= 1u << (i * VN + c);
+        if (tie) {
+          bits |= 1u << (i * VN + c);
+          if (kMode == kWriteZeroSel) set_comp(out[i], c, (T)0);  // top-k at n = 1: ties are zeroed too
+        }
       }
   }
   constexpr unsigned VMASK = (1u << VN) - 1u;
@@ -247,7 +249,16 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       if ((bits >> (i * VN)) & VMASK) prefetch_l2_keep((const T*)a.model + base + (i * 32 + lane) * VN);
   }
   if (kMode != kWriteNone) {
-    if (elems == UE) {
+    if (kNoG && kMode == kWriteZeroSel && elems == UE) {
+      // e already holds acc (top-k, one worker): only the 32-byte sectors
+      // holding a selection change; lanes 2k and 2k+1 share sector k
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        const bool sec = ((bits >> (i * VN)) & VMASK) != 0;
+        const bool peer = __shfl_xor_sync(0xffffffffu, sec, 1);
+        if (sec || peer) st_hint(reinterpret_cast<V*>(E) + i * 32 + lane, out[i], pol_stream);
+      }
+    } else if (elems == UE) {
 #pragma unroll
       for (int i = 0; i < VPL; ++i) st_hint(reinterpret_cast<V*>(E) + i * 32 + lane, out[i], pol_stream);
     } else {
@@ -296,7 +307,8 @@ __global__ void __launch_bounds__(kStreamThreads, kNoG ? 5 : 4) k1_stream(Stream
       if (sec || ((prev >> (16 * i + (lane >> 1))) & 1ull)) {
         V dv;
 #pragma unroll
-        for (int c = 0; c < VN; ++c) set_comp(dv, c, (m & (1u << c)) ? comp(e[i], c) : (T)0);
+        // (0 + acc: the reference's sum from +0, so a selected -0 (top-k) is +0)
+        for (int c = 0; c < VN; ++c) set_comp(dv, c, (m & (1u << c)) ? add_rn((T)0, comp(e[i], c)) : (T)0);
         if (elems == UE) {
           st_hint(reinterpret_cast<V*>(D) + i * 32 + lane, dv, pol_stream);
         } else {
@@ -548,12 +560,12 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
       const int m = m0 + 32 * q;
       if (m < lim) {
         j[q] = si[m];
-        v[q] = sv[m];
+        v[q] = add_rn((T)0, sv[m]);  // the sum from +0 (= v, except a selected -0 -> +0: top-k)
         oi[m] = j[q];
         ov[m] = v[q];
       }
     }
-    if (x) {  // n = 1: the sum is 0 + v and g/n = (0 + v) / 1 = v exactly (v != +-0)
+    if (x) {  // n = 1: g/n = (0 + v) / 1
 #pragma unroll
       for (int q = 0; q < kG; ++q)
         if (m0 + 32 * q < lim) xv[q] = kWide ? ld_rand(x + j[q]) : x[j[q]];
