@@ -364,6 +364,9 @@ int launch_k1_stream(micro_ctx* c, int i, const void* grad, double eta, int64_t 
   b.count = c->counts + i;
   b.flags = c->flags;
   b.model = c->sel_is_union ? c->model : nullptr;  // n = 1: the union is this selection, g/n = acc
+  // (its values are then the union's sums: a selected -0 is stored as +0;
+  // the value-level selections keep the raw acc)
+  b.sum_from_zero = c->sel_is_union ? 1 : 0;
   if ((b.num_runs + b.super_runs - 1) / b.super_runs > kMaxSupers)
     return fail(MICRO_ECAPACITY, "super-block workspace too small");
   if (c->fuse_step) {

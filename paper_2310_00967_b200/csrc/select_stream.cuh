@@ -423,6 +423,7 @@ struct CompactArgs {
   // would — K, history, threshold update (sparsifier.cpp:77-81) — so the
   // iteration is two launches.  fin_delta == NULL: not fused.
   double* fin_delta;
+  int sum_from_zero;       // the selection is the union (one worker): write 0 + v, the reference's sum
   int fin_fixed;           // the hard threshold (n = 1): record delta_0, never update it
   unsigned long long k_target;
   double alpha, min_threshold;
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
       const int m = m0 + 32 * q;
       if (m < lim) {
         j[q] = si[m];
-        v[q] = add_rn((T)0, sv[m]);  // the sum from +0 (= v, except a selected -0 -> +0: top-k)
+        v[q] = a.sum_from_zero ? add_rn((T)0, sv[m]) : sv[m];  // 0 + v = v, except a selected -0 (top-k) -> +0
         oi[m] = j[q];
         ov[m] = v[q];
       }

@@ -175,6 +175,11 @@ def test_select_topk_examples_and_oracle(dtype):
         S.select_topk(acc, full(acc), 5)
     tie = vec([2, -2, 2], dtype)
     assert S.select_topk(tie, full(tie), 2).indices.tolist() == [0, 1]
+    # zeros among the k largest: the raw acc values come back, sign bits included
+    z = vec([0.0, -0.0, 3.0, -0.0, 1.0], dtype)
+    got = S.select_topk(z, full(z), 4)
+    assert got.indices.tolist() == [0, 1, 2, 4]
+    assert torch.signbit(got.values).tolist() == [False, True, False, False]
     rng = np.random.default_rng(7)
     for rep in range(150):
         n = int(rng.integers(1, 401)) if rep < 140 else int(rng.integers(100_000, 300_000))
