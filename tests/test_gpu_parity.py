@@ -331,15 +331,18 @@ def test_gpu_records_to_reference_format(tmp_path):
     m.close()
 
 
-@pytest.mark.parametrize("n_g", [1_000_003, 65_536 * 3 + 17])
-def test_gpu_step_host_pipelined_matches_device_step(n_g):
+@pytest.mark.parametrize("n_g,grad32", [(1_000_003, False), (65_536 * 3 + 17, False), (1_000_003, True)])
+def test_gpu_step_host_pipelined_matches_device_step(n_g, grad32):
     """micro_step_host (gradient copied in chunks on a copy stream, K1
-    streaming each chunk as it lands) == micro_step on device gradients."""
+    streaming each chunk as it lands) == micro_step on device gradients;
+    grad32: fp32 host gradients into the fp64 engine (half the PCIe bytes)."""
     o = Oracle()
-    a = engine.Micro(n_g, 1, density=0.01, initial_threshold=0.02)
-    b = engine.Micro(n_g, 1, density=0.01, initial_threshold=0.02)
-    xa = torch.zeros(n_g, device="cuda")
-    xb = torch.zeros(n_g, device="cuda")
+    kw = dict(dtype=torch.float64, grad_dtype=torch.float32) if grad32 else {}
+    a = engine.Micro(n_g, 1, density=0.01, initial_threshold=0.02, **kw)
+    b = engine.Micro(n_g, 1, density=0.01, initial_threshold=0.02, **kw)
+    xdt = torch.float64 if grad32 else torch.float32
+    xa = torch.zeros(n_g, device="cuda", dtype=xdt)
+    xb = torch.zeros(n_g, device="cuda", dtype=xdt)
     a.set_model(xa)
     b.set_model(xb)
     for t in range(6):
