@@ -22,7 +22,7 @@ def grads(rng, n, n_g, t, ties, dtype):
     return rng.standard_normal((n, n_g)).astype(dtype)
 
 
-def run(kind, n_g, n, d, ties, dtype=np.float32, ef=True, iters=6, delta0=0.02):
+def run(kind, n_g, n, d, ties, dtype=np.float32, ef=True, iters=6, delta0=0.02, split=False):
     rng = np.random.default_rng(n_g * 7 + n)
     tdt = torch.float32 if dtype == np.float32 else torch.float64
     m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, error_feedback=ef, sparsifier=kind)
@@ -40,7 +40,11 @@ def run(kind, n_g, n, d, ties, dtype=np.float32, ef=True, iters=6, delta0=0.02):
     k_glob = Oracle().global_target_count(d, n_g)
     for t in range(iters):
         G = grads(rng, n, n_g, t, ties, dtype)
-        m.step(list(torch.from_numpy(G).cuda()), 0.01, t)
+        if split:  # micro_compress + micro_aggregate
+            m.compress(list(torch.from_numpy(G).cuda()), 0.01, t)
+            m.aggregate()
+        else:
+            m.step(list(torch.from_numpy(G).cuda()), 0.01, t)
         r = step(G, t)
         st = m.query()
         idx, sums = m.union()
@@ -82,3 +86,17 @@ def test_gpu_baselines_ef_off(kind):
 def test_gpu_topk_large_ties():
     """Ties spread over many 65536-way chunks: the tie index search."""
     run("topk", 2_000_003, 1, 0.0007, True, iters=3)
+
+
+@pytest.mark.parametrize("kind", ["topk", "cltk", "hard"])
+@pytest.mark.parametrize("n_g,d,ties,dtype,ef,split", [
+    (8_192, 0.05, True, np.float32, True, False),     # the tie rule on the one-worker path
+    (10_007, 1.0, False, np.float32, True, False),    # everything selected (top-k's k >= n_g path)
+    (4_096, 0.05, True, np.float64, True, False),     # the reference's own code
+    (9_999, 0.02, False, np.float32, False, False),   # EF off (top-k / CLT-k: the general path)
+    (9_999, 0.02, True, np.float32, True, True),      # micro_compress + micro_aggregate
+])
+def test_gpu_baselines_one_worker(kind, n_g, d, ties, dtype, ef, split):
+    """n = 1: the selection is the union and the single-worker step finishes
+    it (k1_stream + k1_gather, as for MiCRO): bit-exact like the general path."""
+    run(kind, n_g, 1, d, ties, dtype=dtype, ef=ef, split=split)
