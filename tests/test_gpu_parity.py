@@ -36,7 +36,7 @@ def gen(o, n, n_g, t, dtype):
 
 
 def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, oracle="restatement",
-             check_every=1, split=False, unaligned=False, grad32=False):
+             check_every=1, split=False, unaligned=False, grad32=False, alpha=0.01):
     """grad32: fp32 gradients into the fp64 engine (micro_config.grad_dtype);
     the checker runs fp64 on the same values widened."""
     o = Oracle()
@@ -44,13 +44,13 @@ def run_pair(n_g, n, d, delta0, iters, dtype=np.float32, full=False, ef=True, or
     assert not grad32 or dtype == np.float64
     gdt = torch.float32 if grad32 else tdt
     m = engine.Micro(n_g, n, dtype=tdt, density=d, initial_threshold=delta0, target="full" if full else "split",
-                     error_feedback=ef, grad_dtype=gdt)
+                     error_feedback=ef, grad_dtype=gdt, scaling_factor=alpha)
     x = torch.zeros(n_g, dtype=tdt, device="cuda")
     m.set_model(x)
     if oracle == "reference":
-        ref = RefCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, model=True)
+        ref = RefCluster(n_g, n, d, delta0, alpha, 1e-12, full, ef, model=True)
     else:
-        ref = OracleCluster(n_g, n, d, delta0, 0.01, 1e-12, full, ef, dtype=dtype, model=True)
+        ref = OracleCluster(n_g, n, d, delta0, alpha, 1e-12, full, ef, dtype=dtype, model=True)
     recs_want = []  # per step: (K, sum k_i, threshold used, error norm) from the checker
     for t in range(iters):
         thr_used = seq_sum(m.query().deltas) / n
@@ -127,6 +127,14 @@ def test_gpu_fp32_gradients_fp64_state(n_g, n, d, delta0, oracle, k1_kernel):
     own code (and the fp64 restatement) fed the same gradient values widened
     to double — counts, union, sums, thresholds, residuals, dense g/n, model."""
     run_pair(n_g, n, d, delta0, iters=12, dtype=np.float64, oracle=oracle, grad32=True, unaligned=k1_kernel)
+
+
+@pytest.mark.parametrize("alpha", [0.003, 0.001, 0.3])
+def test_gpu_controller_alpha(alpha):
+    """The bench's alpha (0.003) and others: the controller is the same code
+    path, bit-exact with the reference's own code (fp64 on fp32 gradients)."""
+    run_pair(65_537, 1, 0.01, 0.02, iters=30, dtype=np.float64, oracle="reference", grad32=True, alpha=alpha)
+    run_pair(20_011, 3, 0.02, 0.01, iters=15, alpha=alpha)
 
 
 @pytest.fixture(params=["aligned", "unaligned"])
