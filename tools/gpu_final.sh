@@ -12,7 +12,7 @@ fi
 timeout 900 python bench.py --steps 50 --warmup 5 > $O/bench.log 2>&1; echo bench rc=$?; tail -1 $O/bench.log > $O/bench.json
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > $O/ref.log 2>&1; echo ref rc=$?; tail -1 $O/ref.log > $O/ref.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
-  python bench.py --steps 4 --warmup 3 --prime 300 --no-cpu-baseline --no-other-dtype > $O/ncu_launch.log 2>&1; echo launches rc=$?
+  python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-other-dtype > $O/ncu_launch.log 2>&1; echo launches rc=$?
 P="python tools/prof_step.py"
 prof() {  # name, args...
   name=$1; shift
@@ -24,7 +24,7 @@ prof() {  # name, args...
 KEEP=1 prof c3_f64_g32_dense --workload c3 --dtype f64 --grad f32 --dense --steps 2
 prof c3_f64_dense --workload c3 --dtype f64 --dense --steps 2
 prof c3_f32_dense --workload c3 --dtype f32 --dense --steps 2
-prof c1_f64_g32_dense --workload c1 --dtype f64 --grad f32 --dense --steps 2 --flush --prime 1000
-prof c5_d1_f64_g32_dense --workload c5_d1 --dtype f64 --grad f32 --dense --steps 1 --prime 300
+prof c1_f64_g32_dense --workload c1 --dtype f64 --grad f32 --dense --steps 2 --flush --prime 2000
+prof c5_d1_f64_g32_dense --workload c5_d1 --dtype f64 --grad f32 --dense --steps 1 --prime 2000
 if [ -n "$WORKLOADS" ]; then bash tools/gpu_workloads.sh; cp gpurun_out/workloads.jsonl $O/; fi
 du -sh $O
