@@ -24,7 +24,7 @@ prof() {  # name, args...
 KEEP=1 prof c3_f64_g32_dense --workload c3 --dtype f64 --grad f32 --dense --steps 2
 prof c3_f64_dense --workload c3 --dtype f64 --dense --steps 2
 prof c3_f32_dense --workload c3 --dtype f32 --dense --steps 2
-prof c1_f64_g32_dense --workload c1 --dtype f64 --grad f32 --dense --steps 2 --flush --prime 2000
-prof c5_d1_f64_g32_dense --workload c5_d1 --dtype f64 --grad f32 --dense --steps 1 --prime 2000
+prof c1_f64_g32_dense --workload c1 --dtype f64 --grad f32 --dense --steps 2 --flush --prime 3000
+prof c5_d1_f64_g32_dense --workload c5_d1 --dtype f64 --grad f32 --dense --steps 1 --prime 3000
 if [ -n "$WORKLOADS" ]; then bash tools/gpu_workloads.sh; cp gpurun_out/workloads.jsonl $O/; fi
 du -sh $O

@@ -17,6 +17,6 @@ run --workload c5_d1 --steps 20 --warmup 3
 run --workload c5_d1 --steps 20 --warmup 3 --no-dense
 run --workload c1 --cluster-workers 2 --steps 100
 run --workload c1 --cluster-workers 8 --steps 100
-run --workload c3 --cluster-workers 8 --steps 20 --prime 2000
+run --workload c3 --cluster-workers 8 --steps 20 --prime 3000
 for k in topk hard dense; do run --workload c3 --sparsifier $k --steps 20 --prime 200 --dtype f32 --no-dense; done
 for k in topk cltk hard; do run --workload c1 --cluster-workers 8 --sparsifier $k --steps 30 --prime 200 --dtype f32 --no-dense; done

@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--no-model", dest="model", action="store_false")
     ap.add_argument("--mode", default="single", choices=["single", "cluster", "group"])
     ap.add_argument("--n", type=int, default=1)
-    ap.add_argument("--prime", type=int, default=2000)
+    ap.add_argument("--prime", type=int, default=3000)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--flush", action="store_true", help="flush L2 between profiled steps")
     a = ap.parse_args()
