@@ -442,7 +442,7 @@ int launch_baseline(micro_ctx* c, int i, const void* grad, double eta, int64_t t
     k_topk_digit<T><<<1, 1024, 0, st>>>(ts, c->topk_hist, shift, width, shift == 0, n_g);
     CU(cudaGetLastError());
   }
-  const int64_t chunk = (n_g + kTieChunks - 1) / kTieChunks;
+  const int64_t chunk = tie_chunk(n_g);
   const int nch = (int)((n_g + chunk - 1) / chunk);
   k_tie_count<T><<<nch, 256, 0, st>>>(acc, nullptr, eta, n_g, chunk, ts, c->tie_counts);
   CU(cudaGetLastError());

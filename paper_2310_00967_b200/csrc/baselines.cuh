@@ -51,6 +51,14 @@ template <> struct KeyOf<double> {
 
 constexpr int kDigitBits = 11;
 constexpr int kTieChunks = 65536;  // tie counting granularity (k_tie_count / k_tie_find)
+constexpr int64_t kTieMinChunk = 4096;  // >= 16 elements per k_tie_count thread (tiny CTAs were launch bound)
+
+// Elements per tie-counting chunk: at most kTieChunks chunks, at least
+// kTieMinChunk elements each (k_tie_find walks one chunk: <= a few passes).
+inline int64_t tie_chunk(int64_t n) {
+  const int64_t c = (n + kTieChunks - 1) / kTieChunks;
+  return c > kTieMinChunk ? c : kTieMinChunk;
+}
 
 // acc = e + eta*G (K1's arithmetic), or acc itself (g == NULL: the value API)
 template <typename T>
@@ -269,6 +277,7 @@ __global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, cons
   const T P = (T)st->pivot;
   const int64_t lo = (int64_t)blockIdx.x * chunk, hi = min(lo + chunk, n_g);
   unsigned c = 0;
+#pragma unroll 4
   for (int64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) c += absx(acc_at(e, g, eta, j)) == P;
   c = __reduce_add_sync(0xffffffffu, c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
@@ -437,31 +446,25 @@ __global__ void __launch_bounds__(256) k_union_reduce(WorkerPtrs w, int n, const
                                                       const long long* K, T* __restrict__ usum) {
   const long long k = *K;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  // four union entries per thread in flight (random reads, 64-byte L2 fetches)
-  for (long long m0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m0 < k; m0 += 4 * stride) {
-    int32_t j[4];
-    T s[4];
+  // eight workers' entries in flight per thread (random reads, 64-byte L2
+  // fetches; as k_cluster_reduce), then summed strictly in worker order —
+  // one worker per round left every round a full DRAM latency
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += stride) {
+    const int32_t j = uidx[m];
+    T s = (T)0;
+    for (int r0 = 0; r0 < n; r0 += 8) {
+      T v[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      s[q] = (T)0;
-      if (m0 + q * stride < k) j[q] = uidx[m0 + q * stride];
+      for (int u = 0; u < 8; ++u)
+        if (r0 + u < n) v[u] = ld_rand((const T*)w.resid[r0 + u] + j);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u >= n) break;
+        s = add_rn(s, v[u]);
+        if (kZero) ((T*)w.resid[r0 + u])[j] = (T)0;
+      }
     }
-    for (int r = 0; r < n; ++r) {  // worker order
-      T* e = (T*)w.resid[r];
-      T v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (m0 + q * stride < k) v[q] = ld_rand(e + j[q]);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (m0 + q * stride < k) {
-          s[q] = add_rn(s[q], v[q]);
-          if (kZero) e[j[q]] = (T)0;
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (m0 + q * stride < k) usum[m0 + q * stride] = s[q];
+    usum[m] = s;
   }
 }
 

@@ -372,7 +372,7 @@ static int topk_pivot(const T* acc, int64_t m, int64_t k, int64_t base, TopkStat
     k_topk_digit<T><<<1, 1024, 0, s>>>(st, hist, shift, width, shift == 0, base + m);
     CU(cudaGetLastError());
   }
-  const int64_t chunk = (m + kTieChunks - 1) / kTieChunks;
+  const int64_t chunk = tie_chunk(m);
   const int nch = (int)((m + chunk - 1) / chunk);
   k_tie_count<T><<<nch, 256, 0, s>>>(acc, nullptr, 1.0, m, chunk, st, tie_counts);
   CU(cudaGetLastError());
