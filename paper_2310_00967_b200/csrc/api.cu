@@ -451,6 +451,46 @@ int launch_baseline(micro_ctx* c, int i, const void* grad, double eta, int64_t t
   return launch_k1_stream<T>(c, i, grad, eta, 0, n_g, &ts->pivot, &ts->tie_j, /*acc_in_e=*/true);
 }
 
+// Top-k on every worker of a single-device cluster at once (the batched
+// kernels of baselines.cuh: one launch per radix pass for all workers), then
+// each worker's compaction with the tie rule, as launch_baseline does.
+template <typename T>
+int launch_topk_batch(micro_ctx* c, const void* const* grads, double eta) {
+  cudaStream_t st = c->stream;
+  const int n = c->n_local;
+  const int64_t n_g = c->n_g;
+  const long long k = (long long)c->k_global;
+  TopkBatch b{};
+  for (int i = 0; i < n; ++i) {
+    b.e[i] = c->resid[i];
+    b.g[i] = grads[i];
+  }
+  k_topk_init_b<<<1, 64, 0, st>>>(c->topk, n, k);
+  CU(cudaGetLastError());
+  const int bits = KeyOf<T>::kBits;
+  const unsigned hgrid = (unsigned)std::min<int64_t>((n_g + 255) / 256, 4 * (int64_t)num_sms(c->dev));
+  for (int hi = bits; hi > 0; hi -= kDigitBits) {
+    const int width = std::min(kDigitBits, hi);
+    const int shift = hi - width;
+    k_topk_hist_b<T><<<dim3(hgrid, n), 256, 0, st>>>(b, eta, n_g, shift, width, c->topk, c->topk_hist, hi == bits,
+                                                      c->flags);
+    CU(cudaGetLastError());
+    k_topk_digit_b<T><<<n, 1024, 0, st>>>(c->topk, c->topk_hist, shift, width, shift == 0, n_g);
+    CU(cudaGetLastError());
+  }
+  const int64_t chunk = tie_chunk(n_g);
+  const int nch = (int)((n_g + chunk - 1) / chunk);
+  k_tie_count_b<T><<<dim3(nch, n), 256, 0, st>>>(b, n_g, chunk, c->topk, c->tie_counts);
+  CU(cudaGetLastError());
+  k_tie_find_b<T><<<n, 1024, 0, st>>>(b, n_g, chunk, nch, c->topk, c->tie_counts);
+  CU(cudaGetLastError());
+  for (int i = 0; i < n; ++i) {
+    TopkState* ts = c->topk + i;
+    TRY(launch_k1_stream<T>(c, i, grads[i], eta, 0, n_g, &ts->pivot, &ts->tie_j, /*acc_in_e=*/true));
+  }
+  return MICRO_OK;
+}
+
 template <typename T>
 int launch_k1(micro_ctx* c, int i, const void* grad, double eta, int64_t t) {
   if (c->kind) return launch_baseline<T>(c, i, grad, eta, t);  // grad realigned by micro_compress
@@ -598,7 +638,7 @@ int reset_state(micro_ctx* c) {
   if (c->dense_dirty) CU(cudaMemsetAsync(c->dense_dirty, 0, (c->n_g / 256 + 8) * 8, c->stream));
   if (c->super_counts) CU(cudaMemsetAsync(c->super_counts, 0, 2 * kMaxSupers * sizeof(int), c->stream));
   if (c->kind) {
-    CU(cudaMemsetAsync(c->topk_hist, 0, sizeof(unsigned) * kBins, c->stream));
+    CU(cudaMemsetAsync(c->topk_hist, 0, sizeof(unsigned) * kBins * c->n_local, c->stream));
     CU(cudaMemsetAsync(c->bitmap, 0, sizeof(unsigned) * c->nwords, c->stream));
     const double m1 = -1.0;
     CU(cudaMemcpyAsync(c->minus_one, &m1, sizeof m1, cudaMemcpyHostToDevice, c->stream));
@@ -767,8 +807,8 @@ int micro_ctx_create(micro_ctx** out, const micro_config* cfg, void* stream) {
     if ((rc = h_global_target(cfg->density, c->n_g, &c->k_global))) return cleanup(rc);
     c->nwords = (c->n_g + 31) / 32;
     if ((rc = c->alloc((void**)&c->topk, sizeof(TopkState) * c->n_local))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->topk_hist, sizeof(unsigned) * kBins))) return cleanup(rc);
-    if ((rc = c->alloc((void**)&c->tie_counts, sizeof(unsigned) * kTieChunks))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->topk_hist, sizeof(unsigned) * kBins * c->n_local))) return cleanup(rc);
+    if ((rc = c->alloc((void**)&c->tie_counts, sizeof(unsigned) * kTieChunks * c->n_local))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->bitmap, sizeof(unsigned) * c->nwords))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->scan_tmp, sizeof(int) * scan_tiles(c->nwords)))) return cleanup(rc);
     if ((rc = c->alloc((void**)&c->word_off, sizeof(int) * c->nwords))) return cleanup(rc);
@@ -852,6 +892,7 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
   c->t_cur = t;
   c->buf = (int)(c->steps & 1);
   TRY(c->esz == 4 ? fork_dense_clear<float>(c) : fork_dense_clear<double>(c));
+  std::vector<const void*> gs(c->n_local);
   for (int i = 0; i < c->n_local; ++i) {
     const void* g = d_grads[i];
     if ((uintptr_t)g % 16) {
@@ -861,8 +902,17 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
       if (dst != g) CU(cudaMemcpyAsync(dst, g, (size_t)c->n_g * c->gsz, cudaMemcpyDeviceToDevice, c->stream));
       g = dst;
     }
-    if (c->esz == 4) TRY(launch_k1<float>(c, i, g, eta, t));
-    else TRY(launch_k1<double>(c, i, g, eta, t));
+    gs[i] = g;
+  }
+  if (c->kind == 1 && c->n_local > 1 && c->k_global > 0 && (int64_t)c->k_global < c->n_g) {
+    // top-k on several workers: every worker's radix select in the same launches
+    if (c->esz == 4) TRY(launch_topk_batch<float>(c, gs.data(), eta));
+    else TRY(launch_topk_batch<double>(c, gs.data(), eta));
+  } else {
+    for (int i = 0; i < c->n_local; ++i) {
+      if (c->esz == 4) TRY(launch_k1<float>(c, i, gs[i], eta, t));
+      else TRY(launch_k1<double>(c, i, gs[i], eta, t));
+    }
   }
   c->compressed = true;
   return MICRO_OK;

@@ -109,7 +109,7 @@ __device__ __forceinline__ void hist_add(unsigned* s_hist, T acc, unsigned long 
 constexpr int kHistVecs = MICRO_HIST_VECS, kHistVecsG = MICRO_HIST_VECS_G;
 
 template <typename T>
-__global__ void __launch_bounds__(256, 4) k_topk_hist(const T* e, const T* __restrict__ g, double eta_d, int64_t n_g,
+__device__ __forceinline__ void topk_hist_body(const T* e, const T* __restrict__ g, double eta_d, int64_t n_g,
                                                    int shift, int width, const TopkState* st,
                                                    unsigned* __restrict__ hist, T* acc_out = nullptr,
                                                    int* flags = nullptr) {
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256, 4) k_topk_hist(const T* e, const T* __res
 // it into the prefix, clear the histogram.  last: also form the pivot and
 // whether ties must be cut.
 template <typename T>
-__global__ void __launch_bounds__(1024) k_topk_digit(TopkState* st, unsigned* hist, int shift, int width,
+__device__ __forceinline__ void topk_digit_body(TopkState* st, unsigned* hist, int shift, int width,
                                                      int last, int64_t n_g) {
   __shared__ long long s_w[32];
   __shared__ int s_bin;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(1024) k_topk_digit(TopkState* st, unsigned* hi
 
 // Ties at the pivot per contiguous chunk (only when some must be cut).
 template <typename T>
-__global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+__device__ __forceinline__ void tie_count_body(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
                                                    int64_t n_g, int64_t chunk, const TopkState* st,
                                                    unsigned* __restrict__ counts) {
   if (!st->need_tie) return;
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, cons
 // index (ties taken in index order).
 // base: added to the index written (the value API selects inside a range).
 template <typename T>
-__global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+__device__ __forceinline__ void tie_find_body(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
                                                    int64_t n_g, int64_t chunk, int nchunks, TopkState* st,
                                                    const unsigned* __restrict__ counts, int64_t base = 0) {
   if (!st->need_tie) return;
@@ -359,6 +359,81 @@ __global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, cons
     __syncthreads();
   }
   if (tid == 0) st->tie_j = base + s_j;
+}
+
+// The single-range kernels (one worker, or a range of the value API).
+template <typename T>
+__global__ void __launch_bounds__(256, 4) k_topk_hist(const T* e, const T* __restrict__ g, double eta_d, int64_t n_g,
+                                                   int shift, int width, const TopkState* st,
+                                                   unsigned* __restrict__ hist, T* acc_out = nullptr,
+                                                   int* flags = nullptr) {
+  topk_hist_body<T>(e, g, eta_d, n_g, shift, width, st, hist, acc_out, flags);
+}
+template <typename T>
+__global__ void __launch_bounds__(1024) k_topk_digit(TopkState* st, unsigned* hist, int shift, int width, int last,
+                                                     int64_t n_g) {
+  topk_digit_body<T>(st, hist, shift, width, last, n_g);
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_tie_count(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                   int64_t n_g, int64_t chunk, const TopkState* st,
+                                                   unsigned* __restrict__ counts) {
+  tie_count_body<T>(e, g, eta_d, n_g, chunk, st, counts);
+}
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tie_find(const T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                   int64_t n_g, int64_t chunk, int nchunks, TopkState* st,
+                                                   const unsigned* __restrict__ counts, int64_t base = 0) {
+  tie_find_body<T>(e, g, eta_d, n_g, chunk, nchunks, st, counts, base);
+}
+
+// The same selection for every worker of a single-device cluster at once
+// (blockIdx.y = worker): eight workers' radix passes, digit picks and tie
+// searches share each launch instead of running one after another.  Worker
+// y owns st[y], hist[y * kBins ..] and counts[y * kTieChunks ..]; its acc is
+// formed in place in e[y] by the first pass, as in the per-worker path.
+struct TopkBatch {
+  void* e[kMaxWorkers];        // residual -> acc (in place)
+  const void* g[kMaxWorkers];  // gradients (first pass only)
+};
+
+static __global__ void k_topk_init_b(TopkState* st, int n, long long k) {
+  if ((int)threadIdx.x < n) {
+    TopkState* s = st + threadIdx.x;
+    s->prefix = 0;
+    s->mask = 0;
+    s->k_rem = k;
+    s->eq = 0;
+    s->tie_j = 0;
+    s->pivot = 0.0;
+    s->need_tie = 0;
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(256, 4) k_topk_hist_b(TopkBatch b, double eta_d, int64_t n_g, int shift, int width,
+                                                     const TopkState* st, unsigned* __restrict__ hist, int first,
+                                                     int* flags) {
+  const int y = blockIdx.y;
+  T* acc = (T*)b.e[y];
+  topk_hist_body<T>(acc, first ? (const T*)b.g[y] : nullptr, eta_d, n_g, shift, width, st + y, hist + y * kBins,
+                    first ? acc : nullptr, first ? flags : nullptr);
+}
+template <typename T>
+__global__ void __launch_bounds__(1024) k_topk_digit_b(TopkState* st, unsigned* hist, int shift, int width, int last,
+                                                       int64_t n_g) {
+  topk_digit_body<T>(st + blockIdx.x, hist + blockIdx.x * kBins, shift, width, last, n_g);
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_tie_count_b(TopkBatch b, int64_t n_g, int64_t chunk, const TopkState* st,
+                                                     unsigned* __restrict__ counts) {
+  const int y = blockIdx.y;
+  tie_count_body<T>((const T*)b.e[y], nullptr, 1.0, n_g, chunk, st + y, counts + (int64_t)y * kTieChunks);
+}
+template <typename T>
+__global__ void __launch_bounds__(1024) k_tie_find_b(TopkBatch b, int64_t n_g, int64_t chunk, int nchunks,
+                                                     TopkState* st, const unsigned* __restrict__ counts) {
+  const int y = blockIdx.x;
+  tie_find_body<T>((const T*)b.e[y], nullptr, 1.0, n_g, chunk, nchunks, st + y, counts + (int64_t)y * kTieChunks);
 }
 
 // acc = e + eta*G in place with the non-finite probe (workers that select
