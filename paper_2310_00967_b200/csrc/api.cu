@@ -182,11 +182,11 @@ template int launch_finalize<double>(micro_ctx*, const int32_t*, const void*, in
 
 
 
-int bitmap_offsets(const unsigned* bitmap, int64_t nwords, int* off, int* tiles, cudaStream_t st) {
+int bitmap_offsets(const unsigned* bitmap, int64_t nwords, int* off, int* tiles, cudaStream_t st, long long* total) {
   const int64_t nt = scan_tiles(nwords);
   k_scan_totals<true><<<(unsigned)nt, kScanThreads, 0, st>>>(bitmap, nwords, tiles);
   CU(cudaGetLastError());
-  k_scan_top<<<1, kScanThreads, 0, st>>>(tiles, nt, nullptr);
+  k_scan_top<<<1, kScanThreads, 0, st>>>(tiles, nt, total);
   CU(cudaGetLastError());
   k_scan_apply<true><<<(unsigned)nt, kScanThreads, 0, st>>>(bitmap, nwords, tiles, off);
   CU(cudaGetLastError());
@@ -541,15 +541,29 @@ int aggregate_baseline(micro_ctx* c) {
           c->sel_idx[c->buf][i], c->counts + i, c->sel_cap, c->bitmap);
       CU(cudaGetLastError());
     }
-    TRY(bitmap_offsets(c->bitmap, c->nwords, c->word_off, c->scan_tmp, st));
-    k_bitmap_emit<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_off, uidx, K);
+    TRY(bitmap_offsets(c->bitmap, c->nwords, c->word_off, c->scan_tmp, st, K));
+    // Emission + worker-order sums: one pass over the bitmap's words when
+    // the union is dense (K > 15 % of n_g: coalesced residual loads), else
+    // the ordered emission and a gather per union entry.  The scan wrote K;
+    // each path's kernels read it and the other path's return at once.
+    const long long dense_above = (long long)c->nwords * 32 * 3 / 20;
+    const unsigned wgrid = grid_for(c->nwords * 8, c->dev);  // a warp per 4 words
+    if (c->cfg.error_feedback)
+      k_union_words<T, true><<<wgrid, 256, 0, st>>>(w, c->n, c->bitmap, c->nwords, c->word_off, uidx,
+                                                     (T*)c->uni_sum[c->buf], K, dense_above);
+    else
+      k_union_words<T, false><<<wgrid, 256, 0, st>>>(w, c->n, c->bitmap, c->nwords, c->word_off, uidx,
+                                                      (T*)c->uni_sum[c->buf], K, dense_above);
+    CU(cudaGetLastError());
+    k_bitmap_emit<<<grid_for(c->nwords, c->dev), 256, 0, st>>>(c->bitmap, c->nwords, c->word_off, uidx, K,
+                                                                dense_above);
+    CU(cudaGetLastError());
+    if (c->cfg.error_feedback)
+      k_union_reduce<T, true><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf], dense_above);
+    else
+      k_union_reduce<T, false><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf], dense_above);
     CU(cudaGetLastError());
   }
-  if (c->cfg.error_feedback)
-    k_union_reduce<T, true><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf]);
-  else
-    k_union_reduce<T, false><<<grid, 256, 0, st>>>(w, c->n, uidx, K, (T*)c->uni_sum[c->buf]);
-  CU(cudaGetLastError());
   if (!c->cfg.error_feedback)
     for (int i = 0; i < c->n_local; ++i) CU(cudaMemsetAsync(c->resid[i], 0, c->n_g * c->esz, st));
   else if (c->norm)

@@ -247,7 +247,8 @@ void nccl_release(micro_ctx* c);
 int read_flags(micro_ctx* c, int* flags);
 // word offsets of a union bitmap: off[w] = popcount of words [0, w) (scan.cuh);
 // `tiles` holds scan_tiles(nwords) ints of scratch
-int bitmap_offsets(const unsigned* bitmap, int64_t nwords, int* off, int* tiles, cudaStream_t st);
+int bitmap_offsets(const unsigned* bitmap, int64_t nwords, int* off, int* tiles, cudaStream_t st,
+                   long long* total = nullptr);
 // threshold update, history, dense g/n and model after the union is formed
 // (instantiated for float and double in api.cu)
 template <typename T>

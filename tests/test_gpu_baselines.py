@@ -58,10 +58,12 @@ def run(kind, n_g, n, d, ties, dtype=np.float32, ef=True, iters=6, delta0=0.02, 
         dw[r["union_idx"]] = (r["union_sum"] / n).astype(res.dtype) if dtype == np.float64 else \
             (r["union_sum"].astype(np.float32) / np.float32(n))
         assert np.array_equal(m.dense(), dw), t
-    for rec in m.records(iters):  # harness.cpp:135, :170, :226-236
+    recs = m.records(iters)
+    for rec in recs:  # harness.cpp:135, :170, :226-236
         assert rec["threshold"] == (delta0 if kind == "hard" else 0.0)
         assert rec["buildup_factor"] == (rec["K"] / k_glob if rec["total_selected"] else 0.0)
     m.close()
+    return [rec["K"] for rec in recs]
 
 
 @pytest.mark.parametrize("kind", ["topk", "cltk", "hard", "dense"])
@@ -100,3 +102,39 @@ def test_gpu_baselines_one_worker(kind, n_g, d, ties, dtype, ef, split):
     """n = 1: the selection is the union and the single-worker step finishes
     it (k1_stream + k1_gather, as for MiCRO): bit-exact like the general path."""
     run(kind, n_g, 1, d, ties, dtype=dtype, ef=ef, split=split)
+
+
+# The union of overlapping selections takes one of two device paths, chosen
+# on the device from the scan's total K: above 15 % of n_g one pass over the
+# bitmap's words (k_union_words), else the ordered emission and a gather per
+# entry (k_bitmap_emit + k_union_reduce).  Both against the oracle, with the
+# density checked to sit on the intended side (or to cross it mid-run).
+@pytest.mark.parametrize("delta0,dense", [(0.0005, True), (0.03, False)])
+@pytest.mark.parametrize("ef", [True, False])
+def test_gpu_union_paths_hard_n8(delta0, dense, ef):
+    n_g = 50_021
+    Ks = run("hard", n_g, 8, 0.01, False, ef=ef, delta0=delta0)
+    if dense:
+        assert all(K > 0.15 * n_g for K in Ks), Ks
+    else:  # sparse steps first; with EF the union densifies, so both paths run in one context
+        assert any(K <= 0.15 * n_g for K in Ks), Ks
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("delta0", [0.0005, 0.03])
+def test_gpu_union_paths_hard_f64_reference_code(delta0):
+    run("hard", 20_011, 5, 0.01, False, dtype=np.float64, delta0=delta0)
+
+
+# Top-k on several workers runs every worker's radix select in shared
+# launches (blockIdx.y = worker): ties across many tie-count chunks, up to 8
+# workers, fp32 and fp64 (the reference's code).
+@pytest.mark.parametrize("n_g,n,d,ties", [(65_537, 8, 0.02, True), (300_007, 5, 0.01, True),
+                                          (40_000, 8, 0.3, False)])
+def test_gpu_topk_batched_workers(n_g, n, d, ties):
+    run("topk", n_g, n, d, ties)
+
+
+@pytest.mark.ref
+def test_gpu_topk_batched_workers_f64_reference_code():
+    run("topk", 9_001, 6, 0.03, True, dtype=np.float64)
