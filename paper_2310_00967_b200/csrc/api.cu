@@ -536,18 +536,17 @@ int aggregate_baseline(micro_ctx* c) {
     c->vectors_done = true;
     return launch_finalize<T>(c, uidx, c->uni_sum[c->buf], 0);
   } else {
-    for (int i = 0; i < c->n_local; ++i) {
-      k_union_mark<<<grid_for(std::min<int64_t>(c->sel_cap, 2 * (int64_t)c->k_global + 1024), c->dev), 256, 0, st>>>(
-          c->sel_idx[c->buf][i], c->counts + i, c->sel_cap, c->bitmap);
-      CU(cudaGetLastError());
-    }
+    for (int i = 0; i < c->n_local; ++i) w.sel_idx[i] = c->sel_idx[c->buf][i];
+    const unsigned mgrid = grid_for(std::min<int64_t>(c->sel_cap, 2 * (int64_t)c->k_global + 1024), c->dev);
+    k_union_mark<<<dim3(mgrid, c->n_local), 256, 0, st>>>(w, c->counts, c->sel_cap, c->bitmap);
+    CU(cudaGetLastError());
     TRY(bitmap_offsets(c->bitmap, c->nwords, c->word_off, c->scan_tmp, st, K));
     // Emission + worker-order sums: one pass over the bitmap's words when
     // the union is dense (K > 15 % of n_g: coalesced residual loads), else
     // the ordered emission and a gather per union entry.  The scan wrote K;
     // each path's kernels read it and the other path's return at once.
     const long long dense_above = (long long)c->nwords * 32 * 3 / 20;
-    const unsigned wgrid = grid_for(c->nwords * 8, c->dev);  // a warp per 4 words
+    const unsigned wgrid = grid_for(c->nwords * 32 / MICRO_UW_WORDS, c->dev);  // a warp per MICRO_UW_WORDS words
     if (c->cfg.error_feedback)
       k_union_words<T, true><<<wgrid, 256, 0, st>>>(w, c->n, c->bitmap, c->nwords, c->word_off, uidx,
                                                      (T*)c->uni_sum[c->buf], K, dense_above);
@@ -922,6 +921,26 @@ int micro_compress(micro_ctx* c, const void* const* d_grads, double eta, int64_t
     // top-k on several workers: every worker's radix select in the same launches
     if (c->esz == 4) TRY(launch_topk_batch<float>(c, gs.data(), eta));
     else TRY(launch_topk_batch<double>(c, gs.data(), eta));
+  } else if ((c->kind == 2 || c->kind == 4) && c->n_local > 1) {
+    // workers that only accumulate this step (CLT-k's non-leaders, dense: all)
+    // in one launch; the CLT-k leader then selects as in launch_baseline
+    const int leader = c->kind == 2 ? (int)(t % c->n) : -1;
+    TopkBatch b{};
+    for (int i = 0; i < c->n_local; ++i) {
+      b.e[i] = c->resid[i];
+      b.g[i] = gs[i];
+    }
+    const long long count = c->kind == 4 ? (long long)c->n_g : 0;
+    const dim3 grid(grid_for(c->n_g, c->dev), c->n_local);
+    if (c->esz == 4)
+      k_accumulate_probe_b<float><<<grid, 256, 0, c->stream>>>(b, eta, c->n_g, c->flags, leader, c->counts, count);
+    else
+      k_accumulate_probe_b<double><<<grid, 256, 0, c->stream>>>(b, eta, c->n_g, c->flags, leader, c->counts, count);
+    CU(cudaGetLastError());
+    if (leader >= 0) {
+      if (c->esz == 4) TRY(launch_k1<float>(c, leader, gs[leader], eta, t));
+      else TRY(launch_k1<double>(c, leader, gs[leader], eta, t));
+    }
   } else {
     for (int i = 0; i < c->n_local; ++i) {
       if (c->esz == 4) TRY(launch_k1<float>(c, i, gs[i], eta, t));

@@ -439,8 +439,8 @@ __global__ void __launch_bounds__(1024) k_tie_find_b(TopkBatch b, int64_t n_g, i
 // acc = e + eta*G in place with the non-finite probe (workers that select
 // nothing this step: CLT-k non-leaders, dense).
 template <typename T>
-__global__ void __launch_bounds__(256) k_accumulate_probe(T* __restrict__ e, const T* __restrict__ g, double eta_d,
-                                                          int64_t n_g, int* flags) {
+__device__ __forceinline__ void accumulate_probe_body(T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                      int64_t n_g, int* flags) {
   using V = typename Vec<T>::V;
   constexpr int VN = Vec<T>::N;
   constexpr int U = 4;  // vectors per thread in flight
@@ -474,11 +474,28 @@ __global__ void __launch_bounds__(256) k_accumulate_probe(T* __restrict__ e, con
     }
   if (probe != probe) atomicOr(flags, 1);
 }
+template <typename T>
+__global__ void __launch_bounds__(256) k_accumulate_probe(T* __restrict__ e, const T* __restrict__ g, double eta_d,
+                                                          int64_t n_g, int* flags) {
+  accumulate_probe_body<T>(e, g, eta_d, n_g, flags);
+}
+// Every worker of the cluster but `skip` (the CLT-k leader; -1: none) at
+// once (blockIdx.y = worker), and their selection counts set to `count`.
+template <typename T>
+__global__ void __launch_bounds__(256) k_accumulate_probe_b(TopkBatch b, double eta_d, int64_t n_g, int* flags,
+                                                            int skip, long long* counts, long long count) {
+  const int y = blockIdx.y;
+  if (y == skip) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[y] = count;
+  accumulate_probe_body<T>((T*)b.e[y], (const T*)b.g[y], eta_d, n_g, flags);
+}
 
 // ---- union of overlapping selections: bitmap, then ordered emission ----
-static __global__ void __launch_bounds__(256) k_union_mark(const int32_t* __restrict__ idx, const long long* count,
-                                                    long long cap, unsigned* __restrict__ bitmap) {
-  const long long k = min(*count, cap);
+// blockIdx.y = worker: every worker's selection in one launch.
+static __global__ void __launch_bounds__(256) k_union_mark(WorkerPtrs wp, const long long* counts, long long cap,
+                                                    unsigned* __restrict__ bitmap) {
+  const int32_t* __restrict__ idx = wp.sel_idx[blockIdx.y];
+  const long long k = min(counts[blockIdx.y], cap);
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < k; m += (long long)gridDim.x * blockDim.x) {
     const int32_t j = idx[m];
     atomicOr(&bitmap[j >> 5], 1u << (j & 31));
@@ -514,13 +531,19 @@ static __global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict
 // s = 0; s += acc_r for r in worker order (collectives.cpp:44-45); the union
 // lands at off[w] + rank in index order; the bitmap is cleared for the next
 // step (K: the scan's total).
+#ifndef MICRO_UW_WORDS
+#define MICRO_UW_WORDS 2
+#endif
+#ifndef MICRO_UW_MINB
+#define MICRO_UW_MINB 4
+#endif
 template <typename T, bool kZero>
-__global__ void __launch_bounds__(256) k_union_words(WorkerPtrs wp, int n, unsigned* __restrict__ bitmap,
+__global__ void __launch_bounds__(256, MICRO_UW_MINB) k_union_words(WorkerPtrs wp, int n, unsigned* __restrict__ bitmap,
                                                      int64_t nwords, const int* __restrict__ off,
                                                      int32_t* __restrict__ uidx, T* __restrict__ usum, long long* K,
                                                      long long dense_above) {
   if (*K <= dense_above) return;  // sparse union: k_bitmap_emit + k_union_reduce
-  constexpr int kW = 4;
+  constexpr int kW = MICRO_UW_WORDS;  // words per warp and iteration
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -540,7 +563,10 @@ __global__ void __launch_bounds__(256) k_union_words(WorkerPtrs wp, int n, unsig
         if (bits[q]) bitmap[w0 + q] = 0u;
       }
     }
-    if (!(bits[0] | bits[1] | bits[2] | bits[3])) continue;
+    unsigned any = 0;
+#pragma unroll
+    for (int q = 0; q < kW; ++q) any |= bits[q];
+    if (!any) continue;
     T s[kW];
 #pragma unroll
     for (int q = 0; q < kW; ++q) s[q] = (T)0;
