@@ -551,7 +551,9 @@ __global__ void __launch_bounds__(kGatherWarps * 32) k1_gather(CompactArgs a) {
   T* __restrict__ x = (T*)a.model;
   // kG entries per lane in flight: at high density a run holds hundreds of
   // pairs and the model's random read-modify-write is latency bound
-  constexpr int kG = 32 / (int)sizeof(T);  // 8 fp32, 4 fp64 (registers: occupancy)
+  // (dense selections, !kWide: 8 in fp64 too — C5 d = 0.1 f64 10065 -> 9859
+  // us/iter; 16 in fp32 was slower at 80 registers)
+  constexpr int kG = kWide ? 32 / (int)sizeof(T) : 8;  // kWide: 8 fp32, 4 fp64 (registers: occupancy)
   const int lim = n < room ? n : (int)room;
   for (int m0 = lane; m0 < lim; m0 += 32 * kG) {
     int32_t j[kG];
