@@ -532,10 +532,10 @@ static __global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict
 // lands at off[w] + rank in index order; the bitmap is cleared for the next
 // step (K: the scan's total).
 #ifndef MICRO_UW_WORDS
-#define MICRO_UW_WORDS 2
+#define MICRO_UW_WORDS 4
 #endif
 #ifndef MICRO_UW_MINB
-#define MICRO_UW_MINB 4
+#define MICRO_UW_MINB 2
 #endif
 template <typename T, bool kZero>
 __global__ void __launch_bounds__(256, MICRO_UW_MINB) k_union_words(WorkerPtrs wp, int n, unsigned* __restrict__ bitmap,
