@@ -546,7 +546,7 @@ int aggregate_baseline(micro_ctx* c) {
     // the ordered emission and a gather per union entry.  The scan wrote K;
     // each path's kernels read it and the other path's return at once.
     const long long dense_above = (long long)c->nwords * 32 * 3 / 20;
-    const unsigned wgrid = grid_for(c->nwords * 32 / MICRO_UW_WORDS, c->dev);  // a warp per MICRO_UW_WORDS words
+    const unsigned wgrid = grid_for(c->nwords * 32 / kUnionWords, c->dev);  // a warp per kUnionWords words
     if (c->cfg.error_feedback)
       k_union_words<T, true><<<wgrid, 256, 0, st>>>(w, c->n, c->bitmap, c->nwords, c->word_off, uidx,
                                                      (T*)c->uni_sum[c->buf], K, dense_above);

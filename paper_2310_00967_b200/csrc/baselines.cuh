@@ -531,19 +531,16 @@ static __global__ void __launch_bounds__(256) k_bitmap_emit(unsigned* __restrict
 // s = 0; s += acc_r for r in worker order (collectives.cpp:44-45); the union
 // lands at off[w] + rank in index order; the bitmap is cleared for the next
 // step (K: the scan's total).
-#ifndef MICRO_UW_WORDS
-#define MICRO_UW_WORDS 4
-#endif
-#ifndef MICRO_UW_MINB
-#define MICRO_UW_MINB 2
-#endif
+// 4 words per warp and iteration at <= 128 registers (2 CTAs per SM) measured
+// best (profiles/README.md: 2 words at <= 64 registers, 4 at 143 slower)
+constexpr int kUnionWords = 4;
 template <typename T, bool kZero>
-__global__ void __launch_bounds__(256, MICRO_UW_MINB) k_union_words(WorkerPtrs wp, int n, unsigned* __restrict__ bitmap,
+__global__ void __launch_bounds__(256, 2) k_union_words(WorkerPtrs wp, int n, unsigned* __restrict__ bitmap,
                                                      int64_t nwords, const int* __restrict__ off,
                                                      int32_t* __restrict__ uidx, T* __restrict__ usum, long long* K,
                                                      long long dense_above) {
   if (*K <= dense_above) return;  // sparse union: k_bitmap_emit + k_union_reduce
-  constexpr int kW = MICRO_UW_WORDS;  // words per warp and iteration
+  constexpr int kW = kUnionWords;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
