@@ -2,13 +2,15 @@
 and the checker stepped together every iteration, as tests/test_gpu_configs.py
 does, for longer than the suite can afford.
 
-    python tools/long_parity.py [out.json]
+    python tools/long_parity.py [out.json] [--more]
 
   c3_n1_f64_g32: the bench's default step (138M, d = 0.01, n = 1, fp32
       gradients into fp64 state, model + dense g/n) vs the reference's own
       compiled code (oracle/_ref), 150 iterations from the warm delta_0.
   c3_n8_f32: 138M, n = 8, the in-process cluster and the 8-rank peer
       exchange (GroupMicro) vs the C restatement, 20 iterations.
+  --more: C1 (n = 1, fp32) for 2000 iterations (the reference's acceptance-run
+      length, acceptance.cpp:93-118), C4 for 30, C5 d = 0.1 / 0.001 for 10.
 Every iteration: counts, union indices and sums, next thresholds (exact);
 residuals, model and dense g/n at the listed checkpoints."""
 import json
@@ -24,27 +26,51 @@ for _p in (ROOT, os.path.join(ROOT, "oracle")):  # as tests/conftest.py
 from tests.test_gpu_configs import Run, warm_delta0  # noqa: E402
 
 
+OUT = "gpurun_out/long_parity.json"
+RES = []
+
+
 def long_run(tag, iters, checks, **kw):
     t0 = time.time()
     run = Run(**kw)
     for t in range(iters):
         run.step(t, full_check=t in checks)
     run.close()
-    return {"case": tag, "iterations": iters, "full_checks_at": sorted(checks), "result": "bit-exact",
-            "wall_s": round(time.time() - t0, 1)}
+    r = {"case": tag, "iterations": iters, "full_checks_at": sorted(checks), "result": "bit-exact",
+         "wall_s": round(time.time() - t0, 1)}
+    RES.append(r)
+    with open(OUT, "w") as f:  # after every case: a later failure keeps the earlier results
+        json.dump(RES, f, indent=1)
+    return r
+
+
+def more(res):
+    """The acceptance-run length at C1 and longer runs at C4 / C5."""
+    res.append(long_run("c1_n1_f32 vs restatement (acceptance length)", 2000, {0, 999, 1999}, n_g=11_700_000, n=1,
+                        d=0.01, delta0=0.01))
+    print(json.dumps(res[-1]), flush=True)
+    res.append(long_run("c4_n1_f32 vs restatement", 30, {29}, n_g=340_000_000, n=1, d=0.001,
+                        delta0=warm_delta0(0.001)))
+    print(json.dumps(res[-1]), flush=True)
+    for d in (0.1, 0.001):
+        res.append(long_run(f"c5_n1_d{d}_f32 vs restatement", 10, {9}, n_g=1_500_000_000, n=1, d=d,
+                            delta0=warm_delta0(d)))
+        print(json.dumps(res[-1]), flush=True)
 
 
 def main():
-    out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/long_parity.json"
+    global OUT
+    OUT = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else OUT
     res = []
+    if "--more" in sys.argv:
+        more(res)
+        return
     res.append(long_run("c3_n1_f64_g32 vs reference code", 150, {0, 49, 99, 149}, n_g=138_000_000, n=1, d=0.01,
                         delta0=warm_delta0(0.01), dtype=np.float64, checker="reference", grad32=True))
     print(json.dumps(res[-1]), flush=True)
     res.append(long_run("c3_n8_f32 cluster + GroupMicro vs restatement", 20, {0, 9, 19}, n_g=138_000_000, n=8,
                         d=0.01, delta0=warm_delta0(0.01), group=True))
     print(json.dumps(res[-1]), flush=True)
-    with open(out, "w") as f:
-        json.dump(res, f, indent=1)
 
 
 if __name__ == "__main__":
