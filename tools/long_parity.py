@@ -11,6 +11,8 @@ does, for longer than the suite can afford.
       exchange (GroupMicro) vs the C restatement, 20 iterations.
   --more: C1 (n = 1, fp32) for 2000 iterations (the reference's acceptance-run
       length, acceptance.cpp:93-118), C4 for 30, C5 d = 0.1 / 0.001 for 10.
+  --ref: C1 fp64 on fp32 gradients vs the reference's own code for 2000
+      iterations; C2 at n = 8 (cluster + GroupMicro) for 200.
 Every iteration: counts, union indices and sums, next thresholds (exact);
 residuals, model and dense g/n at the listed checkpoints."""
 import json
@@ -58,10 +60,25 @@ def more(res):
         print(json.dumps(res[-1]), flush=True)
 
 
+def ref_long(res):
+    """The acceptance-run length against the reference's own code (fp64), and
+    the partitioned C2 cluster + peer exchange over 200 iterations."""
+    res.append(long_run("c1_n1_f64_g32 vs reference code (acceptance length)", 2000, {0, 999, 1999},
+                        n_g=11_700_000, n=1, d=0.01, delta0=0.01, dtype=np.float64, checker="reference",
+                        grad32=True))
+    print(json.dumps(res[-1]), flush=True)
+    res.append(long_run("c2_n8_f32 cluster + GroupMicro vs restatement", 200, {0, 99, 199}, n_g=11_700_000, n=8,
+                        d=0.01, delta0=warm_delta0(0.01), group=True))
+    print(json.dumps(res[-1]), flush=True)
+
+
 def main():
     global OUT
     OUT = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else OUT
     res = []
+    if "--ref" in sys.argv:
+        ref_long(res)
+        return
     if "--more" in sys.argv:
         more(res)
         return
