@@ -1144,7 +1144,9 @@ int micro_records(micro_ctx* c, int64_t max, micro_record* out, int64_t* written
     r.buildup_factor = r.total_selected == 0 ? 0.0 : (double)r.K / (double)k_global;   // collectives.cpp:59-63
     r.redundant_traffic_factor = r.total_selected == 0 ? 0.0 : (double)r.total_selected / (double)r.K;
     r.error_norm = esum / nl;                                                          // harness.cpp:230-235
-    r.threshold = dsum / nl;                                                           // harness.cpp:149
+    // MiCRO: the workers' mean (harness.cpp:149); the hard threshold records
+    // delta_0 itself (:172), not a mean that need not round back to it
+    r.threshold = c->kind == 3 ? c->cfg.initial_threshold : dsum / nl;
     out[s] = r;
   }
   if (written) *written = n;

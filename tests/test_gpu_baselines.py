@@ -109,7 +109,7 @@ def test_gpu_baselines_one_worker(kind, n_g, d, ties, dtype, ef, split):
 # bitmap's words (k_union_words), else the ordered emission and a gather per
 # entry (k_bitmap_emit + k_union_reduce).  Both against the oracle, with the
 # density checked to sit on the intended side (or to cross it mid-run).
-@pytest.mark.parametrize("delta0,dense", [(0.0005, True), (0.03, False)])
+@pytest.mark.parametrize("delta0,dense", [(0.0005, True), (0.03, False), (0.0258, False)])
 @pytest.mark.parametrize("ef", [True, False])
 def test_gpu_union_paths_hard_n8(delta0, dense, ef):
     n_g = 50_021

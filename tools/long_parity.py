@@ -11,6 +11,7 @@ does, for longer than the suite can afford.
       exchange (GroupMicro) vs the C restatement, 20 iterations.
   --more: C1 (n = 1, fp32) for 2000 iterations (the reference's acceptance-run
       length, acceptance.cpp:93-118), C4 for 30, C5 d = 0.1 / 0.001 for 10.
+  --baselines: top-k / CLT-k / hard threshold at C1 x 8, 20 iterations.
   --ref: C1 fp64 on fp32 gradients vs the reference's own code for 2000
       iterations; C2 at n = 8 (cluster + GroupMicro) for 200.
 Every iteration: counts, union indices and sums, next thresholds (exact);
@@ -72,10 +73,34 @@ def ref_long(res):
     print(json.dumps(res[-1]), flush=True)
 
 
+def baselines(res):
+    """The comparison sparsifiers at C1 x 8 (batched top-k, union by words /
+    by gather) vs the restatement (BaselineCluster), 20 iterations, every
+    quantity every iteration (tests/test_gpu_baselines.py's run)."""
+    from tests.test_gpu_baselines import run as brun
+    kinds = os.environ.get("KINDS", "topk,cltk,hard").split(",")
+    for kind, delta0 in (("topk", 0.02), ("cltk", 0.02), ("hard", 0.0258)):
+        if kind not in kinds:
+            continue
+        t0 = time.time()
+        Ks = brun(kind, 11_700_000, 8, 0.01, False, iters=20, delta0=delta0)
+        r = {"case": f"c1_n8_{kind}_f32 vs restatement", "iterations": 20, "full_checks_at": list(range(20)),
+             "result": "bit-exact", "union_density": [round(K / 11_700_000, 4) for K in Ks[:3]] + ["..."] +
+             [round(Ks[-1] / 11_700_000, 4)], "wall_s": round(time.time() - t0, 1)}
+        RES.append(r)
+        with open(OUT, "w") as f:
+            json.dump(RES, f, indent=1)
+        res.append(r)
+        print(json.dumps(r), flush=True)
+
+
 def main():
     global OUT
     OUT = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else OUT
     res = []
+    if "--baselines" in sys.argv:
+        baselines(res)
+        return
     if "--ref" in sys.argv:
         ref_long(res)
         return
